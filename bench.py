@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""bench.py — graph-view masked attention (arXiv 2502.01659) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+
+One "step" is one pass of the whole hot path (neighbour enumeration, scores, online
+softmax, aggregation — one ga_attention call per shard, plus the halo exchange at N>1)
+over the configuration's full synthetic input.  Default workload: BASELINE.json configs[1]
+(L=65536, 8 heads, d=64, bf16, dilated window w=256 r=2) on one B200.  N>1 (torchrun,
+one process per GPU) is weak scaling: every rank owns L query rows of an N*L-token
+sequence and exchanges a K/V halo with its neighbours each step (NCCL over NVLink).
+
+metric: attention edges/s = (mask nnz x heads) / step time, whole job.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "attention edges/sec (graph-view masked attention; edges = mask nnz x heads)"
+CONFIGS = {
+    "cfg1": dict(L=1024, H=1, d=64, dtype="f32", mask=("window", 32, 1)),
+    "cfg2": dict(L=65536, H=8, d=64, dtype="bf16", mask=("window", 256, 2)),
+    "cfg3": dict(L=2 ** 20, H=1, d=64, dtype="bf16", mask=("bigbird", 128, 64, 64)),
+    "cfg4": dict(L=2 ** 24, H=1, d=64, dtype="bf16", mask=("longnet", 2048, 2)),
+    "cfg5": dict(L=160_000_000, H=1, d=64, dtype="bf16", mask=("window", 128, 1)),
+}
+SEEDS = {"cfg1": 0x5EED0001, "cfg2": 0x5EED0002, "cfg3": 0x5EED0003, "cfg4": 0x5EED0004, "cfg5": 0x5EED0005}
+BIGBIRD_SEED = 0xB16B12D
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def mask_desc(cfg):
+    kind, *a = cfg["mask"]
+    if kind == "window":
+        return f"Window(w={a[0]}, r={a[1]})"
+    if kind == "bigbird":
+        return f"BigBird(window={a[0]}, globals={a[1]} evenly spaced, random={a[2]}/row) as explicit CSR"
+    return f"LongNet(w0={a[0]}, alpha={a[1]}) implicit"
+
+
+def eb(dtype):
+    return 4 if dtype == "f32" else 2
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ oracle arm
+_ORACLE_INPUTS = {}
+
+
+def oracle_rate(cfg_name, budget_s=15.0, max_rows=None):
+    """Time the fp64 oracle (as it stands) on a bounded row sample of the workload.
+    Returns (edges/s, threads, sample description, edges, seconds)."""
+    import numpy as np
+
+    import oracle
+
+    cfg = CONFIGS[cfg_name]
+    L, H, d = cfg["L"], cfg["H"], cfg["d"]
+    seed = SEEDS[cfg_name]
+    kind, *a = cfg["mask"]
+    om = {"window": lambda: oracle.window(L, a[0], a[1]),
+          "bigbird": lambda: oracle.bigbird(L, a[0], a[1], a[2], BIGBIRD_SEED),
+          "longnet": lambda: oracle.longnet(L, a[0], a[1])}[kind]()
+    arrays = 3 * L * H * d * 8 <= 4 << 30
+    if arrays:
+        if cfg_name not in _ORACLE_INPUTS:
+            _ORACLE_INPUTS[cfg_name] = oracle.inputs(seed, L, H, d, cfg["dtype"])
+        qkv = _ORACLE_INPUTS[cfg_name]
+
+    def run(rows):
+        t0 = time.perf_counter()
+        if arrays:
+            _, e = oracle.attention(*qkv, om, rows=rows)
+        else:
+            _, e = oracle.attention_seeded(seed, cfg["dtype"], om, H, d, rows=rows)
+        return e, time.perf_counter() - t0
+
+    rng = np.random.default_rng(0)
+    n = 32
+    e, t = run(np.sort(rng.choice(L, n, replace=False)))
+    while t < budget_s / 8 and n < L:
+        n = min(L, n * 4)
+        e, t = run(np.sort(rng.choice(L, n, replace=False)))
+    target = int(n * budget_s / max(t, 1e-3))
+    n = max(32, min(L, target, max_rows or L))
+    rows = np.sort(rng.choice(L, n, replace=False))
+    e, t = run(rows)
+    sample = (f"{n} uniformly sampled query rows of {L} ({'fp64 arrays' if arrays else 'rows regenerated from the seed'}"
+              f", all {H} heads), {e} edges")
+    return e / t, oracle.num_threads(), sample, e, t
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "edge", "window", "tc"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        return reference_arm(args, cfg, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2502_01659_b200 as ga
+    from paper_2502_01659_b200 import dist as gdist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L_local, H, d = cfg["L"], cfg["H"], cfg["d"]
+    L = L_local * world
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[cfg["dtype"]]
+    seed = SEEDS[args.config]
+    kind, *a = cfg["mask"]
+    r0, r1 = rank * L_local, (rank + 1) * L_local
+
+    # ---- inputs (resident in HBM before timing) and the step function
+    ws = None
+    if kind == "window":
+        mask = ga.Window(a[0], a[1])
+        nnz = ga.mask_count(mask, L)
+        halo = gdist.window_halo(mask) if world > 1 else 0
+        buf = gdist.alloc_halo(L, r0, r1, halo, H, d, tdt, dev)
+        q = torch.empty((L_local, H, d), dtype=tdt, device=dev)
+        ga.fill_inputs(q, seed, 0, r0 * H * d)
+        ga.fill_inputs(buf.local_k, seed, 1, r0 * H * d)
+        ga.fill_inputs(buf.local_v, seed, 2, r0 * H * d)
+        out = torch.empty_like(q)
+        comm = torch.cuda.Stream() if world > 1 else None
+
+        def step():
+            if world > 1:
+                gdist.sharded_window_attention(q, buf, mask, L, out=out, comm_stream=comm)
+            else:
+                ga.attention(q, buf.k, buf.v, mask, out, kernel=args.kernel)
+    else:
+        if world > 1:
+            raise SystemExit(f"--gpus > 1 is implemented for window masks (cfg2/cfg5); {args.config} is 1-GPU")
+        if kind == "bigbird":
+            mask = ga.mask_to_csr(ga.BigBird(a[0], a[1], a[2], seed=BIGBIRD_SEED), L)
+            nnz = mask.nnz
+            ws = torch.empty(ga.workspace_size(mask, L, d, H, tdt), dtype=torch.uint8, device=dev)
+        else:
+            mask = ga.LongNet(a[0], a[1])
+            nnz = ga.mask_count(mask, L)
+        q, k, v = ga.qkv_device(seed, L, H, d, tdt, device=dev)
+        out = torch.empty_like(q)
+
+        def step():
+            ga.attention(q, k, v, mask, out, kernel=args.kernel, workspace=ws)
+
+    edges_total = nnz * H  # all ranks together (global mask over the N*L sequence)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    lib = ga._abi.lib()
+    launches0 = lib.ga_launch_count()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    for s in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        if world > 1:
+            dist.barrier()
+        starts[s].record()
+        step()
+        ends[s].record()
+    barrier()
+    launches = lib.ga_launch_count() - launches0
+    clocks = sampler.stop()
+    per_step = [st.elapsed_time(en) for st, en in zip(starts, ends)]
+    total_ms = torch.tensor([sum(per_step)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+    ms = total_ms.item() / args.steps
+    value = edges_total / (ms / 1e3)
+
+    # ---- roofline for the dominant kernel (the attention kernel; one launch per step at N=1)
+    peaks, peak_src = load_peaks()
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    flops_per_edge = 4 * d  # q.k (2d) + p*v (2d) per head-edge, SURVEY §8(d)
+    kernel_ms = statistics.median(per_step)
+    achieved_tflops = edges_total / world * flops_per_edge / (kernel_ms / 1e3) / 1e12
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12  # FP32 FMA pipe, all SMs, max clock
+    gather_bytes_edge = 2 * d * eb(cfg["dtype"]) + (4 if kind == "bigbird" else 0)
+    gather_gbs = edges_total / world * gather_bytes_edge / (kernel_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"{args.config}:{args.kernel}")
+    roofline = {"bound": "alu", "achieved": round(achieved_tflops, 3), "peak": round(fp32_peak, 2), "unit": "TFLOP/s",
+                "frac": round(achieved_tflops / fp32_peak, 4), "traffic": traffic,
+                "peak_source": "derived: 148 SMs x 128 FP32 FMA/clk x 2 flop x sm_max_mhz "
+                               f"({sm_max:.0f} MHz, {peak_src} MEASURED_PEAKS.json)",
+                "algorithmic": f"{flops_per_edge} flop per head-edge x {edges_total // world} head-edges per launch",
+                "kernel_ms_median": round(kernel_ms, 4)}
+    gather = {"bytes_per_edge": gather_bytes_edge, "GBps": round(gather_gbs, 1),
+              "frac_of_8TBps": round(gather_gbs / 8000.0, 3),
+              "frac_of_measured_hbm": round(gather_gbs / peaks["hbm_gbs"], 3),
+              "note": "north-star gather model: every edge pulls K_j and V_j; window masks reuse K/V on chip, "
+                      "so this can exceed 1 (the kernel is ALU-bound, see roofline)"}
+
+    # ---- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(args, ga, gdist, cfg, mask, world, rank, r0, L, H, d, tdt, seed, dev, edges_total,
+                          buf if kind == "window" else None, ws)
+
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, cores, sample, _, _ = oracle_rate(args.config, args.cpu_budget)
+        cpu = {"value": rate, "unit": "edges/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": cfg["dtype"], "accum": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: L={L_local}{'x' + str(world) if world > 1 else ''} tokens, "
+                                   f"{H} heads, d={d}, {cfg['dtype']}, {mask_desc(cfg)}",
+                       "L": L, "heads": H, "d": d, "mask": mask_desc(cfg), "nnz": nnz,
+                       "kernel": args.kernel, "parallelism": f"query-range shards x{world}" + (
+                           ", NCCL halo exchange" if world > 1 else ""),
+                       "l2": "flushed between timed steps (256 MiB write outside the events); inputs > L2"},
+            "clocks": clocks, "roofline": roofline, "gather_model": gather, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure_e2e(args, ga, gdist, cfg, mask, world, rank, r0, L, H, d, tdt, seed, dev, edges_total, buf, ws):
+    """Same metric through the public API with pinned HOST buffers: H2D of the step's
+    inputs and D2H of its output inside the timed region."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+
+    L_local = cfg["L"]
+    n = L_local * H * d
+    steps = max(3, min(args.steps, 5))
+    if world == 1 and cfg["mask"][0] == "window":
+        host = []
+        for t in range(3):  # generate on device, stage in pinned host memory (setup, untimed)
+            x = torch.empty((L_local, H, d), dtype=tdt, device=dev)
+            ga.fill_inputs(x, seed, t)
+            host.append(x.cpu().pin_memory())
+        hout = torch.empty_like(host[0]).pin_memory()
+        s = torch.cuda.current_stream()
+        for _ in range(2):
+            ga.attention_host(*host, mask, hout, stream=s)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            ga.attention_host(*host, mask, hout, stream=s)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        h2d, d2h = 3 * n * host[0].element_size(), n * host[0].element_size()
+    elif world > 1:
+        hq = torch.empty((L_local, H, d), dtype=tdt).pin_memory()
+        hk, hv = torch.empty_like(hq).pin_memory(), torch.empty_like(hq).pin_memory()
+        for h_, t in ((hq, 0), (hk, 1), (hv, 2)):
+            x = torch.empty((L_local, H, d), dtype=tdt, device=dev)
+            ga.fill_inputs(x, seed, t, r0 * H * d)
+            h_.copy_(x.cpu())
+        q = torch.empty((L_local, H, d), dtype=tdt, device=dev)
+        out = torch.empty_like(q)
+        hout = torch.empty_like(hq).pin_memory()
+
+        def step():
+            q.copy_(hq, non_blocking=True)
+            buf.local_k.copy_(hk, non_blocking=True)
+            buf.local_v.copy_(hv, non_blocking=True)
+            gdist.sharded_window_attention(q, buf, mask, L, out=out)
+            hout.copy_(out, non_blocking=True)
+
+        for _ in range(2):
+            step()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+        h2d, d2h = 3 * n * hq.element_size(), n * hq.element_size()
+    else:
+        # explicit-CSR / LongNet configs: host Q,K,V copied in, output copied out each step
+        hq = torch.empty((L_local, H, d), dtype=tdt).pin_memory()
+        hk, hv = torch.empty_like(hq).pin_memory(), torch.empty_like(hq).pin_memory()
+        for h_, t in ((hq, 0), (hk, 1), (hv, 2)):
+            x = torch.empty((L_local, H, d), dtype=tdt, device=dev)
+            ga.fill_inputs(x, seed, t)
+            h_.copy_(x.cpu())
+        q, k, v = (torch.empty((L_local, H, d), dtype=tdt, device=dev) for _ in range(3))
+        out = torch.empty_like(q)
+        hout = torch.empty_like(hq).pin_memory()
+
+        def step():
+            q.copy_(hq, non_blocking=True)
+            k.copy_(hk, non_blocking=True)
+            v.copy_(hv, non_blocking=True)
+            ga.attention(q, k, v, mask, out, workspace=ws)
+            hout.copy_(out, non_blocking=True)
+
+        step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        h2d, d2h = 3 * n * hq.element_size(), n * hq.element_size()
+    return {"value": edges_total / (ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": h2d * world,
+            "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": steps,
+            "path": "ga_attention_host (C ABI, pinned host buffers)" if world == 1 and cfg["mask"][0] == "window"
+            else "pinned host -> device copies + ga_attention_ex + device -> host copy"}
+
+
+def reference_arm(args, cfg, world, rank):
+    """The reference arm for this tier is the fp64 CPU oracle, timed as it stands on the
+    host cores; each step is a bounded row sample of the same workload."""
+    if rank != 0:
+        return
+    budget = max(1.0, min(10.0, 120.0 / max(1, args.steps + args.warmup)))
+    rates, edges, secs = [], 0, 0.0
+    sample = None
+    cores = None
+    for s in range(args.warmup + args.steps):
+        rate, cores, sample, e, t = oracle_rate(args.config, budget_s=budget)
+        if s >= args.warmup:
+            rates.append(rate)
+            edges += e
+            secs += t
+    value = edges / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: L={cfg['L']}, {cfg['H']} heads, d={cfg['d']}, {cfg['dtype']} inputs, "
+                               f"{mask_desc(cfg)}", "note": "fp64 CPU oracle (oracle/oracle.c), OpenMP over rows"},
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

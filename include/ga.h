@@ -1,0 +1,190 @@
+/*
+ * ga.h — C ABI of libga.so: B200-native graph-view masked attention
+ * (Tomczak & Kuppannagari, "Longer Attention Span", arXiv 2502.01659).
+ *
+ * Tokens are graph nodes and attention-mask nonzeros are directed edges
+ * (§4.1 "Modeling").  For every query node i and every edge (i,j) the
+ * library computes, in ONE fused pass per row (Algorithm 1):
+ *
+ *     s_ij = q_i . k_j / sqrt(d)                       (Eq. 1; reading R4)
+ *     m_i, l_i  <- online softmax over j in N(i)        (Alg. 1)
+ *     o_i   = sum_j exp(s_ij - m_i) v_j / l_i           (Alg. 1; deferred /l, R5)
+ *     o_i   = 0 if N(i) is empty                        (Alg. 1 init; R6)
+ *
+ * and never forms the L x L matrix: only the nnz(mask) dot products are computed
+ * ("work optimal").
+ *
+ * Conventions for every entry point
+ *   Layout      Q, K, V, out are row-major [tokens, heads, d] ("BSHD" with B = 1): element
+ *               (t, h, c) lives at ((t*heads + h)*d + c).  Rows must be 16-byte aligned.
+ *   Dtypes      fp32 / bf16 / fp16 storage; all arithmetic in fp32 (reading R15); the
+ *               output is rounded to the input dtype (RNE).
+ *   d           32, 64 or 128.
+ *   Ownership   every pointer is caller-owned; the library never frees or retains
+ *               anything past the call (device memory comes from torch / cudaMalloc).
+ *   Streams     `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *               stream).  All device work is enqueued on it; no entry point synchronises
+ *               the device unless its comment says so.
+ *   Errors      a ga_status is returned; GA_OK = 0.  Argument errors are detected
+ *               synchronously before anything is enqueued.  Launch errors are caught with
+ *               cudaPeekAtLastError (GA_ERR_CUDA).  Device faults surface at the
+ *               caller's next synchronisation.  ga_last_error() returns a thread-local
+ *               message describing the last non-OK status.  No exceptions cross the ABI
+ *               and the library never aborts the process.
+ */
+#ifndef GA_H
+#define GA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GA_OK = 0,
+    GA_ERR_INVALID_ARG = -1, /* bad pointer / shape / parameter / alignment          */
+    GA_ERR_UNSUPPORTED = -2, /* valid but not implemented (e.g. d not in {32,64,128}) */
+    GA_ERR_CUDA = -3,        /* a CUDA runtime call or kernel launch failed           */
+    GA_ERR_OOM = -5,         /* workspace too small / allocation failed               */
+    GA_ERR_MASK = -6         /* ga_mask_validate found a malformed CSR                */
+} ga_status;
+
+typedef enum { GA_F32 = 0, GA_BF16 = 1, GA_F16 = 2 } ga_dtype;
+
+/* Mask families (§4.2 list, :224-237; SURVEY §8(c) readings). */
+typedef enum {
+    /* explicit binary CSR: row_ptr int64 [L+1], col_idx int32 [nnz], columns of each row
+       strictly increasing (reading R7 — no values vector). */
+    GA_MASK_CSR = 0,
+    /* |i-j| < w  and  |i-j| mod r == 0: local window (r = 1) and 1D
+       dilated window (readings R1, R2). */
+    GA_MASK_WINDOW = 1,
+    /* LongNet exponentially dilated: OR over k = 0..K of BLOCK_DILATED(w0*alpha^k, alpha^k),
+       K = max{k : w0*alpha^k <= L} (reading R11). */
+    GA_MASK_LONGNET = 2,
+    /* BigBird / Longformer: window(w) UNION global rows and columns UNION n_random random
+       columns per non-global row (readings R8-R10).  Materialise with
+       ga_mask_to_csr; ga_attention rejects it (GA_ERR_UNSUPPORTED) — the paper itself runs
+       the composed mask through the CSR kernel. */
+    GA_MASK_BIGBIRD = 3,
+    /* 2D dilation: floor(i/seg)==floor(j/seg) and (i mod seg) mod r == 0 and
+       (j mod seg) mod r == 0 (reading R3). */
+    GA_MASK_BLOCK_DILATED = 4
+} ga_mask_kind;
+
+/* Mask descriptor: the paper's "attention-specific parameters P_a" or explicit graph G
+   (Algorithm 1 input).  Unused fields are ignored; zero-initialise. */
+typedef struct ga_mask {
+    int32_t kind;              /* ga_mask_kind                                          */
+    int32_t reserved0;
+    int64_t L;                 /* number of graph nodes (global sequence length)         */
+    const int64_t *row_ptr;    /* CSR: DEVICE int64 [L+1], row_ptr[0]=0, nondecreasing     */
+    const int32_t *col_idx;    /* CSR: DEVICE int32 [nnz], sorted strictly per row        */
+    int64_t nnz;               /* CSR: number of edges (= row_ptr[L])                     */
+    int64_t w, r;              /* WINDOW / BIGBIRD window w >= 1; dilation r >= 1          */
+    int64_t w0, alpha;         /* LONGNET: first segment w0 >= 1, ratio alpha >= 2         */
+    int64_t seg;               /* BLOCK_DILATED segment length >= 1 (r as above)          */
+    const int64_t *global_idx; /* BIGBIRD: DEVICE int64 [n_global] sorted, or NULL for the
+                                  evenly spaced set {floor(k*L/n_global)} (reading R9)    */
+    int64_t n_global;          /* BIGBIRD global token count                             */
+    int64_t n_random;          /* BIGBIRD random columns per non-global row (<= 256)     */
+    uint64_t seed;             /* BIGBIRD random-column seed (reading R10)                */
+} ga_mask;
+
+/* Kernel selection (ga_opts.kernel). AUTO picks the fastest kernel implemented for the
+   (mask, dtype, d) triple; the others force one path (tests compare them). */
+typedef enum {
+    GA_KERNEL_AUTO = 0,
+    GA_KERNEL_EDGE = 1,   /* generic warp-per-(row,head) edge traversal, every family      */
+    GA_KERNEL_WINDOW = 2, /* tiled window/dilated kernel: K/V band staged in shared memory  */
+    GA_KERNEL_TC = 3      /* bf16/fp16 window: tcgen05 dense tiles + CUDA-core triangles    */
+} ga_kernel;
+
+/* Optional controls for ga_attention_ex.  Zero-initialise, then set what you need. */
+typedef struct ga_opts {
+    /* Query-range sharding: process global query rows
+       [q_begin, q_begin + q_rows).  Q and out hold exactly those rows (row 0 = q_begin).
+       q_rows = 0 means L - q_begin. */
+    int64_t q_begin, q_rows;
+    /* K and V hold global token rows [kv_begin, kv_begin + kv_rows); every neighbour of
+       every processed row must lie inside (halo / all-gather responsibility of the caller).
+       kv_rows = 0 means L - kv_begin. */
+    int64_t kv_begin, kv_rows;
+    /* Device workspace (needed by CSR inputs with rows above the heavy-row threshold);
+       size from ga_workspace_size. */
+    void *workspace;
+    size_t workspace_bytes;
+    /* Debug / work-optimality probes ("probe build").  When non-NULL a slower
+       instrumented kernel runs:
+         edge_counter      DEVICE u64, atomically += number of q.k dot products computed
+         row_fingerprint   DEVICE u64 [q_rows*3]: per processed row (head 0): degree,
+                           sum of j, sum of splitmix64(j), all mod 2^64. */
+    unsigned long long *edge_counter;
+    unsigned long long *row_fingerprint;
+    int32_t kernel;          /* ga_kernel */
+    int32_t heavy_threshold; /* CSR rows with more edges are split into chunks of this size
+                                and merged (0 = default 4096) */
+} ga_opts;
+
+/* The north-star entry point: O = masked-softmax attention of (Q,K,V) over mask.
+   Q,K,V,out: DEVICE [L, heads, d] in `dtype`.  `out` must not alias K or V; it may alias
+   Q only for implicit masks (one launch owns each row).  Returns GA_ERR_UNSUPPORTED for
+   GA_MASK_BIGBIRD (use ga_mask_to_csr) and for CSR masks whose rows exceed the heavy-row
+   threshold (those need ga_attention_ex with a workspace). */
+ga_status ga_attention(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out,
+                       int64_t L, int32_t d, int32_t heads, ga_dtype dtype, void *stream);
+
+/* ga_attention with sharding offsets, workspace, probes and kernel choice (opts may be NULL). */
+ga_status ga_attention_ex(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out,
+                          int64_t L, int32_t d, int32_t heads, ga_dtype dtype, const ga_opts *opts,
+                          void *stream);
+
+/* End-to-end variant on HOST buffers: copies Q,K,V (host, [L,heads,d]) to the device,
+   runs the attention, copies out back to host `out`, all enqueued on `stream` using the
+   stream-ordered allocator (cudaMallocAsync).  Host buffers should be pinned for
+   asynchronous copies; `out` is valid after the caller synchronises `stream`.  CSR arrays
+   in `mask` must already be DEVICE pointers. */
+ga_status ga_attention_host(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out,
+                            int64_t L, int32_t d, int32_t heads, ga_dtype dtype, void *stream);
+
+/* Workspace bytes ga_attention_ex needs for (mask, shape, opts).  Host only. */
+ga_status ga_workspace_size(const ga_mask *mask, int64_t L, int32_t d, int32_t heads, ga_dtype dtype,
+                            const ga_opts *opts, size_t *bytes);
+
+/* Exact number of edges of an implicit pattern (host; closed forms per family, SURVEY
+   §8(c)).  For GA_MASK_CSR returns mask->nnz.  For BIGBIRD with a device global_idx the
+   list is copied to the host (synchronous). */
+ga_status ga_mask_count(const ga_mask *pattern, int64_t *nnz_out);
+
+/* Materialise an implicit pattern as binary CSR on the device:
+   degrees -> exclusive scan -> fill, columns ascending.  row_ptr: DEVICE int64 [L+1];
+   col_idx: DEVICE int32 [nnz] with nnz from ga_mask_count.  The result equals the CPU
+   enumeration bit for bit.  Temporary scan storage is stream-ordered (cudaMallocAsync). */
+ga_status ga_mask_to_csr(const ga_mask *pattern, int64_t *row_ptr, int32_t *col_idx, void *stream);
+
+/* O(L + nnz) validity check of an explicit CSR (S:97-98 invariants).  Synchronises the
+   stream.  *ok = 1 when valid; returns GA_ERR_MASK (and *ok = 0) otherwise. */
+ga_status ga_mask_validate(const ga_mask *csr, void *stream, int *ok);
+
+/* Synthetic inputs (reading R22): dst[t] = round_dtype(x(e0 + t)) for
+   t in [0, n), x(e) = (splitmix64(splitmix64(seed + tensor) ^ e) >> 40) * 2^-24,
+   plus `shift` (added in fp32 before rounding; 0 for the paper's U[0,1)).  DEVICE dst. */
+ga_status ga_fill_inputs(void *dst, ga_dtype dtype, int64_t n, uint64_t seed, int32_t tensor, int64_t e0,
+                         float shift, void *stream);
+
+/* Thread-local description of the last non-OK status ("" if none). */
+const char *ga_last_error(void);
+
+/* Telemetry: number of CUDA kernels this library has launched since it was loaded
+   (host counter; bench.py reports it as gpu_launches). */
+unsigned long long ga_launch_count(void);
+
+/* Library version string. */
+const char *ga_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GA_H */

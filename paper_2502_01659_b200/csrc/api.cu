@@ -1,0 +1,378 @@
+// api.cu — the C ABI of libga.so (include/ga.h): validation, dispatch, errors.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <atomic>
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ga {
+
+static thread_local std::string g_err;
+static std::atomic<unsigned long long> g_launches{0};
+
+void note_launches(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+void set_error(const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+ga_status cuda_fail(cudaError_t e, const char *where)
+{
+    set_error("%s: %s", where, cudaGetErrorString(e));
+    return GA_ERR_CUDA;
+}
+
+static int64_t longnet_levels(int64_t w0, int64_t alpha, int64_t L)
+{
+    if (w0 > L) return 0;
+    int64_t K = 0;
+    __int128 seg = w0;
+    while (seg * alpha <= L) { seg *= alpha; ++K; }
+    return K;
+}
+
+// Validate a public ga_mask and convert it to the device descriptor.
+static ga_status make_devmask(const ga_mask *m, int64_t L, DevMask &M)
+{
+    if (!m) { set_error("mask is NULL"); return GA_ERR_INVALID_ARG; }
+    if (m->L != L || L <= 0) {
+        set_error("mask->L (%lld) must equal L (%lld) > 0", (long long)m->L, (long long)L);
+        return GA_ERR_INVALID_ARG;
+    }
+    if (L > INT32_MAX && (m->kind == GA_MASK_CSR || m->kind == GA_MASK_BIGBIRD)) {
+        set_error("explicit CSR uses int32 column indices: L must be < 2^31");
+        return GA_ERR_UNSUPPORTED;
+    }
+    M = DevMask{};
+    M.kind = m->kind;
+    M.L = L;
+    switch (m->kind) {
+    case GA_MASK_CSR:
+        if (!m->row_ptr || (m->nnz > 0 && !m->col_idx) || m->nnz < 0) {
+            set_error("CSR mask needs device row_ptr/col_idx and nnz >= 0");
+            return GA_ERR_INVALID_ARG;
+        }
+        M.row_ptr = m->row_ptr;
+        M.col_idx = m->col_idx;
+        M.nnz = m->nnz;
+        return GA_OK;
+    case GA_MASK_WINDOW:
+        if (m->w < 1 || m->r < 1) { set_error("window needs w >= 1 and r >= 1"); return GA_ERR_INVALID_ARG; }
+        M.w = m->w;
+        M.r = m->r;
+        M.m = (m->w - 1) / m->r;
+        return GA_OK;
+    case GA_MASK_LONGNET:
+        if (m->w0 < 1 || m->alpha < 2) { set_error("LongNet needs w0 >= 1 and alpha >= 2"); return GA_ERR_INVALID_ARG; }
+        M.w0 = m->w0;
+        M.alpha = m->alpha;
+        M.K = longnet_levels(m->w0, m->alpha, L);
+        return GA_OK;
+    case GA_MASK_BLOCK_DILATED:
+        if (m->seg < 1 || m->r < 1) { set_error("block dilation needs seg >= 1, r >= 1"); return GA_ERR_INVALID_ARG; }
+        M.seg = m->seg;
+        M.r = m->r;
+        return GA_OK;
+    case GA_MASK_BIGBIRD:
+        if (m->w < 1 || m->n_global < 0 || m->n_random < 0 || m->n_global > L) {
+            set_error("BigBird needs w >= 1, 0 <= n_global <= L, n_random >= 0");
+            return GA_ERR_INVALID_ARG;
+        }
+        M.w = m->w;
+        M.r = 1;
+        M.gidx = m->global_idx;
+        M.ng = m->n_global;
+        M.nrand = m->n_random;
+        M.seed = m->seed;
+        return GA_OK;
+    }
+    set_error("unknown mask kind %d", m->kind);
+    return GA_ERR_INVALID_ARG;
+}
+
+static size_t dtype_bytes(ga_dtype dt) { return dt == GA_F32 ? 4 : 2; }
+
+static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static const int64_t kDefaultHeavy = 4096;
+
+struct Resolved {
+    AttnParams p;
+    int64_t heavy;
+};
+
+static ga_status resolve(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out, int64_t L,
+                         int32_t d, int32_t heads, ga_dtype dtype, const ga_opts *opts, Resolved &R)
+{
+    if (dtype != GA_F32 && dtype != GA_BF16 && dtype != GA_F16) {
+        set_error("dtype %d invalid", (int)dtype);
+        return GA_ERR_INVALID_ARG;
+    }
+    if (d != 32 && d != 64 && d != 128) { set_error("d=%d unsupported (32, 64, 128)", d); return GA_ERR_UNSUPPORTED; }
+    if (heads < 1) { set_error("heads must be >= 1"); return GA_ERR_INVALID_ARG; }
+    if (!Q || !K || !V || !out) { set_error("Q, K, V and out must be non-NULL"); return GA_ERR_INVALID_ARG; }
+    if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(out)) {
+        set_error("Q, K, V, out must be 16-byte aligned");
+        return GA_ERR_INVALID_ARG;
+    }
+    DevMask M;
+    ga_status st = make_devmask(mask, L, M);
+    if (st != GA_OK) return st;
+    if (M.kind == GA_MASK_BIGBIRD) {
+        set_error("BIGBIRD masks are materialised with ga_mask_to_csr and run as CSR");
+        return GA_ERR_UNSUPPORTED;
+    }
+    ga_opts o{};
+    if (opts) o = *opts;
+    if (o.q_begin < 0 || o.q_begin > L || o.q_rows < 0 || o.q_begin + o.q_rows > L) {
+        set_error("query range [%lld, +%lld) outside [0, L)", (long long)o.q_begin, (long long)o.q_rows);
+        return GA_ERR_INVALID_ARG;
+    }
+    if (o.q_rows == 0) o.q_rows = L - o.q_begin;
+    if (o.kv_begin < 0 || o.kv_rows < 0 || o.kv_begin + o.kv_rows > L) {
+        set_error("key/value range outside [0, L)");
+        return GA_ERR_INVALID_ARG;
+    }
+    if (o.kv_rows == 0) o.kv_rows = L - o.kv_begin;
+    const size_t row_bytes = (size_t)heads * d * dtype_bytes(dtype);
+    {   // out must not overlap K or V (it is written while they are read)
+        const char *ob = (const char *)out, *oe = ob + (size_t)o.q_rows * row_bytes;
+        const char *kb = (const char *)K, *ke = kb + (size_t)o.kv_rows * row_bytes;
+        const char *vb = (const char *)V, *ve = vb + (size_t)o.kv_rows * row_bytes;
+        if ((ob < ke && kb < oe) || (ob < ve && vb < oe)) {
+            set_error("out must not alias K or V");
+            return GA_ERR_INVALID_ARG;
+        }
+    }
+    AttnParams &p = R.p;
+    p = AttnParams{};
+    p.Q = Q;
+    p.K = K;
+    p.V = V;
+    p.out = out;
+    p.mask = M;
+    p.q_begin = o.q_begin;
+    p.q_rows = o.q_rows;
+    p.kv_begin = o.kv_begin;
+    p.kv_rows = o.kv_rows;
+    p.H = heads;
+    p.d = d;
+    p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+    p.nnz = M.kind == GA_MASK_CSR ? mask->nnz : 0;
+    p.edge_counter = o.edge_counter;
+    p.row_fingerprint = o.row_fingerprint;
+    R.heavy = o.heavy_threshold > 0 ? o.heavy_threshold : kDefaultHeavy;
+    return GA_OK;
+}
+
+} // namespace ga
+
+using namespace ga;
+
+extern "C" {
+
+const char *ga_last_error(void) { return g_err.c_str(); }
+
+unsigned long long ga_launch_count(void) { return g_launches.load(); }
+
+const char *ga_version(void) { return "libga 0.1 (sm_100a; graph-view masked attention, arXiv 2502.01659)"; }
+
+ga_status ga_workspace_size(const ga_mask *mask, int64_t L, int32_t d, int32_t heads, ga_dtype dtype,
+                            const ga_opts *opts, size_t *bytes)
+{
+    if (!bytes) { set_error("bytes is NULL"); return GA_ERR_INVALID_ARG; }
+    *bytes = 0;
+    DevMask M;
+    ga_status st = make_devmask(mask, L, M);
+    if (st != GA_OK) return st;
+    (void)dtype;
+    if (M.kind != GA_MASK_CSR) return GA_OK;
+    int64_t q_rows = opts && opts->q_rows > 0 ? opts->q_rows : L - (opts ? opts->q_begin : 0);
+    int64_t C = opts && opts->heavy_threshold > 0 ? opts->heavy_threshold : kDefaultHeavy;
+    *bytes = csr_heavy_workspace(q_rows, mask->nnz, heads, d, C);
+    return GA_OK;
+}
+
+ga_status ga_attention_ex(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out, int64_t L,
+                          int32_t d, int32_t heads, ga_dtype dtype, const ga_opts *opts, void *stream)
+{
+    Resolved R;
+    ga_status st = resolve(Q, K, V, mask, out, L, d, heads, dtype, opts, R);
+    if (st != GA_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    AttnParams &p = R.p;
+    const int kernel = opts ? opts->kernel : GA_KERNEL_AUTO;
+    const bool probe = p.edge_counter || p.row_fingerprint;
+
+    if (p.mask.kind == GA_MASK_CSR) {
+        const bool split = opts && opts->workspace && opts->workspace_bytes > 0;
+        if (split) {
+            p.heavy_threshold = R.heavy;
+            st = launch_edge(p, dtype, s); // light rows
+            if (st != GA_OK) return st;
+            if (probe) { set_error("probes are not supported with the heavy-row split"); return GA_ERR_UNSUPPORTED; }
+            return launch_csr_heavy(p, dtype, opts->workspace, opts->workspace_bytes, s);
+        }
+        return launch_edge(p, dtype, s);
+    }
+    if (!probe && (kernel == GA_KERNEL_TC || kernel == GA_KERNEL_AUTO) && window_tc_supported(p, dtype))
+        return launch_window_tc(p, dtype, s);
+    if (kernel == GA_KERNEL_TC) { set_error("tcgen05 path does not support this (mask, dtype, d)"); return GA_ERR_UNSUPPORTED; }
+    if (!probe && (kernel == GA_KERNEL_WINDOW || kernel == GA_KERNEL_AUTO) && window_tiled_supported(p, dtype))
+        return launch_window_tiled(p, dtype, s);
+    if (kernel == GA_KERNEL_WINDOW) { set_error("tiled window path does not support this (mask, dtype, d)"); return GA_ERR_UNSUPPORTED; }
+    return launch_edge(p, dtype, s);
+}
+
+ga_status ga_attention(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out, int64_t L,
+                       int32_t d, int32_t heads, ga_dtype dtype, void *stream)
+{
+    return ga_attention_ex(Q, K, V, mask, out, L, d, heads, dtype, nullptr, stream);
+}
+
+ga_status ga_attention_host(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out, int64_t L,
+                            int32_t d, int32_t heads, ga_dtype dtype, void *stream)
+{
+    if (!Q || !K || !V || !out) { set_error("host buffers must be non-NULL"); return GA_ERR_INVALID_ARG; }
+    if (dtype != GA_F32 && dtype != GA_BF16 && dtype != GA_F16) { set_error("dtype invalid"); return GA_ERR_INVALID_ARG; }
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX; // keep freed blocks in the pool between calls
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t bytes = (size_t)L * heads * d * dtype_bytes(dtype);
+    void *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
+    cudaError_t e;
+    if ((e = cudaMallocAsync(&dq, bytes, s)) != cudaSuccess || (e = cudaMallocAsync(&dk, bytes, s)) != cudaSuccess ||
+        (e = cudaMallocAsync(&dv, bytes, s)) != cudaSuccess || (e = cudaMallocAsync(&dout, bytes, s)) != cudaSuccess) {
+        if (dq) cudaFreeAsync(dq, s);
+        if (dk) cudaFreeAsync(dk, s);
+        if (dv) cudaFreeAsync(dv, s);
+        set_error("ga_attention_host: cudaMallocAsync: %s", cudaGetErrorString(e));
+        return GA_ERR_OOM;
+    }
+    ga_status st = GA_OK;
+    if ((e = cudaMemcpyAsync(dq, Q, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dk, K, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dv, V, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) {
+        st = cuda_fail(e, "ga_attention_host: H2D");
+    }
+    if (st == GA_OK) st = ga_attention_ex(dq, dk, dv, mask, dout, L, d, heads, dtype, nullptr, stream);
+    if (st == GA_OK && (e = cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        st = cuda_fail(e, "ga_attention_host: D2H");
+    cudaFreeAsync(dq, s);
+    cudaFreeAsync(dk, s);
+    cudaFreeAsync(dv, s);
+    cudaFreeAsync(dout, s);
+    return st;
+}
+
+ga_status ga_mask_count(const ga_mask *pattern, int64_t *nnz_out)
+{
+    if (!pattern || !nnz_out) { set_error("NULL argument"); return GA_ERR_INVALID_ARG; }
+    const int64_t L = pattern->L;
+    DevMask M;
+    ga_status st = make_devmask(pattern, L, M);
+    if (st != GA_OK) return st;
+    switch (M.kind) {
+    case GA_MASK_CSR: *nnz_out = pattern->nnz; return GA_OK;
+    case GA_MASK_WINDOW: { // L + 2 sum_{t=1}^{m'} (L - t r)
+        const int64_t mp = imin(M.m, (L - 1) / M.r);
+        *nnz_out = L + 2 * (mp * L - M.r * (mp * (mp + 1) / 2));
+        return GA_OK;
+    }
+    case GA_MASK_BLOCK_DILATED: { // sum over segments of ceil(len/r)^2
+        int64_t n = 0;
+        for (int64_t s0 = 0; s0 < L; s0 += M.seg) {
+            const int64_t c = ceil_div(imin(M.seg, L - s0), M.r);
+            n += c * c;
+        }
+        *nnz_out = n;
+        return GA_OK;
+    }
+    case GA_MASK_LONGNET: {
+        // Per level t and level-t segment [s0,s1): rows with s = min(nu(i),K) == t contribute
+        // all U multiples of alpha^t in the segment; rows with s > t contribute the U -
+        // ceil(U/alpha) of them whose valuation is exactly t (masks.cuh decomposition).
+        auto multiples = [](int64_t a, int64_t b, int64_t q) { // multiples of q in [a, b)
+            return (b - 1) / q - (a > 0 ? (a - 1) / q : -1);
+        };
+        int64_t n = 0, stp = 1;
+        for (int64_t t = 0; t <= M.K; ++t) {
+            const int64_t segw = M.w0 * stp;
+            for (int64_t s0 = 0; s0 < L; s0 += segw) {
+                const int64_t s1 = imin(L, s0 + segw);
+                const int64_t U = multiples(s0, s1, stp);
+                const int64_t gt = t < M.K ? multiples(s0, s1, stp * M.alpha) : 0;
+                n += gt * (U - ceil_div(U, M.alpha)) + (U - gt) * U;
+            }
+            stp *= M.alpha;
+        }
+        *nnz_out = n;
+        return GA_OK;
+    }
+    case GA_MASK_BIGBIRD: {
+        std::vector<int64_t> g;
+        if (M.gidx && M.ng > 0) {
+            g.resize(M.ng);
+            cudaError_t e = cudaMemcpy(g.data(), M.gidx, sizeof(int64_t) * M.ng, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) return cuda_fail(e, "ga_mask_count: copy global_idx");
+            M.gidx = g.data();
+        }
+        int64_t n = 0;
+        for (int64_t i = 0; i < L; ++i) n += bb_degree(M, i);
+        *nnz_out = n;
+        return GA_OK;
+    }
+    }
+    set_error("unknown mask kind");
+    return GA_ERR_INVALID_ARG;
+}
+
+ga_status ga_mask_to_csr(const ga_mask *pattern, int64_t *row_ptr, int32_t *col_idx, void *stream)
+{
+    if (!pattern || !row_ptr) { set_error("NULL argument"); return GA_ERR_INVALID_ARG; }
+    DevMask M;
+    ga_status st = make_devmask(pattern, pattern->L, M);
+    if (st != GA_OK) return st;
+    if (M.kind == GA_MASK_CSR) { set_error("mask is already CSR"); return GA_ERR_INVALID_ARG; }
+    if (M.L > INT32_MAX) { set_error("CSR columns are int32: L must be < 2^31"); return GA_ERR_UNSUPPORTED; }
+    return maskgen_to_csr(M, row_ptr, col_idx, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ga_status ga_mask_validate(const ga_mask *csr, void *stream, int *ok)
+{
+    if (!csr || !ok) { set_error("NULL argument"); return GA_ERR_INVALID_ARG; }
+    *ok = 0;
+    if (csr->kind != GA_MASK_CSR) { set_error("not a CSR mask"); return GA_ERR_INVALID_ARG; }
+    DevMask M;
+    ga_status st = make_devmask(csr, csr->L, M);
+    if (st != GA_OK) return st;
+    return mask_validate(M, reinterpret_cast<cudaStream_t>(stream), ok);
+}
+
+ga_status ga_fill_inputs(void *dst, ga_dtype dtype, int64_t n, uint64_t seed, int32_t tensor, int64_t e0, float shift,
+                         void *stream)
+{
+    if (!dst && n > 0) { set_error("dst is NULL"); return GA_ERR_INVALID_ARG; }
+    if (n < 0 || e0 < 0) { set_error("n and e0 must be >= 0"); return GA_ERR_INVALID_ARG; }
+    return fill_inputs(dst, dtype, n, seed, tensor, e0, shift, reinterpret_cast<cudaStream_t>(stream));
+}
+
+} // extern "C"

@@ -1,0 +1,154 @@
+// common.cuh — dtype traits, 16-byte vector conversion, fast exp2, error plumbing.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ga.h"
+#include "masks.cuh"
+
+namespace ga {
+
+// ---------------------------------------------------------------- error plumbing
+void set_error(const char *fmt, ...);
+ga_status cuda_fail(cudaError_t e, const char *where);
+void note_launches(int n); // telemetry: kernels launched by the library (ga_launch_count)
+
+#define GA_CHECK_LAUNCH(where)                                                     \
+    do {                                                                           \
+        ::ga::note_launches(1);                                                    \
+        cudaError_t _e = cudaPeekAtLastError();                                    \
+        if (_e != cudaSuccess) return ::ga::cuda_fail(_e, where);                  \
+    } while (0)
+
+// ---------------------------------------------------------------- math
+__device__ __forceinline__ float ex2(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float rcp(float x) { return __frcp_rn(x); }
+
+// ---------------------------------------------------------------- dtype traits
+template <typename T> struct DT;
+template <> struct DT<float> { static constexpr int VEC = 4; };
+template <> struct DT<__nv_bfloat16> { static constexpr int VEC = 8; };
+template <> struct DT<__half> { static constexpr int VEC = 8; };
+
+__device__ __forceinline__ uint4 ldg16(const void *p)
+{
+    uint4 r;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void stg16(void *p, uint4 v)
+{
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+template <typename T> __device__ __forceinline__ void unpack(const uint4 &u, float *f);
+
+template <> __device__ __forceinline__ void unpack<float>(const uint4 &u, float *f)
+{
+    f[0] = __uint_as_float(u.x);
+    f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z);
+    f[3] = __uint_as_float(u.w);
+}
+
+__device__ __forceinline__ void bf2_to_f(uint32_t w, float &lo, float &hi)
+{
+    lo = __uint_as_float(w << 16);
+    hi = __uint_as_float(w & 0xffff0000u);
+}
+
+template <> __device__ __forceinline__ void unpack<__nv_bfloat16>(const uint4 &u, float *f)
+{
+    bf2_to_f(u.x, f[0], f[1]);
+    bf2_to_f(u.y, f[2], f[3]);
+    bf2_to_f(u.z, f[4], f[5]);
+    bf2_to_f(u.w, f[6], f[7]);
+}
+
+__device__ __forceinline__ void h2_to_f(uint32_t w, float &lo, float &hi)
+{
+    __half2 h = *reinterpret_cast<__half2 *>(&w);
+    float2 f = __half22float2(h);
+    lo = f.x;
+    hi = f.y;
+}
+
+template <> __device__ __forceinline__ void unpack<__half>(const uint4 &u, float *f)
+{
+    h2_to_f(u.x, f[0], f[1]);
+    h2_to_f(u.y, f[2], f[3]);
+    h2_to_f(u.z, f[4], f[5]);
+    h2_to_f(u.w, f[6], f[7]);
+}
+
+template <typename T> __device__ __forceinline__ uint4 pack(const float *f);
+
+template <> __device__ __forceinline__ uint4 pack<float>(const float *f)
+{
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+}
+
+__device__ __forceinline__ uint32_t f2_to_bf2(float lo, float hi)
+{
+    __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t *>(&b);
+}
+
+template <> __device__ __forceinline__ uint4 pack<__nv_bfloat16>(const float *f)
+{
+    return make_uint4(f2_to_bf2(f[0], f[1]), f2_to_bf2(f[2], f[3]), f2_to_bf2(f[4], f[5]), f2_to_bf2(f[6], f[7]));
+}
+
+__device__ __forceinline__ uint32_t f2_to_h2(float lo, float hi)
+{
+    __half2 h = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+
+template <> __device__ __forceinline__ uint4 pack<__half>(const float *f)
+{
+    return make_uint4(f2_to_h2(f[0], f[1]), f2_to_h2(f[2], f[3]), f2_to_h2(f[4], f[5]), f2_to_h2(f[6], f[7]));
+}
+
+// ---------------------------------------------------------------- kernel parameters
+struct AttnParams {
+    const void *Q, *K, *V;
+    void *out;
+    DevMask mask;
+    int64_t q_begin, q_rows, kv_begin, kv_rows;
+    int32_t H, d;
+    float scale_log2; // log2(e) / sqrt(d)
+    int64_t nnz;             // CSR edge count (upper bound for the heavy-row plan)
+    int64_t heavy_threshold; // CSR: rows above this are skipped by the light kernel (0 = none)
+    unsigned long long *edge_counter;
+    unsigned long long *row_fingerprint;
+};
+
+// launchers (defined in the kernel translation units)
+ga_status launch_edge(const AttnParams &p, ga_dtype dt, cudaStream_t s);
+ga_status launch_csr_heavy(const AttnParams &p, ga_dtype dt, void *ws, size_t ws_bytes, cudaStream_t s);
+size_t csr_heavy_workspace(int64_t L, int64_t nnz, int32_t H, int32_t d, int64_t C);
+bool window_tiled_supported(const AttnParams &p, ga_dtype dt);
+ga_status launch_window_tiled(const AttnParams &p, ga_dtype dt, cudaStream_t s);
+bool window_tc_supported(const AttnParams &p, ga_dtype dt);
+ga_status launch_window_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s);
+
+ga_status maskgen_to_csr(const DevMask &M, int64_t *row_ptr, int32_t *col_idx, cudaStream_t s);
+ga_status mask_validate(const DevMask &M, cudaStream_t s, int *ok);
+ga_status scan_exclusive_i64(int64_t *data, int64_t n, cudaStream_t s);
+ga_status fill_inputs(void *dst, ga_dtype dt, int64_t n, uint64_t seed, int32_t tensor, int64_t e0, float shift,
+                      cudaStream_t s);
+
+} // namespace ga

@@ -1,0 +1,129 @@
+// edge_core.cuh — the per-(row, head) edge loop shared by the generic edge kernel and the
+// CSR heavy-row chunk kernel.  See edge_kernel.cu for the mapping onto lanes.
+#pragma once
+#include "common.cuh"
+
+namespace ga {
+
+template <typename T, int D, bool PROBE> struct EdgeAcc {
+    static constexpr int VEC = DT<T>::VEC;
+    static constexpr int G = D / VEC; // lanes per (edge, head) vector
+    static constexpr int E = 32 / G;  // edges in flight per warp
+    float q[VEC], o[VEC];
+    float m, l;
+    unsigned long long n_edges, sum_j, sum_h;
+    int g, sub;
+    const char *Kb, *Vb;
+    size_t row_bytes;
+    int64_t kv_begin;
+
+    __device__ __forceinline__ void init(const AttnParams &p, int64_t t, int h, int lane)
+    {
+        g = lane / G;
+        sub = lane % G;
+        const T *Qp = reinterpret_cast<const T *>(p.Q) + ((size_t)t * p.H + h) * D + sub * VEC;
+        Kb = reinterpret_cast<const char *>(p.K) + ((size_t)h * D + sub * VEC) * sizeof(T);
+        Vb = reinterpret_cast<const char *>(p.V) + ((size_t)h * D + sub * VEC) * sizeof(T);
+        row_bytes = (size_t)p.H * D * sizeof(T);
+        kv_begin = p.kv_begin;
+        uint4 raw = ldg16(Qp);
+        unpack<T>(raw, q);
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) { q[c] *= p.scale_log2; o[c] = 0.f; }
+        m = -INFINITY;
+        l = 0.f;
+        n_edges = sum_j = sum_h = 0;
+    }
+
+    // neighbours k in [kb, ke) of piece P (warp-uniform bounds)
+    __device__ __forceinline__ void run(const Piece &P, int64_t kb, int64_t ke)
+    {
+        for (int64_t k0 = kb; k0 < ke; k0 += 2 * E) {
+            const int64_t ka = k0 + g, kk = k0 + E + g;
+            const bool va = ka < ke, vb = kk < ke;
+            uint4 kra = make_uint4(0, 0, 0, 0), vra = kra, krb = kra, vrb = kra;
+            int64_t ja = 0, jb = 0;
+            if (va) {
+                ja = piece_at(P, ka);
+                const size_t off = (size_t)(ja - kv_begin) * row_bytes;
+                kra = ldg16(Kb + off);
+                vra = ldg16(Vb + off);
+            }
+            if (vb) {
+                jb = piece_at(P, kk);
+                const size_t off = (size_t)(jb - kv_begin) * row_bytes;
+                krb = ldg16(Kb + off);
+                vrb = ldg16(Vb + off);
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const bool valid = u == 0 ? va : vb;
+                if (u == 1 && k0 + E >= ke) break; // warp-uniform: no group has work
+                float kf[VEC], vf[VEC];
+                unpack<T>(u == 0 ? kra : krb, kf);
+                float s = 0.f;
+#pragma unroll
+                for (int c = 0; c < VEC; ++c) s = fmaf(q[c], kf[c], s);
+#pragma unroll
+                for (int off = 1; off < G; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+                if (valid) {
+                    if (s > m) { // lazy rescale: only when the running max grows
+                        const float a = ex2(m - s);
+                        l *= a;
+#pragma unroll
+                        for (int c = 0; c < VEC; ++c) o[c] *= a;
+                        m = s;
+                    }
+                    const float pr = ex2(s - m);
+                    l += pr;
+                    unpack<T>(u == 0 ? vra : vrb, vf);
+#pragma unroll
+                    for (int c = 0; c < VEC; ++c) o[c] = fmaf(pr, vf[c], o[c]);
+                    if (PROBE) {
+                        const int64_t j = u == 0 ? ja : jb;
+                        n_edges += 1;
+                        sum_j += (unsigned long long)j;
+                        sum_h += splitmix64((uint64_t)j);
+                    }
+                }
+            }
+        }
+    }
+
+    // merge the E lane-group states: (m,l,o) (+) (m',l',o'), m* = max, rescaled sums
+    __device__ __forceinline__ void merge_groups()
+    {
+#pragma unroll
+        for (int off = G; off < 32; off <<= 1) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+            const float l2 = __shfl_xor_sync(0xffffffffu, l, off);
+            const float mn = fmaxf(m, m2);
+            const float a = (m == -INFINITY) ? 0.f : ex2(m - mn);
+            const float b = (m2 == -INFINITY) ? 0.f : ex2(m2 - mn);
+            l = l * a + l2 * b;
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) {
+                const float o2 = __shfl_xor_sync(0xffffffffu, o[c], off);
+                o[c] = o[c] * a + o2 * b;
+            }
+            m = mn;
+        }
+    }
+
+    // warp totals of the probe counters (one lane per group counts)
+    __device__ __forceinline__ void probe_totals(unsigned long long &ne, unsigned long long &sj,
+                                                 unsigned long long &sh) const
+    {
+        ne = sub == 0 ? n_edges : 0;
+        sj = sub == 0 ? sum_j : 0;
+        sh = sub == 0 ? sum_h : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            ne += __shfl_xor_sync(0xffffffffu, ne, off);
+            sj += __shfl_xor_sync(0xffffffffu, sj, off);
+            sh += __shfl_xor_sync(0xffffffffu, sh, off);
+        }
+    }
+};
+
+} // namespace ga

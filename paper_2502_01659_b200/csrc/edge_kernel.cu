@@ -1,0 +1,103 @@
+// edge_kernel.cu — generic fused graph-attention kernel (every mask family, every dtype).
+//
+// Algorithm 1 with the paper's outer loop "for 1 <= i <= L in
+// parallel" mapped to one warp per (query row i, head h), and its inner loop over
+// j in Get_Neighbors(G,i,P_a) mapped to lane GROUPS: a (row,head) vector of d elements is
+// G = d*sizeof(T)/16 lanes x 16 bytes, so a warp keeps E = 32/G edges in flight:
+//
+//   lane group g takes neighbours k = g, g+E, g+2E, ... of each piece (masks.cuh)
+//   Pull K_j  -> one coalesced 16-byte load per lane (ld.global.nc.v4), fp32 convert
+//   W = q.k   -> G-lane xor-shuffle reduction; q is pre-scaled by log2(e)/sqrt(d) so the
+//                score is already in the exp2 domain (Eq. 1 scale, reading R4)
+//   m,l       -> per-group online softmax, lazy rescale only when the max grows
+//   Pull V_j  -> 16-byte load issued together with K_j; o += p*v (unnormalised, R5)
+//   end       -> E group states merged with the associative (m,l,o) combine, o /= l,
+//                empty rows -> 0 (R6), RNE store in the input dtype.
+//
+// The L x L matrix is never formed and exactly |N(i)| dot products are computed per
+// (row, head) (work optimality); the PROBE instantiation counts them.
+#include "edge_core.cuh"
+
+namespace ga {
+
+template <typename T, int D, bool PROBE>
+__global__ void __launch_bounds__(256) edge_kernel(AttnParams p)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int H = p.H;
+    if (gw >= p.q_rows * H) return;
+    const int64_t t = gw / H;
+    const int h = (int)(gw - t * H);
+    const int64_t i = p.q_begin + t;
+    if (p.heavy_threshold > 0 && degree(p.mask, i) > p.heavy_threshold) return; // split path
+
+    EdgeAcc<T, D, PROBE> acc;
+    acc.init(p, t, h, lane);
+    const int np = num_pieces(p.mask, i);
+    for (int pc = 0; pc < np; ++pc) {
+        const Piece P = get_piece(p.mask, i, pc);
+        acc.run(P, 0, P.count);
+    }
+    acc.merge_groups();
+    if (PROBE) {
+        unsigned long long ne, sj, sh;
+        acc.probe_totals(ne, sj, sh);
+        if (lane == 0) {
+            if (p.edge_counter) atomicAdd(p.edge_counter, ne);
+            if (p.row_fingerprint && h == 0) {
+                p.row_fingerprint[3 * t + 0] = ne;
+                p.row_fingerprint[3 * t + 1] = sj;
+                p.row_fingerprint[3 * t + 2] = sh;
+            }
+        }
+    }
+    if (acc.g == 0) {
+        constexpr int VEC = DT<T>::VEC;
+        const float inv = acc.l > 0.f ? 1.f / acc.l : 0.f;
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) acc.o[c] *= inv;
+        T *Op = reinterpret_cast<T *>(p.out) + ((size_t)t * H + h) * D + acc.sub * VEC;
+        stg16(Op, pack<T>(acc.o));
+    }
+}
+
+template <typename T, int D>
+static ga_status launch_edge_t(const AttnParams &p, cudaStream_t s)
+{
+    const int64_t warps = p.q_rows * p.H;
+    if (warps == 0) return GA_OK;
+    const int threads = 256;
+    const int64_t blocks = (warps + 7) / 8;
+    if (p.edge_counter || p.row_fingerprint)
+        edge_kernel<T, D, true><<<(unsigned)blocks, threads, 0, s>>>(p);
+    else
+        edge_kernel<T, D, false><<<(unsigned)blocks, threads, 0, s>>>(p);
+    GA_CHECK_LAUNCH("edge_kernel launch");
+    return GA_OK;
+}
+
+template <typename T>
+static ga_status launch_edge_d(const AttnParams &p, cudaStream_t s)
+{
+    switch (p.d) {
+    case 32: return launch_edge_t<T, 32>(p, s);
+    case 64: return launch_edge_t<T, 64>(p, s);
+    case 128: return launch_edge_t<T, 128>(p, s);
+    }
+    set_error("d=%d unsupported (32, 64, 128)", p.d);
+    return GA_ERR_UNSUPPORTED;
+}
+
+ga_status launch_edge(const AttnParams &p, ga_dtype dt, cudaStream_t s)
+{
+    switch (dt) {
+    case GA_F32: return launch_edge_d<float>(p, s);
+    case GA_BF16: return launch_edge_d<__nv_bfloat16>(p, s);
+    case GA_F16: return launch_edge_d<__half>(p, s);
+    }
+    set_error("unknown dtype %d", (int)dt);
+    return GA_ERR_INVALID_ARG;
+}
+
+} // namespace ga

@@ -1,0 +1,105 @@
+"""Multi-process (world_size 2 and 3, gloo, CPU) tests of the sharding host logic:
+shard ranges, halo exchange and the K/V all-gather produce exactly the rows the sharded
+kernels need (the kernels themselves are covered by the GPU tests)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2502_01659_b200 import dist as gdist
+from paper_2502_01659_b200.masks import Window
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, fn, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fn(rank, world)
+        q.put((rank, None))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(fn, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, fn, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    errs = [e for _, e in res if e]
+    assert not errs, errs[0]
+
+
+def _global(L, H, d):
+    g = torch.Generator().manual_seed(0)
+    return torch.rand((L, H, d), generator=g), torch.rand((L, H, d), generator=g)
+
+
+def _halo_case(rank, world):
+    L, H, d = 1000, 2, 8
+    mask = Window(40, 3)
+    halo = gdist.window_halo(mask)
+    assert halo == 39
+    K, V = _global(L, H, d)
+    r0, r1 = gdist.shard_range(L, world, rank)
+    buf = gdist.alloc_halo(L, r0, r1, halo, H, d, torch.float32, "cpu")
+    buf.k.fill_(-1)
+    buf.v.fill_(-1)
+    buf.local_k.copy_(K[r0:r1])
+    buf.local_v.copy_(V[r0:r1])
+    gdist.exchange_halo(buf)
+    assert torch.equal(buf.k, K[buf.kv_begin:buf.kv_end])
+    assert torch.equal(buf.v, V[buf.kv_begin:buf.kv_end])
+    # every neighbour of every local row lies inside the halo'd buffer
+    for i in (r0, r1 - 1):
+        lo, hi = i - ((mask.w - 1) // mask.r) * mask.r, i + ((mask.w - 1) // mask.r) * mask.r
+        assert buf.kv_begin <= max(0, lo) and min(L - 1, hi) < buf.kv_end
+
+
+def _allgather_case(rank, world):
+    L, H, d = 999, 1, 4
+    K, _ = _global(L, H, d)
+    per = -(-L // world)
+    local = torch.zeros((per, H, d))
+    r0, r1 = rank * per, min(L, (rank + 1) * per)
+    local[:r1 - r0] = K[r0:r1]
+    full = gdist.allgather_rows(local, L)
+    assert torch.equal(full, K)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_exchange_gloo(world):
+    _spawn(_halo_case, world)
+
+
+def test_allgather_gloo():
+    _spawn(_allgather_case, 2)
+
+
+def test_shard_ranges_cover_exactly():
+    for L, world, align in [(65536, 8, 128), (1000, 3, 1), (160_000_000, 8, 128), (10, 4, 1), (7, 8, 1)]:
+        got = [gdist.shard_range(L, world, r, align) for r in range(world)]
+        assert got[0][0] == 0 and got[-1][1] == L
+        for (a0, a1), (b0, b1) in zip(got, got[1:]):
+            assert a1 == b0 and a0 <= a1
+        if L >= world * align:
+            assert all((r1 - r0) % align == 0 for r0, r1 in got[:-1])

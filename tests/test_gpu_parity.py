@@ -1,0 +1,339 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Tolerances (BASELINE.json north_star): max abs error 1e-4 for fp32 and 2e-2 for
+bf16/fp16 against the oracle on identical inputs; the paper's own protocol (PAPER.md:302:
+L=256, d=32, U[0,1), atol 1e-8 + rtol 1e-5) additionally at fp32.  CSR construction and
+the work counters are compared bit for bit.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 1e-4, "bf16": 2e-2, "f16": 2e-2}
+TDT = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}
+
+
+@pytest.fixture(scope="module")
+def ga():
+    import paper_2502_01659_b200 as ga
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return ga
+
+
+def _pair(ga, orc, fam, L, args):
+    """(product mask, oracle mask) for a family."""
+    if fam == "window":
+        return ga.Window(*args), orc.window(L, *args)
+    if fam == "block":
+        return ga.BlockDilated(*args), orc.block_dilated(L, *args)
+    if fam == "longnet":
+        return ga.LongNet(*args), orc.longnet(L, *args)
+    if fam == "bigbird":
+        return ga.BigBird(*args), orc.bigbird(L, *args)
+    raise ValueError(fam)
+
+
+def _inputs(L, H, d, dt, seed, centred=False):
+    q, k, v = synth.qkv(seed, L, H, d, dt, centred=centred)
+    return (q, k, v), tuple(synth.as_f64(x) for x in (q, k, v))
+
+
+def _run(ga, cpu_qkv, mask, **kw):
+    q, k, v = (x.cuda() for x in cpu_qkv)
+    out = ga.attention(q, k, v, mask, **kw)
+    torch.cuda.synchronize()
+    return out.double().cpu().numpy()
+
+
+def _csr_from_oracle(ga, orc_mask):
+    import oracle
+
+    rp, ci, nnz = oracle.mask_to_csr(orc_mask)
+    return ga.CSR(torch.from_numpy(rp).cuda(), torch.from_numpy(ci.astype(np.int32)).cuda()), (rp, ci)
+
+
+# ---------------------------------------------------------------- paper protocol E0
+@pytest.mark.parametrize("fam,args", [("window", (9, 1)), ("window", (40, 3)), ("block", (32, 2)),
+                                      ("longnet", (16, 2)), ("window", (300, 1))])
+def test_paper_protocol_fp32(ga, orc, fam, args):
+    """L=256, d_k=32, U[0,1), allclose(atol=1e-8, rtol=1e-5) at fp32."""
+    L, H, d = 256, 1, 32
+    cpu, f64 = _inputs(L, H, d, "f32", 302)
+    m, om = _pair(ga, orc, fam, L, args)
+    want, _ = orc.attention(*f64, om)
+    got = _run(ga, cpu, m, kernel="edge")
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-8)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_paper_protocol_random_csr(ga, orc, seed):
+    """20 seeded random masks of varied sparsity, explicit CSR (S:492 acceptance 1)."""
+    L, H, d = 256, 1, 32
+    rng = np.random.default_rng(seed)
+    dense = rng.random((L, L)) < [0.001, 0.01, 0.1, 0.5][seed % 4]
+    rp = np.concatenate([[0], np.cumsum(dense.sum(1))]).astype(np.int64)
+    ci = np.nonzero(dense)[1].astype(np.int32)
+    om = orc.csr(L, rp, ci)
+    cpu, f64 = _inputs(L, H, d, "f32", 1000 + seed)
+    want, _ = orc.attention(*f64, om)
+    m = ga.CSR(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+    got = _run(ga, cpu, m)
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-8)
+
+
+# ---------------------------------------------------------------- families x dtypes x d
+CASES = [
+    ("window", 1031, (33, 1)), ("window", 1500, (64, 2)), ("window", 777, (200, 3)),
+    ("block", 1000, (64, 2)), ("longnet", 2048, (64, 2)), ("longnet", 1800, (27, 3)),
+]
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16", "f16"])
+@pytest.mark.parametrize("d", [32, 64, 128])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}{c[1]}")
+def test_families_dtypes_dims(ga, orc, dt, d, case):
+    fam, L, args = case
+    H = 2
+    cpu, f64 = _inputs(L, H, d, dt, 11 + d, centred=True)
+    m, om = _pair(ga, orc, fam, L, args)
+    want, _ = orc.attention(*f64, om)
+    for kernel in ("edge", "auto"):
+        got = _run(ga, cpu, m, kernel=kernel)
+        err = np.abs(got - want).max()
+        assert err <= TOL[dt], (kernel, err)
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_csr_bigbird_with_heavy_split(ga, orc, dt):
+    """BigBird via device CSR; heavy global rows through the split+merge path (a7)."""
+    L, H, d = 4096, 2, 64
+    m = ga.BigBird(32, 8, 16, seed=77)
+    om = orc.bigbird(L, 32, 8, 16, 77)
+    csr = ga.mask_to_csr(m, L)
+    cpu, f64 = _inputs(L, H, d, dt, 5)
+    want, _ = orc.attention(*f64, om)
+    q, k, v = (x.cuda() for x in cpu)
+    for C in (256, 1000, 0):
+        ws = torch.empty(ga.workspace_size(csr, L, d, H, TDT[dt], heavy_threshold=C), dtype=torch.uint8,
+                         device="cuda")
+        out = ga.attention(q, k, v, csr, workspace=ws, heavy_threshold=C)
+        err = (out.double().cpu().numpy() - want).__abs__().max()
+        assert err <= TOL[dt], (C, err)
+    out = ga.attention(q, k, v, csr)  # no workspace: unsplit rows
+    assert np.abs(out.double().cpu().numpy() - want).max() <= TOL[dt]
+
+
+def test_empty_rows_and_ragged_csr(ga, orc):
+    L, H, d = 300, 1, 64
+    rng = np.random.default_rng(3)
+    deg = rng.integers(0, 5, L)
+    deg[::7] = 0
+    deg[5] = 300
+    rows = [np.sort(rng.choice(L, k, replace=False)) for k in deg]
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    ci = np.concatenate(rows).astype(np.int32)
+    cpu, f64 = _inputs(L, H, d, "f32", 8)
+    want, _ = orc.attention(*f64, orc.csr(L, rp, ci))
+    m = ga.CSR(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+    got = _run(ga, cpu, m)
+    assert np.all(got[deg == 0] == 0)
+    assert np.abs(got - want).max() <= 1e-4
+
+
+# ---------------------------------------------------------------- work optimality (T4)
+@pytest.mark.parametrize("fam,L,args", [("window", 2000, (100, 3)), ("longnet", 4096, (64, 2)),
+                                        ("block", 1000, (50, 4))])
+def test_edge_counter_and_fingerprints(ga, orc, fam, L, args):
+    """Dot products computed == nnz(mask) x heads exactly; per-row (deg, sum j,
+    sum splitmix64(j)) fingerprints equal the oracle's neighbour lists (S:281 probe build)."""
+    H, d = 3, 64
+    m, om = _pair(ga, orc, fam, L, args)
+    rp, ci, nnz = orc.mask_to_csr(om)
+    q, k, v = ga.qkv_device(1, L, H, d, torch.bfloat16)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    fp = torch.zeros(L * 3, dtype=torch.int64, device="cuda")
+    ga.attention(q, k, v, m, edge_counter=cnt, row_fingerprint=fp)
+    assert int(cnt.item()) == nnz * H
+    fp = fp.cpu().numpy().view(np.uint64).reshape(L, 3)
+    deg = np.diff(rp).astype(np.uint64)
+    assert np.array_equal(fp[:, 0], deg)
+    with np.errstate(over="ignore"):
+        sj = np.add.reduceat(ci.astype(np.uint64), rp[:-1]) if nnz else np.zeros(L, np.uint64)
+        sh = np.add.reduceat(synth.splitmix64_np(ci.astype(np.uint64)), rp[:-1])
+    sj[deg == 0] = 0
+    sh[deg == 0] = 0
+    assert np.array_equal(fp[:, 1], sj)
+    assert np.array_equal(fp[:, 2], sh)
+
+
+# ---------------------------------------------------------------- CSR generator (T5)
+@pytest.mark.parametrize("fam,L,args", [
+    ("window", 3000, (128, 1)), ("window", 4097, (256, 2)), ("block", 3000, (100, 3)),
+    ("longnet", 8192, (64, 2)), ("longnet", 5000, (27, 3)), ("bigbird", 1024, (8, 4, 4, 0xB16B12D)),
+    ("bigbird", 5000, (64, 16, 64, 99)), ("bigbird", 300, (20, 3, 500, 1)),
+])
+def test_csr_generator_bit_exact(ga, orc, fam, L, args):
+    m, om = _pair(ga, orc, fam, L, args)
+    csr = ga.mask_to_csr(m, L)
+    rp, ci, nnz = orc.mask_to_csr(om)
+    assert np.array_equal(csr.row_ptr.cpu().numpy(), rp)
+    assert np.array_equal(csr.col_idx.cpu().numpy(), ci)
+    assert ga.mask_validate(csr, L)
+
+
+def test_mask_validate_rejects_malformed(ga):
+    L = 10
+    rp = torch.tensor([0, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2], dtype=torch.int64, device="cuda")
+    bad = ga.CSR(rp, torch.tensor([3, 3], dtype=torch.int32, device="cuda"))  # not strictly increasing
+    assert not ga.mask_validate(bad, L)
+    bad2 = ga.CSR(rp, torch.tensor([1, 10], dtype=torch.int32, device="cuda"))  # out of range
+    assert not ga.mask_validate(bad2, L)
+
+
+# ---------------------------------------------------------------- inputs (a0)
+def test_device_input_generator_matches_golden_and_numpy(ga):
+    from tests.conftest import golden
+
+    g = {r.split()[0]: r.split()[1] for r in golden("rng.txt")}
+    seed = int(g["seed"], 16)
+    for dt in ("f32", "bf16", "f16"):
+        q, k, v = ga.qkv_device(seed, 64, 8, 64, TDT[dt])
+        ref = synth.qkv(seed, 64, 8, 64, dt)
+        for a, b in zip((q, k, v), ref):
+            assert torch.equal(a.cpu(), b)
+    q, _, _ = ga.qkv_device(seed, 2, 8, 64, torch.float32)
+    assert q[0, 0, 0].item() == float(g["Q_e0_f32"])
+    assert q[1, 0, 0].item() == float(g["Q_e512_f32"])
+
+
+# ---------------------------------------------------------------- properties (T3)
+def test_properties(ga, orc):
+    L, H, d = 513, 2, 64
+    q, k, v = ga.qkv_device(4, L, H, d, torch.float32)
+    out = ga.attention(q, k, v, ga.Window(1))
+    assert torch.equal(out, v)  # identity mask -> O = V exactly
+    vc = torch.full_like(v, 0.375)
+    out = ga.attention(q, k, vc, ga.LongNet(16, 2))
+    assert (out - 0.375).abs().max().item() < 1e-6
+    full = ga.attention(q, k, v, ga.Window(L + 10))
+    ref = torch.nn.functional.scaled_dot_product_attention(q.transpose(0, 1).double(), k.transpose(0, 1).double(),
+                                                           v.transpose(0, 1).double()).transpose(0, 1)
+    assert (full.double() - ref).abs().max().item() < 1e-5
+    r1 = ga.attention(q, k, v, ga.Window(40, 1))
+    r2 = ga.attention(q, k, v, ga.mask_to_csr(ga.Window(40), L))
+    assert (r1 - r2).abs().max().item() < 1e-6
+    shifted = ga.attention(q + 1000.0, k, v, ga.Window(7))
+    assert torch.isfinite(shifted).all()
+
+
+def test_sharded_offsets_bitwise(ga):
+    """Query-range shards with halo'd K/V buffers reproduce the 1-GPU rows bit for bit
+    (T7-i logical shards on one GPU)."""
+    L, H, d = 4096, 4, 64
+    q, k, v = ga.qkv_device(9, L, H, d, torch.bfloat16)
+    m = ga.Window(256, 2)
+    full = ga.attention(q, k, v, m)
+    halo = 255 * 2
+    for r0, r1 in ((0, 1024), (1024, 3000), (3000, 4096)):
+        k0, k1 = max(0, r0 - halo), min(L, r1 + halo)
+        part = ga.attention(q[r0:r1].contiguous(), k[k0:k1].contiguous(), v[k0:k1].contiguous(), m, L=L,
+                            q_begin=r0, kv_begin=k0)
+        assert torch.equal(part, full[r0:r1])
+
+
+def test_host_entry_point_matches_device(ga):
+    L, H, d = 2048, 8, 64
+    cpu = synth.qkv(21, L, H, d, "bf16")
+    q, k, v = (x.cuda() for x in cpu)
+    m = ga.Window(256, 2)
+    dev = ga.attention(q, k, v, m)
+    pinned = [x.pin_memory() for x in cpu]
+    out = torch.empty_like(pinned[0]).pin_memory()
+    ga.attention_host(*pinned, m, out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, dev.cpu())
+
+
+def test_errors_are_reported(ga):
+    L, H, d = 128, 1, 64
+    q, k, v = ga.qkv_device(1, L, H, d, torch.bfloat16)
+    with pytest.raises(ga.GaError, match="INVALID_ARG"):
+        ga.attention(q, k, v, ga.Window(8), out=k)
+    with pytest.raises(ga.GaError, match="UNSUPPORTED"):
+        ga.attention(q, k, v, ga.BigBird(8, 2, 2))
+    q48 = torch.zeros(L, 1, 48, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ga.GaError, match="UNSUPPORTED"):
+        ga.attention(q48, q48.clone(), q48.clone(), ga.Window(8))
+
+
+# ---------------------------------------------------------------- full-size sampled parity
+def _sample_rows(L, extra=(), n=256, seed=0):
+    rng = np.random.default_rng(seed)
+    rows = set(range(0, min(L, 64))) | set(range(max(0, L - 64), L)) | set(int(x) for x in rng.integers(0, L, n))
+    rows |= {int(x) for x in extra if 0 <= x < L}
+    return np.array(sorted(rows), dtype=np.int64)
+
+
+def test_cfg2_full_size_sampled(ga, orc):
+    """BASELINE cfg2 (bench workload): L=65536, H=8, d=64, bf16, Window(256, r=2)."""
+    L, H, d, seed = 65536, 8, 64, 0x5EED0002
+    q, k, v = ga.qkv_device(seed, L, H, d, torch.bfloat16)
+    m = ga.Window(256, 2)
+    out = ga.attention(q, k, v, m).double().cpu().numpy()
+    rows = _sample_rows(L, extra=range(32000, 33000, 7))
+    want, edges = orc.attention_seeded(seed, "bf16", orc.window(L, 256, 2), H, d, rows=rows)
+    assert np.abs(out[rows] - want).max() <= 2e-2
+
+
+def test_cfg3_bigbird_full_size_sampled(ga, orc):
+    """BASELINE cfg3: L=2^20, BigBird (64 global, Window(128), 64 random) explicit CSR.
+    CSR rows bit-exact on samples (incl. all global rows); attention sampled."""
+    L, H, d, seed = 2 ** 20, 1, 64, 0x5EED0003
+    m = ga.BigBird(128, 64, 64, seed=0xB16B12D)
+    om = orc.bigbird(L, 128, 64, 64, 0xB16B12D)
+    csr = ga.mask_to_csr(m, L)
+    assert csr.nnz == 468_656_702
+    rp = csr.row_ptr.cpu().numpy()
+    G = [kk * L // 64 for kk in range(64)]
+    rows = _sample_rows(L, extra=G[:4] + [g + 1 for g in G] + [g - 1 for g in G], n=128)
+    for i in rows:
+        nb = orc.neighbors(om, int(i))
+        assert np.array_equal(csr.col_idx[rp[i]:rp[i + 1]].cpu().numpy(), nb)
+    q, k, v = ga.qkv_device(seed, L, H, d, torch.bfloat16)
+    ws = torch.empty(ga.workspace_size(csr, L, d, H, torch.bfloat16), dtype=torch.uint8, device="cuda")
+    out = ga.attention(q, k, v, csr, workspace=ws).double().cpu().numpy()
+    want, _ = orc.attention_seeded(seed, "bf16", om, H, d, rows=rows)
+    assert np.abs(out[rows] - want).max() <= 2e-2
+
+
+def test_cfg4_longnet_full_size_sampled(ga, orc):
+    """BASELINE cfg4: L=2^24, LongNet(w0=2048, alpha=2), implicit, sampled rows incl. high-nu rows."""
+    L, H, d, seed = 2 ** 24, 1, 64, 0x5EED0004
+    q, k, v = ga.qkv_device(seed, L, H, d, torch.bfloat16)
+    out = ga.attention(q, k, v, ga.LongNet(2048, 2))
+    rows = _sample_rows(L, extra=[0, 2 ** 13, 2 ** 23, 3 * 2 ** 22, 2 ** 24 - 2 ** 12, 12345 * 64], n=64)
+    got = out[torch.from_numpy(rows).cuda()].double().cpu().numpy()
+    want, _ = orc.attention_seeded(seed, "bf16", orc.longnet(L, 2048, 2), H, d, rows=rows)
+    assert np.abs(got - want).max() <= 2e-2
+
+
+def test_cfg5_160M_window_sampled(ga, orc):
+    """BASELINE cfg5 on one GPU: L=160,000,000, Window(128), bf16, sampled rows incl. the
+    8-way shard boundaries."""
+    L, H, d, seed = 160_000_000, 1, 64, 0x5EED0005
+    free, _ = torch.cuda.mem_get_info()
+    need = 4 * L * H * d * 2
+    assert free > need * 1.05, f"needs {need / 1e9:.1f} GB"
+    q, k, v = ga.qkv_device(seed, L, H, d, torch.bfloat16)
+    out = ga.attention(q, k, v, ga.Window(128))
+    del k, v
+    bounds = [s * (L // 8) + o for s in range(1, 8) for o in (-300, -128, -1, 0, 1, 127, 300)]
+    rows = _sample_rows(L, extra=bounds, n=256)
+    got = out[torch.from_numpy(rows).cuda()].double().cpu().numpy()
+    want, _ = orc.attention_seeded(seed, "bf16", orc.window(L, 128), H, d, rows=rows)
+    assert np.abs(got - want).max() <= 2e-2
