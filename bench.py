@@ -274,31 +274,7 @@ def main():
     value = edges_total / (ms / 1e3)
 
     # ---- roofline for the dominant kernel (the attention kernel; one launch per step at N=1)
-    peaks, peak_src = load_peaks()
-    sm_max = peaks.get("sm_max_mhz", 1965.0)
-    flops_per_edge = 4 * d  # q.k (2d) + p*v (2d) per head-edge, SURVEY §8(d)
-    kernel_ms = statistics.median(per_step)
-    achieved_tflops = edges_total / world * flops_per_edge / (kernel_ms / 1e3) / 1e12
-    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12  # FP32 FMA pipe, all SMs, max clock
-    gather_bytes_edge = 2 * d * eb(cfg["dtype"]) + (4 if kind == "bigbird" else 0)
-    gather_gbs = edges_total / world * gather_bytes_edge / (kernel_ms / 1e3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            traffic = json.load(f).get(f"{args.config}:{args.kernel}")
-    roofline = {"bound": "alu", "achieved": round(achieved_tflops, 3), "peak": round(fp32_peak, 2), "unit": "TFLOP/s",
-                "frac": round(achieved_tflops / fp32_peak, 4), "traffic": traffic,
-                "peak_source": "derived: 148 SMs x 128 FP32 FMA/clk x 2 flop x sm_max_mhz "
-                               f"({sm_max:.0f} MHz, {peak_src} MEASURED_PEAKS.json)",
-                "algorithmic": f"{flops_per_edge} flop per head-edge x {edges_total // world} head-edges per launch",
-                "kernel_ms_median": round(kernel_ms, 4)}
-    gather = {"bytes_per_edge": gather_bytes_edge, "GBps": round(gather_gbs, 1),
-              "frac_of_8TBps": round(gather_gbs / 8000.0, 3),
-              "frac_of_measured_hbm": round(gather_gbs / peaks["hbm_gbs"], 3),
-              "note": "north-star gather model: every edge pulls K_j and V_j; window masks reuse K/V on chip, "
-                      "so this can exceed 1 (the kernel is ALU-bound, see roofline)"}
-
+    roofline, gather = roofline_for(args, cfg, kind, edges_total // world, L_local, H, d, nnz, per_step)
     # ---- end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -328,6 +304,56 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def roofline_for(args, cfg, kind, head_edges, L_local, H, d, nnz, per_step):
+    """Roofline of the attention kernel.
+
+    Algorithmic bytes per launch = Q, K, V read once + O written once (+ row_ptr and col_idx
+    for explicit CSR): no implementation can move less.  Algorithmic flops = 4d per
+    head-edge (2d for q.k, 2d for p*v).  The bound is whichever resource's
+    lower-bound time is larger at the measured peaks (HBM copy GB/s vs bf16 tensor TFLOP/s;
+    fp32 inputs use the FP32 FMA pipe).  The north-star "gather model" (every edge pulls
+    K_j and V_j from memory) is reported separately."""
+    peaks, peak_src = load_peaks()
+    kernel_ms = statistics.median(per_step)
+    e = eb(cfg["dtype"])
+    bytes_alg = 4 * L_local * H * d * e + ((L_local + 1) * 8 + nnz * 4 if kind == "bigbird" else 0)
+    flops_alg = 4 * d * head_edges
+    hbm = peaks["hbm_gbs"]
+    if cfg["dtype"] == "f32":
+        fpeak, funit = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, "fp32 FMA pipe (derived)"
+    else:
+        fpeak, funit = peaks["bf16_tflops"], f"bf16 dense tensor ({peak_src})"
+    t_mem, t_fl = bytes_alg / (hbm * 1e9), flops_alg / (fpeak * 1e12)
+    s = kernel_ms / 1e3
+    if t_mem >= t_fl:
+        ach = bytes_alg / s / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+                "peak_source": f"hbm_gbs, {peak_src} MEASURED_PEAKS.json (copy bandwidth)"}
+    else:
+        ach = flops_alg / s / 1e12
+        roof = {"bound": "tensor" if cfg["dtype"] != "f32" else "alu", "achieved": round(ach, 2), "peak": fpeak,
+                "unit": "TFLOP/s", "frac": round(ach / fpeak, 4), "peak_source": funit}
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"{args.config}:{args.kernel}")
+    roof.update({
+        "traffic": traffic,
+        "algorithmic": f"{bytes_alg} B (Q,K,V,O once{' + CSR' if kind == 'bigbird' else ''}) and {flops_alg} flop "
+                       f"(4d x {head_edges} head-edges) per launch",
+        "lower_bound_us": {"hbm": round(t_mem * 1e6, 2), "flops": round(t_fl * 1e6, 2)},
+        "tensor_tflops_achieved": round(flops_alg / s / 1e12, 2),
+        "kernel_ms_median": round(kernel_ms, 4)})
+    gbe = 2 * d * e + (4 if kind == "bigbird" else 0)
+    ggbs = head_edges * gbe / s / 1e9
+    gather = {"bytes_per_edge": gbe, "GBps": round(ggbs, 1), "frac_of_8TBps": round(ggbs / 8000.0, 3),
+              "frac_of_measured_hbm": round(ggbs / hbm, 3),
+              "note": "north-star gather model (every edge pulls K_j and V_j); window/LongNet masks reuse K/V "
+                      "on chip, so it can exceed 1 — the roofline above is the binding bound"}
+    return roof, gather
 
 
 def measure_e2e(args, ga, gdist, cfg, mask, world, rank, r0, L, H, d, tdt, seed, dev, edges_total, buf, ws):

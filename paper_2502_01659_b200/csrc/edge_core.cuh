@@ -110,6 +110,18 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
         }
     }
 
+    // normalise and store the row (lane group 0 holds the merged state)
+    __device__ __forceinline__ void store(const AttnParams &p, int64_t t, int h) const
+    {
+        if (g != 0) return;
+        float r[VEC];
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) r[c] = o[c] * inv;
+        T *Op = reinterpret_cast<T *>(p.out) + ((size_t)t * p.H + h) * D + sub * VEC;
+        stg16(Op, pack<T>(r));
+    }
+
     // warp totals of the probe counters (one lane per group counts)
     __device__ __forceinline__ void probe_totals(unsigned long long &ne, unsigned long long &sj,
                                                  unsigned long long &sh) const
@@ -125,5 +137,22 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
         }
     }
 };
+
+// One (row, head) of Algorithm 1 by one warp: all pieces of N(i), merge, store.
+// t = local query row (global row q_begin + t).
+template <typename T, int D>
+__device__ __forceinline__ void edge_row(const AttnParams &p, int64_t t, int h, int lane)
+{
+    EdgeAcc<T, D, false> acc;
+    acc.init(p, t, h, lane);
+    const int64_t i = p.q_begin + t;
+    const int np = num_pieces(p.mask, i);
+    for (int pc = 0; pc < np; ++pc) {
+        const Piece P = get_piece(p.mask, i, pc);
+        acc.run(P, 0, P.count);
+    }
+    acc.merge_groups();
+    acc.store(p, t, h);
+}
 
 } // namespace ga

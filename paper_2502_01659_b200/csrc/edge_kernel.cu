@@ -52,14 +52,7 @@ __global__ void __launch_bounds__(256) edge_kernel(AttnParams p)
             }
         }
     }
-    if (acc.g == 0) {
-        constexpr int VEC = DT<T>::VEC;
-        const float inv = acc.l > 0.f ? 1.f / acc.l : 0.f;
-#pragma unroll
-        for (int c = 0; c < VEC; ++c) acc.o[c] *= inv;
-        T *Op = reinterpret_cast<T *>(p.out) + ((size_t)t * H + h) * D + acc.sub * VEC;
-        stg16(Op, pack<T>(acc.o));
-    }
+    acc.store(p, t, h);
 }
 
 template <typename T, int D>

@@ -1,13 +1,525 @@
-// window_tiled.cu — tiled window/dilated kernel (placeholder until implemented).
-#include "common.cuh"
+// window_tiled.cu — tensor-core band kernel for Window(w, r) masks (bf16 / fp16).
+//
+// Residue class c of a dilated window is a pure band: class rows a (token c + a*r) see class
+// rows b with |a - b| <= m, m = floor((w-1)/r) (readings R1/R2).  A CTA takes
+// ROWS = 64 consecutive class rows of one (class, head) and stages the Q tile and the K/V
+// band they reach in shared memory (cp.async 16-byte chunks, XOR swizzle so ldmatrix and
+// per-lane row reads are bank-conflict free).  Each warp owns 16 rows; the keys they reach
+// split into
+//
+//   F  = keys every one of the 16 rows sees      -> 16-key blocks on the tensor cores
+//        (mma.sync m16n8k16: S = Q K^T, online softmax in registers, O += P V)
+//   U\F plus F's ragged tail (< 16 keys)        -> CUDA cores, ONLY the valid pairs,
+//        with FHFMA (bf16 x bf16 + f32) so no per-element conversion is needed
+//
+// so no masked-out product is computed (work optimality) and the tensor
+// cores only see dense contractions.  For interior warps U\F is two 16x15 triangles; the
+// pairing "row x takes its 15-x left keys and x right keys" gives every lane exactly 15
+// edges (no idle lanes).  Warps whose band is clipped by the sequence ends, or whose tile
+// is cut by the query range, use a predicated general loop for U\F.  The CUDA-core state
+// seeds the MMA phase's running (m, l, O) through a per-warp shared-memory hand-off.
+#include "edge_core.cuh"
 
 namespace ga {
+namespace band {
 
-bool window_tiled_supported(const AttnParams &, ga_dtype) { return false; }
+constexpr int WARPS = 4;
+constexpr int ROWS = 16 * WARPS;
+constexpr int THREADS = 32 * WARPS;
+constexpr int MAX_GEN = 48; // keys of U\F (+ tail) a clipped warp may have: <= 15 + 15 + 15
 
-ga_status launch_window_tiled(const AttnParams &, ga_dtype, cudaStream_t)
+template <int D> struct Geo {
+    static constexpr int RB = 2 * D;    // bytes per (token, head) row
+    static constexpr int NC = RB / 16;  // 16-byte chunks per row
+    static constexpr int HC = NC / 2;   // chunks per half row (CUDA-core lanes)
+    static constexpr int KS = D / 16;   // k16 steps over d for Q K^T
+    static constexpr int NB8 = D / 8;   // n8 blocks over d for P V
+};
+
+// byte offset of chunk `ch` of row `row` in a swizzled [rows][RB] tile
+template <int D> __device__ __forceinline__ uint32_t swz(int row, int ch)
 {
-    set_error("tiled window kernel not built");
+    constexpr int NC = Geo<D>::NC;
+    const int f = NC >= 8 ? (row & 7) : ((row >> 1) & 3);
+    return (uint32_t)(row * Geo<D>::RB + ((ch ^ f) * 16));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+
+__device__ __forceinline__ uint4 lds16(uint32_t a)
+{
+    uint4 u;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "r"(a));
+    return u;
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t a, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3)
+{
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(a));
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t a, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3)
+{
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(a));
+}
+
+template <typename T>
+__device__ __forceinline__ void mma16816(float *c, const uint32_t *a, uint32_t b0, uint32_t b1);
+
+template <>
+__device__ __forceinline__ void mma16816<__nv_bfloat16>(float *c, const uint32_t *a, uint32_t b0, uint32_t b1)
+{
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <>
+__device__ __forceinline__ void mma16816<__half>(float *c, const uint32_t *a, uint32_t b0, uint32_t b1)
+{
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <typename T> __device__ __forceinline__ uint32_t pack2(float lo, float hi);
+template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) { return f2_to_bf2(lo, hi); }
+template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) { return f2_to_h2(lo, hi); }
+
+// c + x.lo*y.lo + x.hi*y.hi with 16-bit inputs and f32 accumulation (FHFMA)
+template <typename T> __device__ __forceinline__ float fma2h(uint32_t x, uint32_t y, float c);
+
+template <> __device__ __forceinline__ float fma2h<__nv_bfloat16>(uint32_t x, uint32_t y, float c)
+{
+    float d;
+    asm("{ .reg .b16 xl, xh, yl, yh; .reg .f32 t; mov.b32 {xl, xh}, %1; mov.b32 {yl, yh}, %2;\n\t"
+        "fma.rn.f32.bf16 t, xl, yl, %3; fma.rn.f32.bf16 %0, xh, yh, t; }"
+        : "=f"(d)
+        : "r"(x), "r"(y), "f"(c));
+    return d;
+}
+
+template <> __device__ __forceinline__ float fma2h<__half>(uint32_t x, uint32_t y, float c)
+{
+    float d;
+    asm("{ .reg .b16 xl, xh, yl, yh; .reg .f32 t; mov.b32 {xl, xh}, %1; mov.b32 {yl, yh}, %2;\n\t"
+        "fma.rn.f32.f16 t, xl, yl, %3; fma.rn.f32.f16 %0, xh, yh, t; }"
+        : "=f"(d)
+        : "r"(x), "r"(y), "f"(c));
+    return d;
+}
+
+// (o0, o1) += p * (v.lo, v.hi), p held in the low half of a 16x2 register
+template <typename T> __device__ __forceinline__ void axpy2h(uint32_t p16x2, uint32_t v, float &o0, float &o1);
+
+template <> __device__ __forceinline__ void axpy2h<__nv_bfloat16>(uint32_t p, uint32_t v, float &o0, float &o1)
+{
+    asm("{ .reg .b16 pl, ph, vl, vh; mov.b32 {pl, ph}, %2; mov.b32 {vl, vh}, %3;\n\t"
+        "fma.rn.f32.bf16 %0, pl, vl, %0; fma.rn.f32.bf16 %1, pl, vh, %1; }"
+        : "+f"(o0), "+f"(o1)
+        : "r"(p), "r"(v));
+}
+
+template <> __device__ __forceinline__ void axpy2h<__half>(uint32_t p, uint32_t v, float &o0, float &o1)
+{
+    asm("{ .reg .b16 pl, ph, vl, vh; mov.b32 {pl, ph}, %2; mov.b32 {vl, vh}, %3;\n\t"
+        "fma.rn.f32.f16 %0, pl, vl, %0; fma.rn.f32.f16 %1, pl, vh, %1; }"
+        : "+f"(o0), "+f"(o1)
+        : "r"(p), "r"(v));
+}
+
+struct BandParams {
+    AttnParams p;
+    int64_t m;          // band half-width in class rows
+    int64_t r;          // dilation = number of classes
+    int64_t tiles;      // tiles per (class, head) (max over classes)
+    int64_t edge_tiles; // tiles at each end whose band may be clipped (scheduled first)
+    uint32_t smem_bytes;
+};
+
+template <int D> __host__ __device__ constexpr uint32_t band_smem(int64_t m)
+{
+    return (uint32_t)(ROWS * Geo<D>::RB                // Q tile (reused to stage the output)
+                      + 2 * (ROWS + 2 * m) * Geo<D>::RB // K and V band
+                      + WARPS * 16 * (D + 2) * 4);      // CUDA-core -> MMA state hand-off
+}
+
+// One CUDA-core edge: score of (q half, key half) -> full score via the lane pair.
+template <typename T, int D>
+__device__ __forceinline__ float half_dot(const uint32_t *qv, uint32_t rowaddr, int key, int hf)
+{
+    constexpr int HC = Geo<D>::HC;
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < HC; ++k) {
+        const uint4 u = lds16(rowaddr + swz<D>(key, hf * HC + k));
+        s0 = fma2h<T>(qv[4 * k], u.x, s0);
+        s1 = fma2h<T>(qv[4 * k + 1], u.y, s1);
+        s0 = fma2h<T>(qv[4 * k + 2], u.z, s0);
+        s1 = fma2h<T>(qv[4 * k + 3], u.w, s1);
+    }
+    float s = s0 + s1;
+    return s + __shfl_xor_sync(0xffffffffu, s, 1);
+}
+
+template <typename T, int D>
+__device__ __forceinline__ void half_axpy(float *oc, float pr, uint32_t vaddr, int key, int hf)
+{
+    constexpr int HC = Geo<D>::HC;
+    const uint32_t p2 = pack2<T>(pr, pr);
+#pragma unroll
+    for (int k = 0; k < HC; ++k) {
+        const uint4 u = lds16(vaddr + swz<D>(key, hf * HC + k));
+        axpy2h<T>(p2, u.x, oc[8 * k + 0], oc[8 * k + 1]);
+        axpy2h<T>(p2, u.y, oc[8 * k + 2], oc[8 * k + 3]);
+        axpy2h<T>(p2, u.z, oc[8 * k + 4], oc[8 * k + 5]);
+        axpy2h<T>(p2, u.w, oc[8 * k + 6], oc[8 * k + 7]);
+    }
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const BandParams bp)
+{
+    using G = Geo<D>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const AttnParams &p = bp.p;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int H = p.H;
+    const int64_t r = bp.r, m = bp.m, L = p.mask.L;
+
+    const int64_t ch = (int64_t)blockIdx.x % (r * H);
+    // tile order: the tiles at both sequence ends (clipped bands, predicated paths) run first
+    const int64_t ord = (int64_t)blockIdx.x / (r * H);
+    const int64_t nb = imin(bp.edge_tiles, bp.tiles / 2);
+    const int64_t tile = ord < nb ? ord : ord < 2 * nb ? bp.tiles - 1 - (ord - nb) : ord - nb;
+    const int64_t c = ch / H;
+    const int h = (int)(ch % H);
+    if (c >= L) return;
+    const int64_t Nc = (L - c + r - 1) / r; // class rows in [0, L)
+    const int64_t q_end = p.q_begin + p.q_rows;
+    const int64_t a_lo = p.q_begin > c ? (p.q_begin - c + r - 1) / r : 0;
+    const int64_t a_hi = q_end > c ? imin((q_end - c + r - 1) / r, Nc) : 0;
+    // tiles are anchored at absolute class-row multiples of ROWS, so a query-range shard
+    // aligned to ROWS*r tokens computes every row exactly as the unsharded launch does
+    const int64_t a0 = (a_lo / ROWS) * ROWS + tile * ROWS;
+    if (a0 >= a_hi) return;
+    const int64_t v_lo = imax(a0, a_lo), v_hi = imin(a0 + ROWS, a_hi); // valid rows [v_lo, v_hi)
+    const bool interior = v_lo == a0 && v_hi == a0 + ROWS && a0 - m >= 0 && a0 + ROWS - 1 + m <= Nc - 1;
+
+    const int64_t NB = ROWS + 2 * m; // band rows; band-local 0 = class row a0 - m
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t sQ = sbase, sK = sQ + ROWS * G::RB, sV = sK + (uint32_t)(NB * G::RB);
+    float *scratch = reinterpret_cast<float *>(smem + ROWS * G::RB + 2 * NB * G::RB) + warp * 16 * (D + 2);
+
+    // ---- per-warp key geometry (band-local indices; abs = a0 - m + local)
+    const int w16 = warp * 16;
+    const int64_t x0 = a0 + w16; // first absolute class row of this warp
+    const int64_t wv_lo = imax(x0, v_lo), wv_hi = imin(x0 + 16, v_hi);
+    const bool warp_live = wv_lo < wv_hi;
+    const int64_t base = a0 - m;
+    const int Ulo = (int)(imax(0, x0 - m) - base), Uhi = (int)(imin(Nc - 1, x0 + 15 + m) - base);
+    const int Flo = (int)(imax(0, x0 + 15 - m) - base), Fhi = (int)(imin(Nc - 1, x0 + m) - base);
+    const int nF = Fhi - Flo + 1;            // >= 2m - 14 - clipping > 0 for m >= 15
+    const int q16 = nF > 0 ? nF / 16 : 0;    // dense 16-key blocks (tensor cores)
+    const int rem = nF > 0 ? nF % 16 : 0;    // ragged dense tail (CUDA cores)
+
+    // ---- stage Q rows and the K/V band rows the valid rows reach (16-byte cp.async)
+    const size_t row_bytes = (size_t)H * D * sizeof(T);
+    const char *Qg = reinterpret_cast<const char *>(p.Q) + (size_t)h * D * sizeof(T);
+    const char *Kg = reinterpret_cast<const char *>(p.K) + (size_t)h * D * sizeof(T);
+    const char *Vg = reinterpret_cast<const char *>(p.V) + (size_t)h * D * sizeof(T);
+    const int ld_lo = (int)(imax(0, v_lo - m) - base), ld_hi = (int)(imin(Nc - 1, v_hi - 1 + m) - base) + 1;
+    auto load_band = [&](int r0, int r1) {
+        r0 = max(r0, ld_lo);
+        r1 = min(r1, ld_hi);
+        for (int idx = r0 * G::NC + tid; idx < r1 * G::NC; idx += THREADS) {
+            const int row = idx / G::NC, cc = idx % G::NC;
+            const int64_t j = c + (base + row) * r;
+            const size_t off = (size_t)(j - p.kv_begin) * row_bytes + cc * 16;
+            cp_async16(sK + swz<D>(row, cc), Kg + off);
+            cp_async16(sV + swz<D>(row, cc), Vg + off);
+        }
+    };
+    for (int idx = tid; idx < ROWS * G::NC; idx += THREADS) {
+        const int row = idx / G::NC, cc = idx % G::NC;
+        if (a0 + row < v_lo || a0 + row >= v_hi) continue;
+        const int64_t i = c + (a0 + row) * r;
+        cp_async16(sQ + swz<D>(row, cc), Qg + (size_t)(i - p.q_begin) * row_bytes + cc * 16);
+    }
+    // stage 0: rows the CUDA-core phase reads (ends of the band); stage 1: the dense middle,
+    // which lands while the CUDA-core phase runs
+    const int mid0 = 63, mid1 = max(mid0, (int)(2 * m + 1) - 16);
+    load_band(0, mid0);
+    load_band(mid1, (int)NB);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    load_band(mid0, mid1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (interior) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory"); // clipped: CUDA keys may be anywhere
+    __syncthreads();
+
+    const float sl2 = p.scale_log2;
+
+    // ================= CUDA-core phase: U\F and F's ragged tail =================
+    if (warp_live) {
+        const int x = lane >> 1, hf = lane & 1;
+        uint32_t qv[G::HC * 4];
+#pragma unroll
+        for (int k = 0; k < G::HC; ++k) {
+            const uint4 u = lds16(sQ + swz<D>(w16 + x, hf * G::HC + k));
+            qv[4 * k] = u.x; qv[4 * k + 1] = u.y; qv[4 * k + 2] = u.z; qv[4 * k + 3] = u.w;
+        }
+        float mc = -INFINITY, lc = 0.f, oc[D / 2];
+#pragma unroll
+        for (int e = 0; e < D / 2; ++e) oc[e] = 0.f;
+        if (interior) {
+            // exact triangles: row x takes left keys Ulo+x..Ulo+14 and right keys
+            // Fhi+1..Fhi+x, then the ragged tail Flo+16*q16 ..; 15 + rem steps, all lanes busy
+            const int steps = 15 + rem; // <= 30
+            auto key_of = [&](int t) {
+                if (t < 15) return (t < 15 - x) ? (Ulo + x + t) : (Fhi + 1 + (t - 15 + x));
+                return Flo + 16 * q16 + (t - 15);
+            };
+            float sc[30]; // pass 1: scores and their exact max (no rescaling needed)
+#pragma unroll
+            for (int t = 0; t < 30; ++t) {
+                if (t >= steps) break;
+                sc[t] = half_dot<T, D>(qv, sK, key_of(t), hf) * sl2;
+                mc = fmaxf(mc, sc[t]);
+            }
+#pragma unroll
+            for (int t = 0; t < 30; ++t) { // pass 2: weights, weighted sum of V
+                if (t >= steps) break;
+                const float pr = ex2(sc[t] - mc);
+                lc += pr;
+                half_axpy<T, D>(oc, pr, sV, key_of(t), hf);
+            }
+        } else {
+            // clipped / cut warp: candidates [Ulo,Flo) U [Flo+16*q16, Fhi] U (Fhi, Uhi],
+            // each pair predicated on |row - key| <= m and the row being valid
+            const int64_t xa = x0 + x;
+            const bool row_ok = xa >= wv_lo && xa < wv_hi;
+            const int n_left = Flo - Ulo, n_tail = rem, n_right = Uhi - Fhi;
+            const int n_all = n_left + n_tail + n_right;
+            for (int t = 0; t < n_all; ++t) {
+                const int key = t < n_left ? Ulo + t : t < n_left + n_tail ? Flo + 16 * q16 + (t - n_left)
+                                                                             : Fhi + 1 + (t - n_left - n_tail);
+                const int64_t ka = base + key;
+                const bool ok = row_ok && ka >= xa - m && ka <= xa + m;
+                if (!__any_sync(0xffffffffu, ok)) continue;
+                const float s = half_dot<T, D>(qv, sK, key, hf) * sl2;
+                if (ok) {
+                    if (s > mc) { // online update with rescale (rare path)
+                        const float a = ex2(mc - s);
+                        lc *= a;
+#pragma unroll
+                        for (int e = 0; e < D / 2; ++e) oc[e] *= a;
+                        mc = s;
+                    }
+                    const float pr = ex2(s - mc);
+                    lc += pr;
+                    half_axpy<T, D>(oc, pr, sV, key, hf);
+                }
+            }
+        }
+        // hand-off: row x, dims [hf*D/2, (hf+1)*D/2)
+        float *srow = scratch + x * (D + 2);
+#pragma unroll
+        for (int e = 0; e < D / 2; ++e) srow[2 + hf * (D / 2) + e] = oc[e];
+        if (hf == 0) { srow[0] = mc; srow[1] = lc; }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads(); // dense rows landed (and the hand-off is visible within the warp)
+    if (!warp_live) return; // no further CTA-wide barriers
+
+    // ================= tensor-core phase: dense 16x16 blocks of F =================
+    const int g = lane >> 2, t4 = lane & 3;
+    uint32_t qa[G::KS][4];
+#pragma unroll
+    for (int kk = 0; kk < G::KS; ++kk) {
+        const int row = w16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int chk = 2 * kk + (lane >> 4);
+        ldsm_x4(sQ + swz<D>(row, chk), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+    }
+    float o[G::NB8][4];
+    float mr[2], lr[2];
+    {
+        const float *r0 = scratch + g * (D + 2), *r1 = scratch + (g + 8) * (D + 2);
+        mr[0] = r0[0];
+        mr[1] = r1[0];
+        lr[0] = t4 == 0 ? r0[1] : 0.f;
+        lr[1] = t4 == 0 ? r1[1] : 0.f;
+#pragma unroll
+        for (int j = 0; j < G::NB8; ++j) {
+            o[j][0] = r0[2 + 8 * j + 2 * t4];
+            o[j][1] = r0[2 + 8 * j + 2 * t4 + 1];
+            o[j][2] = r1[2 + 8 * j + 2 * t4];
+            o[j][3] = r1[2 + 8 * j + 2 * t4 + 1];
+        }
+    }
+    // per-lane ldmatrix row offsets are block-invariant up to +16*b*RB
+    const int krow = Flo + (lane & 7) + (lane >> 4) * 8;        // K (non-trans) row for block 0
+    const int vrow = Flo + (lane & 7) + ((lane >> 3) & 1) * 8;  // V (trans) row for block 0
+#pragma unroll 2
+    for (int b = 0; b < q16; ++b) {
+        float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int kk = 0; kk < G::KS; ++kk) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(sK + swz<D>(krow + 16 * b, 2 * kk + ((lane >> 3) & 1)), b0, b1, b2, b3);
+            mma16816<T>(s[0], qa[kk], b0, b1);
+            mma16816<T>(s[1], qa[kk], b2, b3);
+        }
+        // online softmax on rows g (s[.][0..1]) and g+8 (s[.][2..3])
+        float bm0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
+        float bm1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 1));
+        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
+        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 1));
+        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
+        // lazy rescale: keep the reference max unless a score exceeds it by more than
+        // 2^kTau (exact: l and O share the reference; weights stay <= 2^kTau, no overflow)
+        constexpr float kTau = 8.f;
+        const float bs0 = bm0 * sl2, bs1 = bm1 * sl2;
+        const bool need = bs0 > mr[0] + kTau || bs1 > mr[1] + kTau;
+        if (__any_sync(0xffffffffu, need)) {
+            const float mn0 = fmaxf(mr[0], bs0), mn1 = fmaxf(mr[1], bs1);
+            const float a0s = ex2(mr[0] - mn0), a1s = ex2(mr[1] - mn1);
+            lr[0] *= a0s;
+            lr[1] *= a1s;
+#pragma unroll
+            for (int j = 0; j < G::NB8; ++j) {
+                o[j][0] *= a0s;
+                o[j][1] *= a0s;
+                o[j][2] *= a1s;
+                o[j][3] *= a1s;
+            }
+            mr[0] = mn0;
+            mr[1] = mn1;
+        }
+        float pp[2][4];
+#pragma unroll
+        for (int nb2 = 0; nb2 < 2; ++nb2) {
+            pp[nb2][0] = ex2(fmaf(s[nb2][0], sl2, -mr[0]));
+            pp[nb2][1] = ex2(fmaf(s[nb2][1], sl2, -mr[0]));
+            pp[nb2][2] = ex2(fmaf(s[nb2][2], sl2, -mr[1]));
+            pp[nb2][3] = ex2(fmaf(s[nb2][3], sl2, -mr[1]));
+            lr[0] += pp[nb2][0] + pp[nb2][1];
+            lr[1] += pp[nb2][2] + pp[nb2][3];
+        }
+        uint32_t pa[4];
+        pa[0] = pack2<T>(pp[0][0], pp[0][1]);
+        pa[1] = pack2<T>(pp[0][2], pp[0][3]);
+        pa[2] = pack2<T>(pp[1][0], pp[1][1]);
+        pa[3] = pack2<T>(pp[1][2], pp[1][3]);
+#pragma unroll
+        for (int jj = 0; jj < G::NB8 / 2; ++jj) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(sV + swz<D>(vrow + 16 * b, 2 * jj + (lane >> 4)), b0, b1, b2, b3);
+            mma16816<T>(o[2 * jj], pa, b0, b1);
+            mma16816<T>(o[2 * jj + 1], pa, b2, b3);
+        }
+    }
+    // ---- finalise: l = quad sum, normalise, stage through this warp's Q rows, store
+    lr[0] += __shfl_xor_sync(0xffffffffu, lr[0], 1);
+    lr[0] += __shfl_xor_sync(0xffffffffu, lr[0], 2);
+    lr[1] += __shfl_xor_sync(0xffffffffu, lr[1], 1);
+    lr[1] += __shfl_xor_sync(0xffffffffu, lr[1], 2);
+    const float inv0 = lr[0] > 0.f ? 1.f / lr[0] : 0.f, inv1 = lr[1] > 0.f ? 1.f / lr[1] : 0.f;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < G::NB8; ++j) {
+        const uint32_t w0 = pack2<T>(o[j][0] * inv0, o[j][1] * inv0);
+        const uint32_t w1 = pack2<T>(o[j][2] * inv1, o[j][3] * inv1);
+        // element (row, col 8j + 2t4) sits in chunk j, byte 4*t4
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(sQ + swz<D>(w16 + g, j) + 4 * t4), "r"(w0));
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(sQ + swz<D>(w16 + g + 8, j) + 4 * t4), "r"(w1));
+    }
+    __syncwarp();
+    char *Og = reinterpret_cast<char *>(p.out) + (size_t)h * D * sizeof(T);
+#pragma unroll
+    for (int idx = lane; idx < 16 * G::NC; idx += 32) {
+        const int row = idx / G::NC, cc = idx % G::NC;
+        const int64_t xa = x0 + row;
+        if (xa < wv_lo || xa >= wv_hi) continue;
+        const int64_t i = c + xa * r;
+        stg16(Og + (size_t)(i - p.q_begin) * row_bytes + cc * 16, lds16(sQ + swz<D>(w16 + row, cc)));
+    }
+}
+
+static constexpr uint32_t kMaxSmem = 227 * 1024;
+
+template <typename T, int D> static ga_status launch_t(const BandParams &bp, cudaStream_t s)
+{
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(band_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+        if (e != cudaSuccess) return cuda_fail(e, "band_kernel: set smem");
+        configured = true;
+    }
+    const int64_t blocks = bp.tiles * bp.r * bp.p.H;
+    if (blocks == 0) return GA_OK;
+    band_kernel<T, D><<<(unsigned)blocks, THREADS, bp.smem_bytes, s>>>(bp);
+    GA_CHECK_LAUNCH("band_kernel");
+    return GA_OK;
+}
+
+} // namespace band
+
+static uint32_t band_smem_for(int d, int64_t m)
+{
+    switch (d) {
+    case 32: return band::band_smem<32>(m);
+    case 64: return band::band_smem<64>(m);
+    default: return band::band_smem<128>(m);
+    }
+}
+
+bool window_tiled_supported(const AttnParams &p, ga_dtype dt)
+{
+    if (p.mask.kind != K_WINDOW || (dt != GA_BF16 && dt != GA_F16)) return false;
+    if (p.mask.m < 15) return false;
+    return band_smem_for(p.d, p.mask.m) <= band::kMaxSmem;
+}
+
+ga_status launch_window_tiled(const AttnParams &p, ga_dtype dt, cudaStream_t s)
+{
+    band::BandParams bp;
+    bp.p = p;
+    bp.m = p.mask.m;
+    bp.r = p.mask.r;
+    // class rows of the query range per class: at most ceil(q_rows / r) + 1
+    const int64_t per_class = (p.q_rows + bp.r - 1) / bp.r + 1;
+    bp.tiles = (per_class + band::ROWS - 1) / band::ROWS + 1; // +1: grid anchored at ROWS multiples
+    bp.edge_tiles = (bp.m + band::ROWS - 1) / band::ROWS + 2;
+    bp.smem_bytes = band_smem_for(p.d, bp.m);
+    if (bp.r * p.H * bp.tiles > (int64_t)INT32_MAX) {
+        set_error("band kernel grid too large");
+        return GA_ERR_UNSUPPORTED;
+    }
+    if (dt == GA_BF16) {
+        switch (p.d) {
+        case 32: return band::launch_t<__nv_bfloat16, 32>(bp, s);
+        case 64: return band::launch_t<__nv_bfloat16, 64>(bp, s);
+        case 128: return band::launch_t<__nv_bfloat16, 128>(bp, s);
+        }
+    } else {
+        switch (p.d) {
+        case 32: return band::launch_t<__half, 32>(bp, s);
+        case 64: return band::launch_t<__half, 64>(bp, s);
+        case 128: return band::launch_t<__half, 128>(bp, s);
+        }
+    }
+    set_error("band kernel: unsupported d");
     return GA_ERR_UNSUPPORTED;
 }
 
