@@ -89,7 +89,7 @@ typedef struct ga_mask {
     const int64_t *global_idx; /* BIGBIRD: DEVICE int64 [n_global] sorted, or NULL for the
                                   evenly spaced set {floor(k*L/n_global)} (reading R9)    */
     int64_t n_global;          /* BIGBIRD global token count                             */
-    int64_t n_random;          /* BIGBIRD random columns per non-global row (<= 256)     */
+    int64_t n_random;          /* BIGBIRD random columns per non-global row (<= 320)     */
     uint64_t seed;             /* BIGBIRD random-column seed (reading R10)                */
 } ga_mask;
 

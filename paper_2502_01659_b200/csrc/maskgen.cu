@@ -161,7 +161,7 @@ __global__ void fill_pieces_kernel(DevMask M, const int64_t *row_ptr, int32_t *c
 
 // BigBird: warp per row.  Global rows: lanes write 0..L-1.  Others: lane 0 draws the random
 // columns (reading R10), sorts them, and merges window U (G \ W) U R in ascending order.
-static constexpr int MAX_RANDOM = 256;
+static constexpr int MAX_RANDOM = 320;
 
 __global__ void fill_bigbird_kernel(DevMask M, const int64_t *row_ptr, int32_t *col_idx)
 {
@@ -224,7 +224,9 @@ __global__ void fill_bigbird_kernel(DevMask M, const int64_t *row_ptr, int32_t *
 
 ga_status maskgen_to_csr(const DevMask &M, int64_t *row_ptr, int32_t *col_idx, cudaStream_t s)
 {
-    if (M.kind == K_BIGBIRD && M.nrand > MAX_RANDOM) {
+    // a row draws min(n_random, L - |W_i U G|) columns and |W_i| >= w, so only patterns that
+    // can draw more than MAX_RANDOM columns for some row are rejected
+    if (M.kind == K_BIGBIRD && M.nrand > MAX_RANDOM && M.L - M.w > MAX_RANDOM) {
         set_error("n_random=%lld exceeds %d", (long long)M.nrand, MAX_RANDOM);
         return GA_ERR_UNSUPPORTED;
     }

@@ -23,7 +23,7 @@
 namespace ga {
 namespace band {
 
-constexpr int WARPS = 4;
+constexpr int WARPS = 7; // 112 rows: two CTAs (28 KB Q + 94 KB band each) fit one SM at m=127
 constexpr int ROWS = 16 * WARPS;
 constexpr int THREADS = 32 * WARPS;
 constexpr int MAX_GEN = 48; // keys of U\F (+ tail) a clipped warp may have: <= 15 + 15 + 15
@@ -148,9 +148,8 @@ struct BandParams {
 
 template <int D> __host__ __device__ constexpr uint32_t band_smem(int64_t m)
 {
-    return (uint32_t)(ROWS * Geo<D>::RB                // Q tile (reused to stage the output)
-                      + 2 * (ROWS + 2 * m) * Geo<D>::RB // K and V band
-                      + WARPS * 16 * (D + 2) * 4);      // CUDA-core -> MMA state hand-off
+    return (uint32_t)(ROWS * Geo<D>::RB                 // Q tile (hand-off + output staging)
+                      + 2 * (ROWS + 2 * m) * Geo<D>::RB); // K and V band
 }
 
 // One CUDA-core edge: score of (q half, key half) -> full score via the lane pair.
@@ -218,7 +217,6 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
     const int64_t NB = ROWS + 2 * m; // band rows; band-local 0 = class row a0 - m
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
     const uint32_t sQ = sbase, sK = sQ + ROWS * G::RB, sV = sK + (uint32_t)(NB * G::RB);
-    float *scratch = reinterpret_cast<float *>(smem + ROWS * G::RB + 2 * NB * G::RB) + warp * 16 * (D + 2);
 
     // ---- per-warp key geometry (band-local indices; abs = a0 - m + local)
     const int w16 = warp * 16;
@@ -257,7 +255,7 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
     }
     // stage 0: rows the CUDA-core phase reads (ends of the band); stage 1: the dense middle,
     // which lands while the CUDA-core phase runs
-    const int mid0 = 63, mid1 = max(mid0, (int)(2 * m + 1) - 16);
+    const int mid0 = ROWS - 1, mid1 = max(mid0, (int)(2 * m + 1) - 16);
     load_band(0, mid0);
     load_band(mid1, (int)NB);
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -268,6 +266,20 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
     __syncthreads();
 
     const float sl2 = p.scale_log2;
+
+    // A fragments of Q for the tensor-core phase, taken before the Q rows are reused
+    const int g = lane >> 2, t4 = lane & 3;
+    uint32_t qa[G::KS][4];
+    if (warp_live) {
+#pragma unroll
+        for (int kk = 0; kk < G::KS; ++kk) {
+            const int row = w16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+            const int chk = 2 * kk + (lane >> 4);
+            ldsm_x4(sQ + swz<D>(row, chk), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+        }
+    }
+    float o[G::NB8][4];
+    float mr[2], lr[2];
 
     // ================= CUDA-core phase: U\F and F's ragged tail =================
     if (warp_live) {
@@ -331,68 +343,82 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
                 }
             }
         }
-        // hand-off: row x, dims [hf*D/2, (hf+1)*D/2)
-        float *srow = scratch + x * (D + 2);
+        // ---- hand-off into the MMA layout (lane (g,t4): rows g, g+8; dims 8j+2t4, +1):
+        // m and l by shuffles, o through this warp's 16 Q rows (one half-row per round;
+        // a half-row of fp32 is exactly one Q row of bytes)
+        __syncwarp(); // every lane has finished reading its Q rows
+        mr[0] = __shfl_sync(0xffffffffu, mc, 2 * g);
+        mr[1] = __shfl_sync(0xffffffffu, mc, 2 * (g + 8));
+        const float l0 = __shfl_sync(0xffffffffu, lc, 2 * g), l1 = __shfl_sync(0xffffffffu, lc, 2 * (g + 8));
+        lr[0] = t4 == 0 ? l0 : 0.f;
+        lr[1] = t4 == 0 ? l1 : 0.f;
 #pragma unroll
-        for (int e = 0; e < D / 2; ++e) srow[2 + hf * (D / 2) + e] = oc[e];
-        if (hf == 0) { srow[0] = mc; srow[1] = lc; }
+        for (int hh = 0; hh < 2; ++hh) {
+            if (hf == hh) {
+#pragma unroll
+                for (int k = 0; k < G::NC; ++k)
+                    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(sQ + swz<D>(w16 + x, k)),
+                                 "f"(oc[4 * k]), "f"(oc[4 * k + 1]), "f"(oc[4 * k + 2]), "f"(oc[4 * k + 3]));
+            }
+            __syncwarp();
+#pragma unroll
+            for (int jl = 0; jl < G::NB8 / 2; ++jl) {
+                const int j = hh * (G::NB8 / 2) + jl, chunk = 2 * jl + (t4 >> 1);
+                float2 v0, v1;
+                asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v0.x), "=f"(v0.y)
+                             : "r"(sQ + swz<D>(w16 + g, chunk) + (t4 & 1) * 8));
+                asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v1.x), "=f"(v1.y)
+                             : "r"(sQ + swz<D>(w16 + g + 8, chunk) + (t4 & 1) * 8));
+                o[j][0] = v0.x;
+                o[j][1] = v0.y;
+                o[j][2] = v1.x;
+                o[j][3] = v1.y;
+            }
+            __syncwarp();
+        }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads(); // dense rows landed (and the hand-off is visible within the warp)
+    __syncthreads(); // dense rows landed
     if (!warp_live) return; // no further CTA-wide barriers
 
     // ================= tensor-core phase: dense 16x16 blocks of F =================
-    const int g = lane >> 2, t4 = lane & 3;
-    uint32_t qa[G::KS][4];
-#pragma unroll
-    for (int kk = 0; kk < G::KS; ++kk) {
-        const int row = w16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        const int chk = 2 * kk + (lane >> 4);
-        ldsm_x4(sQ + swz<D>(row, chk), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
-    }
-    float o[G::NB8][4];
-    float mr[2], lr[2];
-    {
-        const float *r0 = scratch + g * (D + 2), *r1 = scratch + (g + 8) * (D + 2);
-        mr[0] = r0[0];
-        mr[1] = r1[0];
-        lr[0] = t4 == 0 ? r0[1] : 0.f;
-        lr[1] = t4 == 0 ? r1[1] : 0.f;
-#pragma unroll
-        for (int j = 0; j < G::NB8; ++j) {
-            o[j][0] = r0[2 + 8 * j + 2 * t4];
-            o[j][1] = r0[2 + 8 * j + 2 * t4 + 1];
-            o[j][2] = r1[2 + 8 * j + 2 * t4];
-            o[j][3] = r1[2 + 8 * j + 2 * t4 + 1];
-        }
-    }
     // per-lane ldmatrix row offsets are block-invariant up to +16*b*RB
-    const int krow = Flo + (lane & 7) + (lane >> 4) * 8;        // K (non-trans) row for block 0
-    const int vrow = Flo + (lane & 7) + ((lane >> 3) & 1) * 8;  // V (trans) row for block 0
+    // per-lane ldmatrix addresses of block 0; block b adds 16*b rows (the swizzle phase
+    // repeats every 8 rows, so the offset is a plain add)
+    uint32_t kaddr[G::KS], vaddr[G::NB8 / 2];
+    {
+        const int krow = Flo + (lane & 7) + (lane >> 4) * 8;       // K (non-trans) rows
+        const int vrow = Flo + (lane & 7) + ((lane >> 3) & 1) * 8; // V (trans) rows
+#pragma unroll
+        for (int kk = 0; kk < G::KS; ++kk) kaddr[kk] = sK + swz<D>(krow, 2 * kk + ((lane >> 3) & 1));
+#pragma unroll
+        for (int jj = 0; jj < G::NB8 / 2; ++jj) vaddr[jj] = sV + swz<D>(vrow, 2 * jj + (lane >> 4));
+    }
 #pragma unroll 2
     for (int b = 0; b < q16; ++b) {
+        const uint32_t boff = (uint32_t)(b * 16 * G::RB);
         float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
         for (int kk = 0; kk < G::KS; ++kk) {
             uint32_t b0, b1, b2, b3;
-            ldsm_x4(sK + swz<D>(krow + 16 * b, 2 * kk + ((lane >> 3) & 1)), b0, b1, b2, b3);
+            ldsm_x4(kaddr[kk] + boff, b0, b1, b2, b3);
             mma16816<T>(s[0], qa[kk], b0, b1);
             mma16816<T>(s[1], qa[kk], b2, b3);
         }
-        // online softmax on rows g (s[.][0..1]) and g+8 (s[.][2..3])
-        float bm0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
-        float bm1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
-        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 1));
-        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
-        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 1));
-        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
-        // lazy rescale: keep the reference max unless a score exceeds it by more than
-        // 2^kTau (exact: l and O share the reference; weights stay <= 2^kTau, no overflow)
+        // online softmax on rows g (s[.][0..1]) and g+8 (s[.][2..3]).  Lazy rescale: keep
+        // the reference max unless a score exceeds it by more than 2^kTau (exact: l and O
+        // share the reference; weights stay <= 2^kTau, no overflow).  The common case needs
+        // only per-lane maxima and one warp vote, no shuffle reductions.
         constexpr float kTau = 8.f;
-        const float bs0 = bm0 * sl2, bs1 = bm1 * sl2;
-        const bool need = bs0 > mr[0] + kTau || bs1 > mr[1] + kTau;
+        const float lm0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
+        const float lm1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+        const bool need = lm0 * sl2 > mr[0] + kTau || lm1 * sl2 > mr[1] + kTau;
         if (__any_sync(0xffffffffu, need)) {
-            const float mn0 = fmaxf(mr[0], bs0), mn1 = fmaxf(mr[1], bs1);
+            float bm0 = fmaxf(lm0, __shfl_xor_sync(0xffffffffu, lm0, 1));
+            bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
+            float bm1 = fmaxf(lm1, __shfl_xor_sync(0xffffffffu, lm1, 1));
+            bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
+            const float mn0 = fmaxf(mr[0], bm0 * sl2), mn1 = fmaxf(mr[1], bm1 * sl2);
             const float a0s = ex2(mr[0] - mn0), a1s = ex2(mr[1] - mn1);
             lr[0] *= a0s;
             lr[1] *= a1s;
@@ -424,7 +450,7 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
 #pragma unroll
         for (int jj = 0; jj < G::NB8 / 2; ++jj) {
             uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(sV + swz<D>(vrow + 16 * b, 2 * jj + (lane >> 4)), b0, b1, b2, b3);
+            ldsm_x4_t(vaddr[jj] + boff, b0, b1, b2, b3);
             mma16816<T>(o[2 * jj], pa, b0, b1);
             mma16816<T>(o[2 * jj + 1], pa, b2, b3);
         }
