@@ -273,8 +273,8 @@ def test_sharded_offsets_bitwise(ga):
     halo = 127 * 2
     for kernel in ("edge", "auto"):
         full = ga.attention(q, k, v, m, kernel=kernel)
-        # shard boundaries aligned to the band kernel's tile (64 class rows x r tokens)
-        for r0, r1 in ((0, 1024), (1024, 3072), (3072, 8192)):
+        # shard boundaries aligned to the band kernel's tile (112 class rows x r tokens)
+        for r0, r1 in ((0, 2240), (2240, 4480), (4480, 8192)):
             k0, k1 = max(0, r0 - halo), min(L, r1 + halo)
             part = ga.attention(q[r0:r1].contiguous(), k[k0:k1].contiguous(), v[k0:k1].contiguous(), m, L=L,
                                 q_begin=r0, kv_begin=k0, kernel=kernel)
