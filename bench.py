@@ -168,7 +168,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "edge", "window", "tc"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "edge", "tiled", "window", "tc"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

@@ -97,9 +97,12 @@ typedef struct ga_mask {
    (mask, dtype, d) triple; the others force one path (tests compare them). */
 typedef enum {
     GA_KERNEL_AUTO = 0,
-    GA_KERNEL_EDGE = 1,   /* generic warp-per-(row,head) edge traversal, every family      */
-    GA_KERNEL_WINDOW = 2, /* tiled window/dilated kernel: K/V band staged in shared memory  */
-    GA_KERNEL_TC = 3      /* bf16/fp16 window: tcgen05 dense tiles + CUDA-core triangles    */
+    GA_KERNEL_EDGE = 1,  /* generic warp-per-(row,head) edge traversal, every family, every dtype */
+    GA_KERNEL_TILED = 2, /* bf16/fp16 tensor-core kernel of the family: WINDOW -> band kernel
+                            (K/V band in shared memory, mma.sync on fully dense 16x16 blocks,
+                            CUDA cores on the partial triangles); LONGNET -> dense-group kernel
+                            (rows sharing a neighbour set x their strided key pieces) */
+    GA_KERNEL_TC = 3     /* bf16 window: tcgen05 dense core (not built in this version) */
 } ga_kernel;
 
 /* Optional controls for ga_attention_ex.  Zero-initialise, then set what you need. */

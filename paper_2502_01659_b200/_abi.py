@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(_PKG, "libga.so")
 GA_OK, GA_ERR_INVALID_ARG, GA_ERR_UNSUPPORTED, GA_ERR_CUDA, GA_ERR_OOM, GA_ERR_MASK = 0, -1, -2, -3, -5, -6
 GA_F32, GA_BF16, GA_F16 = 0, 1, 2
 GA_MASK_CSR, GA_MASK_WINDOW, GA_MASK_LONGNET, GA_MASK_BIGBIRD, GA_MASK_BLOCK_DILATED = 0, 1, 2, 3, 4
-GA_KERNEL_AUTO, GA_KERNEL_EDGE, GA_KERNEL_WINDOW, GA_KERNEL_TC = 0, 1, 2, 3
+GA_KERNEL_AUTO, GA_KERNEL_EDGE, GA_KERNEL_TILED, GA_KERNEL_TC = 0, 1, 2, 3
 
 STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_INVALID_ARG", -2: "GA_ERR_UNSUPPORTED", -3: "GA_ERR_CUDA",
                 -5: "GA_ERR_OOM", -6: "GA_ERR_MASK"}

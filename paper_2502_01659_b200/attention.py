@@ -14,7 +14,7 @@ from . import _abi
 from .masks import CSR, Mask
 
 _DT = {torch.float32: _abi.GA_F32, torch.bfloat16: _abi.GA_BF16, torch.float16: _abi.GA_F16}
-_KERNELS = {"auto": _abi.GA_KERNEL_AUTO, "edge": _abi.GA_KERNEL_EDGE, "window": _abi.GA_KERNEL_WINDOW,
+_KERNELS = {"auto": _abi.GA_KERNEL_AUTO, "edge": _abi.GA_KERNEL_EDGE, "tiled": _abi.GA_KERNEL_TILED, "window": _abi.GA_KERNEL_TILED,
             "tc": _abi.GA_KERNEL_TC}
 
 

@@ -229,9 +229,11 @@ ga_status ga_attention_ex(const void *Q, const void *K, const void *V, const ga_
     if (!probe && (kernel == GA_KERNEL_TC || kernel == GA_KERNEL_AUTO) && window_tc_supported(p, dtype))
         return launch_window_tc(p, dtype, s);
     if (kernel == GA_KERNEL_TC) { set_error("tcgen05 path does not support this (mask, dtype, d)"); return GA_ERR_UNSUPPORTED; }
-    if (!probe && (kernel == GA_KERNEL_WINDOW || kernel == GA_KERNEL_AUTO) && window_tiled_supported(p, dtype))
-        return launch_window_tiled(p, dtype, s);
-    if (kernel == GA_KERNEL_WINDOW) { set_error("tiled window path does not support this (mask, dtype, d)"); return GA_ERR_UNSUPPORTED; }
+    if (!probe && (kernel == GA_KERNEL_TILED || kernel == GA_KERNEL_AUTO)) {
+        if (window_tiled_supported(p, dtype)) return launch_window_tiled(p, dtype, s);
+        if (longnet_tc_supported(p, dtype)) return launch_longnet_tc(p, dtype, s);
+    }
+    if (kernel == GA_KERNEL_TILED) { set_error("no tiled tensor-core kernel for this (mask, dtype, d)"); return GA_ERR_UNSUPPORTED; }
     return launch_edge(p, dtype, s);
 }
 
@@ -320,7 +322,9 @@ ga_status ga_mask_count(const ga_mask *pattern, int64_t *nnz_out)
                 const int64_t s1 = imin(L, s0 + segw);
                 const int64_t U = multiples(s0, s1, stp);
                 const int64_t gt = t < M.K ? multiples(s0, s1, stp * M.alpha) : 0;
-                n += gt * (U - ceil_div(U, M.alpha)) + (U - gt) * U;
+                const int64_t rx = (M.alpha - (s0 / stp) % M.alpha) % M.alpha; // excluded residue
+                const int64_t keep = U - (U > rx ? (U - 1 - rx) / M.alpha + 1 : 0);
+                n += gt * keep + (U - gt) * U;
             }
             stp *= M.alpha;
         }

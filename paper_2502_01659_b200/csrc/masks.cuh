@@ -55,7 +55,9 @@ struct DevMask {
 struct Piece {
     int64_t base, step, count;
     int32_t mode;
-    int32_t alpha; // SKIPMUL
+    int32_t alpha; // SKIPMUL: u ranges over the integers with u mod alpha != rexcl
+    int32_t rexcl;
+    int32_t pad;
     const int32_t *cols;
 };
 
@@ -98,6 +100,8 @@ GA_HD Piece get_piece(const DevMask &M, int64_t i, int pc)
     Piece P;
     P.mode = P_AFFINE;
     P.alpha = 0;
+    P.rexcl = 0;
+    P.pad = 0;
     P.cols = nullptr;
     switch (M.kind) {
     case K_WINDOW: {
@@ -132,9 +136,15 @@ GA_HD Piece get_piece(const DevMask &M, int64_t i, int pc)
         P.base = s0;
         P.step = stp;
         if (pc < s) {
+            // keep j = s0 + a^t u with nu(j) == t exactly, i.e. (s0/a^t + u) mod a != 0:
+            // exclude the residue u == -(s0/a^t) (mod a)  (s0 is a multiple of a^t, and of
+            // a^(t+1) only when a | w0 * (segment index))
+            const int64_t c0 = (s0 / stp) % M.alpha;
+            const int64_t rx = (M.alpha - c0) % M.alpha;
             P.mode = P_SKIPMUL;
             P.alpha = (int32_t)M.alpha;
-            P.count = U - ceil_div(U, M.alpha); // u in [0,U) with alpha !| u
+            P.rexcl = (int32_t)rx;
+            P.count = U - (U > rx ? (U - 1 - rx) / M.alpha + 1 : 0);
         } else {
             P.count = U;
         }
@@ -148,8 +158,10 @@ GA_HD int64_t piece_at(const Piece &P, int64_t k)
 {
     if (P.mode == P_AFFINE) return P.base + k * P.step;
     if (P.mode == P_CSR) return (int64_t)P.cols[P.base + k];
-    int64_t a1 = P.alpha - 1;
-    int64_t u = (k / a1) * P.alpha + (k % a1) + 1;
+    if (P.alpha == 2) return P.base + P.step * (2 * k + (P.rexcl == 0 ? 1 : 0)); // the common alpha
+    const int64_t a1 = P.alpha - 1;
+    const int64_t idx = k % a1;
+    const int64_t u = (k / a1) * P.alpha + (idx < P.rexcl ? idx : idx + 1);
     return P.base + P.step * u;
 }
 

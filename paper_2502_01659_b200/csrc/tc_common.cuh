@@ -1,0 +1,227 @@
+// tc_common.cuh — shared-memory staging and mma.sync helpers for the tensor-core kernels
+// (band kernel for windows, dense-group kernel for LongNet).
+#pragma once
+#include "edge_core.cuh"
+
+namespace ga {
+namespace tc {
+
+template <int D> struct Geo {
+    static constexpr int RB = 2 * D;    // bytes per (token, head) row (bf16/fp16)
+    static constexpr int NC = RB / 16;  // 16-byte chunks per row
+    static constexpr int HC = NC / 2;   // chunks per half row (CUDA-core lanes)
+    static constexpr int KS = D / 16;   // k16 steps over d for Q K^T
+    static constexpr int NB8 = D / 8;   // n8 blocks over d for P V
+};
+
+// byte offset of chunk `ch` of row `row` in a swizzled [rows][RB] tile: the 16-byte chunk
+// index is XORed with the row's low bits so 8 consecutive rows hit 8 different bank groups
+template <int D> __device__ __forceinline__ uint32_t swz(int row, int ch)
+{
+    constexpr int NC = Geo<D>::NC;
+    const int f = NC >= 8 ? (row & 7) : ((row >> 1) & 3);
+    return (uint32_t)(row * Geo<D>::RB + ((ch ^ f) * 16));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+template <int N> __device__ __forceinline__ void cp_async_wait()
+{
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ uint4 lds16(uint32_t a)
+{
+    uint4 u;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "r"(a));
+    return u;
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t a, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3)
+{
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(a));
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t a, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3)
+{
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(a));
+}
+
+template <typename T>
+__device__ __forceinline__ void mma16816(float *c, const uint32_t *a, uint32_t b0, uint32_t b1);
+
+template <>
+__device__ __forceinline__ void mma16816<__nv_bfloat16>(float *c, const uint32_t *a, uint32_t b0, uint32_t b1)
+{
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <>
+__device__ __forceinline__ void mma16816<__half>(float *c, const uint32_t *a, uint32_t b0, uint32_t b1)
+{
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <typename T> __device__ __forceinline__ uint32_t pack2(float lo, float hi);
+template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) { return f2_to_bf2(lo, hi); }
+template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) { return f2_to_h2(lo, hi); }
+
+// c + x.lo*y.lo + x.hi*y.hi with 16-bit inputs and f32 accumulation (FHFMA)
+template <typename T> __device__ __forceinline__ float fma2h(uint32_t x, uint32_t y, float c);
+
+template <> __device__ __forceinline__ float fma2h<__nv_bfloat16>(uint32_t x, uint32_t y, float c)
+{
+    float d;
+    asm("{ .reg .b16 xl, xh, yl, yh; .reg .f32 t; mov.b32 {xl, xh}, %1; mov.b32 {yl, yh}, %2;\n\t"
+        "fma.rn.f32.bf16 t, xl, yl, %3; fma.rn.f32.bf16 %0, xh, yh, t; }"
+        : "=f"(d)
+        : "r"(x), "r"(y), "f"(c));
+    return d;
+}
+
+template <> __device__ __forceinline__ float fma2h<__half>(uint32_t x, uint32_t y, float c)
+{
+    float d;
+    asm("{ .reg .b16 xl, xh, yl, yh; .reg .f32 t; mov.b32 {xl, xh}, %1; mov.b32 {yl, yh}, %2;\n\t"
+        "fma.rn.f32.f16 t, xl, yl, %3; fma.rn.f32.f16 %0, xh, yh, t; }"
+        : "=f"(d)
+        : "r"(x), "r"(y), "f"(c));
+    return d;
+}
+
+// (o0, o1) += p * (v.lo, v.hi), p held in the low half of a 16x2 register
+template <typename T> __device__ __forceinline__ void axpy2h(uint32_t p16x2, uint32_t v, float &o0, float &o1);
+
+template <> __device__ __forceinline__ void axpy2h<__nv_bfloat16>(uint32_t p, uint32_t v, float &o0, float &o1)
+{
+    asm("{ .reg .b16 pl, ph, vl, vh; mov.b32 {pl, ph}, %2; mov.b32 {vl, vh}, %3;\n\t"
+        "fma.rn.f32.bf16 %0, pl, vl, %0; fma.rn.f32.bf16 %1, pl, vh, %1; }"
+        : "+f"(o0), "+f"(o1)
+        : "r"(p), "r"(v));
+}
+
+template <> __device__ __forceinline__ void axpy2h<__half>(uint32_t p, uint32_t v, float &o0, float &o1)
+{
+    asm("{ .reg .b16 pl, ph, vl, vh; mov.b32 {pl, ph}, %2; mov.b32 {vl, vh}, %3;\n\t"
+        "fma.rn.f32.f16 %0, pl, vl, %0; fma.rn.f32.f16 %1, pl, vh, %1; }"
+        : "+f"(o0), "+f"(o1)
+        : "r"(p), "r"(v));
+}
+
+// Running flash-attention state of one warp's 16 rows in the m16n8 accumulator layout:
+// lane (g = lane/4, t4 = lane%4) owns rows g and g+8 and dims 8j + 2*t4 + {0,1}.
+template <typename T, int D> struct MmaRows {
+    using G = Geo<D>;
+    uint32_t qa[G::KS][4]; // A fragments of the 16 query rows
+    float o[G::NB8][4];
+    float mr[2], lr[2];     // reference max (exp2 domain) and per-lane partial sums
+
+    __device__ __forceinline__ void load_q(uint32_t sQ, int row0, int lane)
+    {
+#pragma unroll
+        for (int kk = 0; kk < G::KS; ++kk) {
+            const int row = row0 + (lane & 7) + ((lane >> 3) & 1) * 8;
+            const int chk = 2 * kk + (lane >> 4);
+            ldsm_x4(sQ + swz<D>(row, chk), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+        }
+    }
+
+    __device__ __forceinline__ void init_empty()
+    {
+        mr[0] = mr[1] = -INFINITY;
+        lr[0] = lr[1] = 0.f;
+#pragma unroll
+        for (int j = 0; j < G::NB8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    }
+
+    // One fully dense block of 16 keys whose rows start at kaddr/vaddr (per-lane ldmatrix
+    // addresses prepared by the caller: kaddr[kk] for chunk 2kk + ((lane>>3)&1) of key row
+    // (lane&7) + (lane>>4)*8, vaddr[jj] for chunk 2jj + (lane>>4) of key row
+    // (lane&7) + ((lane>>3)&1)*8).
+    __device__ __forceinline__ void block16(const uint32_t *kaddr, const uint32_t *vaddr, uint32_t off, float sl2)
+    {
+        float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int kk = 0; kk < G::KS; ++kk) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(kaddr[kk] + off, b0, b1, b2, b3);
+            mma16816<T>(s[0], qa[kk], b0, b1);
+            mma16816<T>(s[1], qa[kk], b2, b3);
+        }
+        // lazy rescale: keep the reference max unless a score exceeds it by more than 2^kTau
+        // (exact: l and O share the reference; weights stay <= 2^kTau); the common case
+        // needs only per-lane maxima and one warp vote.
+        constexpr float kTau = 8.f;
+        const float lm0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
+        const float lm1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+        const bool need = lm0 * sl2 > mr[0] + kTau || lm1 * sl2 > mr[1] + kTau;
+        if (__any_sync(0xffffffffu, need)) {
+            float bm0 = fmaxf(lm0, __shfl_xor_sync(0xffffffffu, lm0, 1));
+            bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
+            float bm1 = fmaxf(lm1, __shfl_xor_sync(0xffffffffu, lm1, 1));
+            bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
+            const float mn0 = fmaxf(mr[0], bm0 * sl2), mn1 = fmaxf(mr[1], bm1 * sl2);
+            const float a0s = ex2(mr[0] - mn0), a1s = ex2(mr[1] - mn1);
+            lr[0] *= a0s;
+            lr[1] *= a1s;
+#pragma unroll
+            for (int j = 0; j < G::NB8; ++j) {
+                o[j][0] *= a0s;
+                o[j][1] *= a0s;
+                o[j][2] *= a1s;
+                o[j][3] *= a1s;
+            }
+            mr[0] = mn0;
+            mr[1] = mn1;
+        }
+        float pp[2][4];
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) {
+            pp[nb][0] = ex2(fmaf(s[nb][0], sl2, -mr[0]));
+            pp[nb][1] = ex2(fmaf(s[nb][1], sl2, -mr[0]));
+            pp[nb][2] = ex2(fmaf(s[nb][2], sl2, -mr[1]));
+            pp[nb][3] = ex2(fmaf(s[nb][3], sl2, -mr[1]));
+            lr[0] += pp[nb][0] + pp[nb][1];
+            lr[1] += pp[nb][2] + pp[nb][3];
+        }
+        uint32_t pa[4];
+        pa[0] = pack2<T>(pp[0][0], pp[0][1]);
+        pa[1] = pack2<T>(pp[0][2], pp[0][3]);
+        pa[2] = pack2<T>(pp[1][0], pp[1][1]);
+        pa[3] = pack2<T>(pp[1][2], pp[1][3]);
+#pragma unroll
+        for (int jj = 0; jj < G::NB8 / 2; ++jj) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(vaddr[jj] + off, b0, b1, b2, b3);
+            mma16816<T>(o[2 * jj], pa, b0, b1);
+            mma16816<T>(o[2 * jj + 1], pa, b2, b3);
+        }
+    }
+
+    // sum the per-lane partial l over the quad
+    __device__ __forceinline__ void reduce_l()
+    {
+        lr[0] += __shfl_xor_sync(0xffffffffu, lr[0], 1);
+        lr[0] += __shfl_xor_sync(0xffffffffu, lr[0], 2);
+        lr[1] += __shfl_xor_sync(0xffffffffu, lr[1], 1);
+        lr[1] += __shfl_xor_sync(0xffffffffu, lr[1], 2);
+    }
+};
+
+} // namespace tc
+} // namespace ga

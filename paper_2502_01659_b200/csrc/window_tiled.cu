@@ -195,18 +195,25 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
     const int H = p.H;
     const int64_t r = bp.r, m = bp.m, L = p.mask.L;
 
-    const int64_t ch = (int64_t)blockIdx.x % (r * H);
+    // CTA geometry (32-bit divisions: the grid and r*H fit in 32 bits; 64-bit only for
+    // sequences beyond 2^31 tokens)
+    const uint32_t rH = (uint32_t)(r * H), bid = blockIdx.x;
+    const uint32_t ch = bid % rH;
     // tile order: the tiles at both sequence ends (clipped bands, predicated paths) run first
-    const int64_t ord = (int64_t)blockIdx.x / (r * H);
+    const int64_t ord = bid / rH;
     const int64_t nb = imin(bp.edge_tiles, bp.tiles / 2);
     const int64_t tile = ord < nb ? ord : ord < 2 * nb ? bp.tiles - 1 - (ord - nb) : ord - nb;
-    const int64_t c = ch / H;
-    const int h = (int)(ch % H);
+    const int64_t c = ch / (uint32_t)H;
+    const int h = (int)(ch - (uint32_t)c * (uint32_t)H);
     if (c >= L) return;
-    const int64_t Nc = (L - c + r - 1) / r; // class rows in [0, L)
     const int64_t q_end = p.q_begin + p.q_rows;
-    const int64_t a_lo = p.q_begin > c ? (p.q_begin - c + r - 1) / r : 0;
-    const int64_t a_hi = q_end > c ? imin((q_end - c + r - 1) / r, Nc) : 0;
+    auto cdiv = [&](int64_t a) -> int64_t { // ceil(a / r) for a >= 0
+        if (a < (int64_t)0x7fffffff) return (int64_t)(((uint32_t)a + (uint32_t)r - 1u) / (uint32_t)r);
+        return (a + r - 1) / r;
+    };
+    const int64_t Nc = cdiv(L - c); // class rows in [0, L)
+    const int64_t a_lo = p.q_begin > c ? cdiv(p.q_begin - c) : 0;
+    const int64_t a_hi = q_end > c ? imin(cdiv(q_end - c), Nc) : 0;
     // tiles are anchored at absolute class-row multiples of ROWS, so a query-range shard
     // aligned to ROWS*r tokens computes every row exactly as the unsharded launch does
     const int64_t a0 = (a_lo / ROWS) * ROWS + tile * ROWS;
@@ -236,22 +243,25 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
     const char *Kg = reinterpret_cast<const char *>(p.K) + (size_t)h * D * sizeof(T);
     const char *Vg = reinterpret_cast<const char *>(p.V) + (size_t)h * D * sizeof(T);
     const int ld_lo = (int)(imax(0, v_lo - m) - base), ld_hi = (int)(imin(Nc - 1, v_hi - 1 + m) - base) + 1;
+    // band row `row` (class row base+row, token c + (base+row)*r) starts at band0 + row*rstride;
+    // the pointers are formed for in-range rows only (base may be negative for clipped tiles)
+    const uint32_t rstride = (uint32_t)(r * row_bytes); // < 4 GB: one 32x32->64 multiply per row
+    const int64_t band_tok0 = c + base * r - p.kv_begin;
     auto load_band = [&](int r0, int r1) {
         r0 = max(r0, ld_lo);
         r1 = min(r1, ld_hi);
         for (int idx = r0 * G::NC + tid; idx < r1 * G::NC; idx += THREADS) {
             const int row = idx / G::NC, cc = idx % G::NC;
-            const int64_t j = c + (base + row) * r;
-            const size_t off = (size_t)(j - p.kv_begin) * row_bytes + cc * 16;
+            const int64_t off = band_tok0 * (int64_t)row_bytes + (int64_t)((uint64_t)(uint32_t)row * rstride) + cc * 16;
             cp_async16(sK + swz<D>(row, cc), Kg + off);
             cp_async16(sV + swz<D>(row, cc), Vg + off);
         }
     };
-    for (int idx = tid; idx < ROWS * G::NC; idx += THREADS) {
+    const char *Qt = Qg + (c + a0 * r - p.q_begin) * (int64_t)row_bytes;
+    const int q_lo = (int)(v_lo - a0), q_hi = (int)(v_hi - a0);
+    for (int idx = q_lo * G::NC + tid; idx < q_hi * G::NC; idx += THREADS) {
         const int row = idx / G::NC, cc = idx % G::NC;
-        if (a0 + row < v_lo || a0 + row >= v_hi) continue;
-        const int64_t i = c + (a0 + row) * r;
-        cp_async16(sQ + swz<D>(row, cc), Qg + (size_t)(i - p.q_begin) * row_bytes + cc * 16);
+        cp_async16(sQ + swz<D>(row, cc), Qt + (int64_t)((uint64_t)(uint32_t)row * rstride) + cc * 16);
     }
     // stage 0: rows the CUDA-core phase reads (ends of the band); stage 1: the dense middle,
     // which lands while the CUDA-core phase runs

@@ -90,6 +90,7 @@ def test_paper_protocol_random_csr(ga, orc, seed):
 CASES = [
     ("window", 1031, (33, 1)), ("window", 1500, (64, 2)), ("window", 777, (200, 3)),
     ("block", 1000, (64, 2)), ("longnet", 2048, (64, 2)), ("longnet", 1800, (27, 3)),
+    ("longnet", 3000, (100, 3)),
 ]
 
 
@@ -138,6 +139,25 @@ def test_band_kernel_cfg2_shape(ga, orc):
     with pytest.raises(ga.GaError, match="UNSUPPORTED"):
         q32 = torch.zeros(64, 1, 64, device="cuda")
         ga.attention(q32, q32.clone(), q32.clone(), ga.Window(32), kernel="window")
+
+
+@pytest.mark.parametrize("L,w0,alpha", [(8192, 64, 2), (5000, 100, 3), (4096, 16, 2), (3000, 2048, 2),
+                                         (6561, 27, 3), (10000, 40, 4)])
+@pytest.mark.parametrize("dt,d", [("bf16", 64), ("f16", 64), ("bf16", 32), ("bf16", 128)])
+def test_longnet_tiled_vs_oracle(ga, orc, L, w0, alpha, dt, d):
+    """LongNet dense-group tensor-core kernel (forced) vs the oracle; covers ragged key
+    tails (w0 not a multiple of 16), alpha in {2,3,4}, a single partial segment, and a
+    query-range shard (q_begin > 0 with the full K/V)."""
+    H = 2
+    cpu, f64 = _inputs(L, H, d, dt, L + w0, centred=True)
+    om = orc.longnet(L, w0, alpha)
+    want, _ = orc.attention(*f64, om)
+    got = _run(ga, cpu, ga.LongNet(w0, alpha), kernel="tiled")
+    assert np.abs(got - want).max() <= TOL[dt]
+    q, k, v = (x.cuda() for x in cpu)
+    r0, r1 = L // 3, L // 3 + L // 4
+    part = ga.attention(q[r0:r1].contiguous(), k, v, ga.LongNet(w0, alpha), L=L, q_begin=r0, kernel="tiled")
+    assert np.abs(part.double().cpu().numpy() - want[r0:r1]).max() <= TOL[dt]
 
 
 @pytest.mark.parametrize("dt", ["f32", "bf16"])

@@ -33,6 +33,8 @@ def _run_enum(binary, kind, L, a, b):
     (1, 300, 17, 1), (1, 300, 40, 3), (1, 50, 200, 2), (1, 1, 1, 1),
     (4, 257, 16, 3), (4, 100, 100, 1),
     (2, 256, 16, 2), (2, 243, 9, 3), (2, 200, 16, 2), (2, 1000, 8, 4), (2, 50, 64, 2), (2, 4096, 64, 2),
+    # alpha does not divide w0: level-t segment starts are not multiples of alpha^(t+1)
+    (2, 5000, 100, 3), (2, 999, 7, 2), (2, 3000, 10, 4), (2, 4000, 5, 3),
 ])
 def test_enumerator_matches_oracle(orc, enum_bin, kind, L, a, b):
     if kind == 1:
@@ -101,7 +103,7 @@ int main() {
     ("window", 1024, (32, 1)), ("window", 65536, (256, 2)), ("window", 777, (100, 7)), ("window", 10, (50, 1)),
     ("block", 1000, (64, 3)), ("block", 999, (10, 1)),
     ("longnet", 4096, (64, 2)), ("longnet", 5000, (64, 2)), ("longnet", 2187, (27, 3)), ("longnet", 300, (512, 2)),
-    ("longnet", 12345, (16, 4)),
+    ("longnet", 12345, (16, 4)), ("longnet", 5000, (100, 3)), ("longnet", 999, (7, 2)), ("longnet", 3000, (10, 4)),
     ("bigbird", 1024, (8, 4, 4)), ("bigbird", 3000, (64, 7, 20)), ("bigbird", 64, (30, 2, 50)),
 ])
 def test_host_mask_count_equals_oracle(orc, spec):
