@@ -39,10 +39,10 @@ struct LParams {
 
 template <int D> __host__ __device__ constexpr uint32_t smem_bytes()
 {
+    static_assert(WARPS * 16 * (D + 2) * 4 <= 4 * KC * Geo<D>::RB, "scratch must fit the stages");
     return (uint32_t)(ROWS * Geo<D>::RB               // Q tile / output staging
-                      + 2 * 2 * KC * Geo<D>::RB        // K and V, two stages
-                      + WARPS * 16 * (D + 2) * 4       // split-merge scratch
-                      + ROWS * 8 + 64);                // row list + counters
+                      + 2 * 2 * KC * Geo<D>::RB        // K and V, two stages (then scratch)
+                      + ROWS * 8);                     // row list
 }
 
 template <typename T, int D>
@@ -55,12 +55,13 @@ __global__ void __launch_bounds__(THREADS) longnet_kernel(const LParams lp)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int H = p.H;
 
-    // ---- work item: segment fastest, so the heavy (high-s) items of all segments run first
-    const int64_t HB = (int64_t)lp.n_seg * H;
-    const int64_t item = (int64_t)blockIdx.x / HB;
-    const int64_t rem = (int64_t)blockIdx.x - item * HB;
-    const int64_t segl = rem / H;
-    const int h = (int)(rem - segl * H);
+    // ---- work item: segment-major (a segment's groups share its level-0 keys, so they run
+    // together while those K/V rows are in L2), heaviest group first within a segment
+    const int64_t IH = (int64_t)lp.n_items * H;
+    const int64_t segl = (int64_t)blockIdx.x / IH;
+    const int64_t rem = (int64_t)blockIdx.x - segl * IH;
+    const int64_t item = rem / H;
+    const int h = (int)(rem - item * H);
     const int64_t seg = lp.seg0 + segl;
     const int s = lp.item_s[item], tile = lp.item_tile[item];
     const int64_t S0 = seg * M.w0, S1 = imin(M.L, S0 + M.w0);
@@ -70,50 +71,48 @@ __global__ void __launch_bounds__(THREADS) longnet_kernel(const LParams lp)
     const uint32_t sQ = sbase;
     const uint32_t sK0 = sQ + ROWS * G::RB;                 // stage st: sK0 + st*KC*RB
     const uint32_t sV0 = sK0 + 2 * KC * G::RB;
-    float *scratch = reinterpret_cast<float *>(smem + ROWS * G::RB + 4 * KC * G::RB);
-    int64_t *rows = reinterpret_cast<int64_t *>(reinterpret_cast<unsigned char *>(scratch) + WARPS * 16 * (D + 2) * 4);
-    int *counters = reinterpret_cast<int *>(rows + ROWS);
+    // split-merge / ragged-tail scratch aliases the K/V stages (used only after the key loop)
+    float *scratch = reinterpret_cast<float *>(smem + ROWS * G::RB);
+    int64_t *rows = reinterpret_cast<int64_t *>(smem + ROWS * G::RB + 4 * KC * G::RB);
 
-    // ---- rows of G(seg, s) inside the query range, ranks [64*tile, 64*tile + 64)
-    // candidates are the multiples of a^s in the segment (nu(i) >= s); keep min(nu, K) == s
+    // ---- rows of G(seg, s) inside the query range, ranks [64*tile, 64*tile + 64), in closed
+    // form: candidates are the multiples i = a^s (f0 + q) in [lo, hi); for s < K the group
+    // keeps those with a !| (f0 + q) (one excluded residue of q, as in a SKIPMUL piece) —
+    // except i = 0, whose valuation is K by convention; for s = K it keeps every candidate.
     int64_t step = 1;
     for (int t = 0; t < s; ++t) step *= M.alpha;
-    const int64_t first = ((S0 + step - 1) / step) * step;
-    const int64_t ncand = first < S1 ? (S1 - 1 - first) / step + 1 : 0;
-    if (tid == 0) counters[0] = 0;
-    __syncthreads();
-    int base_rank = 0;
-    for (int64_t c0 = 0; c0 < ncand; c0 += THREADS) {
-        const int64_t i = first + (c0 + tid) * step;
-        bool ok = c0 + tid < ncand && i >= p.q_begin && i < q_end;
-        if (ok) ok = valuation(i, M.alpha, M.K) == s;
-        const unsigned bal = __ballot_sync(0xffffffffu, ok);
-        if (lane == 0) counters[1 + warp] = __popc(bal);
-        __syncthreads();
-        int before = base_rank;
-        for (int w = 0; w < warp; ++w) before += counters[1 + w];
-        int total = 0;
-        for (int w = 0; w < WARPS; ++w) total += counters[1 + w];
-        const int rank = before + __popc(bal & ((1u << lane) - 1u));
-        if (ok && rank >= tile * ROWS && rank < (tile + 1) * ROWS) rows[rank - tile * ROWS] = i;
-        base_rank += total;
-        __syncthreads();
-        if (base_rank >= (tile + 1) * ROWS) break;
-    }
-    const int nrows = min(ROWS, base_rank - tile * ROWS);
+    const int64_t lo = imax(S0, p.q_begin), hi = imin(S1, q_end);
+    const int64_t f0 = (lo + step - 1) / step;
+    const int64_t nq = lo < hi && f0 * step < hi ? (hi - 1) / step - f0 + 1 : 0;
+    const bool top = s == (int)M.K;
+    const int64_t rx = (M.alpha - f0 % M.alpha) % M.alpha; // excluded residue of q (s < K)
+    // i = 0 (valuation K) sits at q = 0 when f0 == 0; its residue is the excluded one, so the
+    // s < K groups drop it automatically and the s = K group keeps it
+    const int64_t count = top ? nq : nq - (nq > rx ? (nq - 1 - rx) / M.alpha + 1 : 0);
+    const int nrows = (int)imin(ROWS, count - (int64_t)tile * ROWS);
     if (nrows <= 0) return;
+    if (tid < nrows) {
+        const int64_t r = (int64_t)tile * ROWS + tid;
+        int64_t q = r;
+        if (!top) {
+            const int64_t a1 = M.alpha - 1, idx = r % a1;
+            q = (r / a1) * M.alpha + (idx < rx ? idx : idx + 1);
+        }
+        rows[tid] = (f0 + q) * step;
+    }
+    __syncthreads();
 
     // ---- neighbour pieces shared by the whole group (masks.cuh), from a representative row,
     // cached in shared memory with their prefix offsets
     __shared__ Piece spiece[MAX_PIECES];
-    __shared__ int64_t pstart[MAX_PIECES + 1];
+    __shared__ int pstart[MAX_PIECES + 1]; // key offsets of the pieces (a group has < 2^31 keys)
     const int64_t irep = rows[0];
     const int np = s + 1;
     if (tid < np) spiece[tid] = get_piece(M, irep, tid);
     __syncthreads();
     if (tid == 0) {
         pstart[0] = 0;
-        for (int t = 0; t < np; ++t) pstart[t + 1] = pstart[t] + spiece[t].count;
+        for (int t = 0; t < np; ++t) pstart[t + 1] = pstart[t] + (int)spiece[t].count;
     }
     __syncthreads();
     const int64_t nkeys = pstart[np];
@@ -126,17 +125,20 @@ __global__ void __launch_bounds__(THREADS) longnet_kernel(const LParams lp)
     const char *Kg = reinterpret_cast<const char *>(p.K) + (size_t)h * D * sizeof(T);
     const char *Vg = reinterpret_cast<const char *>(p.V) + (size_t)h * D * sizeof(T);
 
-    auto key_token = [&](int64_t k) -> int64_t { // k-th key of the concatenated pieces
+    auto key_token = [&](int k) -> int64_t { // k-th key of the concatenated pieces
         int t = 0;
         while (t + 1 < np && pstart[t + 1] <= k) ++t;
         return piece_at(spiece[t], k - pstart[t]);
     };
+    // per-thread piece cursor: a thread's key index only grows (by KC per stage)
+    int cur_t = 0;
     auto load_chunk = [&](int64_t c, int st) {
         // 2 threads per key: each moves half of the K row and half of the V row
         const int kl = tid >> 1, hf = tid & 1;
-        const int64_t k = c * KC + kl;
+        const int k = (int)(c * KC) + kl;
         if (k < nblk * 16) {
-            const size_t off = (size_t)(key_token(k) - p.kv_begin) * row_bytes;
+            while (cur_t + 1 < np && pstart[cur_t + 1] <= k) ++cur_t;
+            const size_t off = (size_t)(piece_at(spiece[cur_t], k - pstart[cur_t]) - p.kv_begin) * row_bytes;
 #pragma unroll
             for (int q = 0; q < G::HC; ++q) {
                 const int cc = hf * G::HC + q;
@@ -169,8 +171,38 @@ __global__ void __launch_bounds__(THREADS) longnet_kernel(const LParams lp)
     __syncthreads();
     if (active) st.load_q(sQ, slice * 16, lane);
 
+    // per-lane ldmatrix addresses inside a stage (block b of the stage adds b*16 rows)
+    uint32_t kaddr[G::KS], vaddr[G::NB8 / 2];
+    {
+        const int krow = (lane & 7) + (lane >> 4) * 8, vrow = (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+        for (int kk = 0; kk < G::KS; ++kk) kaddr[kk] = sK0 + swz<D>(krow, 2 * kk + ((lane >> 3) & 1));
+#pragma unroll
+        for (int jj = 0; jj < G::NB8 / 2; ++jj) vaddr[jj] = sV0 + swz<D>(vrow, 2 * jj + (lane >> 4));
+    }
+
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int stg = (int)(c & 1);
+        if (c > 0) { // chunk c landed (one younger group may still be in flight)
+            cp_async_wait<1>();
+            __syncthreads();
+        }
+        if (active) {
+            const int blocks_here = (int)imin(KC / 16, nblk - c * (KC / 16));
+            const uint32_t soff = (uint32_t)(stg * KC * G::RB);
+            int b = split;
+            for (; b + P < blocks_here; b += 2 * P) // pairs: one vote and one rescale check
+                st.block16x2(kaddr, vaddr, soff + b * 16 * G::RB, soff + (b + P) * 16 * G::RB, sl2);
+            if (b < blocks_here) st.block16(kaddr, vaddr, soff + b * 16 * G::RB, sl2);
+        }
+        __syncthreads(); // stage stg free
+        if (c + 2 < nchunks) load_chunk(c + 2, stg);
+        cp_async_commit();
+    }
+    cp_async_wait<0>();
     // ragged tail (< 16 keys, every one valid for every row): CUDA cores, two lanes per row,
-    // folded into the MMA state through this warp's scratch (split 0 only)
+    // merged into the MMA state through this warp's scratch (split 0 only; the scratch
+    // aliases the now idle K/V stages)
     if (ragged > 0 && active && split == 0) {
         const int x = lane >> 1, hf = lane & 1;
         const bool row_ok = slice * 16 + x < nrows;
@@ -225,46 +257,24 @@ __global__ void __launch_bounds__(THREADS) longnet_kernel(const LParams lp)
         __syncwarp();
         const int g = lane >> 2, t4 = lane & 3;
         const float *r0 = scratch + warp * 16 * (D + 2) + g * (D + 2), *r1 = r0 + 8 * (D + 2);
-        st.mr[0] = r0[0];
-        st.mr[1] = r1[0];
-        st.lr[0] = t4 == 0 ? r0[1] : 0.f;
-        st.lr[1] = t4 == 0 ? r1[1] : 0.f;
 #pragma unroll
-        for (int j = 0; j < G::NB8; ++j) {
-            st.o[j][0] = r0[2 + 8 * j + 2 * t4];
-            st.o[j][1] = r0[2 + 8 * j + 2 * t4 + 1];
-            st.o[j][2] = r1[2 + 8 * j + 2 * t4];
-            st.o[j][3] = r1[2 + 8 * j + 2 * t4 + 1];
+        for (int hr = 0; hr < 2; ++hr) { // (m,l,o) (+) (m2,l2,o2)
+            const float *rw = hr == 0 ? r0 : r1;
+            const float m2 = rw[0], l2 = t4 == 0 ? rw[1] : 0.f;
+            const float mn = fmaxf(st.mr[hr], m2);
+            const float a = st.mr[hr] == -INFINITY ? 0.f : ex2(st.mr[hr] - mn);
+            const float b = m2 == -INFINITY ? 0.f : ex2(m2 - mn);
+            st.lr[hr] = st.lr[hr] * a + l2 * b;
+#pragma unroll
+            for (int j = 0; j < G::NB8; ++j) {
+                st.o[j][2 * hr] = st.o[j][2 * hr] * a + rw[2 + 8 * j + 2 * t4] * b;
+                st.o[j][2 * hr + 1] = st.o[j][2 * hr + 1] * a + rw[2 + 8 * j + 2 * t4 + 1] * b;
+            }
+            st.mr[hr] = mn;
         }
         __syncwarp();
     }
 
-    // per-lane ldmatrix addresses inside a stage (block b of the stage adds b*16 rows)
-    uint32_t kaddr[G::KS], vaddr[G::NB8 / 2];
-    {
-        const int krow = (lane & 7) + (lane >> 4) * 8, vrow = (lane & 7) + ((lane >> 3) & 1) * 8;
-#pragma unroll
-        for (int kk = 0; kk < G::KS; ++kk) kaddr[kk] = sK0 + swz<D>(krow, 2 * kk + ((lane >> 3) & 1));
-#pragma unroll
-        for (int jj = 0; jj < G::NB8 / 2; ++jj) vaddr[jj] = sV0 + swz<D>(vrow, 2 * jj + (lane >> 4));
-    }
-
-    for (int64_t c = 0; c < nchunks; ++c) {
-        const int stg = (int)(c & 1);
-        if (c > 0) { // chunk c landed (one younger group may still be in flight)
-            cp_async_wait<1>();
-            __syncthreads();
-        }
-        if (active) {
-            const int64_t blocks_here = imin(KC / 16, nblk - c * (KC / 16));
-            for (int b = split; b < blocks_here; b += P)
-                st.block16(kaddr, vaddr, (uint32_t)(stg * KC * G::RB + b * 16 * G::RB), sl2);
-        }
-        __syncthreads(); // stage stg free
-        if (c + 2 < nchunks) load_chunk(c + 2, stg);
-        cp_async_commit();
-    }
-    cp_async_wait<0>();
 
     // ---- merge key splits, normalise, stage through the Q rows, store
     const int g = lane >> 2, t4 = lane & 3;

@@ -213,6 +213,81 @@ template <typename T, int D> struct MmaRows {
         }
     }
 
+    // Two dense 16-key blocks at offsets off0 and off1: both S tiles first (16 independent
+    // MMAs), one max/vote for the pair, then both P V updates — half the serialisation
+    // points of two block16 calls.
+    __device__ __forceinline__ void block16x2(const uint32_t *kaddr, const uint32_t *vaddr, uint32_t off0,
+                                              uint32_t off1, float sl2)
+    {
+        float s[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s[q][0] = s[q][1] = s[q][2] = s[q][3] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < G::KS; ++kk) {
+            uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
+            ldsm_x4(kaddr[kk] + off0, b0, b1, b2, b3);
+            ldsm_x4(kaddr[kk] + off1, c0, c1, c2, c3);
+            mma16816<T>(s[0], qa[kk], b0, b1);
+            mma16816<T>(s[1], qa[kk], b2, b3);
+            mma16816<T>(s[2], qa[kk], c0, c1);
+            mma16816<T>(s[3], qa[kk], c2, c3);
+        }
+        constexpr float kTau = 8.f;
+        float lm0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
+        float lm1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+        lm0 = fmaxf(lm0, fmaxf(fmaxf(s[2][0], s[2][1]), fmaxf(s[3][0], s[3][1])));
+        lm1 = fmaxf(lm1, fmaxf(fmaxf(s[2][2], s[2][3]), fmaxf(s[3][2], s[3][3])));
+        const bool need = lm0 * sl2 > mr[0] + kTau || lm1 * sl2 > mr[1] + kTau;
+        if (__any_sync(0xffffffffu, need)) {
+            float bm0 = fmaxf(lm0, __shfl_xor_sync(0xffffffffu, lm0, 1));
+            bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
+            float bm1 = fmaxf(lm1, __shfl_xor_sync(0xffffffffu, lm1, 1));
+            bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
+            const float mn0 = fmaxf(mr[0], bm0 * sl2), mn1 = fmaxf(mr[1], bm1 * sl2);
+            const float a0s = ex2(mr[0] - mn0), a1s = ex2(mr[1] - mn1);
+            lr[0] *= a0s;
+            lr[1] *= a1s;
+#pragma unroll
+            for (int j = 0; j < G::NB8; ++j) {
+                o[j][0] *= a0s;
+                o[j][1] *= a0s;
+                o[j][2] *= a1s;
+                o[j][3] *= a1s;
+            }
+            mr[0] = mn0;
+            mr[1] = mn1;
+        }
+        uint32_t pa[2][4];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+            float pp[2][4];
+#pragma unroll
+            for (int nb = 0; nb < 2; ++nb) {
+                const float *sv = s[2 * h2 + nb];
+                pp[nb][0] = ex2(fmaf(sv[0], sl2, -mr[0]));
+                pp[nb][1] = ex2(fmaf(sv[1], sl2, -mr[0]));
+                pp[nb][2] = ex2(fmaf(sv[2], sl2, -mr[1]));
+                pp[nb][3] = ex2(fmaf(sv[3], sl2, -mr[1]));
+                lr[0] += pp[nb][0] + pp[nb][1];
+                lr[1] += pp[nb][2] + pp[nb][3];
+            }
+            pa[h2][0] = pack2<T>(pp[0][0], pp[0][1]);
+            pa[h2][1] = pack2<T>(pp[0][2], pp[0][3]);
+            pa[h2][2] = pack2<T>(pp[1][0], pp[1][1]);
+            pa[h2][3] = pack2<T>(pp[1][2], pp[1][3]);
+        }
+#pragma unroll
+        for (int jj = 0; jj < G::NB8 / 2; ++jj) {
+            uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
+            ldsm_x4_t(vaddr[jj] + off0, b0, b1, b2, b3);
+            ldsm_x4_t(vaddr[jj] + off1, c0, c1, c2, c3);
+            mma16816<T>(o[2 * jj], pa[0], b0, b1);
+            mma16816<T>(o[2 * jj + 1], pa[0], b2, b3);
+            mma16816<T>(o[2 * jj], pa[1], c0, c1);
+            mma16816<T>(o[2 * jj + 1], pa[1], c2, c3);
+        }
+    }
+
     // sum the per-lane partial l over the quad
     __device__ __forceinline__ void reduce_l()
     {
