@@ -172,6 +172,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--max-context", action="store_true",
+                    help="measure the largest Window(128) bf16 sequence that fits (one step + sampled parity)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
@@ -184,6 +186,8 @@ def main():
 
     if args.impl == "reference":
         return reference_arm(args, cfg, world, rank)
+    if args.max_context:
+        return max_context(args, world, rank, local_rank)
 
     import torch
     import torch.distributed as dist
@@ -221,9 +225,28 @@ def main():
                 gdist.sharded_window_attention(q, buf, mask, L, out=out, comm_stream=comm)
             else:
                 ga.attention(q, buf.k, buf.v, mask, out, kernel=args.kernel)
+        e2e_targets = [q, buf.local_k, buf.local_v]
+    elif kind == "longnet" and world > 1:
+        # weak scaling: rank owns rows [r0, r1) of an N*L sequence; full-length K/V buffers hold
+        # the local rows plus, each step, the strided rows gathered from the other ranks
+        mask = ga.LongNet(a[0], a[1])
+        nnz = ga.mask_count(mask, L)
+        stride = gdist.longnet_exchange_stride(L, a[0], a[1], L_local)
+        q = torch.empty((L_local, H, d), dtype=tdt, device=dev)
+        kf = torch.zeros((L, H, d), dtype=tdt, device=dev)
+        vf = torch.zeros_like(kf)
+        ga.fill_inputs(q, seed, 0, r0 * H * d)
+        ga.fill_inputs(kf[r0:r1], seed, 1, r0 * H * d)
+        ga.fill_inputs(vf[r0:r1], seed, 2, r0 * H * d)
+        out = torch.empty_like(q)
+
+        def step():
+            gdist.exchange_longnet(kf, vf, r0, r1, stride)
+            ga.attention(q, kf, vf, mask, out, L=L, q_begin=r0, kv_begin=0, kernel=args.kernel)
+        e2e_targets = [q, kf[r0:r1], vf[r0:r1]]
     else:
         if world > 1:
-            raise SystemExit(f"--gpus > 1 is implemented for window masks (cfg2/cfg5); {args.config} is 1-GPU")
+            raise SystemExit(f"--gpus > 1 is implemented for window (cfg2/cfg5) and LongNet (cfg4) masks")
         if kind == "bigbird":
             mask = ga.mask_to_csr(ga.BigBird(a[0], a[1], a[2], seed=BIGBIRD_SEED), L)
             nnz = mask.nnz
@@ -236,6 +259,7 @@ def main():
 
         def step():
             ga.attention(q, k, v, mask, out, kernel=args.kernel, workspace=ws)
+        e2e_targets = [q, k, v]
 
     edges_total = nnz * H  # all ranks together (global mask over the N*L sequence)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
@@ -278,8 +302,10 @@ def main():
     # ---- end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e(args, ga, gdist, cfg, mask, world, rank, r0, L, H, d, tdt, seed, dev, edges_total,
-                          buf if kind == "window" else None, ws)
+        c_abi = None
+        if world == 1 and kind != "bigbird":
+            c_abi = (mask, q.cpu().pin_memory(), e2e_targets[1].cpu().pin_memory(), e2e_targets[2].cpu().pin_memory())
+        e2e = measure_e2e(args, ga, world, dev, edges_total, e2e_targets, step, out, c_abi)
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None
@@ -356,101 +382,121 @@ def roofline_for(args, cfg, kind, head_edges, L_local, H, d, nnz, per_step):
     return roof, gather
 
 
-def measure_e2e(args, ga, gdist, cfg, mask, world, rank, r0, L, H, d, tdt, seed, dev, edges_total, buf, ws):
-    """Same metric through the public API with pinned HOST buffers: H2D of the step's
-    inputs and D2H of its output inside the timed region."""
+def measure_e2e(args, ga, world, dev, edges_total, targets, run_step, out, c_abi=None):
+    """The same metric end to end with pinned HOST buffers: every step copies this step's
+    inputs host -> device (`targets`: the device tensors the step reads), runs the step, and
+    copies the output device -> host, all inside the timed region.  At N=1 with an implicit
+    mask (`c_abi` = (mask, host q, k, v)) the step is one ga_attention_host call (C ABI with
+    host buffers, copies inside libga)."""
     import torch
     import torch.distributed as dist
 
-    import synth
-
-    L_local = cfg["L"]
-    n = L_local * H * d
     steps = max(3, min(args.steps, 5))
-    if world == 1 and cfg["mask"][0] == "window":
-        host = []
-        for t in range(3):  # generate on device, stage in pinned host memory (setup, untimed)
-            x = torch.empty((L_local, H, d), dtype=tdt, device=dev)
-            ga.fill_inputs(x, seed, t)
-            host.append(x.cpu().pin_memory())
-        hout = torch.empty_like(host[0]).pin_memory()
+    if c_abi is not None:
+        mask, hq, hk, hv = c_abi
+        hout = torch.empty_like(hq).pin_memory()
         s = torch.cuda.current_stream()
-        for _ in range(2):
-            ga.attention_host(*host, mask, hout, stream=s)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
-            ga.attention_host(*host, mask, hout, stream=s)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / steps
-        h2d, d2h = 3 * n * host[0].element_size(), n * host[0].element_size()
-    elif world > 1:
-        hq = torch.empty((L_local, H, d), dtype=tdt).pin_memory()
-        hk, hv = torch.empty_like(hq).pin_memory(), torch.empty_like(hq).pin_memory()
-        for h_, t in ((hq, 0), (hk, 1), (hv, 2)):
-            x = torch.empty((L_local, H, d), dtype=tdt, device=dev)
-            ga.fill_inputs(x, seed, t, r0 * H * d)
-            h_.copy_(x.cpu())
-        q = torch.empty((L_local, H, d), dtype=tdt, device=dev)
-        out = torch.empty_like(q)
-        hout = torch.empty_like(hq).pin_memory()
 
         def step():
-            q.copy_(hq, non_blocking=True)
-            buf.local_k.copy_(hk, non_blocking=True)
-            buf.local_v.copy_(hv, non_blocking=True)
-            gdist.sharded_window_attention(q, buf, mask, L, out=out)
-            hout.copy_(out, non_blocking=True)
-
-        for _ in range(2):
-            step()
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
-            step()
-        e1.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
-        h2d, d2h = 3 * n * hq.element_size(), n * hq.element_size()
+            ga.attention_host(hq, hk, hv, mask, hout, stream=s)
+        h2d = 3 * hq.numel() * hq.element_size()
+        path = "ga_attention_host (C ABI, pinned host buffers, copies inside libga)"
     else:
-        # explicit-CSR / LongNet configs: host Q,K,V copied in, output copied out each step
-        hq = torch.empty((L_local, H, d), dtype=tdt).pin_memory()
-        hk, hv = torch.empty_like(hq).pin_memory(), torch.empty_like(hq).pin_memory()
-        for h_, t in ((hq, 0), (hk, 1), (hv, 2)):
-            x = torch.empty((L_local, H, d), dtype=tdt, device=dev)
-            ga.fill_inputs(x, seed, t)
-            h_.copy_(x.cpu())
-        q, k, v = (torch.empty((L_local, H, d), dtype=tdt, device=dev) for _ in range(3))
-        out = torch.empty_like(q)
-        hout = torch.empty_like(hq).pin_memory()
+        hosts = [t.detach().cpu().pin_memory() for t in targets]
+        hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
 
         def step():
-            q.copy_(hq, non_blocking=True)
-            k.copy_(hk, non_blocking=True)
-            v.copy_(hv, non_blocking=True)
-            ga.attention(q, k, v, mask, out, workspace=ws)
+            for t, h in zip(targets, hosts):
+                t.copy_(h, non_blocking=True)
+            run_step()
             hout.copy_(out, non_blocking=True)
-
+        h2d = sum(h.numel() * h.element_size() for h in hosts)
+        path = "pinned host -> device copies + ga_attention_ex step + device -> host copy"
+    d2h = hout.numel() * hout.element_size()
+    for _ in range(2):
         step()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
-            step()
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / steps
-        h2d, d2h = 3 * n * hq.element_size(), n * hq.element_size()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
     return {"value": edges_total / (ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": h2d * world,
-            "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": steps,
-            "path": "ga_attention_host (C ABI, pinned host buffers)" if world == 1 and cfg["mask"][0] == "window"
-            else "pinned host -> device copies + ga_attention_ex + device -> host copy"}
+            "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": steps, "path": path}
+
+
+def max_context(args, world, rank, local_rank):
+    """Largest Window(128) bf16 d=64 sequence that fits in HBM: Q, K, V
+    resident and the output written over Q (one launch owns each row, so the band and edge
+    kernels allow it for implicit masks).  At N>1 every rank holds L tokens plus the halo.
+    One step runs; rows at the start, the end and the shard boundaries are checked against
+    the oracle (which regenerates them from the seed)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2502_01659_b200 as ga
+    from paper_2502_01659_b200 import dist as gdist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    H, d, w, seed = 1, 64, 128, 0x5EED0005
+    mask = ga.Window(w)
+    halo = gdist.window_halo(mask) if world > 1 else 0
+    free, total = torch.cuda.mem_get_info(dev)
+    row = H * d * 2
+    reserve = 2 << 30  # context, workspace of the runtime, halo buffers, clocks
+    L_local = int((free - reserve) // (3 * row)) - 2 * halo
+    L_local = (L_local // 224) * 224  # band-kernel tile multiple (112 rows x r=1) x 2
+    L = L_local * world
+    r0, r1 = rank * L_local, (rank + 1) * L_local
+    buf = gdist.alloc_halo(L, r0, r1, halo, H, d, torch.bfloat16, dev)
+    q = torch.empty((L_local, H, d), dtype=torch.bfloat16, device=dev)
+    ga.fill_inputs(q, seed, 0, r0 * H * d)
+    ga.fill_inputs(buf.local_k, seed, 1, r0 * H * d)
+    ga.fill_inputs(buf.local_v, seed, 2, r0 * H * d)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    if world > 1:
+        gdist.sharded_window_attention(q, buf, mask, L, out=q)
+    else:
+        ga.attention(q, buf.k, buf.v, mask, q)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    import oracle
+
+    local = np.unique(np.clip(np.concatenate([np.arange(r0, r0 + 64), np.arange(r1 - 64, r1),
+                                              np.random.default_rng(rank).integers(r0, r1, 64)]), r0, r1 - 1))
+    got = q[torch.from_numpy(local - r0).to(dev)].double().cpu().numpy()
+    want, _ = oracle.attention_seeded(seed, "bf16", oracle.window(L, w), H, d, rows=local)
+    err = torch.tensor([float(np.abs(got - want).max())], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(err, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "max context length (Window(128), bf16, d=64, 1 head; out aliased on Q)", "value": L,
+            "unit": "tokens", "n_gpus": world, "higher_is_better": True, "scaling": "weak",
+            "per_gpu_tokens": L_local, "hbm_total_bytes": total, "bytes_per_token": 3 * row,
+            "step_ms": ms.item(), "edges": ga.mask_count(mask, L),
+            "parity_max_abs_err_sampled": err.item(), "parity_ok": err.item() <= 2e-2,
+            "paper_context": "160,000,000 tokens on one A100 80GB (PAPER.md:22, :452)"}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def reference_arm(args, cfg, world, rank):

@@ -18,7 +18,7 @@
 // edges (no idle lanes).  Warps whose band is clipped by the sequence ends, or whose tile
 // is cut by the query range, use a predicated general loop for U\F.  The CUDA-core state
 // seeds the MMA phase's running (m, l, O) through a per-warp shared-memory hand-off.
-#include "edge_core.cuh"
+#include "tc_common.cuh"
 
 namespace ga {
 namespace band {
@@ -279,7 +279,11 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
 
     // A fragments of Q for the tensor-core phase, taken before the Q rows are reused
     const int g = lane >> 2, t4 = lane & 3;
-    uint32_t qa[G::KS][4];
+    tc::MmaRows<T, D> rs; // running (m, l, O) of the warp's 16 rows in the mma layout
+    auto &qa = rs.qa;
+    auto &o = rs.o;
+    auto &mr = rs.mr;
+    auto &lr = rs.lr;
     if (warp_live) {
 #pragma unroll
         for (int kk = 0; kk < G::KS; ++kk) {
@@ -288,8 +292,6 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
             ldsm_x4(sQ + swz<D>(row, chk), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
         }
     }
-    float o[G::NB8][4];
-    float mr[2], lr[2];
 
     // ================= CUDA-core phase: U\F and F's ragged tail =================
     if (warp_live) {
@@ -404,66 +406,12 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
 #pragma unroll
         for (int jj = 0; jj < G::NB8 / 2; ++jj) vaddr[jj] = sV + swz<D>(vrow, 2 * jj + (lane >> 4));
     }
-#pragma unroll 2
-    for (int b = 0; b < q16; ++b) {
-        const uint32_t boff = (uint32_t)(b * 16 * G::RB);
-        float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-        for (int kk = 0; kk < G::KS; ++kk) {
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4(kaddr[kk] + boff, b0, b1, b2, b3);
-            mma16816<T>(s[0], qa[kk], b0, b1);
-            mma16816<T>(s[1], qa[kk], b2, b3);
-        }
-        // online softmax on rows g (s[.][0..1]) and g+8 (s[.][2..3]).  Lazy rescale: keep
-        // the reference max unless a score exceeds it by more than 2^kTau (exact: l and O
-        // share the reference; weights stay <= 2^kTau, no overflow).  The common case needs
-        // only per-lane maxima and one warp vote, no shuffle reductions.
-        constexpr float kTau = 8.f;
-        const float lm0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
-        const float lm1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
-        const bool need = lm0 * sl2 > mr[0] + kTau || lm1 * sl2 > mr[1] + kTau;
-        if (__any_sync(0xffffffffu, need)) {
-            float bm0 = fmaxf(lm0, __shfl_xor_sync(0xffffffffu, lm0, 1));
-            bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
-            float bm1 = fmaxf(lm1, __shfl_xor_sync(0xffffffffu, lm1, 1));
-            bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
-            const float mn0 = fmaxf(mr[0], bm0 * sl2), mn1 = fmaxf(mr[1], bm1 * sl2);
-            const float a0s = ex2(mr[0] - mn0), a1s = ex2(mr[1] - mn1);
-            lr[0] *= a0s;
-            lr[1] *= a1s;
-#pragma unroll
-            for (int j = 0; j < G::NB8; ++j) {
-                o[j][0] *= a0s;
-                o[j][1] *= a0s;
-                o[j][2] *= a1s;
-                o[j][3] *= a1s;
-            }
-            mr[0] = mn0;
-            mr[1] = mn1;
-        }
-        float pp[2][4];
-#pragma unroll
-        for (int nb2 = 0; nb2 < 2; ++nb2) {
-            pp[nb2][0] = ex2(fmaf(s[nb2][0], sl2, -mr[0]));
-            pp[nb2][1] = ex2(fmaf(s[nb2][1], sl2, -mr[0]));
-            pp[nb2][2] = ex2(fmaf(s[nb2][2], sl2, -mr[1]));
-            pp[nb2][3] = ex2(fmaf(s[nb2][3], sl2, -mr[1]));
-            lr[0] += pp[nb2][0] + pp[nb2][1];
-            lr[1] += pp[nb2][2] + pp[nb2][3];
-        }
-        uint32_t pa[4];
-        pa[0] = pack2<T>(pp[0][0], pp[0][1]);
-        pa[1] = pack2<T>(pp[0][2], pp[0][3]);
-        pa[2] = pack2<T>(pp[1][0], pp[1][1]);
-        pa[3] = pack2<T>(pp[1][2], pp[1][3]);
-#pragma unroll
-        for (int jj = 0; jj < G::NB8 / 2; ++jj) {
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(vaddr[jj] + boff, b0, b1, b2, b3);
-            mma16816<T>(o[2 * jj], pa, b0, b1);
-            mma16816<T>(o[2 * jj + 1], pa, b2, b3);
-        }
+    {
+        tc::MmaRows<T, D> &st = rs;
+        int b = 0;
+        for (; b + 1 < q16; b += 2) // pairs: both S tiles, one vote, both P V updates
+            st.block16x2(kaddr, vaddr, (uint32_t)(b * 16 * G::RB), (uint32_t)((b + 1) * 16 * G::RB), sl2);
+        if (b < q16) st.block16(kaddr, vaddr, (uint32_t)(b * 16 * G::RB), sl2);
     }
     // ---- finalise: l = quad sum, normalise, stage through this warp's Q rows, store
     lr[0] += __shfl_xor_sync(0xffffffffu, lr[0], 1);

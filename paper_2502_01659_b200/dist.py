@@ -89,6 +89,46 @@ def exchange_halo(buf: HaloBuffers, group=None) -> None:
             r.wait()
 
 
+def longnet_exchange_stride(L: int, w0: int, alpha: int, shard: int) -> int:
+    """alpha^k0 for LongNet query shards of `shard` rows.
+
+    Levels whose segment w0*alpha^t fits a shard (and the shards are aligned to it) only
+    reach keys inside the shard.  The first level k0 with w0*alpha^k0 > shard reaches
+    across shards, and every key a level t >= k0 piece contains is a multiple of alpha^t,
+    hence of alpha^k0.  So the exchange is an all-gather of the rows j with alpha^k0 | j.
+    Returns 0 when no level crosses a shard (no exchange)."""
+    K = 0
+    if w0 <= L:
+        while w0 * alpha ** (K + 1) <= L:
+            K += 1
+    for t in range(K + 1):
+        if w0 * alpha ** t > shard:
+            return alpha ** t
+    return 0
+
+
+def exchange_longnet(k_full: torch.Tensor, v_full: torch.Tensor, r0: int, r1: int, stride: int,
+                     group=None) -> None:
+    """Fill, in the full-length K/V buffers, the rows j = multiple of `stride` owned by the
+    other ranks (this rank's rows [r0, r1) are already in place).  Equal, stride-aligned
+    shards: every rank contributes (r1 - r0) / stride rows to one all_gather_into_tensor."""
+    if stride == 0:
+        return
+    world = dist.get_world_size(group)
+    n = (r1 - r0) // stride
+    mine = torch.stack([k_full[r0:r1:stride], v_full[r0:r1:stride]])  # [2, n, H, d]
+    flat = torch.empty((world * 2,) + tuple(mine.shape[1:]), dtype=mine.dtype, device=mine.device)
+    dist.all_gather_into_tensor(flat, mine.contiguous(), group=group)
+    gathered = flat.view((world, 2) + tuple(mine.shape[1:]))
+    L = k_full.shape[0]
+    per = r1 - r0
+    for p in range(world):
+        a = p * per
+        k_full[a:a + per:stride] = gathered[p, 0, :n]
+        v_full[a:a + per:stride] = gathered[p, 1, :n]
+    assert world * per == L, "LongNet exchange assumes equal shards covering the sequence"
+
+
 def allgather_rows(local: torch.Tensor, L: int, group=None) -> torch.Tensor:
     """All-gather equal-size row shards into a full [L, ...] tensor (LongNet / CSR masks)."""
     world = dist.get_world_size(group)

@@ -103,3 +103,40 @@ def test_shard_ranges_cover_exactly():
             assert a1 == b0 and a0 <= a1
         if L >= world * align:
             assert all((r1 - r0) % align == 0 for r0, r1 in got[:-1])
+
+
+def _longnet_case(rank, world):
+    """Each rank keeps only its shard + the gathered strided rows; every neighbour of every
+    local row (oracle enumeration) must then hold the true value."""
+    import oracle
+
+    L, H, d, w0, alpha = 4096, 1, 4, 64, 2
+    K, V = _global(L, H, d)
+    per = L // world
+    r0, r1 = rank * per, (rank + 1) * per
+    stride = gdist.longnet_exchange_stride(L, w0, alpha, per)
+    assert stride == 2 ** {2: 6, 3: 6}.get(world, 6) or stride > 0
+    kf = torch.full_like(K, float("nan"))
+    vf = torch.full_like(V, float("nan"))
+    kf[r0:r1] = K[r0:r1]
+    vf[r0:r1] = V[r0:r1]
+    gdist.exchange_longnet(kf, vf, r0, r1, stride)
+    om = oracle.longnet(L, w0, alpha)
+    for i in range(r0, r1, 7):
+        nb = oracle.neighbors(om, i)
+        assert torch.equal(kf[nb], K[nb]), i
+        assert torch.equal(vf[nb], V[nb]), i
+
+
+def test_longnet_strided_allgather_gloo():
+    _spawn(_longnet_case, 2)
+
+
+def test_longnet_exchange_stride_cfg4():
+    """cfg4 (L=2^24, w0=2048, alpha=2): k0 = 13/12/11 for 2/4/8 shards (SURVEY §8(e));
+    the gathered volume L/alpha^k0 rows x 256 B (K and V, bf16, d=64) is 0.52/1.05/2.10 MB."""
+    L = 2 ** 24
+    for world, k0 in ((2, 13), (4, 12), (8, 11)):
+        st = gdist.longnet_exchange_stride(L, 2048, 2, L // world)
+        assert st == 2 ** k0
+        assert round(L // st * 256 / 1e6, 2) == {2: 0.52, 4: 1.05, 8: 2.10}[world]
