@@ -228,10 +228,12 @@ ga_status ga_attention_ex(const void *Q, const void *K, const void *V, const ga_
     }
     if (!probe && (kernel == GA_KERNEL_TC || kernel == GA_KERNEL_AUTO) && window_tc_supported(p, dtype))
         return launch_window_tc(p, dtype, s);
+    if (!probe && (kernel == GA_KERNEL_TC || kernel == GA_KERNEL_AUTO) && longnet_tc_supported(p, dtype))
+        return launch_longnet_tc(p, dtype, s, /*use_umma=*/true); // tcgen05 groups + mma.sync rest
     if (kernel == GA_KERNEL_TC) { set_error("tcgen05 path does not support this (mask, dtype, d)"); return GA_ERR_UNSUPPORTED; }
     if (!probe && (kernel == GA_KERNEL_TILED || kernel == GA_KERNEL_AUTO)) {
         if (window_tiled_supported(p, dtype)) return launch_window_tiled(p, dtype, s);
-        if (longnet_tc_supported(p, dtype)) return launch_longnet_tc(p, dtype, s);
+        if (longnet_tc_supported(p, dtype)) return launch_longnet_tc(p, dtype, s, /*use_umma=*/false);
     }
     if (kernel == GA_KERNEL_TILED) { set_error("no tiled tensor-core kernel for this (mask, dtype, d)"); return GA_ERR_UNSUPPORTED; }
     return launch_edge(p, dtype, s);

@@ -143,7 +143,7 @@ size_t csr_heavy_workspace(int64_t L, int64_t nnz, int32_t H, int32_t d, int64_t
 bool window_tiled_supported(const AttnParams &p, ga_dtype dt);
 ga_status launch_window_tiled(const AttnParams &p, ga_dtype dt, cudaStream_t s);
 bool longnet_tc_supported(const AttnParams &p, ga_dtype dt);
-ga_status launch_longnet_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s);
+ga_status launch_longnet_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s, bool use_umma);
 bool window_tc_supported(const AttnParams &p, ga_dtype dt);
 ga_status launch_window_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s);
 

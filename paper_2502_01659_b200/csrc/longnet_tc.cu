@@ -357,7 +357,10 @@ bool longnet_tc_supported(const AttnParams &p, ga_dtype dt)
     return p.mask.K + 1 <= lnet::MAX_PIECES && p.mask.w0 >= 16;
 }
 
-ga_status launch_longnet_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s)
+ga_status launch_longnet_umma(const AttnParams &p, ga_dtype dt, int64_t seg0, int64_t n_seg, int s_max,
+                              cudaStream_t s);
+
+ga_status launch_longnet_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s, bool use_umma)
 {
     lnet::LParams lp;
     lp.p = p;
@@ -375,7 +378,22 @@ ga_status launch_longnet_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s)
         cnt[t] = M.w0 / stp + 1;
         stp *= M.alpha;
     }
-    for (int t = (int)M.K; t >= 0; --t) {
+    // groups that fill 128-row tiles (about w0/a^t - w0/a^(t+1) rows) run on tcgen05 (d = 64)
+    int s_umma = -1;
+    if (use_umma && p.d == 64 && (dt == GA_BF16 || dt == GA_F16)) {
+        int64_t st2 = 1;
+        for (int t = 0; t <= M.K; ++t) {
+            const int64_t rows_t = t < M.K ? M.w0 / st2 - M.w0 / (st2 * M.alpha) : M.w0 / st2;
+            if (rows_t < 128) break;
+            s_umma = t;
+            st2 *= M.alpha;
+        }
+    }
+    if (s_umma >= 0) {
+        ga_status st = launch_longnet_umma(p, dt, lp.seg0, lp.n_seg, s_umma, s);
+        if (st != GA_OK) return st;
+    }
+    for (int t = (int)M.K; t > s_umma; --t) {
         const int64_t tiles = (cnt[t] + lnet::ROWS - 1) / lnet::ROWS;
         for (int64_t k = 0; k < tiles; ++k) {
             if (n >= lnet::MAX_ITEMS) { set_error("LongNet: too many work items"); return GA_ERR_UNSUPPORTED; }
@@ -385,6 +403,7 @@ ga_status launch_longnet_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s)
         }
     }
     lp.n_items = n;
+    if (n == 0) return GA_OK;
     if ((int64_t)n * lp.n_seg * p.H > (int64_t)INT32_MAX) { set_error("LongNet grid too large"); return GA_ERR_UNSUPPORTED; }
     if (dt == GA_BF16) {
         switch (p.d) {

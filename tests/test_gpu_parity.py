@@ -160,6 +160,23 @@ def test_longnet_tiled_vs_oracle(ga, orc, L, w0, alpha, dt, d):
     assert np.abs(part.double().cpu().numpy() - want[r0:r1]).max() <= TOL[dt]
 
 
+@pytest.mark.parametrize("L,w0,alpha,dt", [(32768, 2048, 2, "bf16"), (4096, 256, 2, "bf16"), (8192, 512, 2, "f16"),
+                                            (20000, 1000, 3, "bf16"), (5000, 300, 2, "bf16")])
+def test_longnet_tcgen05_vs_oracle(ga, orc, L, w0, alpha, dt):
+    """tcgen05/TMEM path (groups of >= 128 rows: S and P V on tcgen05.mma, softmax from
+    TMEM) + mma.sync for the small groups, against the oracle; full and query-shard runs.
+    (1000, alpha 3) and 300 give ragged key tails and partial 128-row tiles."""
+    H, d = 1, 64
+    cpu, f64 = _inputs(L, H, d, dt, w0 + L, centred=True)
+    want, _ = orc.attention(*f64, orc.longnet(L, w0, alpha))
+    got = _run(ga, cpu, ga.LongNet(w0, alpha), kernel="tc")
+    assert np.abs(got - want).max() <= TOL[dt]
+    q, k, v = (x.cuda() for x in cpu)
+    r0, r1 = L // 4, L // 4 + L // 3
+    part = ga.attention(q[r0:r1].contiguous(), k, v, ga.LongNet(w0, alpha), L=L, q_begin=r0, kernel="tc")
+    assert np.abs(part.double().cpu().numpy() - want[r0:r1]).max() <= TOL[dt]
+
+
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
 def test_csr_bigbird_with_heavy_split(ga, orc, dt):
     """BigBird via device CSR; heavy global rows through the split+merge path (a7)."""
