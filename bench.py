@@ -195,10 +195,7 @@ def main():
     import paper_2502_01659_b200 as ga
     from paper_2502_01659_b200 import dist as gdist
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = _init_dist(torch, dist, world, local_rank)
     L_local, H, d = cfg["L"], cfg["H"], cfg["d"]
     L = L_local * world
     tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[cfg["dtype"]]
@@ -432,6 +429,21 @@ def measure_e2e(args, ga, world, dev, edges_total, targets, run_step, out, c_abi
             "d2h_bytes_per_step": d2h * world, "ms_per_step": ms, "steps": steps, "path": path}
 
 
+def _init_dist(torch, dist, world, local_rank):
+    """One process per GPU over NCCL.  GA_DIST_BACKEND=gloo with GA_FORCE_DEVICE=0 lets
+    several ranks share one GPU for a functional check of the N>1 code (not a timing)."""
+    dev_index = int(os.environ.get("GA_FORCE_DEVICE", local_rank))
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    if world > 1:
+        backend = os.environ.get("GA_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return dev
+
+
 def max_context(args, world, rank, local_rank):
     """Largest Window(128) bf16 d=64 sequence that fits in HBM: Q, K, V
     resident and the output written over Q (one launch owns each row, so the band and edge
@@ -445,10 +457,7 @@ def max_context(args, world, rank, local_rank):
     import paper_2502_01659_b200 as ga
     from paper_2502_01659_b200 import dist as gdist
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = _init_dist(torch, dist, world, local_rank)
     H, d, w, seed = 1, 64, 128, 0x5EED0005
     mask = ga.Window(w)
     halo = gdist.window_halo(mask) if world > 1 else 0

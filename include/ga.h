@@ -156,6 +156,13 @@ ga_status ga_attention_host(const void *Q, const void *K, const void *V, const g
 ga_status ga_workspace_size(const ga_mask *mask, int64_t L, int32_t d, int32_t heads, ga_dtype dtype,
                             const ga_opts *opts, size_t *bytes);
 
+/* Query-range alignment in tokens (host): launches whose [q_begin, q_begin + q_rows)
+   boundaries are multiples of *tokens compute every row exactly as one launch over the whole
+   range does (same tiles, same reduction order), so sharded outputs are bit-identical to the
+   single-GPU output.  Band kernel (WINDOW, bf16/fp16): 112 * r; LongNet tensor-core
+   kernels: w0 (one level-0 segment); edge kernel: 1. */
+ga_status ga_query_alignment(const ga_mask *mask, int32_t d, ga_dtype dtype, int64_t *tokens);
+
 /* Exact number of edges of an implicit pattern (host; closed forms per family, SURVEY
    §8(c)).  For GA_MASK_CSR returns mask->nnz.  For BIGBIRD with a device global_idx the
    list is copied to the host (synchronous). */

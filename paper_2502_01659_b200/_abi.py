@@ -50,6 +50,7 @@ SIGNATURES = [
     ("ga_attention_host", ctypes.c_int, [_V, _V, _V, _PM, _V, _I64, _I32, _I32, ctypes.c_int, _V]),
     ("ga_workspace_size", ctypes.c_int, [_PM, _I64, _I32, _I32, ctypes.c_int, _PO, ctypes.POINTER(_SZ)]),
     ("ga_mask_count", ctypes.c_int, [_PM, ctypes.POINTER(_I64)]),
+    ("ga_query_alignment", ctypes.c_int, [_PM, _I32, ctypes.c_int, ctypes.POINTER(_I64)]),
     ("ga_mask_to_csr", ctypes.c_int, [_PM, _V, _V, _V]),
     ("ga_mask_validate", ctypes.c_int, [_PM, _V, ctypes.POINTER(ctypes.c_int)]),
     ("ga_fill_inputs", ctypes.c_int, [_V, ctypes.c_int, _I64, _U64, _I32, _I64, _F, _V]),

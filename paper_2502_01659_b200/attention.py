@@ -104,6 +104,14 @@ def mask_count(mask: Mask, L: int) -> int:
     return n.value
 
 
+def query_alignment(mask: Mask, L: int, d: int, dtype=torch.bfloat16) -> int:
+    """Token alignment under which sharded launches are bit-identical to one launch."""
+    cm = mask.to_c(L)
+    n = ctypes.c_int64()
+    _abi.check(_abi.lib().ga_query_alignment(ctypes.byref(cm), d, dtype_code(dtype), ctypes.byref(n)))
+    return n.value
+
+
 def mask_to_csr(mask: Mask, L: int, device="cuda") -> CSR:
     """Materialise an implicit pattern as device CSR (degrees -> scan -> fill)."""
     nnz = mask_count(mask, L)

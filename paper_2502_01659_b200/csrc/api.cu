@@ -287,6 +287,21 @@ ga_status ga_attention_host(const void *Q, const void *K, const void *V, const g
     return st;
 }
 
+ga_status ga_query_alignment(const ga_mask *mask, int32_t d, ga_dtype dtype, int64_t *tokens)
+{
+    if (!mask || !tokens) { set_error("NULL argument"); return GA_ERR_INVALID_ARG; }
+    DevMask M;
+    ga_status st = make_devmask(mask, mask->L, M);
+    if (st != GA_OK) return st;
+    AttnParams p{};
+    p.mask = M;
+    p.d = d;
+    *tokens = 1;
+    if (window_tiled_supported(p, dtype)) *tokens = band_tile_rows() * M.r;
+    else if (longnet_tc_supported(p, dtype)) *tokens = M.w0;
+    return GA_OK;
+}
+
 ga_status ga_mask_count(const ga_mask *pattern, int64_t *nnz_out)
 {
     if (!pattern || !nnz_out) { set_error("NULL argument"); return GA_ERR_INVALID_ARG; }

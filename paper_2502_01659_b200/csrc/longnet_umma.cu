@@ -44,8 +44,8 @@ template <int D> __host__ __device__ constexpr uint32_t smem_bytes()
            64 /* mbarriers, tmem base */;
 }
 
-// TMEM columns: S [0, KC), P [KC, KC + KC/2), O [128, 128 + D)
-constexpr uint32_t COL_S = 0, COL_P = KC, COL_O = 128;
+// TMEM columns: S[2] at 0 and KC, P[2] (16-bit pairs) at 2KC and 2KC + KC/2, O at 3KC
+constexpr uint32_t COL_S = 0, COL_P = 2 * KC, COL_O = 3 * KC; // S0 S1 | P0 P1 | O  (256 columns at d=64)
 
 template <typename T, int D>
 __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams up)
@@ -61,9 +61,9 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
     const uint32_t sV0 = sK0 + STAGES * KC * RB;
     int64_t *rows = reinterpret_cast<int64_t *>(sgen + ROWS * RB + 2 * STAGES * KC * RB);
     uint64_t *mbars = reinterpret_cast<uint64_t *>(rows + ROWS);
-    uint32_t *tmem_base_smem = reinterpret_cast<uint32_t *>(mbars + 2);
-    const uint32_t mbS = (uint32_t)__cvta_generic_to_shared(&mbars[0]);
-    const uint32_t mbO = (uint32_t)__cvta_generic_to_shared(&mbars[1]);
+    uint32_t *tmem_base_smem = reinterpret_cast<uint32_t *>(mbars + 4);
+    const uint32_t mbS[2] = {(uint32_t)__cvta_generic_to_shared(&mbars[0]), (uint32_t)__cvta_generic_to_shared(&mbars[1])};
+    const uint32_t mbO[2] = {(uint32_t)__cvta_generic_to_shared(&mbars[2]), (uint32_t)__cvta_generic_to_shared(&mbars[3])};
 
     const AttnParams &p = up.p;
     const DevMask &M = p.mask;
@@ -108,8 +108,10 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (tid == 0) {
-        mbar_init(mbS, 1);
-        mbar_init(mbO, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(mbS[b], 1);
+            mbar_init(mbO[b], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     fence_before();
@@ -167,39 +169,58 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
     constexpr float kTau = 8.f;
     float m_run = -INFINITY, l_run = 0.f;
     const uint32_t idS = idesc<T>(ROWS, KC, false), idO = idesc<T>(ROWS, D, true);
-    uint32_t phS = 0, phO = 0;
-
-    for (int c = 0; c < nchunks; ++c) {
-        const int st = c % STAGES;
-        cp_async_wait<STAGES - 2>(); // chunk c (and Q) landed for this thread
-        fence_proxy_async();         // make the cp.async data visible to the tensor core
-        __syncthreads();
+    // Software pipeline: S_{c+1} runs on the tensor core while chunk c's softmax runs.
+    // S_c -> TMEM S[c&1] (mbarrier mbS[c&1]); P_c -> P[c&1]; P V_c -> O (mbO[c&1]).  The
+    // k-th use of a double-buffer slot completes its mbarrier phase with parity k & 1.
+    auto issue_S = [&](int c) {
         if (tid == 0) {
             fence_after();
-            const uint32_t aq = sQ, bk = sK0 + st * KC * RB;
+            const uint32_t bk = sK0 + (c % STAGES) * KC * RB;
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) // K = 16 per MMA: +32 B inside the swizzle atom
-                mma_ss(tmem + COL_S, sdesc_sw128(aq + kk * 32), sdesc_sw128(bk + kk * 32), idS, kk > 0);
-            mma_commit(mbS);
+                mma_ss(tmem + COL_S + (c & 1) * KC, sdesc_sw128(sQ + kk * 32), sdesc_sw128(bk + kk * 32), idS,
+                       kk > 0);
+            mma_commit(mbS[c & 1]);
         }
-        mbar_wait(mbS, phS);
-        phS ^= 1;
+    };
+    auto wait_O = [&](int c) { // P V_c complete
+        mbar_wait(mbO[c & 1], (c >> 1) & 1);
+        fence_after();
+    };
+    if (nchunks > 0) { // prologue: chunk 0 (and Q) landed -> S_0
+        cp_async_wait<STAGES - 2>();
+        fence_proxy_async();
+        __syncthreads();
+        issue_S(0);
+    }
+    for (int c = 0; c < nchunks; ++c) {
+        const int st = c % STAGES;
+        // 1. S_{c+1} (chunks 0..c+2 committed; c+1 must have landed)
+        if (c + 1 < nchunks) {
+            cp_async_wait<STAGES - 3>();
+            fence_proxy_async();
+            fence_before(); // the reads of S[(c+1)&1] (chunk c-1) are complete
+            __syncthreads();
+            issue_S(c + 1);
+        }
+        // 2. S_c
+        mbar_wait(mbS[c & 1], (c >> 1) & 1);
         fence_after();
         float sv[KC];
-        tmem_ld32(tlane + COL_S, sv);
-        tmem_ld32(tlane + COL_S + 32, sv + 32);
+        tmem_ld32(tlane + COL_S + (c & 1) * KC, sv);
+        tmem_ld32(tlane + COL_S + (c & 1) * KC + 32, sv + 32);
         tmem_wait_ld();
-        float lm = sv[0];
+        float lmx[8]; // 8 independent max chains (a 63-deep serial chain is latency-bound)
 #pragma unroll
-        for (int i = 1; i < KC; ++i) lm = fmaxf(lm, sv[i]);
-        // the previous P V must be done before P and O are touched (and its V stage reused)
-        if (c > 0) {
-            mbar_wait(mbO, phO);
-            phO ^= 1;
-            fence_after();
-        }
+        for (int j = 0; j < 8; ++j) lmx[j] = sv[j];
+#pragma unroll
+        for (int i = 8; i < KC; ++i) lmx[i & 7] = fmaxf(lmx[i & 7], sv[i]);
+        const float lm = fmaxf(fmaxf(fmaxf(lmx[0], lmx[1]), fmaxf(lmx[2], lmx[3])),
+                               fmaxf(fmaxf(lmx[4], lmx[5]), fmaxf(lmx[6], lmx[7])));
+        // 3. lazy rescale (O must be stable: the last issued P V is P V_{c-1})
         const bool need = lm * sl2 > m_run + kTau;
         if (__syncthreads_or(need)) {
+            if (c > 0) wait_O(c - 1);
             const float mn = fmaxf(m_run, lm * sl2);
             const float a = ex2(m_run - mn);
             // tcgen05.ld/st are .sync.aligned: the whole warp takes the branch (a = 1 rows
@@ -220,14 +241,18 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
             l_run *= a;
             m_run = mn;
         }
+        // 4. P_c into P[c&1] (last read by P V_{c-2})
+        if (c >= 2) wait_O(c - 2);
         uint32_t pk[KC / 2];
+        float ls[4] = {0.f, 0.f, 0.f, 0.f}; // independent partial sums
 #pragma unroll
         for (int i = 0; i < KC / 2; ++i) {
             const float p0 = ex2(fmaf(sv[2 * i], sl2, -m_run)), p1 = ex2(fmaf(sv[2 * i + 1], sl2, -m_run));
-            l_run += p0 + p1;
+            ls[i & 3] += p0 + p1;
             pk[i] = pack2<T>(p0, p1);
         }
-        tmem_st32(tlane + COL_P, pk);
+        l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        tmem_st32(tlane + COL_P + (c & 1) * (KC / 2), pk);
         tmem_wait_st();
         fence_before();
         __syncthreads();
@@ -236,17 +261,16 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
             const uint32_t bv = sV0 + st * KC * RB;
 #pragma unroll
             for (int kk = 0; kk < KC / 16; ++kk) // 16 keys per MMA: 8 P columns, 16 V rows
-                mma_ts(tmem + COL_O, tmem + COL_P + kk * 8, sdesc_sw128(bv + kk * 16 * RB), idO, (c > 0 || kk > 0));
-            mma_commit(mbO);
+                mma_ts(tmem + COL_O, tmem + COL_P + (c & 1) * (KC / 2) + kk * 8, sdesc_sw128(bv + kk * 16 * RB), idO,
+                       (c > 0 || kk > 0));
+            mma_commit(mbO[c & 1]);
         }
-        // refill: stage (c + S - 1) % S held chunk c - 1, whose P V completed above
+        // 5. refill the stage of chunk c-1 (free once P V_{c-1} is done) with chunk c+3
+        if (c >= 1) wait_O(c - 1);
         load_chunk(c + STAGES - 1 < nchunks ? c + STAGES - 1 : nchunks + STAGES); // no-op past the end
     }
     cp_async_wait<0>();
-    if (nchunks > 0) {
-        mbar_wait(mbO, phO);
-        fence_after();
-    }
+    if (nchunks > 0) wait_O(nchunks - 1);
     // ---- O row from TMEM (+ ragged tail on CUDA cores), normalise, store
     const bool row_ok = tid < nrows;
     float o[D];

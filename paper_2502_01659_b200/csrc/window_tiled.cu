@@ -468,6 +468,8 @@ static uint32_t band_smem_for(int d, int64_t m)
     }
 }
 
+int64_t band_tile_rows() { return band::ROWS; }
+
 bool window_tiled_supported(const AttnParams &p, ga_dtype dt)
 {
     if (p.mask.kind != K_WINDOW || (dt != GA_BF16 && dt != GA_F16)) return false;

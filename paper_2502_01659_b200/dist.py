@@ -73,6 +73,13 @@ def exchange_halo(buf: HaloBuffers, group=None) -> None:
     Requires every shard to hold at least `halo` rows.
     """
     world, rank = dist.get_world_size(group), dist.get_rank(group)
+    staged = dist.get_backend(group) == "gloo" and buf.k.is_cuda  # gloo p2p moves host memory only
+    if staged:
+        host = HaloBuffers(buf.k.cpu(), buf.v.cpu(), buf.r0, buf.r1, buf.kv_begin, buf.kv_end, buf.halo)
+        exchange_halo(host, group)
+        buf.k.copy_(host.k)
+        buf.v.copy_(host.v)
+        return
     ops = []
     left = buf.r0 - buf.kv_begin          # rows of left halo present in the buffer
     right = buf.kv_end - buf.r1
@@ -142,18 +149,24 @@ def sharded_window_attention(q_local: torch.Tensor, buf: HaloBuffers, mask: Wind
                              group=None) -> torch.Tensor:
     """One sharded step: interior rows start while the halo is exchanged on a side stream;
     the boundary rows run once it has landed.  Returns this rank's output rows."""
-    from .attention import attention
+    from .attention import attention, query_alignment
 
     if out is None:
         out = torch.empty_like(q_local)
     n = buf.r1 - buf.r0
     h = buf.halo
+    # interior/boundary split points on the kernel's tile grid, so every row is computed as
+    # in a single launch over the whole sequence
+    al = query_alignment(mask, L, q_local.shape[2], q_local.dtype)
+    up = lambda x: -(-x // al) * al
+    h_lo = min(n, up(buf.r0 + h) - buf.r0)
+    h_hi = min(n, buf.r1 - (buf.r1 - h) // al * al)
     main = torch.cuda.current_stream()
     comm = comm_stream or torch.cuda.Stream()
     comm.wait_stream(main)
     with torch.cuda.stream(comm):
         exchange_halo(buf, group)
-    a, b = min(h, n), max(min(h, n), n - h)  # interior rows [a, b) need no halo
+    a, b = h_lo, max(h_lo, n - h_hi)  # interior rows [a, b) need no halo
     if b > a:
         attention(q_local[a:b], buf.k, buf.v, mask, out[a:b], L=L, q_begin=buf.r0 + a, kv_begin=buf.kv_begin)
     main.wait_stream(comm)
