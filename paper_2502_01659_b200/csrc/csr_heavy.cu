@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) heavy_chunk_kernel(AttnParams p, const in
     const Piece P = get_piece(p.mask, i, 0);
     const int64_t kb = c * p.heavy_threshold;
     const int64_t ke = kb + p.heavy_threshold < P.count ? kb + p.heavy_threshold : P.count;
-    acc.run(P, kb, ke);
+    acc.template run_csr<4>(P.cols + P.base, kb, ke);
     acc.merge_groups();
     if (acc.g == 0) {
         constexpr int VEC = DT<T>::VEC;

@@ -9,7 +9,10 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
     static constexpr int VEC = DT<T>::VEC;
     static constexpr int G = D / VEC; // lanes per (edge, head) vector
     static constexpr int E = 32 / G;  // edges in flight per warp
+    static constexpr bool H16 = sizeof(T) == 2; // bf16/fp16: FHFMA on packed pairs
     float q[VEC], o[VEC];
+    uint32_t qp[4]; // packed 16-bit q (H16)
+    float sl2;      // log2(e)/sqrt(d), applied after the reduction on the H16 path
     float m, l;
     unsigned long long n_edges, sum_j, sum_h;
     int g, sub;
@@ -27,6 +30,8 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
         row_bytes = (size_t)p.H * D * sizeof(T);
         kv_begin = p.kv_begin;
         uint4 raw = ldg16(Qp);
+        qp[0] = raw.x; qp[1] = raw.y; qp[2] = raw.z; qp[3] = raw.w;
+        sl2 = p.scale_log2;
         unpack<T>(raw, q);
 #pragma unroll
         for (int c = 0; c < VEC; ++c) { q[c] *= p.scale_log2; o[c] = 0.f; }
@@ -57,34 +62,100 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
             }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                const bool valid = u == 0 ? va : vb;
                 if (u == 1 && k0 + E >= ke) break; // warp-uniform: no group has work
-                float kf[VEC], vf[VEC];
-                unpack<T>(u == 0 ? kra : krb, kf);
-                float s = 0.f;
+                const float sc = score(u == 0 ? kra : krb);
+                update(sc, u == 0 ? vra : vrb, u == 0 ? va : vb, u == 0 ? ja : jb);
+            }
+        }
+    }
+
+    // one (key, value) edge into the group state (score already reduced over the group)
+    __device__ __forceinline__ void update(float s, const uint4 &vraw, bool valid, int64_t j)
+    {
+        if (!valid) return;
+        if (s > m) { // lazy rescale: only when the running max grows
+            const float a = ex2(m - s);
+            l *= a;
 #pragma unroll
-                for (int c = 0; c < VEC; ++c) s = fmaf(q[c], kf[c], s);
+            for (int c = 0; c < VEC; ++c) o[c] *= a;
+            m = s;
+        }
+        const float pr = ex2(s - m);
+        l += pr;
+        if constexpr (H16) { // o += p v with p rounded to the input type (as on the MMA paths)
+            const uint32_t p2 = pack2<T>(pr, pr);
+            axpy2h<T>(p2, vraw.x, o[0], o[1]);
+            axpy2h<T>(p2, vraw.y, o[2], o[3]);
+            axpy2h<T>(p2, vraw.z, o[4], o[5]);
+            axpy2h<T>(p2, vraw.w, o[6], o[7]);
+        } else {
+            float vf[VEC];
+            unpack<T>(vraw, vf);
 #pragma unroll
-                for (int off = 1; off < G; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-                if (valid) {
-                    if (s > m) { // lazy rescale: only when the running max grows
-                        const float a = ex2(m - s);
-                        l *= a;
+            for (int c = 0; c < VEC; ++c) o[c] = fmaf(pr, vf[c], o[c]);
+        }
+        if (PROBE) {
+            n_edges += 1;
+            sum_j += (unsigned long long)j;
+            sum_h += splitmix64((uint64_t)j);
+        }
+    }
+
+    // q.k over the group (exp2 domain: scaled by log2(e)/sqrt(d))
+    __device__ __forceinline__ float score(const uint4 &kraw) const
+    {
+        float s;
+        if constexpr (H16) { // bf16 x bf16 + f32 without unpacking (FHFMA)
+            const float s0 = fma2h<T>(qp[2], kraw.z, fma2h<T>(qp[0], kraw.x, 0.f));
+            const float s1 = fma2h<T>(qp[3], kraw.w, fma2h<T>(qp[1], kraw.y, 0.f));
+            s = s0 + s1;
+        } else {
+            float kf[VEC];
+            unpack<T>(kraw, kf);
+            s = 0.f;
 #pragma unroll
-                        for (int c = 0; c < VEC; ++c) o[c] *= a;
-                        m = s;
+            for (int c = 0; c < VEC; ++c) s = fmaf(q[c], kf[c], s);
+        }
+#pragma unroll
+        for (int off = 1; off < G; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        return H16 ? s * sl2 : s;
+    }
+
+    // Explicit CSR piece, gather-bound: a warp loads 32 column indices with one coalesced
+    // load and broadcasts them to the lane groups by shuffle, then issues the K/V loads of
+    // DEPTH edge steps before consuming any (DEPTH * E edges in flight per warp), so the
+    // random row gathers overlap instead of waiting on dependent index loads.
+    template <int DEPTH>
+    __device__ __forceinline__ void run_csr(const int32_t *cols, int64_t kb, int64_t ke)
+    {
+        static_assert(32 % (E * DEPTH) == 0 || E * DEPTH >= 32, "batch shape");
+        constexpr int STEP = E * DEPTH; // edges per pass
+        const int lane = (int)(threadIdx.x & 31);
+        for (int64_t b0 = kb; b0 < ke; b0 += 32) {
+            const int64_t kl = b0 + lane;
+            const int my_j = kl < ke ? cols[kl] : -1;
+#pragma unroll 1
+            for (int e0 = 0; e0 < 32 && b0 + e0 < ke; e0 += STEP) {
+                uint4 kr[DEPTH], vr[DEPTH];
+                int jj[DEPTH];
+#pragma unroll
+                for (int u = 0; u < DEPTH; ++u) {
+                    const int src = e0 + u * E + g;
+                    jj[u] = __shfl_sync(0xffffffffu, my_j, src & 31);
+                    if (src >= 32) jj[u] = -1;
+                    if (jj[u] >= 0) {
+                        const size_t off = (size_t)(jj[u] - kv_begin) * row_bytes;
+                        kr[u] = ldg16(Kb + off);
+                        vr[u] = ldg16(Vb + off);
+                    } else {
+                        kr[u] = vr[u] = make_uint4(0, 0, 0, 0);
                     }
-                    const float pr = ex2(s - m);
-                    l += pr;
-                    unpack<T>(u == 0 ? vra : vrb, vf);
+                }
 #pragma unroll
-                    for (int c = 0; c < VEC; ++c) o[c] = fmaf(pr, vf[c], o[c]);
-                    if (PROBE) {
-                        const int64_t j = u == 0 ? ja : jb;
-                        n_edges += 1;
-                        sum_j += (unsigned long long)j;
-                        sum_h += splitmix64((uint64_t)j);
-                    }
+                for (int u = 0; u < DEPTH; ++u) {
+                    if (e0 + u * E >= 32 || b0 + e0 + u * E >= ke) break; // warp-uniform
+                    const float s = score(kr[u]);
+                    update(s, vr[u], jj[u] >= 0, jj[u]);
                 }
             }
         }

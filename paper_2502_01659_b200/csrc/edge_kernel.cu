@@ -37,7 +37,10 @@ __global__ void __launch_bounds__(256) edge_kernel(AttnParams p)
     const int np = num_pieces(p.mask, i);
     for (int pc = 0; pc < np; ++pc) {
         const Piece P = get_piece(p.mask, i, pc);
-        acc.run(P, 0, P.count);
+        if (P.mode == P_CSR)
+            acc.template run_csr<4>(P.cols + P.base, 0, P.count);
+        else
+            acc.run(P, 0, P.count);
     }
     acc.merge_groups();
     if (PROBE) {

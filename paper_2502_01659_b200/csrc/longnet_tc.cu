@@ -148,10 +148,15 @@ __global__ void __launch_bounds__(THREADS) longnet_kernel(const LParams lp)
         }
     };
 
-    // Q rows of the tile, then the first two key stages
-    for (int idx = tid; idx < nrows * G::NC; idx += THREADS) {
+    // Q rows of the tile, then the first two key stages.  Pad rows of the last 16-row slice
+    // are zeroed: they take part in the warp's rescale vote, so stale shared memory there
+    // would change the rounding of the valid rows from launch to launch.
+    for (int idx = tid; idx < ((nrows + 15) & ~15) * G::NC; idx += THREADS) {
         const int r = idx / G::NC, cc = idx % G::NC;
-        cp_async16(sQ + swz<D>(r, cc), Qg + (size_t)(rows[r] - p.q_begin) * row_bytes + cc * 16);
+        if (r < nrows)
+            cp_async16(sQ + swz<D>(r, cc), Qg + (size_t)(rows[r] - p.q_begin) * row_bytes + cc * 16);
+        else
+            sts_zero16(sQ + swz<D>(r, cc));
     }
     if (nchunks > 0) load_chunk(0, 0);
     cp_async_commit();

@@ -153,12 +153,24 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
                 cp_async16(sK0 + st * KC * RB + swz<D>(kl, cc), Kg + off + cc * 16);
                 cp_async16(sV0 + st * KC * RB + swz<D>(kl, cc), Vg + off + cc * 16);
             }
+        } else if (c < nchunks) { // keys past the last whole block in the final chunk: zero
+            // K/V rows (the stage holds an older chunk's keys), their scores are masked below
+#pragma unroll
+            for (int q = 0; q < D / 16; ++q) {
+                const int cc = hf * (D / 16) + q;
+                sts_zero16(sK0 + st * KC * RB + swz<D>(kl, cc));
+                sts_zero16(sV0 + st * KC * RB + swz<D>(kl, cc));
+            }
         }
         cp_async_commit();
     };
-    for (int idx = tid; idx < nrows * (RB / 16); idx += THREADS) {
+    // pad rows (>= nrows) are zeroed: they join the warp-uniform rescale vote
+    for (int idx = tid; idx < ROWS * (RB / 16); idx += THREADS) {
         const int r = idx / (RB / 16), cc = idx % (RB / 16);
-        cp_async16(sQ + swz<D>(r, cc), Qg + (size_t)(rows[r] - p.q_begin) * row_bytes + cc * 16);
+        if (r < nrows)
+            cp_async16(sQ + swz<D>(r, cc), Qg + (size_t)(rows[r] - p.q_begin) * row_bytes + cc * 16);
+        else
+            sts_zero16(sQ + swz<D>(r, cc));
     }
 #pragma unroll
     for (int c = 0; c < STAGES - 1; ++c) load_chunk(c); // stages 0..S-2 (empty groups are fine)
@@ -210,6 +222,11 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
         tmem_ld32(tlane + COL_S + (c & 1) * KC, sv);
         tmem_ld32(tlane + COL_S + (c & 1) * KC + 32, sv + 32);
         tmem_wait_ld();
+        const int valid = nblk * 16 - c * KC; // keys of this chunk (< KC only in the last one)
+        if (valid < KC) {
+#pragma unroll
+            for (int i = 0; i < KC; ++i) sv[i] = i < valid ? sv[i] : -INFINITY;
+        }
         float lmx[8]; // 8 independent max chains (a 63-deep serial chain is latency-bound)
 #pragma unroll
         for (int j = 0; j < 8; ++j) lmx[j] = sv[j];

@@ -35,6 +35,11 @@ template <int N> __device__ __forceinline__ void cp_async_wait()
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+__device__ __forceinline__ void sts_zero16(uint32_t a)
+{
+    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(a), "r"(0u));
+}
+
 __device__ __forceinline__ uint4 lds16(uint32_t a)
 {
     uint4 u;
@@ -75,52 +80,6 @@ __device__ __forceinline__ void mma16816<__half>(float *c, const uint32_t *a, ui
                  "{%0,%1,%2,%3};"
                  : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
                  : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-template <typename T> __device__ __forceinline__ uint32_t pack2(float lo, float hi);
-template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) { return f2_to_bf2(lo, hi); }
-template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) { return f2_to_h2(lo, hi); }
-
-// c + x.lo*y.lo + x.hi*y.hi with 16-bit inputs and f32 accumulation (FHFMA)
-template <typename T> __device__ __forceinline__ float fma2h(uint32_t x, uint32_t y, float c);
-
-template <> __device__ __forceinline__ float fma2h<__nv_bfloat16>(uint32_t x, uint32_t y, float c)
-{
-    float d;
-    asm("{ .reg .b16 xl, xh, yl, yh; .reg .f32 t; mov.b32 {xl, xh}, %1; mov.b32 {yl, yh}, %2;\n\t"
-        "fma.rn.f32.bf16 t, xl, yl, %3; fma.rn.f32.bf16 %0, xh, yh, t; }"
-        : "=f"(d)
-        : "r"(x), "r"(y), "f"(c));
-    return d;
-}
-
-template <> __device__ __forceinline__ float fma2h<__half>(uint32_t x, uint32_t y, float c)
-{
-    float d;
-    asm("{ .reg .b16 xl, xh, yl, yh; .reg .f32 t; mov.b32 {xl, xh}, %1; mov.b32 {yl, yh}, %2;\n\t"
-        "fma.rn.f32.f16 t, xl, yl, %3; fma.rn.f32.f16 %0, xh, yh, t; }"
-        : "=f"(d)
-        : "r"(x), "r"(y), "f"(c));
-    return d;
-}
-
-// (o0, o1) += p * (v.lo, v.hi), p held in the low half of a 16x2 register
-template <typename T> __device__ __forceinline__ void axpy2h(uint32_t p16x2, uint32_t v, float &o0, float &o1);
-
-template <> __device__ __forceinline__ void axpy2h<__nv_bfloat16>(uint32_t p, uint32_t v, float &o0, float &o1)
-{
-    asm("{ .reg .b16 pl, ph, vl, vh; mov.b32 {pl, ph}, %2; mov.b32 {vl, vh}, %3;\n\t"
-        "fma.rn.f32.bf16 %0, pl, vl, %0; fma.rn.f32.bf16 %1, pl, vh, %1; }"
-        : "+f"(o0), "+f"(o1)
-        : "r"(p), "r"(v));
-}
-
-template <> __device__ __forceinline__ void axpy2h<__half>(uint32_t p, uint32_t v, float &o0, float &o1)
-{
-    asm("{ .reg .b16 pl, ph, vl, vh; mov.b32 {pl, ph}, %2; mov.b32 {vl, vh}, %3;\n\t"
-        "fma.rn.f32.f16 %0, pl, vl, %0; fma.rn.f32.f16 %1, pl, vh, %1; }"
-        : "+f"(o0), "+f"(o1)
-        : "r"(p), "r"(v));
 }
 
 // Running flash-attention state of one warp's 16 rows in the m16n8 accumulator layout:

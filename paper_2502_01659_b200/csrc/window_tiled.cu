@@ -263,6 +263,12 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
         const int row = idx / G::NC, cc = idx % G::NC;
         cp_async16(sQ + swz<D>(row, cc), Qt + (int64_t)((uint64_t)(uint32_t)row * rstride) + cc * 16);
     }
+    if (!interior) { // pad rows of a clipped tile join the rescale votes: make them defined
+        for (int idx = tid; idx < ROWS * G::NC; idx += THREADS) {
+            const int row = idx / G::NC;
+            if (row < q_lo || row >= q_hi) tc::sts_zero16(sQ + swz<D>(row, idx % G::NC));
+        }
+    }
     // stage 0: rows the CUDA-core phase reads (ends of the band); stage 1: the dense middle,
     // which lands while the CUDA-core phase runs
     const int mid0 = ROWS - 1, mid1 = max(mid0, (int)(2 * m + 1) - 16);

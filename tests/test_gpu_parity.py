@@ -323,6 +323,50 @@ def test_sharded_offsets_bitwise(ga):
     assert (part.float() - full[r0:r1].float()).abs().max().item() < 2e-2
 
 
+@pytest.mark.parametrize("fam,args,kernel", [("longnet", (256, 2), "tiled"), ("longnet", (256, 2), "tc"),
+                                             ("longnet", (100, 3), "auto"), ("window", (256, 2), "auto"),
+                                             ("window", (100, 1), "auto"), ("bigbird", (64, 8, 6, 5), "auto")])
+def test_repeat_launches_bitwise(ga, fam, args, kernel):
+    """Every kernel is deterministic: the same launch repeated, with other kernels run in
+    between to leave different data in shared memory, gives identical bytes.  (Pad rows of
+    partial tiles used to take part in the rescale vote uninitialised.)"""
+    L, H, d = 10000, 2, 64
+    q, k, v = ga.qkv_device(31, L, H, d, torch.bfloat16)
+    mask = {"window": ga.Window, "longnet": ga.LongNet, "bigbird": ga.BigBird}[fam](*args)
+    if fam == "bigbird":
+        mask = ga.mask_to_csr(mask, L)
+    ref = ga.attention(q, k, v, mask, kernel=kernel)
+    dirt = [ga.Window(300, 3), ga.LongNet(64, 2), ga.Window(40, 1)]
+    for dm in dirt:
+        ga.attention(q * 7.0, k * -3.0, v, dm)
+        again = ga.attention(q, k, v, mask, kernel=kernel)
+        assert torch.equal(again, ref), (fam, args, kernel, dm)
+    # a query sub-range computes the same rows (tiles are anchored absolutely)
+    al = ga.query_alignment(mask, L, d, torch.bfloat16)
+    r0 = (L // 3 // al) * al
+    part = ga.attention(q[r0:].contiguous(), k, v, mask, L=L, q_begin=r0, kv_begin=0, kernel=kernel)
+    assert torch.equal(part, ref[r0:])
+
+
+@pytest.mark.parametrize("fam,L,args,kernel", [
+    ("longnet", 10000, (256, 2), "tc"), ("longnet", 5000, (300, 2), "tc"), ("longnet", 20000, (1000, 3), "tc"),
+    ("longnet", 10000, (100, 3), "tiled"), ("longnet", 10000, (256, 2), "edge"),
+    ("window", 3001, (256, 2), "window"), ("window", 3001, (41, 1), "window"), ("bigbird", 3000, (64, 8, 6, 5), "auto")])
+def test_uniform_attention_is_neighbour_mean(ga, orc, fam, L, args, kernel):
+    """q = 0 makes every softmax weight exactly 1 (no rounding of P), so each row must be the
+    plain mean of V over N(i).  The tight tolerance (bf16 output rounding of |mean| <= 0.2)
+    catches a missing, duplicated or extra key that the general 2e-2 bound can hide."""
+    H, d = 2, 64
+    cpu, f64 = _inputs(L, H, d, "bf16", 77 + L, centred=True)
+    q0 = torch.zeros_like(cpu[0])
+    m, om = _pair(ga, orc, fam, L, args)
+    if fam == "bigbird":
+        m = ga.mask_to_csr(m, L)
+    want, _ = orc.attention(np.zeros_like(f64[0]), f64[1], f64[2], om)
+    got = _run(ga, (q0, cpu[1], cpu[2]), m, kernel=kernel)
+    assert np.abs(got - want).max() <= 1e-3
+
+
 def test_host_entry_point_matches_device(ga):
     L, H, d = 2048, 8, 64
     cpu = synth.qkv(21, L, H, d, "bf16")
