@@ -47,6 +47,7 @@ typedef enum {
     GA_ERR_INVALID_ARG = -1, /* bad pointer / shape / parameter / alignment          */
     GA_ERR_UNSUPPORTED = -2, /* valid but not implemented (e.g. d not in {32,64,128}) */
     GA_ERR_CUDA = -3,        /* a CUDA runtime call or kernel launch failed           */
+    GA_ERR_COMM = -4,        /* multi-GPU bootstrap / exchange failed (ga_comm_*)      */
     GA_ERR_OOM = -5,         /* workspace too small / allocation failed               */
     GA_ERR_MASK = -6         /* ga_mask_validate found a malformed CSR                */
 } ga_status;
@@ -183,6 +184,70 @@ ga_status ga_mask_validate(const ga_mask *csr, void *stream, int *ok);
    plus `shift` (added in fp32 before rounding; 0 for the paper's U[0,1)).  DEVICE dst. */
 ga_status ga_fill_inputs(void *dst, ga_dtype dtype, int64_t n, uint64_t seed, int32_t tensor, int64_t e0,
                          float shift, void *stream);
+
+/* ------------------------------------------------------------------------------------
+ * Multi-GPU (SURVEY §8(b) comm entry points, §8(e) partitioning).  One process per GPU;
+ * the sequence is cut into equal contiguous query shards, rank q owning token rows
+ * [q*S, min(L, (q+1)*S)), S = ceil(L / world) (rows are independent).
+ * K and V shards live in SYMMETRIC buffers (ga_comm_alloc) that every rank maps with CUDA
+ * IPC, so the attention kernels read the rows they need from other ranks directly over
+ * NVLink while they compute — the window halo (PAPER.md:124-136 masks reach w-1 rows past a
+ * shard edge) and LongNet's strided long-range rows — with no separate exchange launch.
+ * Explicit CSR masks (unstructured columns) all-gather K/V with copy engines first.
+ * One node: the bootstrap rendezvous is a TCP socket on 127.0.0.1.
+ * ------------------------------------------------------------------------------------ */
+typedef struct ga_comm ga_comm; /* opaque */
+#define GA_COMM_ID_BYTES 128
+
+/* Rank 0 only: create the 128-byte bootstrap id (opens a listening socket on 127.0.0.1 in
+   this process) and hand it to the other ranks (e.g. torch.distributed broadcast). */
+ga_status ga_comm_get_unique_id(void *id128);
+
+/* Collective over `world` processes: connect to rank 0 through the id, then (device >= 0)
+   allocate the device barrier flags on CUDA device `device`.  device = -1 creates a
+   host-only comm (bootstrap and ga_comm_host_allgather only).  Blocks until every rank has
+   joined (timeout 120 s -> GA_ERR_COMM).  *comm is owned by the caller until
+   ga_comm_destroy. */
+ga_status ga_comm_create(int32_t world, int32_t rank, const void *id128, int32_t device, ga_comm **comm);
+
+/* Collective: allocate `bytes` (same on every rank) of DEVICE memory whose copies on all
+   ranks are mapped into each other's address space.  *local is this rank's copy (owned by
+   the comm; released by ga_comm_free / ga_comm_destroy).  Put the K and V shards
+   ([S, heads, d]) of ga_attention_sharded here. */
+ga_status ga_comm_alloc(ga_comm *comm, size_t bytes, void **local);
+
+/* Collective: release a ga_comm_alloc buffer (synchronises the device). */
+ga_status ga_comm_free(ga_comm *comm, void *local);
+
+/* Device-side barrier enqueued on `stream`: returns once every rank's stream has reached
+   its matching barrier (all ranks call barriers in the same order).  A rank that does not
+   arrive within 60 s releases the others and sets the flag read by ga_comm_status. */
+ga_status ga_comm_barrier(ga_comm *comm, void *stream);
+
+/* Host all-gather of `bytes` per rank into all[world * bytes] over the bootstrap sockets
+   (small control data; also the CPU test hook of the bootstrap). */
+ga_status ga_comm_host_allgather(ga_comm *comm, const void *mine, size_t bytes, void *all);
+
+/* *timed_out = 1 if a device barrier of this comm gave up waiting for a peer (synchronous). */
+ga_status ga_comm_status(ga_comm *comm, int *timed_out);
+
+/* Sharded attention: this rank's query rows [row_begin, row_end) of a length-L sequence.
+   Q, out: DEVICE [row_end - row_begin, heads, d] (local rows).  K, V: this rank's shard of
+   the keys/values, [row_end - row_begin, heads, d], inside ga_comm_alloc buffers at the
+   same offset on every rank.  row_begin/row_end must be this rank's shard as defined above.
+   WINDOW / LONGNET / BLOCK_DILATED read remote rows in-kernel over peer memory; CSR (row_ptr
+   and col_idx are the full GLOBAL arrays, on every rank) all-gathers K and V into a
+   comm-owned [L, heads, d] buffer first.  Enqueued on `stream` between two device barriers:
+   the entry barrier makes every rank's K/V visible, the exit barrier keeps them unchanged
+   until every rank has finished reading.  opts: kernel choice, CSR workspace, probes (its
+   q_/kv_ ranges are ignored).  Shards that are multiples of ga_query_alignment produce
+   rows bit-identical to ga_attention on one GPU. */
+ga_status ga_attention_sharded(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out,
+                               int64_t L, int64_t row_begin, int64_t row_end, int32_t d, int32_t heads,
+                               ga_dtype dtype, const ga_opts *opts, ga_comm *comm, void *stream);
+
+/* Collective: free every symmetric buffer and close the bootstrap sockets. */
+ga_status ga_comm_destroy(ga_comm *comm);
 
 /* Thread-local description of the last non-OK status ("" if none). */
 const char *ga_last_error(void);

@@ -10,13 +10,14 @@ import os
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libga.so")
 
-GA_OK, GA_ERR_INVALID_ARG, GA_ERR_UNSUPPORTED, GA_ERR_CUDA, GA_ERR_OOM, GA_ERR_MASK = 0, -1, -2, -3, -5, -6
+GA_OK, GA_ERR_INVALID_ARG, GA_ERR_UNSUPPORTED, GA_ERR_CUDA, GA_ERR_COMM, GA_ERR_OOM, GA_ERR_MASK = 0, -1, -2, -3, -4, -5, -6
+GA_COMM_ID_BYTES = 128
 GA_F32, GA_BF16, GA_F16 = 0, 1, 2
 GA_MASK_CSR, GA_MASK_WINDOW, GA_MASK_LONGNET, GA_MASK_BIGBIRD, GA_MASK_BLOCK_DILATED = 0, 1, 2, 3, 4
 GA_KERNEL_AUTO, GA_KERNEL_EDGE, GA_KERNEL_TILED, GA_KERNEL_TC = 0, 1, 2, 3
 
 STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_INVALID_ARG", -2: "GA_ERR_UNSUPPORTED", -3: "GA_ERR_CUDA",
-                -5: "GA_ERR_OOM", -6: "GA_ERR_MASK"}
+                -4: "GA_ERR_COMM", -5: "GA_ERR_OOM", -6: "GA_ERR_MASK"}
 
 
 class GaMask(ctypes.Structure):
@@ -54,6 +55,16 @@ SIGNATURES = [
     ("ga_mask_to_csr", ctypes.c_int, [_PM, _V, _V, _V]),
     ("ga_mask_validate", ctypes.c_int, [_PM, _V, ctypes.POINTER(ctypes.c_int)]),
     ("ga_fill_inputs", ctypes.c_int, [_V, ctypes.c_int, _I64, _U64, _I32, _I64, _F, _V]),
+    ("ga_comm_get_unique_id", ctypes.c_int, [_V]),
+    ("ga_comm_create", ctypes.c_int, [_I32, _I32, _V, _I32, ctypes.POINTER(_V)]),
+    ("ga_comm_alloc", ctypes.c_int, [_V, _SZ, ctypes.POINTER(_V)]),
+    ("ga_comm_free", ctypes.c_int, [_V, _V]),
+    ("ga_comm_barrier", ctypes.c_int, [_V, _V]),
+    ("ga_comm_host_allgather", ctypes.c_int, [_V, _V, _SZ, _V]),
+    ("ga_comm_status", ctypes.c_int, [_V, ctypes.POINTER(ctypes.c_int)]),
+    ("ga_attention_sharded", ctypes.c_int, [_V, _V, _V, _PM, _V, _I64, _I64, _I64, _I32, _I32, ctypes.c_int, _PO, _V,
+                                            _V]),
+    ("ga_comm_destroy", ctypes.c_int, [_V]),
     ("ga_last_error", ctypes.c_char_p, []),
     ("ga_launch_count", ctypes.c_ulonglong, []),
     ("ga_version", ctypes.c_char_p, []),

@@ -8,7 +8,7 @@
 #include <string>
 #include <vector>
 
-#include "common.cuh"
+#include "comm.cuh"
 
 namespace ga {
 
@@ -176,6 +176,36 @@ static ga_status resolve(const void *Q, const void *K, const void *V, const ga_m
     return GA_OK;
 }
 
+// Kernel choice for resolved parameters (shared by ga_attention_ex and the sharded path).
+static ga_status dispatch(AttnParams &p, ga_dtype dtype, const ga_opts *opts, int64_t heavy, cudaStream_t s)
+{
+    const int kernel = opts ? opts->kernel : GA_KERNEL_AUTO;
+    const bool probe = p.edge_counter || p.row_fingerprint;
+    ga_status st;
+    if (p.mask.kind == GA_MASK_CSR) {
+        const bool split = opts && opts->workspace && opts->workspace_bytes > 0;
+        if (split) {
+            if (probe) { set_error("probes are not supported with the heavy-row split"); return GA_ERR_UNSUPPORTED; }
+            p.heavy_threshold = heavy;
+            st = launch_edge(p, dtype, s); // light rows
+            if (st != GA_OK) return st;
+            return launch_csr_heavy(p, dtype, opts->workspace, opts->workspace_bytes, s);
+        }
+        return launch_edge(p, dtype, s);
+    }
+    if (!probe && (kernel == GA_KERNEL_TC || kernel == GA_KERNEL_AUTO) && window_tc_supported(p, dtype))
+        return launch_window_tc(p, dtype, s);
+    if (!probe && (kernel == GA_KERNEL_TC || kernel == GA_KERNEL_AUTO) && longnet_tc_supported(p, dtype))
+        return launch_longnet_tc(p, dtype, s, /*use_umma=*/true); // tcgen05 groups + mma.sync rest
+    if (kernel == GA_KERNEL_TC) { set_error("tcgen05 path does not support this (mask, dtype, d)"); return GA_ERR_UNSUPPORTED; }
+    if (!probe && (kernel == GA_KERNEL_TILED || kernel == GA_KERNEL_AUTO)) {
+        if (window_tiled_supported(p, dtype)) return launch_window_tiled(p, dtype, s);
+        if (longnet_tc_supported(p, dtype)) return launch_longnet_tc(p, dtype, s, /*use_umma=*/false);
+    }
+    if (kernel == GA_KERNEL_TILED) { set_error("no tiled tensor-core kernel for this (mask, dtype, d)"); return GA_ERR_UNSUPPORTED; }
+    return launch_edge(p, dtype, s);
+}
+
 } // namespace ga
 
 using namespace ga;
@@ -210,33 +240,93 @@ ga_status ga_attention_ex(const void *Q, const void *K, const void *V, const ga_
     Resolved R;
     ga_status st = resolve(Q, K, V, mask, out, L, d, heads, dtype, opts, R);
     if (st != GA_OK) return st;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    AttnParams &p = R.p;
-    const int kernel = opts ? opts->kernel : GA_KERNEL_AUTO;
-    const bool probe = p.edge_counter || p.row_fingerprint;
+    return dispatch(R.p, dtype, opts, R.heavy, reinterpret_cast<cudaStream_t>(stream));
+}
 
-    if (p.mask.kind == GA_MASK_CSR) {
-        const bool split = opts && opts->workspace && opts->workspace_bytes > 0;
-        if (split) {
-            p.heavy_threshold = R.heavy;
-            st = launch_edge(p, dtype, s); // light rows
+ga_status ga_attention_sharded(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out, int64_t L,
+                               int64_t row_begin, int64_t row_end, int32_t d, int32_t heads, ga_dtype dtype,
+                               const ga_opts *opts, ga_comm *comm, void *stream)
+{
+    if (!comm || !mask) { set_error("NULL argument"); return GA_ERR_INVALID_ARG; }
+    if (comm->device < 0) { set_error("comm has no device (created with device = -1)"); return GA_ERR_INVALID_ARG; }
+    if (L <= 0) { set_error("L must be > 0"); return GA_ERR_INVALID_ARG; }
+    const int64_t S = (L + comm->world - 1) / comm->world;
+    const int64_t b = imin(L, (int64_t)comm->rank * S), e = imin(L, b + S);
+    if (row_begin != b || row_end != e) {
+        set_error("rank %d of %d owns rows [%lld, %lld) of L=%lld (got [%lld, %lld))", comm->rank, comm->world,
+                  (long long)b, (long long)e, (long long)L, (long long)row_begin, (long long)row_end);
+        return GA_ERR_INVALID_ARG;
+    }
+    if (mask->kind == GA_MASK_BIGBIRD) {
+        set_error("BIGBIRD masks are materialised with ga_mask_to_csr and run as CSR");
+        return GA_ERR_UNSUPPORTED;
+    }
+    DeviceGuard dg(comm->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t rows = e - b;
+    const size_t row_bytes = (size_t)heads * d * dtype_bytes(dtype);
+    GaSymAlloc *ak = comm_find(comm, K), *av = comm_find(comm, V);
+    if (!ak || !av) { set_error("K and V must live in ga_comm_alloc buffers of this comm"); return GA_ERR_INVALID_ARG; }
+    if ((const char *)K + rows * row_bytes > ak->local + ak->bytes ||
+        (const char *)V + rows * row_bytes > av->local + av->bytes) {
+        set_error("K/V shard overruns its ga_comm_alloc buffer");
+        return GA_ERR_INVALID_ARG;
+    }
+    ga_opts o{};
+    if (opts) o = *opts;
+    ga_status st = comm_device_barrier(comm, s); // every rank's K/V shard is complete
+    if (st != GA_OK) return st;
+    if (rows > 0) {
+        if (mask->kind == GA_MASK_CSR) {
+            // unstructured columns: all-gather K and V (copy engines, peer -> local), then a
+            // local launch over the full-length buffers
+            const size_t full = (size_t)L * row_bytes;
+            if (comm->gather_bytes < full) {
+                if (comm->gather_k) cudaFree(comm->gather_k);
+                if (comm->gather_v) cudaFree(comm->gather_v);
+                comm->gather_k = comm->gather_v = nullptr;
+                comm->gather_bytes = 0;
+                cudaError_t ce = cudaMalloc(&comm->gather_k, full);
+                if (ce == cudaSuccess) ce = cudaMalloc(&comm->gather_v, full);
+                if (ce != cudaSuccess) { set_error("CSR all-gather buffers (%zu B): %s", 2 * full, cudaGetErrorString(ce)); return GA_ERR_OOM; }
+                comm->gather_bytes = full;
+            }
+            const size_t koff = (size_t)((const char *)K - ak->local), voff = (size_t)((const char *)V - av->local);
+            for (int q = 0; q < comm->world; ++q) {
+                const int64_t qb = imin(L, (int64_t)q * S), qn = imin(L, qb + S) - qb;
+                if (qn <= 0) continue;
+                cudaError_t ce = cudaMemcpyAsync((char *)comm->gather_k + qb * row_bytes, ak->peers[q] + koff,
+                                                 qn * row_bytes, cudaMemcpyDefault, s);
+                if (ce == cudaSuccess)
+                    ce = cudaMemcpyAsync((char *)comm->gather_v + qb * row_bytes, av->peers[q] + voff, qn * row_bytes,
+                                         cudaMemcpyDefault, s);
+                if (ce != cudaSuccess) return cuda_fail(ce, "CSR K/V all-gather");
+            }
+            o.q_begin = b;
+            o.q_rows = rows;
+            o.kv_begin = 0;
+            o.kv_rows = L;
+            st = ga_attention_ex(Q, comm->gather_k, comm->gather_v, mask, out, L, d, heads, dtype, &o, stream);
+        } else {
+            const char *const *tk = nullptr, *const *tv = nullptr;
+            st = comm_peer_table(comm, K, &tk);
+            if (st == GA_OK) st = comm_peer_table(comm, V, &tv);
             if (st != GA_OK) return st;
-            if (probe) { set_error("probes are not supported with the heavy-row split"); return GA_ERR_UNSUPPORTED; }
-            return launch_csr_heavy(p, dtype, opts->workspace, opts->workspace_bytes, s);
+            o.q_begin = b;
+            o.q_rows = rows;
+            o.kv_begin = b;
+            o.kv_rows = rows;
+            Resolved R;
+            st = resolve(Q, K, V, mask, out, L, d, heads, dtype, &o, R);
+            if (st != GA_OK) return st;
+            R.p.k_peer = tk;
+            R.p.v_peer = tv;
+            R.p.shard_rows = S;
+            st = dispatch(R.p, dtype, &o, R.heavy, s);
         }
-        return launch_edge(p, dtype, s);
+        if (st != GA_OK) return st;
     }
-    if (!probe && (kernel == GA_KERNEL_TC || kernel == GA_KERNEL_AUTO) && window_tc_supported(p, dtype))
-        return launch_window_tc(p, dtype, s);
-    if (!probe && (kernel == GA_KERNEL_TC || kernel == GA_KERNEL_AUTO) && longnet_tc_supported(p, dtype))
-        return launch_longnet_tc(p, dtype, s, /*use_umma=*/true); // tcgen05 groups + mma.sync rest
-    if (kernel == GA_KERNEL_TC) { set_error("tcgen05 path does not support this (mask, dtype, d)"); return GA_ERR_UNSUPPORTED; }
-    if (!probe && (kernel == GA_KERNEL_TILED || kernel == GA_KERNEL_AUTO)) {
-        if (window_tiled_supported(p, dtype)) return launch_window_tiled(p, dtype, s);
-        if (longnet_tc_supported(p, dtype)) return launch_longnet_tc(p, dtype, s, /*use_umma=*/false);
-    }
-    if (kernel == GA_KERNEL_TILED) { set_error("no tiled tensor-core kernel for this (mask, dtype, d)"); return GA_ERR_UNSUPPORTED; }
-    return launch_edge(p, dtype, s);
+    return comm_device_barrier(comm, s); // no rank changes its K/V while others still read it
 }
 
 ga_status ga_attention(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out, int64_t L,

@@ -1,0 +1,50 @@
+// comm.cuh — internal view of ga_comm (multi-GPU plumbing).
+#pragma once
+#include <list>
+#include <map>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+// One symmetric allocation: the same size on every rank, each rank's copy mapped into every
+// other rank's address space with CUDA IPC (peer loads over NVLink; same-device mappings
+// when several ranks share a GPU).
+struct GaSymAlloc {
+    char *local = nullptr;
+    size_t bytes = 0;
+    std::vector<char *> peers;                          // [world]; peers[rank] == local
+    std::map<size_t, const char **> dev_tables;         // offset -> DEVICE [world] of peers[q]+offset
+};
+
+struct ga_comm {
+    int world = 1, rank = 0, device = -1;
+    std::vector<int> fds;        // rank 0: fds[q] = socket to rank q (q >= 1); others: fds[0] = rank 0
+    std::list<GaSymAlloc> allocs; // stable addresses
+    // device barrier state: flags[q] (in the first symmetric allocation) is written by rank q
+    GaSymAlloc *flag_alloc = nullptr;
+    uint64_t gen = 0;
+    // CSR / BigBird all-gather scratch: full-length K and V (grown on demand)
+    void *gather_k = nullptr, *gather_v = nullptr;
+    size_t gather_bytes = 0;
+};
+
+namespace ga {
+// symmetric allocation owning `p` (any address inside it), or nullptr
+GaSymAlloc *comm_find(ga_comm *c, const void *p);
+// DEVICE table of the peers' copies of `p` (same offset in every rank's allocation)
+ga_status comm_peer_table(ga_comm *c, const void *p, const char *const **table);
+ga_status comm_device_barrier(ga_comm *c, cudaStream_t s);
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+} // namespace ga

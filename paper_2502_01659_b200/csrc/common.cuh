@@ -181,7 +181,31 @@ struct AttnParams {
     int64_t heavy_threshold; // CSR: rows above this are skipped by the light kernel (0 = none)
     unsigned long long *edge_counter;
     unsigned long long *row_fingerprint;
+    // Sharded runs over peer memory (ga_attention_sharded): rank q holds K/V token rows
+    // [q*shard_rows, (q+1)*shard_rows) at k_peer[q] / v_peer[q] (CUDA IPC mappings; the
+    // local rank's own entry is its K/V).  Rows outside [kv_begin, kv_begin + kv_rows) are
+    // read from their owner over NVLink.  NULL = single-buffer mode.
+    const char *const *k_peer;
+    const char *const *v_peer;
+    int64_t shard_rows;
 };
+
+// Base address (head 0, element 0) of K and V token row j: the local buffer when j is in
+// [kv_begin, kv_begin + kv_rows), else the owning peer's buffer (sharded runs).
+__device__ __forceinline__ void kv_row(const AttnParams &p, int64_t j, size_t row_bytes, const char *&kr,
+                                       const char *&vr)
+{
+    const int64_t lj = j - p.kv_begin;
+    if (p.k_peer == nullptr || (uint64_t)lj < (uint64_t)p.kv_rows) {
+        kr = reinterpret_cast<const char *>(p.K) + lj * (int64_t)row_bytes;
+        vr = reinterpret_cast<const char *>(p.V) + lj * (int64_t)row_bytes;
+        return;
+    }
+    const int64_t q = j / p.shard_rows;
+    const int64_t off = (j - q * p.shard_rows) * (int64_t)row_bytes;
+    kr = p.k_peer[q] + off;
+    vr = p.v_peer[q] + off;
+}
 
 // launchers (defined in the kernel translation units)
 ga_status launch_edge(const AttnParams &p, ga_dtype dt, cudaStream_t s);

@@ -16,19 +16,17 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
     float m, l;
     unsigned long long n_edges, sum_j, sum_h;
     int g, sub;
-    const char *Kb, *Vb;
-    size_t row_bytes;
-    int64_t kv_begin;
+    const AttnParams *prm;
+    size_t row_bytes, hoff; // token row stride; this lane's (head, sub-vector) byte offset
 
     __device__ __forceinline__ void init(const AttnParams &p, int64_t t, int h, int lane)
     {
         g = lane / G;
         sub = lane % G;
         const T *Qp = reinterpret_cast<const T *>(p.Q) + ((size_t)t * p.H + h) * D + sub * VEC;
-        Kb = reinterpret_cast<const char *>(p.K) + ((size_t)h * D + sub * VEC) * sizeof(T);
-        Vb = reinterpret_cast<const char *>(p.V) + ((size_t)h * D + sub * VEC) * sizeof(T);
+        prm = &p;
+        hoff = ((size_t)h * D + sub * VEC) * sizeof(T);
         row_bytes = (size_t)p.H * D * sizeof(T);
-        kv_begin = p.kv_begin;
         uint4 raw = ldg16(Qp);
         qp[0] = raw.x; qp[1] = raw.y; qp[2] = raw.z; qp[3] = raw.w;
         sl2 = p.scale_log2;
@@ -50,15 +48,11 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
             int64_t ja = 0, jb = 0;
             if (va) {
                 ja = piece_at(P, ka);
-                const size_t off = (size_t)(ja - kv_begin) * row_bytes;
-                kra = ldg16(Kb + off);
-                vra = ldg16(Vb + off);
+                load(ja, kra, vra);
             }
             if (vb) {
                 jb = piece_at(P, kk);
-                const size_t off = (size_t)(jb - kv_begin) * row_bytes;
-                krb = ldg16(Kb + off);
-                vrb = ldg16(Vb + off);
+                load(jb, krb, vrb);
             }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
@@ -67,6 +61,15 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
                 update(sc, u == 0 ? vra : vrb, u == 0 ? va : vb, u == 0 ? ja : jb);
             }
         }
+    }
+
+    // this lane's 16-byte slices of K_j and V_j (local buffer or the owning peer's)
+    __device__ __forceinline__ void load(int64_t j, uint4 &kraw, uint4 &vraw) const
+    {
+        const char *kr, *vr;
+        kv_row(*prm, j, row_bytes, kr, vr);
+        kraw = ldg16(kr + hoff);
+        vraw = ldg16(vr + hoff);
     }
 
     // one (key, value) edge into the group state (score already reduced over the group)
@@ -144,9 +147,7 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
                     jj[u] = __shfl_sync(0xffffffffu, my_j, src & 31);
                     if (src >= 32) jj[u] = -1;
                     if (jj[u] >= 0) {
-                        const size_t off = (size_t)(jj[u] - kv_begin) * row_bytes;
-                        kr[u] = ldg16(Kb + off);
-                        vr[u] = ldg16(Vb + off);
+                        load(jj[u], kr[u], vr[u]);
                     } else {
                         kr[u] = vr[u] = make_uint4(0, 0, 0, 0);
                     }

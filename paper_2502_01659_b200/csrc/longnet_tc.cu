@@ -122,8 +122,7 @@ __global__ void __launch_bounds__(THREADS) longnet_kernel(const LParams lp)
 
     const size_t row_bytes = (size_t)H * D * sizeof(T);
     const char *Qg = reinterpret_cast<const char *>(p.Q) + (size_t)h * D * sizeof(T);
-    const char *Kg = reinterpret_cast<const char *>(p.K) + (size_t)h * D * sizeof(T);
-    const char *Vg = reinterpret_cast<const char *>(p.V) + (size_t)h * D * sizeof(T);
+    const size_t hoff = (size_t)h * D * sizeof(T);
 
     auto key_token = [&](int k) -> int64_t { // k-th key of the concatenated pieces
         int t = 0;
@@ -138,12 +137,13 @@ __global__ void __launch_bounds__(THREADS) longnet_kernel(const LParams lp)
         const int k = (int)(c * KC) + kl;
         if (k < nblk * 16) {
             while (cur_t + 1 < np && pstart[cur_t + 1] <= k) ++cur_t;
-            const size_t off = (size_t)(piece_at(spiece[cur_t], k - pstart[cur_t]) - p.kv_begin) * row_bytes;
+            const char *kr, *vr;
+            kv_row(p, piece_at(spiece[cur_t], k - pstart[cur_t]), row_bytes, kr, vr);
 #pragma unroll
             for (int q = 0; q < G::HC; ++q) {
                 const int cc = hf * G::HC + q;
-                cp_async16(sK0 + st * KC * G::RB + swz<D>(kl, cc), Kg + off + cc * 16);
-                cp_async16(sV0 + st * KC * G::RB + swz<D>(kl, cc), Vg + off + cc * 16);
+                cp_async16(sK0 + st * KC * G::RB + swz<D>(kl, cc), kr + hoff + cc * 16);
+                cp_async16(sV0 + st * KC * G::RB + swz<D>(kl, cc), vr + hoff + cc * 16);
             }
         }
     };
@@ -224,7 +224,9 @@ __global__ void __launch_bounds__(THREADS) longnet_kernel(const LParams lp)
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
             if (t >= ragged) break;
-            const char *kr = Kg + (size_t)(key_token(nblk * 16 + t) - p.kv_begin) * row_bytes;
+            const char *kr, *vr_unused;
+            kv_row(p, key_token(nblk * 16 + t), row_bytes, kr, vr_unused);
+            kr += hoff;
             float s0 = 0.f, s1 = 0.f;
 #pragma unroll
             for (int q = 0; q < G::HC; ++q) {
@@ -244,7 +246,9 @@ __global__ void __launch_bounds__(THREADS) longnet_kernel(const LParams lp)
             if (t >= ragged) break;
             const float pr = ex2(sc[t] - mc);
             lc += pr;
-            const char *vr = Vg + (size_t)(key_token(nblk * 16 + t) - p.kv_begin) * row_bytes;
+            const char *kr_unused, *vr;
+            kv_row(p, key_token(nblk * 16 + t), row_bytes, kr_unused, vr);
+            vr += hoff;
             const uint32_t p2 = pack2<T>(pr, pr);
 #pragma unroll
             for (int q = 0; q < G::HC; ++q) {

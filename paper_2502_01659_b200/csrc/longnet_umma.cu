@@ -136,8 +136,7 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
 
     const size_t row_bytes = (size_t)H * D * sizeof(T);
     const char *Qg = reinterpret_cast<const char *>(p.Q) + (size_t)h * D * sizeof(T);
-    const char *Kg = reinterpret_cast<const char *>(p.K) + (size_t)h * D * sizeof(T);
-    const char *Vg = reinterpret_cast<const char *>(p.V) + (size_t)h * D * sizeof(T);
+    const size_t hoff = (size_t)h * D * sizeof(T);
 
     int cur_t = 0;
     auto load_chunk = [&](int c) {
@@ -146,12 +145,13 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
         const int k = c * KC + kl;
         if (k < nblk * 16) {
             while (cur_t + 1 < np && pstart[cur_t + 1] <= k) ++cur_t;
-            const size_t off = (size_t)(piece_at(spiece[cur_t], k - pstart[cur_t]) - p.kv_begin) * row_bytes;
+            const char *kr, *vr;
+            kv_row(p, piece_at(spiece[cur_t], k - pstart[cur_t]), row_bytes, kr, vr);
 #pragma unroll
             for (int q = 0; q < D / 16; ++q) {
                 const int cc = hf * (D / 16) + q;
-                cp_async16(sK0 + st * KC * RB + swz<D>(kl, cc), Kg + off + cc * 16);
-                cp_async16(sV0 + st * KC * RB + swz<D>(kl, cc), Vg + off + cc * 16);
+                cp_async16(sK0 + st * KC * RB + swz<D>(kl, cc), kr + hoff + cc * 16);
+                cp_async16(sV0 + st * KC * RB + swz<D>(kl, cc), vr + hoff + cc * 16);
             }
         } else if (c < nchunks) { // keys past the last whole block in the final chunk: zero
             // K/V rows (the stage holds an older chunk's keys), their scores are masked below
@@ -308,11 +308,14 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
             const int k = nblk * 16 + t;
             int pt = 0;
             while (pt + 1 < np && pstart[pt + 1] <= k) ++pt;
-            const size_t off = (size_t)(piece_at(spiece[pt], k - pstart[pt]) - p.kv_begin) * row_bytes;
+            const char *kr, *vr;
+            kv_row(p, piece_at(spiece[pt], k - pstart[pt]), row_bytes, kr, vr);
+            kr += hoff;
+            vr += hoff;
             float sdot = 0.f, kf[8];
 #pragma unroll
             for (int q = 0; q < D / 8; ++q) {
-                unpack<T>(ldg16(Kg + off + q * 16), kf);
+                unpack<T>(ldg16(kr + q * 16), kf);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) sdot = fmaf(qf[8 * q + e], kf[e], sdot);
             }
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
             l_run += pr;
 #pragma unroll
             for (int q = 0; q < D / 8; ++q) {
-                unpack<T>(ldg16(Vg + off + q * 16), kf);
+                unpack<T>(ldg16(vr + q * 16), kf);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) o[8 * q + e] = fmaf(pr, kf[e], o[8 * q + e]);
             }

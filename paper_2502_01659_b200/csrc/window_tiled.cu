@@ -247,14 +247,30 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
     // the pointers are formed for in-range rows only (base may be negative for clipped tiles)
     const uint32_t rstride = (uint32_t)(r * row_bytes); // < 4 GB: one 32x32->64 multiply per row
     const int64_t band_tok0 = c + base * r - p.kv_begin;
+    // sharded runs: a tile at a shard edge reaches rows owned by the neighbour ranks and
+    // reads them from their memory (kv_row); every other tile takes the strided fast path
+    const bool band_local = p.k_peer == nullptr ||
+                            (band_tok0 + ld_lo * r >= 0 && band_tok0 + (int64_t)(ld_hi - 1) * r < p.kv_rows);
+    const size_t hoff = (size_t)h * D * sizeof(T);
     auto load_band = [&](int r0, int r1) {
         r0 = max(r0, ld_lo);
         r1 = min(r1, ld_hi);
-        for (int idx = r0 * G::NC + tid; idx < r1 * G::NC; idx += THREADS) {
-            const int row = idx / G::NC, cc = idx % G::NC;
-            const int64_t off = band_tok0 * (int64_t)row_bytes + (int64_t)((uint64_t)(uint32_t)row * rstride) + cc * 16;
-            cp_async16(sK + swz<D>(row, cc), Kg + off);
-            cp_async16(sV + swz<D>(row, cc), Vg + off);
+        if (band_local) {
+            for (int idx = r0 * G::NC + tid; idx < r1 * G::NC; idx += THREADS) {
+                const int row = idx / G::NC, cc = idx % G::NC;
+                const int64_t off =
+                    band_tok0 * (int64_t)row_bytes + (int64_t)((uint64_t)(uint32_t)row * rstride) + cc * 16;
+                cp_async16(sK + swz<D>(row, cc), Kg + off);
+                cp_async16(sV + swz<D>(row, cc), Vg + off);
+            }
+        } else {
+            for (int idx = r0 * G::NC + tid; idx < r1 * G::NC; idx += THREADS) {
+                const int row = idx / G::NC, cc = idx % G::NC;
+                const char *kr, *vr;
+                kv_row(p, c + (base + row) * r, row_bytes, kr, vr);
+                cp_async16(sK + swz<D>(row, cc), kr + hoff + cc * 16);
+                cp_async16(sV + swz<D>(row, cc), vr + hoff + cc * 16);
+            }
         }
     };
     const char *Qt = Qg + (c + a0 * r - p.q_begin) * (int64_t)row_bytes;

@@ -140,3 +140,63 @@ def test_longnet_exchange_stride_cfg4():
         st = gdist.longnet_exchange_stride(L, 2048, 2, L // world)
         assert st == 2 ** k0
         assert round(L // st * 256 / 1e6, 2) == {2: 0.52, 4: 1.05, 8: 2.10}[world]
+
+
+# ---------------------------------------------------------------- C-ABI comm bootstrap
+def _comm_bootstrap_case(rank, world):
+    import ctypes
+
+    from paper_2502_01659_b200 import _abi
+    from paper_2502_01659_b200.comm import Comm
+
+    c = Comm(device=-1)  # host-only: TCP bootstrap through the libga C ABI
+    assert (c.rank, c.world) == (rank, world)
+    got = c.host_allgather(bytes([rank] * 5) + b"xyz")
+    assert got == [bytes([q] * 5) + b"xyz" for q in range(world)]
+    for _ in range(3):  # repeated exchanges stay in step
+        got = c.host_allgather(rank.to_bytes(8, "little"))
+        assert [int.from_bytes(g, "little") for g in got] == list(range(world))
+    # a host-only comm refuses device work
+    with pytest.raises(_abi.GaError, match="INVALID_ARG"):
+        c.empty((4,), torch.float32)
+    c.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_comm_bootstrap_host_allgather(world):
+    _spawn(_comm_bootstrap_case, world)
+
+
+def test_comm_create_errors():
+    import ctypes
+
+    from paper_2502_01659_b200 import _abi
+
+    lib = _abi.lib()
+    h = ctypes.c_void_p()
+    bad = ctypes.create_string_buffer(128)  # no magic
+    assert lib.ga_comm_create(2, 0, bad, -1, ctypes.byref(h)) == _abi.GA_ERR_INVALID_ARG
+    idb = ctypes.create_string_buffer(128)
+    assert lib.ga_comm_get_unique_id(idb) == _abi.GA_OK
+    assert lib.ga_comm_create(2, 2, idb, -1, ctypes.byref(h)) == _abi.GA_ERR_INVALID_ARG  # rank >= world
+    # world 1 needs no peers
+    assert lib.ga_comm_create(1, 0, idb, -1, ctypes.byref(h)) == _abi.GA_OK
+    out = ctypes.create_string_buffer(4)
+    assert lib.ga_comm_host_allgather(h, b"abcd", 4, out) == _abi.GA_OK and out.raw == b"abcd"
+    assert lib.ga_comm_destroy(h) == _abi.GA_OK
+    # sharded attention validates its comm before touching the device
+    m = _abi.GaMask()
+    m.kind, m.L, m.w, m.r = _abi.GA_MASK_WINDOW, 100, 8, 1
+    assert lib.ga_attention_sharded(None, None, None, ctypes.byref(m), None, 100, 0, 100, 64, 1, 1, None, None,
+                                    None) == _abi.GA_ERR_INVALID_ARG
+
+
+def test_comm_shard_rows():
+    from paper_2502_01659_b200.comm import shard_rows
+
+    for L in (1, 7, 100, 2 ** 20 + 3):
+        for world in (1, 2, 3, 8):
+            spans = [shard_rows(L, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == L
+            for (a, b), (c, _) in zip(spans, spans[1:]):
+                assert b == c and a <= b

@@ -2,6 +2,7 @@
 has one GPU), run the production sharding code — halo exchange for windows, strided
 all-gather for LongNet — and must reproduce the single-GPU output bit for bit (shards are
 aligned to the kernels' tiles, so each row is computed exactly as in the 1-GPU launch)."""
+import functools
 import os
 import socket
 
@@ -98,3 +99,54 @@ def test_sharded_window_two_ranks():
 
 def test_sharded_longnet_two_ranks():
     _spawn(_longnet_case)
+
+
+# ------------------------------------------------------------ C-ABI comm over IPC peer memory
+def _comm_case(rank, world, fam, kernel="auto"):
+    """ga_attention_sharded: K/V shards in symmetric (IPC-mapped) buffers, remote rows read
+    in-kernel from the other rank's memory (window halo, LongNet strided rows) or
+    all-gathered (CSR).  Both ranks share cuda:0 here; across GPUs the same mappings go over
+    NVLink."""
+    import paper_2502_01659_b200 as ga
+    from paper_2502_01659_b200.comm import Comm, shard_rows
+
+    comm = Comm()
+    try:
+        if fam == "window":
+            H, d, L, mask, exact = 8, 64, 224 * 40 * world, ga.Window(256, 2), True
+        elif fam == "window_unaligned":
+            H, d, L, mask, exact = 2, 64, 10001, ga.Window(300, 3), False
+        elif fam == "longnet":
+            H, d, L, mask, exact = 1, 64, 2 ** 16, ga.LongNet(256, 2), True
+        elif fam == "longnet_a3":
+            H, d, L, mask, exact = 2, 32, 9000, ga.LongNet(100, 3), False
+        else:  # BigBird materialised as CSR: K/V all-gather path
+            H, d, L, exact = 2, 64, 8192, True
+            mask = ga.mask_to_csr(ga.BigBird(64, 8, 16, 7), L)
+        q, k, v = ga.qkv_device(17, L, H, d, torch.bfloat16)
+        full = ga.attention(q, k, v, mask, kernel=kernel)
+        b, e = shard_rows(L, world, rank)
+        S = -(-L // world)
+        ks = comm.empty((S, H, d), torch.bfloat16)
+        vs = comm.empty((S, H, d), torch.bfloat16)
+        ks[: e - b].copy_(k[b:e])
+        vs[: e - b].copy_(v[b:e])
+        for _ in range(2):  # reuse of the comm and its buffers
+            out = comm.attention(q[b:e].contiguous(), ks[: e - b], vs[: e - b], mask, L, kernel=kernel)
+            torch.cuda.synchronize()
+            if exact:
+                assert torch.equal(out, full[b:e]), fam
+            else:
+                assert (out.float() - full[b:e].float()).abs().max().item() < 2e-2, fam
+        assert not comm.timed_out()
+        comm.free(ks)
+        comm.free(vs)
+    finally:
+        comm.close()
+
+
+@pytest.mark.parametrize("fam,kernel", [("window", "auto"), ("window", "edge"), ("window_unaligned", "auto"),
+                                        ("longnet", "auto"), ("longnet", "tiled"), ("longnet", "edge"),
+                                        ("longnet_a3", "auto"), ("bigbird_csr", "auto")])
+def test_comm_sharded_attention_two_ranks(fam, kernel):
+    _spawn(functools.partial(_comm_case, fam=fam, kernel=kernel))
