@@ -4,11 +4,12 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
 
 One "step" is one pass of the whole hot path (neighbour enumeration, scores, online
-softmax, aggregation — one ga_attention call per shard, plus the halo exchange at N>1)
+softmax, aggregation — one ga_attention call, or one ga_attention_sharded call per rank at N>1)
 over the configuration's full synthetic input.  Default workload: BASELINE.json configs[1]
 (L=65536, 8 heads, d=64, bf16, dilated window w=256 r=2) on one B200.  N>1 (torchrun,
 one process per GPU) is weak scaling: every rank owns L query rows of an N*L-token
-sequence and exchanges a K/V halo with its neighbours each step (NCCL over NVLink).
+sequence; its K/V shard sits in a symmetric CUDA-IPC buffer and the kernels read the halo /
+long-range rows they need from the other ranks' HBM over NVLink (CSR: K/V all-gather).
 
 metric: attention edges/s = (mask nnz x heads) / step time, whole job.
 """
@@ -193,7 +194,6 @@ def main():
     import torch.distributed as dist
 
     import paper_2502_01659_b200 as ga
-    from paper_2502_01659_b200 import dist as gdist
 
     dev = _init_dist(torch, dist, world, local_rank)
     L_local, H, d = cfg["L"], cfg["H"], cfg["d"]
@@ -208,55 +208,38 @@ def main():
     if kind == "window":
         mask = ga.Window(a[0], a[1])
         nnz = ga.mask_count(mask, L)
-        halo = gdist.window_halo(mask) if world > 1 else 0
-        buf = gdist.alloc_halo(L, r0, r1, halo, H, d, tdt, dev)
-        q = torch.empty((L_local, H, d), dtype=tdt, device=dev)
-        ga.fill_inputs(q, seed, 0, r0 * H * d)
-        ga.fill_inputs(buf.local_k, seed, 1, r0 * H * d)
-        ga.fill_inputs(buf.local_v, seed, 2, r0 * H * d)
-        out = torch.empty_like(q)
-        comm = torch.cuda.Stream() if world > 1 else None
-
-        def step():
-            if world > 1:
-                gdist.sharded_window_attention(q, buf, mask, L, out=out, comm_stream=comm)
-            else:
-                ga.attention(q, buf.k, buf.v, mask, out, kernel=args.kernel)
-        e2e_targets = [q, buf.local_k, buf.local_v]
-    elif kind == "longnet" and world > 1:
-        # weak scaling: rank owns rows [r0, r1) of an N*L sequence; full-length K/V buffers hold
-        # the local rows plus, each step, the strided rows gathered from the other ranks
+    elif kind == "bigbird":
+        mask = ga.mask_to_csr(ga.BigBird(a[0], a[1], a[2], seed=BIGBIRD_SEED), L)
+        nnz = mask.nnz
+        ws = torch.empty(ga.workspace_size(mask, L, d, H, tdt, q_begin=r0, q_rows=L_local), dtype=torch.uint8,
+                         device=dev)
+    else:
         mask = ga.LongNet(a[0], a[1])
         nnz = ga.mask_count(mask, L)
-        stride = gdist.longnet_exchange_stride(L, a[0], a[1], L_local)
-        q = torch.empty((L_local, H, d), dtype=tdt, device=dev)
-        kf = torch.zeros((L, H, d), dtype=tdt, device=dev)
-        vf = torch.zeros_like(kf)
-        ga.fill_inputs(q, seed, 0, r0 * H * d)
-        ga.fill_inputs(kf[r0:r1], seed, 1, r0 * H * d)
-        ga.fill_inputs(vf[r0:r1], seed, 2, r0 * H * d)
-        out = torch.empty_like(q)
+    q = torch.empty((L_local, H, d), dtype=tdt, device=dev)
+    ga.fill_inputs(q, seed, 0, r0 * H * d)
+    comm = None
+    if world > 1:
+        # weak scaling: rank owns rows [r0, r1) of an N*L sequence; its K/V shard lives in a
+        # symmetric buffer the other ranks read over NVLink (ga_attention_sharded)
+        from paper_2502_01659_b200.comm import Comm
 
-        def step():
-            gdist.exchange_longnet(kf, vf, r0, r1, stride)
-            ga.attention(q, kf, vf, mask, out, L=L, q_begin=r0, kv_begin=0, kernel=args.kernel)
-        e2e_targets = [q, kf[r0:r1], vf[r0:r1]]
+        comm = Comm()
+        k = comm.empty((L_local, H, d), tdt)
+        v = comm.empty((L_local, H, d), tdt)
     else:
-        if world > 1:
-            raise SystemExit(f"--gpus > 1 is implemented for window (cfg2/cfg5) and LongNet (cfg4) masks")
-        if kind == "bigbird":
-            mask = ga.mask_to_csr(ga.BigBird(a[0], a[1], a[2], seed=BIGBIRD_SEED), L)
-            nnz = mask.nnz
-            ws = torch.empty(ga.workspace_size(mask, L, d, H, tdt), dtype=torch.uint8, device=dev)
-        else:
-            mask = ga.LongNet(a[0], a[1])
-            nnz = ga.mask_count(mask, L)
-        q, k, v = ga.qkv_device(seed, L, H, d, tdt, device=dev)
-        out = torch.empty_like(q)
+        k = torch.empty((L_local, H, d), dtype=tdt, device=dev)
+        v = torch.empty_like(k)
+    ga.fill_inputs(k, seed, 1, r0 * H * d)
+    ga.fill_inputs(v, seed, 2, r0 * H * d)
+    out = torch.empty_like(q)
 
-        def step():
+    def step():
+        if comm is not None:
+            comm.attention(q, k, v, mask, L, out=out, kernel=args.kernel, workspace=ws)
+        else:
             ga.attention(q, k, v, mask, out, kernel=args.kernel, workspace=ws)
-        e2e_targets = [q, k, v]
+    e2e_targets = [q, k, v]
 
     edges_total = nnz * H  # all ranks together (global mask over the N*L sequence)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
@@ -319,12 +302,15 @@ def main():
                                    f"{H} heads, d={d}, {cfg['dtype']}, {mask_desc(cfg)}",
                        "L": L, "heads": H, "d": d, "mask": mask_desc(cfg), "nnz": nnz,
                        "kernel": args.kernel, "parallelism": f"query-range shards x{world}" + (
-                           ", NCCL halo exchange" if world > 1 else ""),
+                           ", ga_attention_sharded (remote K/V rows read over NVLink peer memory"
+                           + (", CSR K/V all-gather" if kind == "bigbird" else "") + ")" if world > 1 else ""),
                        "l2": "flushed between timed steps (256 MiB write outside the events); inputs > L2"},
             "clocks": clocks, "roofline": roofline, "gather_model": gather, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -447,7 +433,7 @@ def _init_dist(torch, dist, world, local_rank):
 def max_context(args, world, rank, local_rank):
     """Largest Window(128) bf16 d=64 sequence that fits in HBM: Q, K, V
     resident and the output written over Q (one launch owns each row, so the band and edge
-    kernels allow it for implicit masks).  At N>1 every rank holds L tokens plus the halo.
+    kernels allow it for implicit masks).  At N>1 every rank holds L tokens (no halo copy).
     One step runs; rows at the start, the end and the shard boundaries are checked against
     the oracle (which regenerates them from the seed)."""
     import numpy as np
@@ -455,33 +441,40 @@ def max_context(args, world, rank, local_rank):
     import torch.distributed as dist
 
     import paper_2502_01659_b200 as ga
-    from paper_2502_01659_b200 import dist as gdist
 
     dev = _init_dist(torch, dist, world, local_rank)
     H, d, w, seed = 1, 64, 128, 0x5EED0005
     mask = ga.Window(w)
-    halo = gdist.window_halo(mask) if world > 1 else 0
     free, total = torch.cuda.mem_get_info(dev)
     row = H * d * 2
-    reserve = 2 << 30  # context, workspace of the runtime, halo buffers, clocks
-    L_local = int((free - reserve) // (3 * row)) - 2 * halo
+    reserve = 2 << 30  # context, runtime workspace, clocks
+    L_local = int((free - reserve) // (3 * row))
     L_local = (L_local // 224) * 224  # band-kernel tile multiple (112 rows x r=1) x 2
     L = L_local * world
     r0, r1 = rank * L_local, (rank + 1) * L_local
-    buf = gdist.alloc_halo(L, r0, r1, halo, H, d, torch.bfloat16, dev)
+    comm = None
+    if world > 1:  # K/V shards in symmetric buffers; halo rows read from the neighbours
+        from paper_2502_01659_b200.comm import Comm
+
+        comm = Comm()
+        k = comm.empty((L_local, H, d), torch.bfloat16)
+        v = comm.empty((L_local, H, d), torch.bfloat16)
+    else:
+        k = torch.empty((L_local, H, d), dtype=torch.bfloat16, device=dev)
+        v = torch.empty_like(k)
     q = torch.empty((L_local, H, d), dtype=torch.bfloat16, device=dev)
     ga.fill_inputs(q, seed, 0, r0 * H * d)
-    ga.fill_inputs(buf.local_k, seed, 1, r0 * H * d)
-    ga.fill_inputs(buf.local_v, seed, 2, r0 * H * d)
+    ga.fill_inputs(k, seed, 1, r0 * H * d)
+    ga.fill_inputs(v, seed, 2, r0 * H * d)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    if world > 1:
-        gdist.sharded_window_attention(q, buf, mask, L, out=q)
+    if comm is not None:
+        comm.attention(q, k, v, mask, L, out=q)
     else:
-        ga.attention(q, buf.k, buf.v, mask, q)
+        ga.attention(q, k, v, mask, q)
     e1.record()
     torch.cuda.synchronize()
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
@@ -504,6 +497,8 @@ def max_context(args, world, rank, local_rank):
             "step_ms": ms.item(), "edges": ga.mask_count(mask, L),
             "parity_max_abs_err_sampled": err.item(), "parity_ok": err.item() <= 2e-2,
             "paper_context": "160,000,000 tokens on one A100 80GB (PAPER.md:22, :452)"}), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 
