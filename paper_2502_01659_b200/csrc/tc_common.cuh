@@ -82,6 +82,17 @@ __device__ __forceinline__ void mma16816<__half>(float *c, const uint32_t *a, ui
                  : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// (x0, x1) * s - m for a pair of fp32 values in one FFMA2 (sm_100 packed fp32 FMA)
+__device__ __forceinline__ void ffma2_sm(float &x0, float &x1, float s, float negm)
+{
+    unsigned long long a, b, c, d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(x0), "f"(x1));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(b) : "f"(s));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(negm));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x0), "=f"(x1) : "l"(d));
+}
+
 // Running flash-attention state of one warp's 16 rows in the m16n8 accumulator layout:
 // lane (g = lane/4, t4 = lane%4) owns rows g and g+8 and dims 8j + 2*t4 + {0,1}.
 template <typename T, int D> struct MmaRows {
@@ -106,6 +117,40 @@ template <typename T, int D> struct MmaRows {
         lr[0] = lr[1] = 0.f;
 #pragma unroll
         for (int j = 0; j < G::NB8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    }
+
+    // multiply the state of rows g / g+8 by a0 / a1 (online-softmax rescale)
+    __device__ __forceinline__ void scale_rows(float a0, float a1)
+    {
+        lr[0] *= a0;
+        lr[1] *= a1;
+#pragma unroll
+        for (int j = 0; j < G::NB8; ++j) {
+            o[j][0] *= a0;
+            o[j][1] *= a0;
+            o[j][2] *= a1;
+            o[j][3] *= a1;
+        }
+    }
+
+    // P (fp32 scores in the accumulator layout, 2 n8 blocks) -> exp2(s * sl2 - m) (one
+    // FFMA2 per pair), row partial sums, packed to the input type as the A fragment of P V
+    __device__ __forceinline__ void softmax_pack(float (*sv)[4], float sl2, uint32_t *pa)
+    {
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) {
+            float x0 = sv[nb][0], x1 = sv[nb][1], x2 = sv[nb][2], x3 = sv[nb][3];
+            ffma2_sm(x0, x1, sl2, -mr[0]);
+            ffma2_sm(x2, x3, sl2, -mr[1]);
+            x0 = ex2(x0);
+            x1 = ex2(x1);
+            x2 = ex2(x2);
+            x3 = ex2(x3);
+            lr[0] += x0 + x1;
+            lr[1] += x2 + x3;
+            pa[2 * nb] = pack2<T>(x0, x1);
+            pa[2 * nb + 1] = pack2<T>(x2, x3);
+        }
     }
 
     // One fully dense block of 16 keys whose rows start at kaddr/vaddr (per-lane ldmatrix
@@ -135,34 +180,12 @@ template <typename T, int D> struct MmaRows {
             float bm1 = fmaxf(lm1, __shfl_xor_sync(0xffffffffu, lm1, 1));
             bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
             const float mn0 = fmaxf(mr[0], bm0 * sl2), mn1 = fmaxf(mr[1], bm1 * sl2);
-            const float a0s = ex2(mr[0] - mn0), a1s = ex2(mr[1] - mn1);
-            lr[0] *= a0s;
-            lr[1] *= a1s;
-#pragma unroll
-            for (int j = 0; j < G::NB8; ++j) {
-                o[j][0] *= a0s;
-                o[j][1] *= a0s;
-                o[j][2] *= a1s;
-                o[j][3] *= a1s;
-            }
+            scale_rows(ex2(mr[0] - mn0), ex2(mr[1] - mn1));
             mr[0] = mn0;
             mr[1] = mn1;
         }
-        float pp[2][4];
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb) {
-            pp[nb][0] = ex2(fmaf(s[nb][0], sl2, -mr[0]));
-            pp[nb][1] = ex2(fmaf(s[nb][1], sl2, -mr[0]));
-            pp[nb][2] = ex2(fmaf(s[nb][2], sl2, -mr[1]));
-            pp[nb][3] = ex2(fmaf(s[nb][3], sl2, -mr[1]));
-            lr[0] += pp[nb][0] + pp[nb][1];
-            lr[1] += pp[nb][2] + pp[nb][3];
-        }
         uint32_t pa[4];
-        pa[0] = pack2<T>(pp[0][0], pp[0][1]);
-        pa[1] = pack2<T>(pp[0][2], pp[0][3]);
-        pa[2] = pack2<T>(pp[1][0], pp[1][1]);
-        pa[3] = pack2<T>(pp[1][2], pp[1][3]);
+        softmax_pack(s, sl2, pa);
 #pragma unroll
         for (int jj = 0; jj < G::NB8 / 2; ++jj) {
             uint32_t b0, b1, b2, b3;
@@ -203,38 +226,13 @@ template <typename T, int D> struct MmaRows {
             float bm1 = fmaxf(lm1, __shfl_xor_sync(0xffffffffu, lm1, 1));
             bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
             const float mn0 = fmaxf(mr[0], bm0 * sl2), mn1 = fmaxf(mr[1], bm1 * sl2);
-            const float a0s = ex2(mr[0] - mn0), a1s = ex2(mr[1] - mn1);
-            lr[0] *= a0s;
-            lr[1] *= a1s;
-#pragma unroll
-            for (int j = 0; j < G::NB8; ++j) {
-                o[j][0] *= a0s;
-                o[j][1] *= a0s;
-                o[j][2] *= a1s;
-                o[j][3] *= a1s;
-            }
+            scale_rows(ex2(mr[0] - mn0), ex2(mr[1] - mn1));
             mr[0] = mn0;
             mr[1] = mn1;
         }
         uint32_t pa[2][4];
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-            float pp[2][4];
-#pragma unroll
-            for (int nb = 0; nb < 2; ++nb) {
-                const float *sv = s[2 * h2 + nb];
-                pp[nb][0] = ex2(fmaf(sv[0], sl2, -mr[0]));
-                pp[nb][1] = ex2(fmaf(sv[1], sl2, -mr[0]));
-                pp[nb][2] = ex2(fmaf(sv[2], sl2, -mr[1]));
-                pp[nb][3] = ex2(fmaf(sv[3], sl2, -mr[1]));
-                lr[0] += pp[nb][0] + pp[nb][1];
-                lr[1] += pp[nb][2] + pp[nb][3];
-            }
-            pa[h2][0] = pack2<T>(pp[0][0], pp[0][1]);
-            pa[h2][1] = pack2<T>(pp[0][2], pp[0][3]);
-            pa[h2][2] = pack2<T>(pp[1][0], pp[1][1]);
-            pa[h2][3] = pack2<T>(pp[1][2], pp[1][3]);
-        }
+        softmax_pack(s, sl2, pa[0]);
+        softmax_pack(s + 2, sl2, pa[1]);
 #pragma unroll
         for (int jj = 0; jj < G::NB8 / 2; ++jj) {
             uint32_t b0, b1, b2, b3, c0, c1, c2, c3;
@@ -247,6 +245,7 @@ template <typename T, int D> struct MmaRows {
         }
     }
 
+    // sum the per-lane partial l over the quad
     // sum the per-lane partial l over the quad
     __device__ __forceinline__ void reduce_l()
     {

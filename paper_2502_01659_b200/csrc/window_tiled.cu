@@ -2,7 +2,7 @@
 //
 // Residue class c of a dilated window is a pure band: class rows a (token c + a*r) see class
 // rows b with |a - b| <= m, m = floor((w-1)/r) (readings R1/R2).  A CTA takes
-// ROWS = 64 consecutive class rows of one (class, head) and stages the Q tile and the K/V
+// ROWS = 112 consecutive class rows of one (class, head) and stages the Q tile and the K/V
 // band they reach in shared memory (cp.async 16-byte chunks, XOR swizzle so ldmatrix and
 // per-lane row reads are bank-conflict free).  Each warp owns 16 rows; the keys they reach
 // split into
@@ -28,114 +28,12 @@ constexpr int ROWS = 16 * WARPS;
 constexpr int THREADS = 32 * WARPS;
 constexpr int MAX_GEN = 48; // keys of U\F (+ tail) a clipped warp may have: <= 15 + 15 + 15
 
-template <int D> struct Geo {
-    static constexpr int RB = 2 * D;    // bytes per (token, head) row
-    static constexpr int NC = RB / 16;  // 16-byte chunks per row
-    static constexpr int HC = NC / 2;   // chunks per half row (CUDA-core lanes)
-    static constexpr int KS = D / 16;   // k16 steps over d for Q K^T
-    static constexpr int NB8 = D / 8;   // n8 blocks over d for P V
-};
-
-// byte offset of chunk `ch` of row `row` in a swizzled [rows][RB] tile
-template <int D> __device__ __forceinline__ uint32_t swz(int row, int ch)
-{
-    constexpr int NC = Geo<D>::NC;
-    const int f = NC >= 8 ? (row & 7) : ((row >> 1) & 3);
-    return (uint32_t)(row * Geo<D>::RB + ((ch ^ f) * 16));
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g)
-{
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
-}
-
-__device__ __forceinline__ uint4 lds16(uint32_t a)
-{
-    uint4 u;
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "r"(a));
-    return u;
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t a, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3)
-{
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(a));
-}
-
-__device__ __forceinline__ void ldsm_x4_t(uint32_t a, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3)
-{
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(a));
-}
-
-template <typename T>
-__device__ __forceinline__ void mma16816(float *c, const uint32_t *a, uint32_t b0, uint32_t b1);
-
-template <>
-__device__ __forceinline__ void mma16816<__nv_bfloat16>(float *c, const uint32_t *a, uint32_t b0, uint32_t b1)
-{
-    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-                 "{%0,%1,%2,%3};"
-                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-template <>
-__device__ __forceinline__ void mma16816<__half>(float *c, const uint32_t *a, uint32_t b0, uint32_t b1)
-{
-    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-                 "{%0,%1,%2,%3};"
-                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-template <typename T> __device__ __forceinline__ uint32_t pack2(float lo, float hi);
-template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) { return f2_to_bf2(lo, hi); }
-template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) { return f2_to_h2(lo, hi); }
-
-// c + x.lo*y.lo + x.hi*y.hi with 16-bit inputs and f32 accumulation (FHFMA)
-template <typename T> __device__ __forceinline__ float fma2h(uint32_t x, uint32_t y, float c);
-
-template <> __device__ __forceinline__ float fma2h<__nv_bfloat16>(uint32_t x, uint32_t y, float c)
-{
-    float d;
-    asm("{ .reg .b16 xl, xh, yl, yh; .reg .f32 t; mov.b32 {xl, xh}, %1; mov.b32 {yl, yh}, %2;\n\t"
-        "fma.rn.f32.bf16 t, xl, yl, %3; fma.rn.f32.bf16 %0, xh, yh, t; }"
-        : "=f"(d)
-        : "r"(x), "r"(y), "f"(c));
-    return d;
-}
-
-template <> __device__ __forceinline__ float fma2h<__half>(uint32_t x, uint32_t y, float c)
-{
-    float d;
-    asm("{ .reg .b16 xl, xh, yl, yh; .reg .f32 t; mov.b32 {xl, xh}, %1; mov.b32 {yl, yh}, %2;\n\t"
-        "fma.rn.f32.f16 t, xl, yl, %3; fma.rn.f32.f16 %0, xh, yh, t; }"
-        : "=f"(d)
-        : "r"(x), "r"(y), "f"(c));
-    return d;
-}
-
-// (o0, o1) += p * (v.lo, v.hi), p held in the low half of a 16x2 register
-template <typename T> __device__ __forceinline__ void axpy2h(uint32_t p16x2, uint32_t v, float &o0, float &o1);
-
-template <> __device__ __forceinline__ void axpy2h<__nv_bfloat16>(uint32_t p, uint32_t v, float &o0, float &o1)
-{
-    asm("{ .reg .b16 pl, ph, vl, vh; mov.b32 {pl, ph}, %2; mov.b32 {vl, vh}, %3;\n\t"
-        "fma.rn.f32.bf16 %0, pl, vl, %0; fma.rn.f32.bf16 %1, pl, vh, %1; }"
-        : "+f"(o0), "+f"(o1)
-        : "r"(p), "r"(v));
-}
-
-template <> __device__ __forceinline__ void axpy2h<__half>(uint32_t p, uint32_t v, float &o0, float &o1)
-{
-    asm("{ .reg .b16 pl, ph, vl, vh; mov.b32 {pl, ph}, %2; mov.b32 {vl, vh}, %3;\n\t"
-        "fma.rn.f32.f16 %0, pl, vl, %0; fma.rn.f32.f16 %1, pl, vh, %1; }"
-        : "+f"(o0), "+f"(o1)
-        : "r"(p), "r"(v));
-}
+using tc::Geo;
+using tc::ldsm_x4;
+using tc::ldsm_x4_t;
+using tc::lds16;
+using tc::swz;
+using tc::cp_async16;
 
 struct BandParams {
     AttnParams p;
@@ -157,16 +55,16 @@ template <typename T, int D>
 __device__ __forceinline__ float half_dot(const uint32_t *qv, uint32_t rowaddr, int key, int hf)
 {
     constexpr int HC = Geo<D>::HC;
-    float s0 = 0.f, s1 = 0.f;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f; // four independent FHFMA chains
 #pragma unroll
     for (int k = 0; k < HC; ++k) {
         const uint4 u = lds16(rowaddr + swz<D>(key, hf * HC + k));
         s0 = fma2h<T>(qv[4 * k], u.x, s0);
         s1 = fma2h<T>(qv[4 * k + 1], u.y, s1);
-        s0 = fma2h<T>(qv[4 * k + 2], u.z, s0);
-        s1 = fma2h<T>(qv[4 * k + 3], u.w, s1);
+        s2 = fma2h<T>(qv[4 * k + 2], u.z, s2);
+        s3 = fma2h<T>(qv[4 * k + 3], u.w, s3);
     }
-    float s = s0 + s1;
+    float s = (s0 + s1) + (s2 + s3);
     return s + __shfl_xor_sync(0xffffffffu, s, 1);
 }
 
@@ -436,10 +334,7 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
         if (b < q16) st.block16(kaddr, vaddr, (uint32_t)(b * 16 * G::RB), sl2);
     }
     // ---- finalise: l = quad sum, normalise, stage through this warp's Q rows, store
-    lr[0] += __shfl_xor_sync(0xffffffffu, lr[0], 1);
-    lr[0] += __shfl_xor_sync(0xffffffffu, lr[0], 2);
-    lr[1] += __shfl_xor_sync(0xffffffffu, lr[1], 1);
-    lr[1] += __shfl_xor_sync(0xffffffffu, lr[1], 2);
+    rs.reduce_l();
     const float inv0 = lr[0] > 0.f ? 1.f / lr[0] : 0.f, inv1 = lr[1] > 0.f ? 1.f / lr[1] : 0.f;
     __syncwarp();
 #pragma unroll
