@@ -216,6 +216,8 @@ def main():
     else:
         mask = ga.LongNet(a[0], a[1])
         nnz = ga.mask_count(mask, L)
+        wsb = ga.workspace_size(mask, L, d, H, tdt, q_begin=r0, q_rows=L_local)  # tcgen05 block partials
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
     q = torch.empty((L_local, H, d), dtype=tdt, device=dev)
     ga.fill_inputs(q, seed, 0, r0 * H * d)
     comm = None

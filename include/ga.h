@@ -116,8 +116,11 @@ typedef struct ga_opts {
        every processed row must lie inside (halo / all-gather responsibility of the caller).
        kv_rows = 0 means L - kv_begin. */
     int64_t kv_begin, kv_rows;
-    /* Device workspace (needed by CSR inputs with rows above the heavy-row threshold);
-       size from ga_workspace_size. */
+    /* Device workspace, size from ga_workspace_size: needed by CSR inputs with rows above
+       the heavy-row threshold; optional for LONGNET bf16/fp16 d=64 (partial states of the
+       tcgen05 block path — without it the library takes stream-ordered scratch with
+       cudaMallocAsync from the device's default pool, whose release threshold it raises so
+       freed blocks stay cached). */
     void *workspace;
     size_t workspace_bytes;
     /* Debug / work-optimality probes ("probe build").  When non-NULL a slower
@@ -153,7 +156,8 @@ ga_status ga_attention_ex(const void *Q, const void *K, const void *V, const ga_
 ga_status ga_attention_host(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out,
                             int64_t L, int32_t d, int32_t heads, ga_dtype dtype, void *stream);
 
-/* Workspace bytes ga_attention_ex needs for (mask, shape, opts).  Host only. */
+/* Workspace bytes ga_attention_ex uses for (mask, shape, opts): CSR heavy-row split, or the
+   LongNet tcgen05 block partials ([slots][heads][d+4] fp32).  0 when none.  Host only. */
 ga_status ga_workspace_size(const ga_mask *mask, int64_t L, int32_t d, int32_t heads, ga_dtype dtype,
                             const ga_opts *opts, size_t *bytes);
 

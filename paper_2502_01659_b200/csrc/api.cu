@@ -103,6 +103,26 @@ static ga_status make_devmask(const ga_mask *m, int64_t L, DevMask &M)
 
 static size_t dtype_bytes(ga_dtype dt) { return dt == GA_F32 ? 4 : 2; }
 
+// Stream-ordered scratch (cudaMallocAsync) comes from the current device's default pool;
+// keep freed blocks there between calls instead of returning them to the OS each
+// synchronisation (the default release threshold is 0), so repeated calls do not re-map
+// memory.  Once per device.
+void keep_stream_pool()
+{
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    std::lock_guard<std::mutex> g(mu);
+    if (done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
 static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 static const int64_t kDefaultHeavy = 4096;
@@ -181,6 +201,10 @@ static ga_status dispatch(AttnParams &p, ga_dtype dtype, const ga_opts *opts, in
 {
     const int kernel = opts ? opts->kernel : GA_KERNEL_AUTO;
     const bool probe = p.edge_counter || p.row_fingerprint;
+    if (opts && opts->workspace && opts->workspace_bytes > 0) {
+        p.workspace = opts->workspace;
+        p.workspace_bytes = opts->workspace_bytes;
+    }
     ga_status st;
     if (p.mask.kind == GA_MASK_CSR) {
         const bool split = opts && opts->workspace && opts->workspace_bytes > 0;
@@ -226,9 +250,19 @@ ga_status ga_workspace_size(const ga_mask *mask, int64_t L, int32_t d, int32_t h
     DevMask M;
     ga_status st = make_devmask(mask, L, M);
     if (st != GA_OK) return st;
-    (void)dtype;
-    if (M.kind != GA_MASK_CSR) return GA_OK;
     int64_t q_rows = opts && opts->q_rows > 0 ? opts->q_rows : L - (opts ? opts->q_begin : 0);
+    if (M.kind == GA_MASK_LONGNET) { // tcgen05 block-mode partial states (optional: else stream-ordered)
+        AttnParams p{};
+        p.mask = M;
+        p.d = d;
+        p.H = heads;
+        p.q_begin = opts ? opts->q_begin : 0;
+        p.q_rows = q_rows;
+        const int s_umma = longnet_umma_levels(p, dtype);
+        if (s_umma >= 0 && s_umma < (int)M.K) *bytes = longnet_umma_workspace(p, s_umma + 1);
+        return GA_OK;
+    }
+    if (M.kind != GA_MASK_CSR) return GA_OK;
     int64_t C = opts && opts->heavy_threshold > 0 ? opts->heavy_threshold : kDefaultHeavy;
     *bytes = csr_heavy_workspace(q_rows, mask->nnz, heads, d, C);
     return GA_OK;
@@ -340,15 +374,7 @@ ga_status ga_attention_host(const void *Q, const void *K, const void *V, const g
 {
     if (!Q || !K || !V || !out) { set_error("host buffers must be non-NULL"); return GA_ERR_INVALID_ARG; }
     if (dtype != GA_F32 && dtype != GA_BF16 && dtype != GA_F16) { set_error("dtype invalid"); return GA_ERR_INVALID_ARG; }
-    static std::once_flag once;
-    std::call_once(once, [] {
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX; // keep freed blocks in the pool between calls
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-    });
+    keep_stream_pool();
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const size_t bytes = (size_t)L * heads * d * dtype_bytes(dtype);
     void *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;

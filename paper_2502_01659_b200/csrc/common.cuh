@@ -14,6 +14,7 @@ namespace ga {
 void set_error(const char *fmt, ...);
 ga_status cuda_fail(cudaError_t e, const char *where);
 void note_launches(int n); // telemetry: kernels launched by the library (ga_launch_count)
+void keep_stream_pool();   // default mem pool keeps freed blocks (cudaMallocAsync scratch)
 
 #define GA_CHECK_LAUNCH(where)                                                     \
     do {                                                                           \
@@ -188,6 +189,9 @@ struct AttnParams {
     const char *const *k_peer;
     const char *const *v_peer;
     int64_t shard_rows;
+    // optional caller workspace (ga_opts): CSR heavy-row split, LongNet block partials
+    void *workspace;
+    size_t workspace_bytes;
 };
 
 // Base address (head 0, element 0) of K and V token row j: the local buffer when j is in
@@ -216,6 +220,8 @@ int64_t band_tile_rows(); // class rows per band-kernel tile
 ga_status launch_window_tiled(const AttnParams &p, ga_dtype dt, cudaStream_t s);
 bool longnet_tc_supported(const AttnParams &p, ga_dtype dt);
 ga_status launch_longnet_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s, bool use_umma);
+int longnet_umma_levels(const AttnParams &p, ga_dtype dt);
+size_t longnet_umma_workspace(const AttnParams &p, int h0);
 bool window_tc_supported(const AttnParams &p, ga_dtype dt);
 ga_status launch_window_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s);
 

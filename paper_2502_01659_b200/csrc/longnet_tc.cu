@@ -367,7 +367,26 @@ bool longnet_tc_supported(const AttnParams &p, ga_dtype dt)
 }
 
 ga_status launch_longnet_umma(const AttnParams &p, ga_dtype dt, int64_t seg0, int64_t n_seg, int s_max,
-                              cudaStream_t s);
+                              float *partials, cudaStream_t s);
+size_t longnet_umma_workspace(const AttnParams &p, int h0);
+
+// groups s = 0..s_umma fill 128-row tiles (about w0/a^t - w0/a^(t+1) rows): tcgen05 group
+// mode; -1 when none does (then the mma.sync kernel takes every group)
+int longnet_umma_levels(const AttnParams &p, ga_dtype dt)
+{
+    const DevMask &M = p.mask;
+    int s_umma = -1;
+    if (p.d == 64 && (dt == GA_BF16 || dt == GA_F16)) {
+        int64_t st2 = 1;
+        for (int t = 0; t <= M.K; ++t) {
+            const int64_t rows_t = t < M.K ? M.w0 / st2 - M.w0 / (st2 * M.alpha) : M.w0 / st2;
+            if (rows_t < 128) break;
+            s_umma = t;
+            st2 *= M.alpha;
+        }
+    }
+    return s_umma;
+}
 
 ga_status launch_longnet_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s, bool use_umma)
 {
@@ -387,22 +406,32 @@ ga_status launch_longnet_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s, bo
         cnt[t] = M.w0 / stp + 1;
         stp *= M.alpha;
     }
-    // groups that fill 128-row tiles (about w0/a^t - w0/a^(t+1) rows) run on tcgen05 (d = 64)
-    int s_umma = -1;
-    if (use_umma && p.d == 64 && (dt == GA_BF16 || dt == GA_F16)) {
-        int64_t st2 = 1;
-        for (int t = 0; t <= M.K; ++t) {
-            const int64_t rows_t = t < M.K ? M.w0 / st2 - M.w0 / (st2 * M.alpha) : M.w0 / st2;
-            if (rows_t < 128) break;
-            s_umma = t;
-            st2 *= M.alpha;
-        }
-    }
+    // tcgen05: groups s <= s_umma in group mode, the rows with s > s_umma block-wise with
+    // partial states (workspace: the caller's, else stream-ordered) and a merge
+    const int s_umma = use_umma ? longnet_umma_levels(p, dt) : -1;
+    int s_done = s_umma; // groups s > s_done still need the mma.sync kernel
     if (s_umma >= 0) {
-        ga_status st = launch_longnet_umma(p, dt, lp.seg0, lp.n_seg, s_umma, s);
+        float *partials = nullptr;
+        bool owned = false;
+        if (s_umma < (int)M.K) {
+            const size_t need = longnet_umma_workspace(p, s_umma + 1);
+            if (p.workspace && p.workspace_bytes >= need) {
+                partials = reinterpret_cast<float *>(p.workspace);
+            } else {
+                void *w = nullptr;
+                keep_stream_pool();
+                cudaError_t e = cudaMallocAsync(&w, need, s);
+                if (e != cudaSuccess) return cuda_fail(e, "LongNet partials: cudaMallocAsync");
+                partials = reinterpret_cast<float *>(w);
+                owned = true;
+            }
+        }
+        ga_status st = launch_longnet_umma(p, dt, lp.seg0, lp.n_seg, s_umma, partials, s);
+        if (owned) cudaFreeAsync(partials, s);
         if (st != GA_OK) return st;
+        s_done = (int)M.K;
     }
-    for (int t = (int)M.K; t > s_umma; --t) {
+    for (int t = (int)M.K; t > s_done; --t) {
         const int64_t tiles = (cnt[t] + lnet::ROWS - 1) / lnet::ROWS;
         for (int64_t k = 0; k < tiles; ++k) {
             if (n >= lnet::MAX_ITEMS) { set_error("LongNet: too many work items"); return GA_ERR_UNSUPPORTED; }

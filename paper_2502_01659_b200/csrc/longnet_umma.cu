@@ -15,8 +15,19 @@
 //                     memory, fp32 accumulator in TMEM
 //
 // One elected thread issues the MMAs; completion is signalled through tcgen05.commit ->
-// mbarrier.  Two CTAs per SM overlap one CTA's softmax with the other's MMAs.  Groups with
-// fewer than 128 rows stay on the mma.sync kernel (longnet_tc.cu).
+// mbarrier.  Two CTAs per SM overlap one CTA's softmax with the other's MMAs.
+//
+// Small groups (high valuation s: few rows, many keys) would waste most of a 128-row tile,
+// so the rows with s >= h0 ("high rows") are processed BLOCK-wise instead: the LongNet
+// mask restricted to them is the disjoint union, over levels t and level-t segments sigma,
+// of the dense blocks (SURVEY §8(a) strided-block decomposition)
+//     B(t, sigma) = { i in sigma : alpha^max(t+1,h0) | i } x { j in sigma : nu(j) = t }     t < K
+//     A(t, sigma) = { i in sigma : min(nu(i),K) = t }      x { j in sigma : alpha^t | j }   t >= h0
+// (a high row with s = min(nu(i),K) meets B at levels 0..s-1 and A at level s: exactly its
+// pieces of masks.cuh).  Every block has >= 128 rows at the cfg4 shape, so it runs on the
+// same tcgen05 pipeline; each block writes a partial (m, l, o~) per row and level, and
+// longnet_merge_kernel combines a row's s + 1 partials with the associative (+) (P:374's
+// split-and-merge, as in csr_heavy.cu).
 #include <type_traits>
 
 #include "tc_common.cuh"
@@ -30,12 +41,24 @@ using namespace umma;
 constexpr int ROWS = 128, THREADS = 128, KC = 64, STAGES = 4;
 constexpr int MAX_ITEMS = 64, MAX_PIECES = 64;
 
+constexpr int MAX_BLK = 128; // block-mode work entries (level, kind)
+
 struct UParams {
     AttnParams p;
+    // group mode: items (s, tile) over the level-0 segments seg0 .. seg0 + n_seg
     int64_t seg0, n_seg;
     int32_t n_items;
     int16_t item_s[MAX_ITEMS];
     int16_t item_tile[MAX_ITEMS];
+    // block mode (blocked = 1): entry e covers CTAs [blk_start[e], blk_start[e+1]) =
+    // blk_nseg[e] level-t segments from blk_seg0[e] x blk_tiles[e] row tiles x H
+    int32_t blocked, n_blk, h0;
+    int16_t blk_t[MAX_BLK], blk_kind[MAX_BLK]; // kind 0 = B (nu(j) = t keys), 1 = A (last piece)
+    int32_t blk_tiles[MAX_BLK];
+    int64_t blk_seg0[MAX_BLK], blk_nseg[MAX_BLK], blk_start[MAX_BLK + 1];
+    // partial slots: level t of high row i -> slot_off[t] + i / alpha^max(t,h0) - slot_first[t]
+    int64_t slot_off[MAX_PIECES], slot_first[MAX_PIECES];
+    float *partials; // [slots][H][D + 4]: m, l, (2 pad), o~ — 16-byte aligned o~
 };
 
 template <int D> __host__ __device__ constexpr uint32_t smem_bytes()
@@ -70,31 +93,62 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
     const int tid = threadIdx.x, warp = tid >> 5;
     const int H = p.H;
 
-    const int64_t IH = (int64_t)up.n_items * H;
-    const int64_t segl = (int64_t)blockIdx.x / IH;
-    const int64_t rem = (int64_t)blockIdx.x - segl * IH;
-    const int64_t item = rem / H;
-    const int h = (int)(rem - item * H);
-    const int64_t seg = up.seg0 + segl;
-    const int s = up.item_s[item], tile = up.item_tile[item];
-    const int64_t S0 = seg * M.w0, S1 = imin(M.L, S0 + M.w0);
+    // ---- work item -> (segment [S0, S1), row progression, key pieces)
+    int64_t S0, S1, seg_len, row_step; // rows: candidates (f0 + q) * row_step in [lo, hi)
+    int s, tile, h, np, t_first;      // pieces t_first .. t_first + np - 1 of the rows
+    bool skip_res;                    // drop the candidates whose q has residue rx mod alpha
+    if (!up.blocked) {
+        const int64_t IH = (int64_t)up.n_items * H;
+        const int64_t segl = (int64_t)blockIdx.x / IH;
+        const int64_t rem = (int64_t)blockIdx.x - segl * IH;
+        const int64_t item = rem / H;
+        h = (int)(rem - item * H);
+        s = up.item_s[item];
+        tile = up.item_tile[item];
+        seg_len = M.w0;
+        S0 = (up.seg0 + segl) * M.w0;
+        row_step = 1;
+        for (int t = 0; t < s; ++t) row_step *= M.alpha;
+        skip_res = s != (int)M.K;
+        np = s + 1;
+        t_first = 0;
+    } else {
+        int e = 0;
+        while (e + 1 < up.n_blk && up.blk_start[e + 1] <= (int64_t)blockIdx.x) ++e;
+        const int64_t rel = (int64_t)blockIdx.x - up.blk_start[e];
+        const int64_t TH = (int64_t)up.blk_tiles[e] * H;
+        const int64_t segl = rel / TH, rem = rel - segl * TH;
+        tile = (int)(rem / H);
+        h = (int)(rem - (int64_t)tile * H);
+        const int t = up.blk_t[e];
+        seg_len = M.w0;
+        for (int u = 0; u < t; ++u) seg_len *= M.alpha;
+        S0 = (up.blk_seg0[e] + segl) * seg_len;
+        const int ex = up.blk_kind[e] == 0 ? (t + 1 > up.h0 ? t + 1 : up.h0) : t;
+        row_step = 1;
+        for (int u = 0; u < ex; ++u) row_step *= M.alpha;
+        skip_res = up.blk_kind[e] == 1 && t != (int)M.K; // A rows: valuation exactly t
+        s = t;
+        np = 1;
+        t_first = t;
+    }
+    S1 = imin(M.L, S0 + seg_len);
     const int64_t q_end = p.q_begin + p.q_rows;
 
-    // ---- group rows (closed form, see longnet_tc.cu)
-    int64_t step = 1;
-    for (int t = 0; t < s; ++t) step *= M.alpha;
+    // ---- rows (closed form, see longnet_tc.cu): candidates (f0 + q) * row_step in [lo, hi);
+    // skip_res drops q with residue rx mod alpha (those have a higher valuation)
+    const int64_t step = row_step;
     const int64_t lo = imax(S0, p.q_begin), hi = imin(S1, q_end);
     const int64_t f0 = (lo + step - 1) / step;
     const int64_t nq = lo < hi && f0 * step < hi ? (hi - 1) / step - f0 + 1 : 0;
-    const bool top = s == (int)M.K;
     const int64_t rx = (M.alpha - f0 % M.alpha) % M.alpha;
-    const int64_t count = top ? nq : nq - (nq > rx ? (nq - 1 - rx) / M.alpha + 1 : 0);
+    const int64_t count = !skip_res ? nq : nq - (nq > rx ? (nq - 1 - rx) / M.alpha + 1 : 0);
     const int nrows = (int)imin(ROWS, count - (int64_t)tile * ROWS);
     if (nrows <= 0) return;
     if (tid < nrows) {
         const int64_t r = (int64_t)tile * ROWS + tid;
         int64_t q = r;
-        if (!top) {
+        if (skip_res) {
             const int64_t a1 = M.alpha - 1, idx = r % a1;
             q = (r / a1) * M.alpha + (idx < rx ? idx : idx + 1);
         }
@@ -121,8 +175,7 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
 
     __shared__ Piece spiece[MAX_PIECES];
     __shared__ int pstart[MAX_PIECES + 1];
-    const int np = s + 1;
-    if (tid < np) spiece[tid] = get_piece(M, rows[0], tid);
+    if (tid < np) spiece[tid] = get_piece(M, rows[0], t_first + tid);
     __syncthreads();
     if (tid == 0) {
         pstart[0] = 0;
@@ -337,7 +390,16 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
             }
         }
     }
-    if (row_ok) {
+    if (row_ok && up.blocked) { // partial state of (row, level s) for the merge kernel
+        int64_t stp = 1;
+        for (int u = 0; u < (s > up.h0 ? s : up.h0); ++u) stp *= M.alpha;
+        const int64_t slot = up.slot_off[s] + rows[tid] / stp - up.slot_first[s];
+        float *dst = up.partials + ((size_t)slot * H + h) * (D + 4);
+        *reinterpret_cast<float4 *>(dst) = make_float4(m_run, l_run, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < D / 4; ++q)
+            *reinterpret_cast<float4 *>(dst + 4 + 4 * q) = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+    } else if (row_ok) {
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
         char *Og = reinterpret_cast<char *>(p.out) + (size_t)h * D * sizeof(T) + (size_t)(rows[tid] - p.q_begin) * row_bytes;
 #pragma unroll
@@ -356,7 +418,49 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
     }
 }
 
-template <typename T, int D> static ga_status launch_t(const UParams &up, cudaStream_t s)
+// One warp per (high row, head): combine the row's partials of levels 0..s with the
+// associative (m, l, o~) (+) and store o~ / l (empty -> 0).
+template <typename T, int D>
+__global__ void __launch_bounds__(256) longnet_merge_kernel(const UParams up, int64_t first, int64_t n_high,
+                                                            int64_t step_h0)
+{
+    const AttnParams &p = up.p;
+    const DevMask &M = p.mask;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int H = p.H;
+    if (gw >= n_high * H) return;
+    const int64_t r = gw / H;
+    const int h = (int)(gw - r * H);
+    const int64_t i = (first + r) * step_h0;
+    int s = 0; // min(nu(i), K), nu(0) = K
+    if (i == 0) s = (int)M.K;
+    else for (int64_t x = i; s < (int)M.K && x % M.alpha == 0; x /= M.alpha) ++s;
+    constexpr int PER = D / 32;
+    float m = -INFINITY, l = 0.f, o[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) o[e] = 0.f;
+    int64_t stp = 1;
+    for (int u = 0; u < up.h0; ++u) stp *= M.alpha;
+    for (int t = 0; t <= s; ++t) {
+        if (t > up.h0) stp *= M.alpha; // alpha^max(t, h0)
+        const float *src = up.partials + ((size_t)(up.slot_off[t] + i / stp - up.slot_first[t]) * H + h) * (D + 4);
+        const float m2 = src[0], l2 = src[1];
+        const float mn = fmaxf(m, m2);
+        const float a = m == -INFINITY ? 0.f : ex2(m - mn);
+        const float b = m2 == -INFINITY ? 0.f : ex2(m2 - mn);
+        l = l * a + l2 * b;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) o[e] = o[e] * a + src[4 + lane + 32 * e] * b;
+        m = mn;
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    T *Op = reinterpret_cast<T *>(p.out) + ((size_t)(i - p.q_begin) * H + h) * D;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) Op[lane + 32 * e] = (T)(o[e] * inv);
+}
+
+template <typename T, int D> static ga_status launch_t(const UParams &up, int64_t blocks, cudaStream_t s)
 {
     static bool configured = false;
     if (!configured) {
@@ -365,43 +469,138 @@ template <typename T, int D> static ga_status launch_t(const UParams &up, cudaSt
         if (e != cudaSuccess) return cuda_fail(e, "longnet_umma_kernel: set smem");
         configured = true;
     }
-    const int64_t blocks = (int64_t)up.n_items * up.n_seg * up.p.H;
     if (blocks == 0) return GA_OK;
+    if (blocks > (int64_t)INT32_MAX) { set_error("LongNet tcgen05 grid too large"); return GA_ERR_UNSUPPORTED; }
     longnet_umma_kernel<T, D><<<(unsigned)blocks, THREADS, smem_bytes<D>(), s>>>(up);
     GA_CHECK_LAUNCH("longnet_umma_kernel");
     return GA_OK;
 }
 
+static int64_t ipow(int64_t a, int e)
+{
+    int64_t r = 1;
+    while (e-- > 0) r *= a;
+    return r;
+}
+
+// multiples of q in [a, b): first index ceil(a/q) and count
+static void multiples(int64_t a, int64_t b, int64_t q, int64_t &first, int64_t &n)
+{
+    first = (a + q - 1) / q;
+    n = b > a && first * q < b ? (b - 1) / q - first + 1 : 0;
+}
+
+// Block-mode plan for the high rows (s >= h0) of the query range: work entries and the
+// partial-slot layout.  Returns the number of partial slots.
+static int64_t plan_blocks(const AttnParams &p, int h0, UParams &up, int64_t &blocks)
+{
+    const DevMask &M = p.mask;
+    const int K = (int)M.K;
+    const int64_t qb = p.q_begin, qe = p.q_begin + p.q_rows;
+    int64_t slots = 0;
+    for (int t = 0; t <= K; ++t) {
+        int64_t f, n;
+        multiples(qb, qe, ipow(M.alpha, t > h0 ? t : h0), f, n);
+        up.slot_off[t] = slots;
+        up.slot_first[t] = f;
+        slots += n;
+    }
+    up.blocked = 1;
+    up.h0 = h0;
+    int e = 0;
+    blocks = 0;
+    for (int t = 0; t <= K; ++t) {
+        const int64_t W = M.w0 * ipow(M.alpha, t);
+        const int64_t seg_lo = qb / W, seg_hi = (qe + W - 1) / W;
+        for (int kind = 0; kind < 2; ++kind) {
+            if (kind == 0 && t >= K) continue; // B: t < K
+            if (kind == 1 && t < h0) continue; // A: levels of the high rows' last piece
+            const int ex = kind == 0 ? (t + 1 > h0 ? t + 1 : h0) : t;
+            const int64_t qs = ipow(M.alpha, ex), rows_max = (W + qs - 1) / qs; // most multiples in W tokens
+            if (e >= MAX_BLK) return -1;
+            up.blk_t[e] = (int16_t)t;
+            up.blk_kind[e] = (int16_t)kind;
+            up.blk_tiles[e] = (int32_t)((rows_max + ROWS - 1) / ROWS);
+            up.blk_seg0[e] = seg_lo;
+            up.blk_nseg[e] = seg_hi - seg_lo;
+            up.blk_start[e] = blocks;
+            blocks += (int64_t)up.blk_tiles[e] * up.blk_nseg[e] * p.H;
+            ++e;
+        }
+    }
+    up.n_blk = e;
+    up.blk_start[e] = blocks;
+    return slots;
+}
+
 } // namespace lnet_umma
 
-// Launch the tcgen05 kernel on the groups s = 0..s_max (those that fill 128-row tiles);
-// the caller runs the remaining groups on the mma.sync kernel.
-ga_status launch_longnet_umma(const AttnParams &p, ga_dtype dt, int64_t seg0, int64_t n_seg, int s_max,
-                              cudaStream_t s)
+size_t longnet_umma_workspace(const AttnParams &p, int h0)
 {
-    lnet_umma::UParams up;
-    up.p = p;
-    up.seg0 = seg0;
-    up.n_seg = n_seg;
-    const DevMask &M = p.mask;
-    int n = 0;
-    int64_t stp = 1;
-    for (int t = 0; t <= s_max; ++t) {
-        const int64_t cnt = M.w0 / stp + 1;
-        const int64_t tiles = (cnt + lnet_umma::ROWS - 1) / lnet_umma::ROWS;
-        for (int64_t k = 0; k < tiles; ++k) {
-            if (n >= lnet_umma::MAX_ITEMS) { set_error("LongNet tcgen05: too many items"); return GA_ERR_UNSUPPORTED; }
-            up.item_s[n] = (int16_t)t;
-            up.item_tile[n] = (int16_t)k;
-            ++n;
-        }
-        stp *= M.alpha;
+    lnet_umma::UParams up{};
+    int64_t blocks = 0;
+    const int64_t slots = lnet_umma::plan_blocks(p, h0, up, blocks);
+    return slots < 0 ? 0 : (size_t)slots * p.H * (p.d + 4) * sizeof(float) + 256;
+}
+
+// Launch the tcgen05 kernel on the groups s = 0..s_max (those that fill 128-row tiles);
+// with `partials` (workspace of longnet_umma_workspace bytes) the rows with s > s_max run
+// block-wise on tcgen05 too and are merged; otherwise the caller runs them elsewhere.
+ga_status launch_longnet_umma(const AttnParams &p, ga_dtype dt, int64_t seg0, int64_t n_seg, int s_max,
+                              float *partials, cudaStream_t s)
+{
+    if (!(p.d == 64 && (dt == GA_BF16 || dt == GA_F16))) {
+        set_error("LongNet tcgen05 kernel: unsupported d/dtype");
+        return GA_ERR_UNSUPPORTED;
     }
-    up.n_items = n;
-    if (p.d == 64 && dt == GA_BF16) return lnet_umma::launch_t<__nv_bfloat16, 64>(up, s);
-    if (p.d == 64 && dt == GA_F16) return lnet_umma::launch_t<__half, 64>(up, s);
-    set_error("LongNet tcgen05 kernel: unsupported d/dtype");
-    return GA_ERR_UNSUPPORTED;
+    auto launch = [&](const lnet_umma::UParams &up, int64_t blocks) {
+        return dt == GA_BF16 ? lnet_umma::launch_t<__nv_bfloat16, 64>(up, blocks, s)
+                             : lnet_umma::launch_t<__half, 64>(up, blocks, s);
+    };
+    const DevMask &M = p.mask;
+    if (s_max >= 0) { // group mode
+        lnet_umma::UParams up{};
+        up.p = p;
+        up.seg0 = seg0;
+        up.n_seg = n_seg;
+        int n = 0;
+        int64_t stp = 1;
+        for (int t = 0; t <= s_max; ++t) {
+            const int64_t cnt = (M.w0 + stp - 1) / stp; // most multiples of a^t in a w0 segment
+            const int64_t tiles = (cnt + lnet_umma::ROWS - 1) / lnet_umma::ROWS;
+            for (int64_t k = 0; k < tiles; ++k) {
+                if (n >= lnet_umma::MAX_ITEMS) { set_error("LongNet tcgen05: too many items"); return GA_ERR_UNSUPPORTED; }
+                up.item_s[n] = (int16_t)t;
+                up.item_tile[n] = (int16_t)k;
+                ++n;
+            }
+            stp *= M.alpha;
+        }
+        up.n_items = n;
+        ga_status st = launch(up, (int64_t)n * n_seg * p.H);
+        if (st != GA_OK) return st;
+    }
+    if (!partials || s_max >= (int)M.K) return GA_OK;
+    // block mode for the high rows + merge
+    lnet_umma::UParams ub{};
+    ub.p = p;
+    ub.partials = partials;
+    int64_t blocks = 0;
+    if (lnet_umma::plan_blocks(p, s_max + 1, ub, blocks) < 0) { set_error("LongNet: too many levels"); return GA_ERR_UNSUPPORTED; }
+    ga_status st = launch(ub, blocks);
+    if (st != GA_OK) return st;
+    int64_t first, n_high;
+    const int64_t step_h0 = lnet_umma::ipow(M.alpha, s_max + 1);
+    lnet_umma::multiples(p.q_begin, p.q_begin + p.q_rows, step_h0, first, n_high);
+    const int64_t warps = n_high * p.H;
+    if (warps == 0) return GA_OK;
+    const int64_t mblocks = (warps + 7) / 8;
+    if (dt == GA_BF16)
+        lnet_umma::longnet_merge_kernel<__nv_bfloat16, 64><<<(unsigned)mblocks, 256, 0, s>>>(ub, first, n_high, step_h0);
+    else
+        lnet_umma::longnet_merge_kernel<__half, 64><<<(unsigned)mblocks, 256, 0, s>>>(ub, first, n_high, step_h0);
+    GA_CHECK_LAUNCH("longnet_merge_kernel");
+    return GA_OK;
 }
 
 } // namespace ga

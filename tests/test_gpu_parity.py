@@ -348,6 +348,28 @@ def test_repeat_launches_bitwise(ga, fam, args, kernel):
     assert torch.equal(part, ref[r0:])
 
 
+@pytest.mark.parametrize("L,w0,alpha", [(65536, 2048, 2), (20000, 1000, 3), (5000, 300, 2)])
+def test_longnet_block_partials_workspace(ga, orc, L, w0, alpha):
+    """High-valuation rows run block-wise on tcgen05 with partial states merged at the end;
+    the partials live in the caller's workspace or in stream-ordered scratch: identical
+    bytes either way, and a query sub-range computes the same rows."""
+    H, d = 2, 64
+    q, k, v = ga.qkv_device(L + 3, L, H, d, torch.bfloat16)
+    m = ga.LongNet(w0, alpha)
+    nbytes = ga.workspace_size(m, L, d, H, torch.bfloat16)
+    assert nbytes > 0
+    ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    a = ga.attention(q, k, v, m, kernel="tc")
+    b = ga.attention(q, k, v, m, kernel="tc", workspace=ws)
+    assert torch.equal(a, b)
+    r0 = (L // 3 // w0) * w0
+    part = ga.attention(q[r0:].contiguous(), k, v, m, L=L, q_begin=r0, kernel="tc")
+    assert torch.equal(part, a[r0:])
+    cpu = tuple(x.cpu() for x in (q, k, v))
+    want, _ = orc.attention(*(synth.as_f64(x) for x in cpu), orc.longnet(L, w0, alpha))
+    assert np.abs(a.double().cpu().numpy() - want).max() <= TOL["bf16"]
+
+
 @pytest.mark.parametrize("fam,L,args,kernel", [
     ("longnet", 10000, (256, 2), "tc"), ("longnet", 5000, (300, 2), "tc"), ("longnet", 20000, (1000, 3), "tc"),
     ("longnet", 10000, (100, 3), "tiled"), ("longnet", 10000, (256, 2), "edge"),
