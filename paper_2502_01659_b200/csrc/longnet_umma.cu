@@ -38,7 +38,8 @@ namespace lnet_umma {
 using namespace tc;
 using namespace umma;
 
-constexpr int ROWS = 128, THREADS = 128, KC = 64, STAGES = 4;
+// warps 0-3: softmax (thread = row = TMEM lane); warp 4: loader (cp.async ring); warp 5: MMA
+constexpr int ROWS = 128, SM_THREADS = 128, THREADS = SM_THREADS + 64, KC = 64, STAGES = 4;
 constexpr int MAX_ITEMS = 64, MAX_PIECES = 64;
 
 constexpr int MAX_BLK = 128; // block-mode work entries (level, kind)
@@ -64,7 +65,7 @@ struct UParams {
 template <int D> __host__ __device__ constexpr uint32_t smem_bytes()
 {
     return 1024 /* alignment slack */ + ROWS * 2 * D /* Q */ + STAGES * 2 * KC * 2 * D /* K,V */ + ROWS * 8 /* rows */ +
-           64 /* mbarriers, tmem base */;
+           256 /* mbarriers, tmem base */;
 }
 
 // TMEM columns: S[2] at 0 and KC, P[2] (16-bit pairs) at 2KC and 2KC + KC/2, O at 3KC
@@ -84,9 +85,14 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
     const uint32_t sV0 = sK0 + STAGES * KC * RB;
     int64_t *rows = reinterpret_cast<int64_t *>(sgen + ROWS * RB + 2 * STAGES * KC * RB);
     uint64_t *mbars = reinterpret_cast<uint64_t *>(rows + ROWS);
-    uint32_t *tmem_base_smem = reinterpret_cast<uint32_t *>(mbars + 4);
-    const uint32_t mbS[2] = {(uint32_t)__cvta_generic_to_shared(&mbars[0]), (uint32_t)__cvta_generic_to_shared(&mbars[1])};
-    const uint32_t mbO[2] = {(uint32_t)__cvta_generic_to_shared(&mbars[2]), (uint32_t)__cvta_generic_to_shared(&mbars[3])};
+    uint32_t *tmem_base_smem = reinterpret_cast<uint32_t *>(mbars + 7 + 2 * STAGES);
+    const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(mbars);
+    const uint32_t mbS[2] = {mb0, mb0 + 8};       // S_c complete (tcgen05.commit)
+    const uint32_t mbO[2] = {mb0 + 16, mb0 + 24}; // P V_c complete (tcgen05.commit)
+    const uint32_t mbP[2] = {mb0 + 32, mb0 + 40}; // P_c written by the 128 softmax threads
+    const uint32_t mbQ = mb0 + 48;                // Q tile landed (32 loader lanes)
+    const uint32_t mbFull0 = mb0 + 56;            // stage st landed: mbFull0 + 8 st (32 lanes)
+    const uint32_t mbEmpty0 = mbFull0 + 8 * STAGES; // stage st consumed (P V commit)
 
     const AttnParams &p = up.p;
     const DevMask &M = p.mask;
@@ -165,6 +171,12 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
         for (int b = 0; b < 2; ++b) {
             mbar_init(mbS[b], 1);
             mbar_init(mbO[b], 1);
+            mbar_init(mbP[b], SM_THREADS);
+        }
+        mbar_init(mbQ, 32);
+        for (int st = 0; st < STAGES; ++st) {
+            mbar_init(mbFull0 + 8 * st, 32);
+            mbar_init(mbEmpty0 + 8 * st, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -190,161 +202,166 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
     const size_t row_bytes = (size_t)H * D * sizeof(T);
     const char *Qg = reinterpret_cast<const char *>(p.Q) + (size_t)h * D * sizeof(T);
     const size_t hoff = (size_t)h * D * sizeof(T);
+    const uint32_t idS = idesc<T>(ROWS, KC, false), idO = idesc<T>(ROWS, D, true);
 
-    int cur_t = 0;
-    auto load_chunk = [&](int c) {
-        const int st = c % STAGES;
-        const int kl = tid >> 1, hf = tid & 1; // 2 threads per key
-        const int k = c * KC + kl;
-        if (k < nblk * 16) {
-            while (cur_t + 1 < np && pstart[cur_t + 1] <= k) ++cur_t;
-            const char *kr, *vr;
-            kv_row(p, piece_at(spiece[cur_t], k - pstart[cur_t]), row_bytes, kr, vr);
-#pragma unroll
-            for (int q = 0; q < D / 16; ++q) {
-                const int cc = hf * (D / 16) + q;
-                cp_async16(sK0 + st * KC * RB + swz<D>(kl, cc), kr + hoff + cc * 16);
-                cp_async16(sV0 + st * KC * RB + swz<D>(kl, cc), vr + hoff + cc * 16);
-            }
-        } else if (c < nchunks) { // keys past the last whole block in the final chunk: zero
-            // K/V rows (the stage holds an older chunk's keys), their scores are masked below
-#pragma unroll
-            for (int q = 0; q < D / 16; ++q) {
-                const int cc = hf * (D / 16) + q;
-                sts_zero16(sK0 + st * KC * RB + swz<D>(kl, cc));
-                sts_zero16(sV0 + st * KC * RB + swz<D>(kl, cc));
-            }
+    if (warp == 4) {
+        // =================== loader warp: Q tile, then the K/V ring ===================
+        const int lane = tid & 31;
+        // Q rows (pad rows zeroed: they join the softmax warps' rescale votes)
+        for (int idx = lane; idx < ROWS * (RB / 16); idx += 32) {
+            const int r = idx / (RB / 16), cc = idx % (RB / 16);
+            if (r < nrows)
+                cp_async16(sQ + swz<D>(r, cc), Qg + (size_t)(rows[r] - p.q_begin) * row_bytes + cc * 16);
+            else
+                sts_zero16(sQ + swz<D>(r, cc));
         }
-        cp_async_commit();
-    };
-    // pad rows (>= nrows) are zeroed: they join the warp-uniform rescale vote
-    for (int idx = tid; idx < ROWS * (RB / 16); idx += THREADS) {
-        const int r = idx / (RB / 16), cc = idx % (RB / 16);
-        if (r < nrows)
-            cp_async16(sQ + swz<D>(r, cc), Qg + (size_t)(rows[r] - p.q_begin) * row_bytes + cc * 16);
-        else
-            sts_zero16(sQ + swz<D>(r, cc));
-    }
+        fence_proxy_async();
+        cp_async_mbar_arrive(mbQ);
+        // chunk c -> stage c % STAGES: 32 lanes x 2 keys, whole K and V rows per lane
+        // (16-byte cp.async); keys past the last whole 16-key block are zeroed (masked)
+        int cur_t = 0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int st = c % STAGES;
+            if (c >= STAGES) mbar_wait(mbEmpty0 + 8 * st, ((c / STAGES) - 1) & 1);
 #pragma unroll
-    for (int c = 0; c < STAGES - 1; ++c) load_chunk(c); // stages 0..S-2 (empty groups are fine)
+            for (int half = 0; half < 2; ++half) {
+                const int kl = lane + 32 * half, k = c * KC + kl;
+                if (k < nblk * 16) {
+                    while (cur_t + 1 < np && pstart[cur_t + 1] <= k) ++cur_t;
+                    const char *kr, *vr;
+                    kv_row(p, piece_at(spiece[cur_t], k - pstart[cur_t]), row_bytes, kr, vr);
+#pragma unroll
+                    for (int cc = 0; cc < RB / 16; ++cc) {
+                        cp_async16(sK0 + st * KC * RB + swz<D>(kl, cc), kr + hoff + cc * 16);
+                        cp_async16(sV0 + st * KC * RB + swz<D>(kl, cc), vr + hoff + cc * 16);
+                    }
+                } else {
+#pragma unroll
+                    for (int cc = 0; cc < RB / 16; ++cc) {
+                        sts_zero16(sK0 + st * KC * RB + swz<D>(kl, cc));
+                        sts_zero16(sV0 + st * KC * RB + swz<D>(kl, cc));
+                    }
+                }
+            }
+            fence_proxy_async();
+            cp_async_mbar_arrive(mbFull0 + 8 * st);
+        }
+        cp_async_wait<0>();
+    } else if (warp == 5) {
+        // =================== MMA warp: S_c = Q K_c^T, then O += P_{c-1} V_{c-1} ===================
+        const int lane = tid & 31;
+        auto issue_PV = [&](int c) { // after P_c arrived
+            mbar_wait(mbP[c & 1], (c >> 1) & 1);
+            if (lane == 0) {
+                fence_after();
+                const uint32_t bv = sV0 + (c % STAGES) * KC * RB;
+#pragma unroll
+                for (int kk = 0; kk < KC / 16; ++kk) // 16 keys per MMA: 8 P columns, 16 V rows
+                    mma_ts(tmem + COL_O, tmem + COL_P + (c & 1) * (KC / 2) + kk * 8, sdesc_sw128(bv + kk * 16 * RB),
+                           idO, (c > 0 || kk > 0));
+                mma_commit(mbO[c & 1]);
+                mma_commit(mbEmpty0 + 8 * (c % STAGES)); // S_c and P V_c have read the stage
+            }
+            __syncwarp();
+        };
+        if (nchunks > 0) mbar_wait(mbQ, 0);
+        for (int c = 0; c < nchunks; ++c) {
+            // stage c landed; S buffer c&1 was last read by the softmax of chunk c-2, done
+            // before P_{c-2} arrived (waited in issue_PV(c-2))
+            mbar_wait(mbFull0 + 8 * (c % STAGES), (c / STAGES) & 1);
+            if (lane == 0) {
+                fence_after();
+                const uint32_t bk = sK0 + (c % STAGES) * KC * RB;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) // K = 16 per MMA: +32 B inside the swizzle atom
+                    mma_ss(tmem + COL_S + (c & 1) * KC, sdesc_sw128(sQ + kk * 32), sdesc_sw128(bk + kk * 32), idS,
+                           kk > 0);
+                mma_commit(mbS[c & 1]);
+            }
+            __syncwarp();
+            if (c >= 1) issue_PV(c - 1);
+        }
+        if (nchunks > 0) issue_PV(nchunks - 1);
+    }
 
-    // thread = row = TMEM lane; warp w reads lanes [32w, 32w+32)
-    const uint32_t tlane = tmem + ((uint32_t)(warp * 32) << 16);
+    // =================== softmax warps: thread = row = TMEM lane ===================
+    const uint32_t tlane = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const float sl2 = p.scale_log2;
     constexpr float kTau = 8.f;
     float m_run = -INFINITY, l_run = 0.f;
-    const uint32_t idS = idesc<T>(ROWS, KC, false), idO = idesc<T>(ROWS, D, true);
-    // Software pipeline: S_{c+1} runs on the tensor core while chunk c's softmax runs.
-    // S_c -> TMEM S[c&1] (mbarrier mbS[c&1]); P_c -> P[c&1]; P V_c -> O (mbO[c&1]).  The
-    // k-th use of a double-buffer slot completes its mbarrier phase with parity k & 1.
-    auto issue_S = [&](int c) {
-        if (tid == 0) {
-            fence_after();
-            const uint32_t bk = sK0 + (c % STAGES) * KC * RB;
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) // K = 16 per MMA: +32 B inside the swizzle atom
-                mma_ss(tmem + COL_S + (c & 1) * KC, sdesc_sw128(sQ + kk * 32), sdesc_sw128(bk + kk * 32), idS,
-                       kk > 0);
-            mma_commit(mbS[c & 1]);
-        }
-    };
     auto wait_O = [&](int c) { // P V_c complete
         mbar_wait(mbO[c & 1], (c >> 1) & 1);
         fence_after();
     };
-    if (nchunks > 0) { // prologue: chunk 0 (and Q) landed -> S_0
-        cp_async_wait<STAGES - 2>();
-        fence_proxy_async();
-        __syncthreads();
-        issue_S(0);
-    }
-    for (int c = 0; c < nchunks; ++c) {
-        const int st = c % STAGES;
-        // 1. S_{c+1} (chunks 0..c+2 committed; c+1 must have landed)
-        if (c + 1 < nchunks) {
-            cp_async_wait<STAGES - 3>();
-            fence_proxy_async();
-            fence_before(); // the reads of S[(c+1)&1] (chunk c-1) are complete
-            __syncthreads();
-            issue_S(c + 1);
-        }
-        // 2. S_c
-        mbar_wait(mbS[c & 1], (c >> 1) & 1);
-        fence_after();
-        float sv[KC];
-        tmem_ld32(tlane + COL_S + (c & 1) * KC, sv);
-        tmem_ld32(tlane + COL_S + (c & 1) * KC + 32, sv + 32);
-        tmem_wait_ld();
-        const int valid = nblk * 16 - c * KC; // keys of this chunk (< KC only in the last one)
-        if (valid < KC) {
-#pragma unroll
-            for (int i = 0; i < KC; ++i) sv[i] = i < valid ? sv[i] : -INFINITY;
-        }
-        float lmx[8]; // 8 independent max chains (a 63-deep serial chain is latency-bound)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) lmx[j] = sv[j];
-#pragma unroll
-        for (int i = 8; i < KC; ++i) lmx[i & 7] = fmaxf(lmx[i & 7], sv[i]);
-        const float lm = fmaxf(fmaxf(fmaxf(lmx[0], lmx[1]), fmaxf(lmx[2], lmx[3])),
-                               fmaxf(fmaxf(lmx[4], lmx[5]), fmaxf(lmx[6], lmx[7])));
-        // 3. lazy rescale (O must be stable: the last issued P V is P V_{c-1})
-        const bool need = lm * sl2 > m_run + kTau;
-        if (__syncthreads_or(need)) {
-            if (c > 0) wait_O(c - 1);
-            const float mn = fmaxf(m_run, lm * sl2);
-            const float a = ex2(m_run - mn);
-            // tcgen05.ld/st are .sync.aligned: the whole warp takes the branch (a = 1 rows
-            // multiply by one)
-            if (__any_sync(0xffffffffu, c > 0 && a != 1.f)) { // rescale the rows of O in TMEM
-                float ov[32];
-#pragma unroll
-                for (int q = 0; q < D / 32; ++q) {
-                    tmem_ld32(tlane + COL_O + 32 * q, ov);
-                    tmem_wait_ld();
-                    uint32_t ob[32];
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(ov[i] * a);
-                    tmem_st32(tlane + COL_O + 32 * q, ob);
-                }
-                tmem_wait_st();
-            }
-            l_run *= a;
-            m_run = mn;
-        }
-        // 4. P_c into P[c&1] (last read by P V_{c-2})
-        if (c >= 2) wait_O(c - 2);
-        uint32_t pk[KC / 2];
-        float ls[4] = {0.f, 0.f, 0.f, 0.f}; // independent partial sums
-#pragma unroll
-        for (int i = 0; i < KC / 2; ++i) {
-            const float p0 = ex2(fmaf(sv[2 * i], sl2, -m_run)), p1 = ex2(fmaf(sv[2 * i + 1], sl2, -m_run));
-            ls[i & 3] += p0 + p1;
-            pk[i] = pack2<T>(p0, p1);
-        }
-        l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-        tmem_st32(tlane + COL_P + (c & 1) * (KC / 2), pk);
-        tmem_wait_st();
-        fence_before();
-        __syncthreads();
-        if (tid == 0) {
+    if (warp < 4) {
+        for (int c = 0; c < nchunks; ++c) {
+            // S_c
+            mbar_wait(mbS[c & 1], (c >> 1) & 1);
             fence_after();
-            const uint32_t bv = sV0 + st * KC * RB;
+            float sv[KC];
+            tmem_ld32(tlane + COL_S + (c & 1) * KC, sv);
+            tmem_ld32(tlane + COL_S + (c & 1) * KC + 32, sv + 32);
+            tmem_wait_ld();
+            const int valid = nblk * 16 - c * KC; // keys of this chunk (< KC only in the last one)
+            if (valid < KC) {
 #pragma unroll
-            for (int kk = 0; kk < KC / 16; ++kk) // 16 keys per MMA: 8 P columns, 16 V rows
-                mma_ts(tmem + COL_O, tmem + COL_P + (c & 1) * (KC / 2) + kk * 8, sdesc_sw128(bv + kk * 16 * RB), idO,
-                       (c > 0 || kk > 0));
-            mma_commit(mbO[c & 1]);
+                for (int i = 0; i < KC; ++i) sv[i] = i < valid ? sv[i] : -INFINITY;
+            }
+            float lmx[8]; // 8 independent max chains
+#pragma unroll
+            for (int j = 0; j < 8; ++j) lmx[j] = sv[j];
+#pragma unroll
+            for (int i = 8; i < KC; ++i) lmx[i & 7] = fmaxf(lmx[i & 7], sv[i]);
+            const float lm = fmaxf(fmaxf(fmaxf(lmx[0], lmx[1]), fmaxf(lmx[2], lmx[3])),
+                                   fmaxf(fmaxf(lmx[4], lmx[5]), fmaxf(lmx[6], lmx[7])));
+            // lazy rescale, voted per warp (each warp owns its 32 TMEM lanes of O); O is
+            // stable once P V_{c-1} completed (P V_c is not issued before our P_c arrives)
+            const bool need = lm * sl2 > m_run + kTau;
+            if (__any_sync(0xffffffffu, need)) {
+                if (c > 0) wait_O(c - 1);
+                const float mn = fmaxf(m_run, lm * sl2);
+                const float a = ex2(m_run - mn);
+                if (__any_sync(0xffffffffu, c > 0 && a != 1.f)) { // tcgen05.ld/st: warp-uniform
+                    float ov[32];
+#pragma unroll
+                    for (int q = 0; q < D / 32; ++q) {
+                        tmem_ld32(tlane + COL_O + 32 * q, ov);
+                        tmem_wait_ld();
+                        uint32_t ob[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(ov[i] * a);
+                        tmem_st32(tlane + COL_O + 32 * q, ob);
+                    }
+                    tmem_wait_st();
+                }
+                l_run *= a;
+                m_run = mn;
+            }
+            // P_c into P[c&1] (last read by P V_{c-2})
+            if (c >= 2) wait_O(c - 2);
+            uint32_t pk[KC / 2];
+            float ls[4] = {0.f, 0.f, 0.f, 0.f}; // independent partial sums
+#pragma unroll
+            for (int i = 0; i < KC / 2; ++i) {
+                float x0 = sv[2 * i], x1 = sv[2 * i + 1];
+                ffma2_sm(x0, x1, sl2, -m_run);
+                x0 = ex2(x0);
+                x1 = ex2(x1);
+                ls[i & 3] += x0 + x1;
+                pk[i] = pack2<T>(x0, x1);
+            }
+            l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+            tmem_st32(tlane + COL_P + (c & 1) * (KC / 2), pk);
+            tmem_wait_st();
+            fence_before();
+            mbar_arrive(mbP[c & 1]);
         }
-        // 5. refill the stage of chunk c-1 (free once P V_{c-1} is done) with chunk c+3
-        if (c >= 1) wait_O(c - 1);
-        load_chunk(c + STAGES - 1 < nchunks ? c + STAGES - 1 : nchunks + STAGES); // no-op past the end
     }
-    cp_async_wait<0>();
-    if (nchunks > 0) wait_O(nchunks - 1);
     // ---- O row from TMEM (+ ragged tail on CUDA cores), normalise, store
-    const bool row_ok = tid < nrows;
+    const bool row_ok = warp < 4 && tid < nrows;
     float o[D];
-    if (nchunks > 0) {
+    if (warp < 4 && nchunks > 0) {
+        wait_O(nchunks - 1);
 #pragma unroll
         for (int q = 0; q < D / 32; ++q) tmem_ld32(tlane + COL_O + 32 * q, o + 32 * q);
         tmem_wait_ld();
