@@ -8,7 +8,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libga.so")
+# GA_LIB overrides the library path (A/B timing of two builds); default: the in-tree build
+LIB_PATH = os.environ.get("GA_LIB") or os.path.join(_PKG, "libga.so")
 
 GA_OK, GA_ERR_INVALID_ARG, GA_ERR_UNSUPPORTED, GA_ERR_CUDA, GA_ERR_COMM, GA_ERR_OOM, GA_ERR_MASK = 0, -1, -2, -3, -4, -5, -6
 GA_COMM_ID_BYTES = 128

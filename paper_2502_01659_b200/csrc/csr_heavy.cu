@@ -69,14 +69,14 @@ __global__ void __launch_bounds__(256) heavy_chunk_kernel(AttnParams p, const in
     const Piece P = get_piece(p.mask, i, 0);
     const int64_t kb = c * p.heavy_threshold;
     const int64_t ke = kb + p.heavy_threshold < P.count ? kb + p.heavy_threshold : P.count;
-    acc.template run_csr<4>(P.cols + P.base, kb, ke);
+    acc.template run_csr<csr_depth<T, D>()>(P.cols + P.base, kb, ke);
     acc.merge_groups();
     if (acc.g == 0) {
-        constexpr int VEC = DT<T>::VEC;
+        constexpr int PER = EdgeAcc<T, D, false>::PER;
         float *dst = partials + ((size_t)it * H + h) * (D + 2);
         if (acc.sub == 0) { dst[0] = acc.m; dst[1] = acc.l; }
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) dst[2 + acc.sub * VEC + e] = acc.o[e];
+        for (int e = 0; e < PER; ++e) dst[2 + acc.sub * PER + e] = acc.o[e];
     }
 }
 

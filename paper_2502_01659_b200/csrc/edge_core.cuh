@@ -5,97 +5,124 @@
 
 namespace ga {
 
+// Lane layout: a (row, head) vector of D elements is CH = D*sizeof(T)/16 chunks of 16 bytes;
+// a lane owns NC = min(4, CH) consecutive chunks (64 bytes of K_j and of V_j per edge), so
+// G = CH / NC lanes cover one edge (G = 2 for bf16 d=64, 1 for bf16 d=32, 4 for fp32 d=64)
+// and a warp keeps E = 32 / G edges in flight per step.  The per-edge score needs only
+// log2(G) shuffles, and each lane's softmax state (m, l) is shared by fewer lanes than with
+// 16-byte lane slices.
 template <typename T, int D, bool PROBE> struct EdgeAcc {
-    static constexpr int VEC = DT<T>::VEC;
-    static constexpr int G = D / VEC; // lanes per (edge, head) vector
-    static constexpr int E = 32 / G;  // edges in flight per warp
+    static constexpr int VEC = DT<T>::VEC;      // elements per 16-byte chunk
+    static constexpr int CH = D / VEC;          // chunks per (row, head) vector
+    static constexpr int NCMAX = sizeof(T) == 2 ? 1 : 4; // 16-bit: 16 B per lane (random CSR gathers)
+    static constexpr int NC = CH >= NCMAX ? NCMAX : CH; // chunks per lane
+    static constexpr int G = CH / NC;           // lanes per edge
+    static constexpr int E = 32 / G;            // edges in flight per warp and step
+    static constexpr int PER = NC * VEC;        // elements of o per lane
     static constexpr bool H16 = sizeof(T) == 2; // bf16/fp16: FHFMA on packed pairs
-    float q[VEC], o[VEC];
-    uint32_t qp[4]; // packed 16-bit q (H16)
-    float sl2;      // log2(e)/sqrt(d), applied after the reduction on the H16 path
+    uint4 qraw[NC]; // this lane's slice of q (stored type)
+    float o[PER];
+    float sl2;      // log2(e)/sqrt(d): scores are kept in the exp2 domain
     float m, l;
     unsigned long long n_edges, sum_j, sum_h;
     int g, sub;
     const AttnParams *prm;
-    size_t row_bytes, hoff; // token row stride; this lane's (head, sub-vector) byte offset
+    size_t row_bytes, hoff; // token row stride; this lane's (head, slice) byte offset
 
     __device__ __forceinline__ void init(const AttnParams &p, int64_t t, int h, int lane)
     {
         g = lane / G;
         sub = lane % G;
-        const T *Qp = reinterpret_cast<const T *>(p.Q) + ((size_t)t * p.H + h) * D + sub * VEC;
         prm = &p;
-        hoff = ((size_t)h * D + sub * VEC) * sizeof(T);
+        hoff = ((size_t)h * D + sub * PER) * sizeof(T);
         row_bytes = (size_t)p.H * D * sizeof(T);
-        uint4 raw = ldg16(Qp);
-        qp[0] = raw.x; qp[1] = raw.y; qp[2] = raw.z; qp[3] = raw.w;
-        sl2 = p.scale_log2;
-        unpack<T>(raw, q);
+        const char *Qp = reinterpret_cast<const char *>(p.Q) + (size_t)t * row_bytes + hoff;
 #pragma unroll
-        for (int c = 0; c < VEC; ++c) { q[c] *= p.scale_log2; o[c] = 0.f; }
+        for (int c = 0; c < NC; ++c) qraw[c] = ldg16(Qp + 16 * c);
+        sl2 = p.scale_log2;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) o[e] = 0.f;
         m = -INFINITY;
         l = 0.f;
         n_edges = sum_j = sum_h = 0;
     }
 
-    // neighbours k in [kb, ke) of piece P (warp-uniform bounds)
-    __device__ __forceinline__ void run(const Piece &P, int64_t kb, int64_t ke)
-    {
-        for (int64_t k0 = kb; k0 < ke; k0 += 2 * E) {
-            const int64_t ka = k0 + g, kk = k0 + E + g;
-            const bool va = ka < ke, vb = kk < ke;
-            uint4 kra = make_uint4(0, 0, 0, 0), vra = kra, krb = kra, vrb = kra;
-            int64_t ja = 0, jb = 0;
-            if (va) {
-                ja = piece_at(P, ka);
-                load(ja, kra, vra);
-            }
-            if (vb) {
-                jb = piece_at(P, kk);
-                load(jb, krb, vrb);
-            }
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                if (u == 1 && k0 + E >= ke) break; // warp-uniform: no group has work
-                const float sc = score(u == 0 ? kra : krb);
-                update(sc, u == 0 ? vra : vrb, u == 0 ? va : vb, u == 0 ? ja : jb);
-            }
-        }
-    }
-
-    // this lane's 16-byte slices of K_j and V_j (local buffer or the owning peer's)
-    __device__ __forceinline__ void load(int64_t j, uint4 &kraw, uint4 &vraw) const
+    // this lane's slices of K_j and V_j (local buffer or the owning peer's)
+    __device__ __forceinline__ void load(int64_t j, uint4 *kraw, uint4 *vraw) const
     {
         const char *kr, *vr;
         kv_row(*prm, j, row_bytes, kr, vr);
-        kraw = ldg16(kr + hoff);
-        vraw = ldg16(vr + hoff);
+        kr += hoff;
+        vr += hoff;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) kraw[c] = ldg16(kr + 16 * c);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) vraw[c] = ldg16(vr + 16 * c);
     }
 
-    // one (key, value) edge into the group state (score already reduced over the group)
-    __device__ __forceinline__ void update(float s, const uint4 &vraw, bool valid, int64_t j)
+    // q.k over the edge's G lanes, in the exp2 domain (scaled by log2(e)/sqrt(d))
+    __device__ __forceinline__ float score(const uint4 *kraw) const
+    {
+        float s;
+        if constexpr (H16) { // bf16 x bf16 + f32 without unpacking (FHFMA), 2 chains
+            float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                a0 = fma2h<T>(qraw[c].x, kraw[c].x, a0);
+                a1 = fma2h<T>(qraw[c].y, kraw[c].y, a1);
+                a0 = fma2h<T>(qraw[c].z, kraw[c].z, a0);
+                a1 = fma2h<T>(qraw[c].w, kraw[c].w, a1);
+            }
+            s = a0 + a1;
+        } else {
+            float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                float qf[4], kf[4];
+                unpack<T>(qraw[c], qf);
+                unpack<T>(kraw[c], kf);
+                a0 = fmaf(qf[0], kf[0], a0);
+                a1 = fmaf(qf[1], kf[1], a1);
+                a0 = fmaf(qf[2], kf[2], a0);
+                a1 = fmaf(qf[3], kf[3], a1);
+            }
+            s = a0 + a1;
+        }
+#pragma unroll
+        for (int off = 1; off < G; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        return s * sl2;
+    }
+
+    // one (key, value) edge into the lane group's state
+    __device__ __forceinline__ void update(float s, const uint4 *vraw, bool valid, int64_t j)
     {
         if (!valid) return;
         if (s > m) { // lazy rescale: only when the running max grows
             const float a = ex2(m - s);
             l *= a;
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) o[c] *= a;
+            for (int e = 0; e < PER; ++e) o[e] *= a;
             m = s;
         }
         const float pr = ex2(s - m);
         l += pr;
         if constexpr (H16) { // o += p v with p rounded to the input type (as on the MMA paths)
             const uint32_t p2 = pack2<T>(pr, pr);
-            axpy2h<T>(p2, vraw.x, o[0], o[1]);
-            axpy2h<T>(p2, vraw.y, o[2], o[3]);
-            axpy2h<T>(p2, vraw.z, o[4], o[5]);
-            axpy2h<T>(p2, vraw.w, o[6], o[7]);
-        } else {
-            float vf[VEC];
-            unpack<T>(vraw, vf);
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) o[c] = fmaf(pr, vf[c], o[c]);
+            for (int c = 0; c < NC; ++c) {
+                axpy2h<T>(p2, vraw[c].x, o[8 * c + 0], o[8 * c + 1]);
+                axpy2h<T>(p2, vraw[c].y, o[8 * c + 2], o[8 * c + 3]);
+                axpy2h<T>(p2, vraw[c].z, o[8 * c + 4], o[8 * c + 5]);
+                axpy2h<T>(p2, vraw[c].w, o[8 * c + 6], o[8 * c + 7]);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                float vf[VEC];
+                unpack<T>(vraw[c], vf);
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) o[VEC * c + e] = fmaf(pr, vf[e], o[VEC * c + e]);
+            }
         }
         if (PROBE) {
             n_edges += 1;
@@ -104,24 +131,36 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
         }
     }
 
-    // q.k over the group (exp2 domain: scaled by log2(e)/sqrt(d))
-    __device__ __forceinline__ float score(const uint4 &kraw) const
+    // neighbours k in [kb, ke) of piece P (warp-uniform bounds): two edges per lane group
+    // per step, both loads issued before either is consumed
+    __device__ __forceinline__ void run(const Piece &P, int64_t kb, int64_t ke)
     {
-        float s;
-        if constexpr (H16) { // bf16 x bf16 + f32 without unpacking (FHFMA)
-            const float s0 = fma2h<T>(qp[2], kraw.z, fma2h<T>(qp[0], kraw.x, 0.f));
-            const float s1 = fma2h<T>(qp[3], kraw.w, fma2h<T>(qp[1], kraw.y, 0.f));
-            s = s0 + s1;
-        } else {
-            float kf[VEC];
-            unpack<T>(kraw, kf);
-            s = 0.f;
+        for (int64_t k0 = kb; k0 < ke; k0 += 2 * E) {
+            const int64_t ka = k0 + g, kk = k0 + E + g;
+            const bool va = ka < ke, vb = kk < ke;
+            uint4 kra[NC], vra[NC], krb[NC], vrb[NC];
+            int64_t ja = 0, jb = 0;
+            if (va) {
+                ja = piece_at(P, ka);
+                load(ja, kra, vra);
+            } else {
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) s = fmaf(q[c], kf[c], s);
+                for (int c = 0; c < NC; ++c) kra[c] = vra[c] = make_uint4(0, 0, 0, 0);
+            }
+            if (vb) {
+                jb = piece_at(P, kk);
+                load(jb, krb, vrb);
+            } else {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) krb[c] = vrb[c] = make_uint4(0, 0, 0, 0);
+            }
+            const float sa = score(kra);
+            update(sa, vra, va, ja);
+            if (k0 + E < ke) { // warp-uniform: some group has a second edge
+                const float sb = score(krb);
+                update(sb, vrb, vb, jb);
+            }
         }
-#pragma unroll
-        for (int off = 1; off < G; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        return H16 ? s * sl2 : s;
     }
 
     // Explicit CSR piece, gather-bound: a warp loads 32 column indices with one coalesced
@@ -131,7 +170,6 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
     template <int DEPTH>
     __device__ __forceinline__ void run_csr(const int32_t *cols, int64_t kb, int64_t ke)
     {
-        static_assert(32 % (E * DEPTH) == 0 || E * DEPTH >= 32, "batch shape");
         constexpr int STEP = E * DEPTH; // edges per pass
         const int lane = (int)(threadIdx.x & 31);
         for (int64_t b0 = kb; b0 < ke; b0 += 32) {
@@ -139,7 +177,7 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
             const int my_j = kl < ke ? cols[kl] : -1;
 #pragma unroll 1
             for (int e0 = 0; e0 < 32 && b0 + e0 < ke; e0 += STEP) {
-                uint4 kr[DEPTH], vr[DEPTH];
+                uint4 kr[DEPTH][NC], vr[DEPTH][NC];
                 int jj[DEPTH];
 #pragma unroll
                 for (int u = 0; u < DEPTH; ++u) {
@@ -149,7 +187,8 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
                     if (jj[u] >= 0) {
                         load(jj[u], kr[u], vr[u]);
                     } else {
-                        kr[u] = vr[u] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) kr[u][c] = vr[u][c] = make_uint4(0, 0, 0, 0);
                     }
                 }
 #pragma unroll
@@ -174,9 +213,9 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
             const float b = (m2 == -INFINITY) ? 0.f : ex2(m2 - mn);
             l = l * a + l2 * b;
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) {
-                const float o2 = __shfl_xor_sync(0xffffffffu, o[c], off);
-                o[c] = o[c] * a + o2 * b;
+            for (int e = 0; e < PER; ++e) {
+                const float o2 = __shfl_xor_sync(0xffffffffu, o[e], off);
+                o[e] = o[e] * a + o2 * b;
             }
             m = mn;
         }
@@ -186,12 +225,15 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
     __device__ __forceinline__ void store(const AttnParams &p, int64_t t, int h) const
     {
         if (g != 0) return;
-        float r[VEC];
         const float inv = l > 0.f ? 1.f / l : 0.f;
+        char *Op = reinterpret_cast<char *>(p.out) + (size_t)t * row_bytes + hoff;
 #pragma unroll
-        for (int c = 0; c < VEC; ++c) r[c] = o[c] * inv;
-        T *Op = reinterpret_cast<T *>(p.out) + ((size_t)t * p.H + h) * D + sub * VEC;
-        stg16(Op, pack<T>(r));
+        for (int c = 0; c < NC; ++c) {
+            float r[VEC];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) r[e] = o[VEC * c + e] * inv;
+            stg16(Op + 16 * c, pack<T>(r));
+        }
     }
 
     // warp totals of the probe counters (one lane per group counts)
@@ -209,6 +251,12 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
         }
     }
 };
+
+// edge steps a CSR batch issues before consuming (DEPTH * E edges in flight per warp)
+template <typename T, int D> constexpr int csr_depth()
+{
+    return EdgeAcc<T, D, false>::E >= 16 ? 1 : 32 / EdgeAcc<T, D, false>::E > 4 ? 4 : 32 / EdgeAcc<T, D, false>::E;
+}
 
 // One (row, head) of Algorithm 1 by one warp: all pieces of N(i), merge, store.
 // t = local query row (global row q_begin + t).

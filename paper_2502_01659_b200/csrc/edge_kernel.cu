@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(256) edge_kernel(AttnParams p)
     for (int pc = 0; pc < np; ++pc) {
         const Piece P = get_piece(p.mask, i, pc);
         if (P.mode == P_CSR)
-            acc.template run_csr<4>(P.cols + P.base, 0, P.count);
+            acc.template run_csr<csr_depth<T, D>()>(P.cols + P.base, 0, P.count);
         else
             acc.run(P, 0, P.count);
     }
