@@ -1,0 +1,85 @@
+// tma.cu — host-side tensor-map encoding (driver entry point resolved through cudart, so
+// libga.so needs no libcuda link).
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "tma.cuh"
+
+namespace ga {
+namespace tma {
+
+typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiled encoder()
+{
+    static EncodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiled>(p);
+    });
+    return fn;
+}
+
+struct Key {
+    const void *base;
+    int64_t ntok;
+    int H, D, r, box;
+    bool operator==(const Key &o) const
+    {
+        return base == o.base && ntok == o.ntok && H == o.H && D == o.D && r == o.r && box == o.box;
+    }
+};
+
+static bool encode_uncached(CUtensorMap *map, const void *base, int64_t ntok, int H, int D, int r, int box_rows);
+
+// Encoding is host work on every launch; a small cache keyed by (buffer, shape, stride,
+// box) serves the repeated launches of a training / serving loop.
+bool encode_rows(CUtensorMap *map, const void *base, int64_t ntok, int H, int D, int r, int box_rows)
+{
+    static std::mutex mu;
+    static Key keys[16];
+    static CUtensorMap maps[16];
+    static int n = 0, next = 0;
+    const Key k{base, ntok, H, D, r, box_rows};
+    {
+        std::lock_guard<std::mutex> g(mu);
+        for (int i = 0; i < n; ++i)
+            if (keys[i] == k) { *map = maps[i]; return true; }
+    }
+    if (!encode_uncached(map, base, ntok, H, D, r, box_rows)) return false;
+    std::lock_guard<std::mutex> g(mu);
+    keys[next] = k;
+    maps[next] = *map;
+    next = (next + 1) % 16;
+    if (n < 16) ++n;
+    return true;
+}
+
+static bool encode_uncached(CUtensorMap *map, const void *base, int64_t ntok, int H, int D, int r, int box_rows)
+{
+    const int rb = D * 2;
+    if ((rb != 128 && rb != 64) || r < 1 || r > 8 || box_rows * r > 256 || ntok <= 0 || ntok >= (int64_t)1 << 32)
+        return false;
+    if ((reinterpret_cast<uintptr_t>(base) & 15u) != 0) return false;
+    EncodeTiled enc = encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)ntok};
+    const cuuint64_t strides[2] = {(cuuint64_t)rb, (cuuint64_t)H * rb}; // bytes, dims 1 and 2
+    const cuuint32_t box[3] = {(cuuint32_t)D, 1u, (cuuint32_t)(box_rows * r)};
+    const cuuint32_t estr[3] = {1u, 1u, (cuuint32_t)r};
+    const CUresult e = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           rb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return e == CUDA_SUCCESS;
+}
+
+} // namespace tma
+} // namespace ga

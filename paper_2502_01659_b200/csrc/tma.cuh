@@ -1,0 +1,39 @@
+// tma.cuh — Tensor Memory Accelerator (cp.async.bulk.tensor) helpers for the row-strided
+// [tokens, heads, d] layout of Q/K/V.
+//
+// A residue class of a dilated window (tokens c, c + r, c + 2r, ...) is one TMA tensor-map
+// traversal: a rank-3 map {d, heads, tokens} with element stride r on the token dimension
+// loads `box_rows` class rows of one head into shared memory, 128B- (d = 64) or 64B-swizzled
+// (d = 32) exactly as tc::swz lays them out.  Out-of-range coordinates (negative, or past the
+// buffer) are zero-filled by the hardware.
+#pragma once
+#include <cuda.h> // CUtensorMap and its enums (types only: the encoder comes from cudart's entry point)
+#include <stdint.h>
+
+namespace ga {
+namespace tma {
+
+// Host: encode `map` for a row-major [ntok, H, D] tensor of 16-bit elements at `base`;
+// boxes of `box_rows` token rows of one head with token stride r (box_rows * r <= 256,
+// r <= 8, D * 2 in {64, 128}).  Returns false if TMA cannot express it.
+bool encode_rows(CUtensorMap *map, const void *base, int64_t ntok, int H, int D, int r, int box_rows);
+
+__device__ __forceinline__ void expect_tx(uint32_t mbar, uint32_t bytes)
+{
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(mbar),
+                 "r"(bytes)
+                 : "memory");
+}
+
+// box at coordinates (c0 = element in d, c1 = head, c2 = token) -> shared memory, completing
+// its bytes on `mbar`
+__device__ __forceinline__ void load_3d(uint32_t smem, const CUtensorMap *map, int c0, int c1, int c2, uint32_t mbar)
+{
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                     smem),
+                 "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
+                 : "memory");
+}
+
+} // namespace tma
+} // namespace ga

@@ -19,6 +19,8 @@
 // is cut by the query range, use a predicated general loop for U\F.  The CUDA-core state
 // seeds the MMA phase's running (m, l, O) through a per-warp shared-memory hand-off.
 #include "tc_common.cuh"
+#include "tma.cuh"
+#include "umma.cuh"
 
 namespace ga {
 namespace band {
@@ -35,19 +37,29 @@ using tc::lds16;
 using tc::swz;
 using tc::cp_async16;
 
+constexpr int QBOX = 56; // rows per TMA box of the Q tile (2 boxes)
+constexpr int BBOX = 64; // rows per TMA box of the K/V band
+
 struct BandParams {
+    CUtensorMap tmQ, tmK, tmV; // TMA maps of one residue class x head (element stride r)
     AttnParams p;
     int64_t m;          // band half-width in class rows
     int64_t r;          // dilation = number of classes
     int64_t tiles;      // tiles per (class, head) (max over classes)
     int64_t edge_tiles; // tiles at each end whose band may be clipped (scheduled first)
     uint32_t smem_bytes;
+    int32_t tma;        // 1: tiles whose band is local load through the tensor maps
 };
+
+// band rows allocated: ROWS + 2m rounded up to whole TMA boxes (multiples of 16 rows, so the
+// V band starts on a swizzle period: 1024 B at d = 64, 512 B at d = 32)
+__host__ __device__ constexpr int64_t band_alloc_rows(int64_t m) { return (ROWS + 2 * m + BBOX - 1) / BBOX * BBOX; }
 
 template <int D> __host__ __device__ constexpr uint32_t band_smem(int64_t m)
 {
-    return (uint32_t)(ROWS * Geo<D>::RB                 // Q tile (hand-off + output staging)
-                      + 2 * (ROWS + 2 * m) * Geo<D>::RB); // K and V band
+    return (uint32_t)(1024                                           // alignment slack
+                      + ROWS * Geo<D>::RB                            // Q tile (hand-off + output staging)
+                      + 2 * band_alloc_rows(m) * Geo<D>::RB + 64);   // K and V band, 2 mbarriers
 }
 
 // One CUDA-core edge: score of (q half, key half) -> full score via the lane pair.
@@ -84,10 +96,10 @@ __device__ __forceinline__ void half_axpy(float *oc, float pr, uint32_t vaddr, i
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const BandParams bp)
+__global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const __grid_constant__ BandParams bp)
 {
     using G = Geo<D>;
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     const AttnParams &p = bp.p;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int H = p.H;
@@ -120,8 +132,12 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
     const bool interior = v_lo == a0 && v_hi == a0 + ROWS && a0 - m >= 0 && a0 + ROWS - 1 + m <= Nc - 1;
 
     const int64_t NB = ROWS + 2 * m; // band rows; band-local 0 = class row a0 - m
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-    const uint32_t sQ = sbase, sK = sQ + ROWS * G::RB, sV = sK + (uint32_t)(NB * G::RB);
+    const int64_t NBA = band_alloc_rows(m);
+    // 1024-byte aligned base: the 128B swizzle of TMA follows the address bits, tc::swz the row
+    const uint32_t sraw = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t sbase = (sraw + 1023u) & ~1023u;
+    const uint32_t sQ = sbase, sK = sQ + ROWS * G::RB, sV = sK + (uint32_t)(NBA * G::RB);
+    const uint32_t mb0 = sV + (uint32_t)(NBA * G::RB), mb1 = mb0 + 8; // TMA stage barriers
 
     // ---- per-warp key geometry (band-local indices; abs = a0 - m + local)
     const int w16 = warp * 16;
@@ -171,29 +187,62 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
             }
         }
     };
-    const char *Qt = Qg + (c + a0 * r - p.q_begin) * (int64_t)row_bytes;
-    const int q_lo = (int)(v_lo - a0), q_hi = (int)(v_hi - a0);
-    for (int idx = q_lo * G::NC + tid; idx < q_hi * G::NC; idx += THREADS) {
-        const int row = idx / G::NC, cc = idx % G::NC;
-        cp_async16(sQ + swz<D>(row, cc), Qt + (int64_t)((uint64_t)(uint32_t)row * rstride) + cc * 16);
-    }
-    if (!interior) { // pad rows of a clipped tile join the rescale votes: make them defined
-        for (int idx = tid; idx < ROWS * G::NC; idx += THREADS) {
-            const int row = idx / G::NC;
-            if (row < q_lo || row >= q_hi) tc::sts_zero16(sQ + swz<D>(row, idx % G::NC));
-        }
-    }
     // stage 0: rows the CUDA-core phase reads (ends of the band); stage 1: the dense middle,
     // which lands while the CUDA-core phase runs
     const int mid0 = ROWS - 1, mid1 = max(mid0, (int)(2 * m + 1) - 16);
-    load_band(0, mid0);
-    load_band(mid1, (int)NB);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    load_band(mid0, mid1);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    if (interior) asm volatile("cp.async.wait_group 1;" ::: "memory");
-    else asm volatile("cp.async.wait_group 0;" ::: "memory"); // clipped: CUDA keys may be anywhere
-    __syncthreads();
+    const bool use_tma = bp.tma && band_local;
+    if (use_tma) {
+        // TMA: warp 0 issues the boxes (Q tile and band ends -> barrier 0; band middle ->
+        // barrier 1).  Rows outside the sequence / query range come back as zeros, which
+        // also defines the pad rows of clipped tiles (they join the rescale votes).
+        const int s0 = (mid0 + BBOX - 1) / BBOX, s1 = max(s0, mid1 / BBOX); // stage-1 boxes [s0, s1)
+        const int nbox = (int)(NBA / BBOX);
+        if (tid == 0) {
+            umma::mbar_init(mb0, 1);
+            umma::mbar_init(mb1, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (warp == 0) {
+            constexpr uint32_t QB = QBOX * G::RB, BB = BBOX * G::RB;
+            if (lane == 0) {
+                tma::expect_tx(mb0, (uint32_t)(ROWS / QBOX) * QB + 2u * (uint32_t)(nbox - (s1 - s0)) * BB);
+                tma::expect_tx(mb1, 2u * (uint32_t)(s1 - s0) * BB);
+            }
+            __syncwarp();
+            const int qtok0 = (int)(c + a0 * r - p.q_begin), ktok0 = (int)(c + base * r - p.kv_begin);
+            if (lane < ROWS / QBOX)
+                tma::load_3d(sQ + lane * QB, &bp.tmQ, 0, h, qtok0 + lane * QBOX * (int)r, mb0);
+            if (lane < nbox) {
+                const uint32_t mb = (lane >= s0 && lane < s1) ? mb1 : mb0;
+                tma::load_3d(sK + lane * BB, &bp.tmK, 0, h, ktok0 + lane * BBOX * (int)r, mb);
+                tma::load_3d(sV + lane * BB, &bp.tmV, 0, h, ktok0 + lane * BBOX * (int)r, mb);
+            }
+        }
+        umma::mbar_wait(mb0, 0);
+        if (!interior) umma::mbar_wait(mb1, 0); // clipped: CUDA keys may be anywhere
+    } else {
+        const char *Qt = Qg + (c + a0 * r - p.q_begin) * (int64_t)row_bytes;
+        const int q_lo = (int)(v_lo - a0), q_hi = (int)(v_hi - a0);
+        for (int idx = q_lo * G::NC + tid; idx < q_hi * G::NC; idx += THREADS) {
+            const int row = idx / G::NC, cc = idx % G::NC;
+            cp_async16(sQ + swz<D>(row, cc), Qt + (int64_t)((uint64_t)(uint32_t)row * rstride) + cc * 16);
+        }
+        if (!interior) { // pad rows of a clipped tile join the rescale votes: make them defined
+            for (int idx = tid; idx < ROWS * G::NC; idx += THREADS) {
+                const int row = idx / G::NC;
+                if (row < q_lo || row >= q_hi) tc::sts_zero16(sQ + swz<D>(row, idx % G::NC));
+            }
+        }
+        load_band(0, mid0);
+        load_band(mid1, (int)NB);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        load_band(mid0, mid1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (interior) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;" ::: "memory"); // clipped: CUDA keys may be anywhere
+        __syncthreads();
+    }
 
     const float sl2 = p.scale_log2;
 
@@ -309,8 +358,12 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
             __syncwarp();
         }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads(); // dense rows landed
+    if (use_tma) {
+        umma::mbar_wait(mb1, 0); // dense rows landed
+    } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads(); // dense rows landed
+    }
     if (!warp_live) return; // no further CTA-wide barriers
 
     // ================= tensor-core phase: dense 16x16 blocks of F =================
@@ -405,6 +458,14 @@ ga_status launch_window_tiled(const AttnParams &p, ga_dtype dt, cudaStream_t s)
     bp.tiles = (per_class + band::ROWS - 1) / band::ROWS + 1; // +1: grid anchored at ROWS multiples
     bp.edge_tiles = (bp.m + band::ROWS - 1) / band::ROWS + 2;
     bp.smem_bytes = band_smem_for(p.d, bp.m);
+    // TMA maps of Q (query rows) and K/V (key rows) with element stride r; d = 128 rows
+    // (256 B) exceed one swizzle span and dilations above 8 exceed the traversal stride,
+    // those keep the cp.async path
+    bp.tma = p.d <= 64 && band::BBOX * bp.r <= 256 && band::QBOX * bp.r <= 256 &&
+             band::band_alloc_rows(bp.m) / band::BBOX <= 32 &&
+             tma::encode_rows(&bp.tmQ, p.Q, p.q_rows, p.H, p.d, (int)bp.r, band::QBOX) &&
+             tma::encode_rows(&bp.tmK, p.K, p.kv_rows, p.H, p.d, (int)bp.r, band::BBOX) &&
+             tma::encode_rows(&bp.tmV, p.V, p.kv_rows, p.H, p.d, (int)bp.r, band::BBOX);
     if (bp.r * p.H * bp.tiles > (int64_t)INT32_MAX) {
         set_error("band kernel grid too large");
         return GA_ERR_UNSUPPORTED;
