@@ -75,16 +75,23 @@ typedef enum {
     GA_MASK_BLOCK_DILATED = 4
 } ga_mask_kind;
 
+/* BIGBIRD components (ga_mask.parts): the window W_i, the global rows and columns minus the
+   window (the paper's "global minus local" kernel), the random columns.  They
+   are disjoint and their union is the BigBird mask; Longformer = WINDOW + GLOBAL. */
+typedef enum { GA_BB_WINDOW = 1, GA_BB_GLOBAL = 2, GA_BB_RANDOM = 4 } ga_bigbird_part;
+
 /* Mask descriptor: the paper's "attention-specific parameters P_a" or explicit graph G
    (Algorithm 1 input).  Unused fields are ignored; zero-initialise. */
 typedef struct ga_mask {
     int32_t kind;              /* ga_mask_kind                                          */
-    int32_t reserved0;
+    int32_t parts;             /* BIGBIRD components to include (ga_bigbird_part bits; 0 =
+                                  all): disjoint, so separate calls compose */
     int64_t L;                 /* number of graph nodes (global sequence length)         */
     const int64_t *row_ptr;    /* CSR: DEVICE int64 [L+1], row_ptr[0]=0, nondecreasing     */
     const int32_t *col_idx;    /* CSR: DEVICE int32 [nnz], sorted strictly per row        */
     int64_t nnz;               /* CSR: number of edges (= row_ptr[L])                     */
-    int64_t w, r;              /* WINDOW / BIGBIRD window w >= 1; dilation r >= 1          */
+    int64_t w, r;              /* WINDOW / BIGBIRD window w >= 1; dilation r >= 1 (BIGBIRD:
+                                  0 = 1; its window is WINDOW(w, r))                        */
     int64_t w0, alpha;         /* LONGNET: first segment w0 >= 1, ratio alpha >= 2         */
     int64_t seg;               /* BLOCK_DILATED segment length >= 1 (r as above)          */
     const int64_t *global_idx; /* BIGBIRD: DEVICE int64 [n_global] sorted, or NULL for the
@@ -105,6 +112,24 @@ typedef enum {
                             (rows sharing a neighbour set x their strided key pieces) */
     GA_KERNEL_TC = 3     /* bf16 window: tcgen05 dense core (not built in this version) */
 } ga_kernel;
+
+/* Carried online-softmax state: for query row i and head h over an edge
+   set E (the edges of one call),
+       m = max_{j in E} s_ij * log2(e)          (log2 domain; s_ij = q_i.k_j / sqrt(d))
+       l = sum_{j in E} 2^(s_ij log2(e) - m)
+       o = sum_{j in E} 2^(s_ij log2(e) - m) v_j (fp32, unnormalised)
+   Two states of DISJOINT edge sets combine with the associative operator of PAPER.md:374's
+   split-and-merge (a7): m = max(m1, m2), l = l1 2^(m1-m) + l2 2^(m2-m), o likewise; the
+   attention over the union is o / l (0 when l = 0).  A state with l = 0 is empty (its m is
+   ignored), so zero-filled buffers are valid empty states.  Layout: DEVICE fp32, m and l
+   [rows, heads], o [rows, heads, d], row-major; rows are the call's query rows. */
+typedef struct ga_state {
+    float *m;
+    float *l;
+    float *o;
+} ga_state;
+
+typedef enum { GA_STATE_WRITE = 0, GA_STATE_ACCUMULATE = 1 } ga_state_mode;
 
 /* Optional controls for ga_attention_ex.  Zero-initialise, then set what you need. */
 typedef struct ga_opts {
@@ -133,6 +158,14 @@ typedef struct ga_opts {
     int32_t kernel;          /* ga_kernel */
     int32_t heavy_threshold; /* CSR rows with more edges are split into chunks of this size
                                 and merged (0 = default 4096) */
+    /* Carried state (state.m != NULL): the call also produces the (m, l, o) state of its
+       edges, overwriting (GA_STATE_WRITE) or (+)-combining into (GA_STATE_ACCUMULATE) the
+       buffers; `out` may then be NULL, otherwise it receives the normalised attention of the
+       resulting state.  Runs on the edge kernel (every family); not with the CSR heavy-row
+       split (no workspace). */
+    ga_state state;
+    int32_t state_mode;      /* ga_state_mode */
+    int32_t reserved1;
 } ga_opts;
 
 /* The north-star entry point: O = masked-softmax attention of (Q,K,V) over mask.
@@ -155,6 +188,13 @@ ga_status ga_attention_ex(const void *Q, const void *K, const void *V, const ga_
    in `mask` must already be DEVICE pointers. */
 ga_status ga_attention_host(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out,
                             int64_t L, int32_t d, int32_t heads, ga_dtype dtype, void *stream);
+
+/* out = o / l of a carried state (0 where l = 0), rounded to `dtype`: rows x heads x d.
+   Composition: run the disjoint component masks of a pattern (e.g. WINDOW + BIGBIRD with
+   parts = GA_BB_GLOBAL for Longformer) into one state with
+   GA_STATE_ACCUMULATE, then finalise — equal to one call over the union. */
+ga_status ga_state_finalize(const ga_state *state, int64_t rows, int32_t heads, int32_t d, ga_dtype dtype,
+                            void *out, void *stream);
 
 /* Workspace bytes ga_attention_ex uses for (mask, shape, opts): CSR heavy-row split, or the
    LongNet tcgen05 block partials ([slots][heads][d+4] fp32).  0 when none.  Host only. */

@@ -55,7 +55,7 @@ class _OrcMask(ctypes.Structure):
         ("w0", ctypes.c_int64), ("alpha", ctypes.c_int64),
         ("seg", ctypes.c_int64),
         ("global_idx", ctypes.c_void_p), ("n_global", ctypes.c_int64),
-        ("n_random", ctypes.c_int64), ("seed", ctypes.c_uint64),
+        ("n_random", ctypes.c_int64), ("seed", ctypes.c_uint64), ("parts", ctypes.c_int64),
     ]
 
 
@@ -111,6 +111,7 @@ class Mask:
     n_global: int = 0
     n_random: int = 0
     seed: int = 0
+    parts: int = 0                             # BigBird components (0 = all)
     row_ptr: Optional[np.ndarray] = None       # int64 [L+1]
     col_idx: Optional[np.ndarray] = None       # int32 [nnz]
     _keep: list = field(default_factory=list, repr=False)
@@ -120,6 +121,7 @@ class Mask:
         m.kind, m.L, m.w, m.r = self.kind, self.L, self.w, self.r
         m.w0, m.alpha, m.seg = self.w0, self.alpha, self.seg
         m.n_global, m.n_random, m.seed = self.n_global, self.n_random, self.seed & (2**64 - 1)
+        m.parts = self.parts
         self._keep = []
         if self.global_idx is not None:
             g = np.ascontiguousarray(self.global_idx, dtype=np.int64)
@@ -146,8 +148,13 @@ def longnet(L, w0, alpha=2):
     return Mask(LONGNET, L, w0=w0, alpha=alpha)
 
 
-def bigbird(L, w, n_global, n_random, seed, global_idx=None):
-    return Mask(BIGBIRD, L, w=w, n_global=n_global, n_random=n_random, seed=seed,
+BB_WINDOW, BB_GLOBAL, BB_RANDOM = 1, 2, 4  # BigBird components (disjoint; union = full mask)
+
+
+def bigbird(L, w, n_global, n_random, seed, global_idx=None, r=1, parts=0):
+    """BigBird / Longformer (readings R8-R10), window optionally dilated
+    by r; `parts` selects components (BB_* bits, 0 = all)."""
+    return Mask(BIGBIRD, L, w=w, r=r, n_global=n_global, n_random=n_random, seed=seed, parts=parts,
                 global_idx=None if global_idx is None else np.asarray(global_idx, np.int64))
 
 

@@ -29,7 +29,12 @@
  *   LONGNET(w0,alpha)    OR over k = 0..K of BLOCK_DILATED(w0*alpha^k, alpha^k),
  *                        K = max{k : w0*alpha^k <= L}                (reading R11)
  *   BIGBIRD(w,G,nr,seed) global rows/cols UNION window(w) UNION random
- *                        columns drawn by the counter hash of reading R10
+ *                        columns drawn by the counter hash of reading R10.
+ *                        The window may be dilated (r: |i-j| < w and |i-j| mod r == 0, as
+ *                        WINDOW).  `parts` selects disjoint components (bit 0 window, bit 1
+ *                        global rows/cols minus the window — the paper's "global minus local"
+ *                        kernel, PAPER.md:235 —, bit 2 random; 0 = all): the composition
+ *                        API of SURVEY §8(f) f1 runs them as separate calls.
  *   CSR                  the given row_ptr/col_idx
  *
  * Seeded inputs (reading R22) are regenerated on demand from the counter hash so the
@@ -60,6 +65,7 @@ typedef struct {
     int64_t n_global;
     int64_t n_random;
     uint64_t seed;
+    int64_t parts;          /* BigBird components (0 = all)                    */
 } orc_mask;
 
 enum { ORC_F32 = 0, ORC_BF16 = 1, ORC_F16 = 2, ORC_F64 = 3 };
@@ -150,6 +156,13 @@ static int is_global(const orc_mask *m, int64_t j)
 
 static int in_window(int64_t i, int64_t j, int64_t w) { return i64abs(i - j) < w; }
 
+/* BigBird's window: WINDOW(w, r) (r = 1 unless dilated) */
+static int bb_in_window(const orc_mask *m, int64_t i, int64_t j)
+{
+    int64_t r = m->r > 0 ? m->r : 1;
+    return i64abs(i - j) < m->w && i64abs(i - j) % r == 0;
+}
+
 /* LongNet level count K = max{k : w0 * alpha^k <= L} (reading R11). */
 int64_t orc_longnet_levels(int64_t w0, int64_t alpha, int64_t L)
 {
@@ -188,19 +201,20 @@ int64_t orc_max_degree(const orc_mask *m)
 static int64_t bigbird_random(const orc_mask *m, int64_t i, int64_t *out)
 {
     int64_t L = m->L;
-    /* size of W_i UNION G */
+    /* size of W_i UNION G: the window predicate over the only j that can pass, plus the
+       globals outside it */
     int64_t lo = i - m->w + 1 < 0 ? 0 : i - m->w + 1;
     int64_t hi = i + m->w - 1 > L - 1 ? L - 1 : i + m->w - 1;
-    int64_t wg = hi - lo + 1;
-    for (int64_t k = 0; k < m->n_global; ++k) {
-        int64_t g = global_at(m, k);
-        if (!in_window(i, g, m->w)) ++wg;
-    }
+    int64_t wg = 0;
+    for (int64_t j = lo; j <= hi; ++j)
+        if (bb_in_window(m, i, j)) ++wg;
+    for (int64_t k = 0; k < m->n_global; ++k)
+        if (!bb_in_window(m, i, global_at(m, k))) ++wg;
     int64_t complement = L - wg;
     if (complement <= m->n_random) {
         int64_t n = 0;
         for (int64_t j = 0; j < L; ++j)
-            if (!in_window(i, j, m->w) && !is_global(m, j)) out[n++] = j;
+            if (!bb_in_window(m, i, j) && !is_global(m, j)) out[n++] = j;
         return n;
     }
     uint64_t base = orc_splitmix64(m->seed);
@@ -208,7 +222,7 @@ static int64_t bigbird_random(const orc_mask *m, int64_t i, int64_t *out)
     for (uint64_t t = 0; n < m->n_random; ++t) {
         uint64_t h = orc_splitmix64(base ^ ((uint64_t)i * (1ULL << 20) + t));
         int64_t c = (int64_t)(((__int128)(h >> 32) * L) >> 32);
-        if (in_window(i, c, m->w) || is_global(m, c)) continue;
+        if (bb_in_window(m, i, c) || is_global(m, c)) continue;
         int dup = 0;
         for (int64_t q = 0; q < n; ++q)
             if (out[q] == c) { dup = 1; break; }
@@ -255,15 +269,24 @@ int64_t orc_row_neighbors(const orc_mask *m, int64_t i, int64_t *out)
         return sort_unique(out, n);
     }
     case ORC_BIGBIRD: {
+        int64_t parts = m->parts ? m->parts : 7;
         if (is_global(m, i)) { /* a global token attends to every token */
-            for (int64_t j = 0; j < L; ++j) out[n++] = j;
+            for (int64_t j = 0; j < L; ++j) {
+                int w = bb_in_window(m, i, j);
+                if ((w && (parts & 1)) || (!w && (parts & 2))) out[n++] = j;
+            }
             return n;
         }
-        int64_t lo = i - m->w + 1 < 0 ? 0 : i - m->w + 1;
-        int64_t hi = i + m->w - 1 > L - 1 ? L - 1 : i + m->w - 1;
-        for (int64_t j = lo; j <= hi; ++j) out[n++] = j;                        /* window  */
-        for (int64_t k = 0; k < m->n_global; ++k) out[n++] = global_at(m, k);   /* columns */
-        n += bigbird_random(m, i, out + n);                                    /* random  */
+        if (parts & 1) {                                                       /* window  */
+            int64_t lo = i - m->w + 1 < 0 ? 0 : i - m->w + 1;
+            int64_t hi = i + m->w - 1 > L - 1 ? L - 1 : i + m->w - 1;
+            for (int64_t j = lo; j <= hi; ++j)
+                if (bb_in_window(m, i, j)) out[n++] = j;
+        }
+        if (parts & 2)                                              /* global columns \ W */
+            for (int64_t k = 0; k < m->n_global; ++k)
+                if (!bb_in_window(m, i, global_at(m, k))) out[n++] = global_at(m, k);
+        if (parts & 4) n += bigbird_random(m, i, out + n);                     /* random  */
         return sort_unique(out, n);
     }
     }

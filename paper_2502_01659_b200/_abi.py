@@ -16,6 +16,7 @@ GA_COMM_ID_BYTES = 128
 GA_F32, GA_BF16, GA_F16 = 0, 1, 2
 GA_MASK_CSR, GA_MASK_WINDOW, GA_MASK_LONGNET, GA_MASK_BIGBIRD, GA_MASK_BLOCK_DILATED = 0, 1, 2, 3, 4
 GA_KERNEL_AUTO, GA_KERNEL_EDGE, GA_KERNEL_TILED, GA_KERNEL_TC = 0, 1, 2, 3
+GA_BB_WINDOW, GA_BB_GLOBAL, GA_BB_RANDOM = 1, 2, 4
 
 STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_INVALID_ARG", -2: "GA_ERR_UNSUPPORTED", -3: "GA_ERR_CUDA",
                 -4: "GA_ERR_COMM", -5: "GA_ERR_OOM", -6: "GA_ERR_MASK"}
@@ -23,7 +24,7 @@ STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_INVALID_ARG", -2: "GA_ERR_UNSUPPORTED", 
 
 class GaMask(ctypes.Structure):
     _fields_ = [
-        ("kind", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("L", ctypes.c_int64),
+        ("kind", ctypes.c_int32), ("parts", ctypes.c_int32), ("L", ctypes.c_int64),
         ("row_ptr", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("nnz", ctypes.c_int64),
         ("w", ctypes.c_int64), ("r", ctypes.c_int64),
         ("w0", ctypes.c_int64), ("alpha", ctypes.c_int64),
@@ -33,6 +34,13 @@ class GaMask(ctypes.Structure):
     ]
 
 
+class GaState(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_void_p), ("l", ctypes.c_void_p), ("o", ctypes.c_void_p)]
+
+
+GA_STATE_WRITE, GA_STATE_ACCUMULATE = 0, 1
+
+
 class GaOpts(ctypes.Structure):
     _fields_ = [
         ("q_begin", ctypes.c_int64), ("q_rows", ctypes.c_int64),
@@ -40,6 +48,7 @@ class GaOpts(ctypes.Structure):
         ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
         ("edge_counter", ctypes.c_void_p), ("row_fingerprint", ctypes.c_void_p),
         ("kernel", ctypes.c_int32), ("heavy_threshold", ctypes.c_int32),
+        ("state", GaState), ("state_mode", ctypes.c_int32), ("reserved1", ctypes.c_int32),
     ]
 
 
@@ -56,6 +65,7 @@ SIGNATURES = [
     ("ga_mask_to_csr", ctypes.c_int, [_PM, _V, _V, _V]),
     ("ga_mask_validate", ctypes.c_int, [_PM, _V, ctypes.POINTER(ctypes.c_int)]),
     ("ga_fill_inputs", ctypes.c_int, [_V, ctypes.c_int, _I64, _U64, _I32, _I64, _F, _V]),
+    ("ga_state_finalize", ctypes.c_int, [ctypes.POINTER(GaState), _I64, _I32, _I32, ctypes.c_int, _V, _V]),
     ("ga_comm_get_unique_id", ctypes.c_int, [_V]),
     ("ga_comm_create", ctypes.c_int, [_I32, _I32, _V, _I32, ctypes.POINTER(_V)]),
     ("ga_comm_alloc", ctypes.c_int, [_V, _SZ, ctypes.POINTER(_V)]),

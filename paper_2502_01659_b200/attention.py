@@ -28,8 +28,31 @@ def dtype_code(t: torch.dtype) -> int:
     return _DT[t]
 
 
-def _opts(q_begin, q_rows, kv_begin, kv_rows, workspace, edge_counter, row_fingerprint, kernel, heavy):
+class State:
+    """Carried online-softmax state (m, l, o) of `rows` query rows x `heads` (include/ga.h
+    ga_state): fp32 CUDA tensors m, l [rows, heads] and o [rows, heads, d].
+    Zero-filled = empty (l == 0)."""
+
+    def __init__(self, m: torch.Tensor, l: torch.Tensor, o: torch.Tensor):
+        self.m, self.l, self.o = m, l, o
+
+    @classmethod
+    def empty(cls, rows: int, heads: int, d: int, device="cuda") -> "State":
+        z = lambda *s: torch.zeros(s, dtype=torch.float32, device=device)
+        return cls(z(rows, heads), z(rows, heads), z(rows, heads, d))
+
+    def c(self) -> _abi.GaState:
+        st = _abi.GaState()
+        st.m, st.l, st.o = self.m.data_ptr(), self.l.data_ptr(), self.o.data_ptr()
+        return st
+
+
+def _opts(q_begin, q_rows, kv_begin, kv_rows, workspace, edge_counter, row_fingerprint, kernel, heavy,
+          state: Optional[State] = None, accumulate: bool = False):
     o = _abi.GaOpts()
+    if state is not None:
+        o.state = state.c()
+        o.state_mode = _abi.GA_STATE_ACCUMULATE if accumulate else _abi.GA_STATE_WRITE
     o.q_begin, o.q_rows, o.kv_begin, o.kv_rows = q_begin, q_rows, kv_begin, kv_rows
     if workspace is not None:
         o.workspace = workspace.data_ptr()
@@ -56,12 +79,16 @@ def workspace_size(mask: Mask, L: int, d: int, heads: int, dtype=torch.bfloat16,
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: Mask, out: Optional[torch.Tensor] = None, *,
               L: Optional[int] = None, q_begin: int = 0, kv_begin: int = 0, kernel: str = "auto",
               workspace: Optional[torch.Tensor] = None, edge_counter: Optional[torch.Tensor] = None,
-              row_fingerprint: Optional[torch.Tensor] = None, heavy_threshold: int = 0) -> torch.Tensor:
+              row_fingerprint: Optional[torch.Tensor] = None, heavy_threshold: int = 0,
+              state: Optional[State] = None, accumulate: bool = False) -> Optional[torch.Tensor]:
     """Graph-view masked attention (Algorithm 1) via ga_attention_ex.
 
     q: [q_rows, H, d] rows q_begin.. of the global sequence; k, v: [kv_rows, H, d] rows
     kv_begin..; L: global length (default q.shape[0]).  CSR masks with heavy rows should
     pass `workspace` (uint8 CUDA tensor of workspace_size(...) bytes) to use the split path.
+    With `state` (a State of q's rows) the call also writes — or with accumulate=True
+    (+)-combines into — the carried (m, l, o) of its edges; `out` is then only produced when
+    given (returns out, or None).
     """
     if not (q.is_cuda and k.is_cuda and v.is_cuda):
         raise ValueError("q, k, v must be CUDA tensors (no CPU path)")
@@ -74,13 +101,37 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: Mask, out
             raise ValueError("q, k, v must be contiguous")
     rows, H, d = q.shape
     L = rows if L is None else L
-    if out is None:
+    if out is None and state is None:
         out = torch.empty_like(q)
     cm = mask.to_c(L)
-    o = _opts(q_begin, rows, kv_begin, k.shape[0], workspace, edge_counter, row_fingerprint, kernel, heavy_threshold)
-    _abi.check(_abi.lib().ga_attention_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), ctypes.byref(cm), out.data_ptr(),
-                                          L, d, H, dtype_code(q.dtype), ctypes.byref(o), _stream(q.device)))
+    o = _opts(q_begin, rows, kv_begin, k.shape[0], workspace, edge_counter, row_fingerprint, kernel, heavy_threshold,
+              state, accumulate)
+    _abi.check(_abi.lib().ga_attention_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), ctypes.byref(cm),
+                                          out.data_ptr() if out is not None else None, L, d, H, dtype_code(q.dtype),
+                                          ctypes.byref(o), _stream(q.device)))
     return out
+
+
+def state_finalize(state: State, dtype=torch.bfloat16, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """out = o / l of a carried state (ga_state_finalize)."""
+    rows, H, d = state.o.shape
+    if out is None:
+        out = torch.empty((rows, H, d), dtype=dtype, device=state.o.device)
+    st = state.c()
+    _abi.check(_abi.lib().ga_state_finalize(ctypes.byref(st), rows, H, d, dtype_code(out.dtype), out.data_ptr(),
+                                            _stream(out.device)))
+    return out
+
+
+def compose(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, components, *, L: Optional[int] = None,
+            q_begin: int = 0, kv_begin: int = 0) -> torch.Tensor:
+    """Attention over the union of DISJOINT component masks as sequential calls carrying one
+    state (the paper composes its kernels this way)."""
+    rows, H, d = q.shape
+    st = State.empty(rows, H, d, device=q.device)
+    for c in components:
+        attention(q, k, v, c, L=L, q_begin=q_begin, kv_begin=kv_begin, state=st, accumulate=True)
+    return state_finalize(st, q.dtype)
 
 
 def attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: Mask, out: torch.Tensor,

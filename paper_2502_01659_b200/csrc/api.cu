@@ -85,12 +85,14 @@ static ga_status make_devmask(const ga_mask *m, int64_t L, DevMask &M)
         M.r = m->r;
         return GA_OK;
     case GA_MASK_BIGBIRD:
-        if (m->w < 1 || m->n_global < 0 || m->n_random < 0 || m->n_global > L) {
-            set_error("BigBird needs w >= 1, 0 <= n_global <= L, n_random >= 0");
+        if (m->w < 1 || m->n_global < 0 || m->n_random < 0 || m->n_global > L || m->r < 0 || m->parts < 0 ||
+            m->parts > 7) {
+            set_error("BigBird needs w >= 1, 0 <= n_global <= L, n_random >= 0, r >= 0, parts in [0, 7]");
             return GA_ERR_INVALID_ARG;
         }
         M.w = m->w;
-        M.r = 1;
+        M.r = m->r > 0 ? m->r : 1; // dilated window (0 = 1)
+        M.parts = m->parts;
         M.gidx = m->global_idx;
         M.ng = m->n_global;
         M.nrand = m->n_random;
@@ -141,8 +143,24 @@ static ga_status resolve(const void *Q, const void *K, const void *V, const ga_m
     }
     if (d != 32 && d != 64 && d != 128) { set_error("d=%d unsupported (32, 64, 128)", d); return GA_ERR_UNSUPPORTED; }
     if (heads < 1) { set_error("heads must be >= 1"); return GA_ERR_INVALID_ARG; }
-    if (!Q || !K || !V || !out) { set_error("Q, K, V and out must be non-NULL"); return GA_ERR_INVALID_ARG; }
-    if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(out)) {
+    const bool with_state = opts && opts->state.m;
+    if (with_state) {
+        const ga_state &st = opts->state;
+        if (!st.l || !st.o || !aligned16(st.o) || (reinterpret_cast<uintptr_t>(st.m) & 3u) ||
+            (reinterpret_cast<uintptr_t>(st.l) & 3u)) {
+            set_error("state needs m, l (4-byte aligned) and o (16-byte aligned) device buffers");
+            return GA_ERR_INVALID_ARG;
+        }
+        if (opts->state_mode != GA_STATE_WRITE && opts->state_mode != GA_STATE_ACCUMULATE) {
+            set_error("state_mode must be GA_STATE_WRITE or GA_STATE_ACCUMULATE");
+            return GA_ERR_INVALID_ARG;
+        }
+    }
+    if (!Q || !K || !V || (!out && !with_state)) {
+        set_error("Q, K, V and out (unless a state is requested) must be non-NULL");
+        return GA_ERR_INVALID_ARG;
+    }
+    if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || (out && !aligned16(out))) {
         set_error("Q, K, V, out must be 16-byte aligned");
         return GA_ERR_INVALID_ARG;
     }
@@ -166,7 +184,7 @@ static ga_status resolve(const void *Q, const void *K, const void *V, const ga_m
     }
     if (o.kv_rows == 0) o.kv_rows = L - o.kv_begin;
     const size_t row_bytes = (size_t)heads * d * dtype_bytes(dtype);
-    {   // out must not overlap K or V (it is written while they are read)
+    if (out) { // out must not overlap K or V (it is written while they are read)
         const char *ob = (const char *)out, *oe = ob + (size_t)o.q_rows * row_bytes;
         const char *kb = (const char *)K, *ke = kb + (size_t)o.kv_rows * row_bytes;
         const char *vb = (const char *)V, *ve = vb + (size_t)o.kv_rows * row_bytes;
@@ -192,6 +210,10 @@ static ga_status resolve(const void *Q, const void *K, const void *V, const ga_m
     p.nnz = M.kind == GA_MASK_CSR ? mask->nnz : 0;
     p.edge_counter = o.edge_counter;
     p.row_fingerprint = o.row_fingerprint;
+    if (with_state) {
+        p.state = o.state;
+        p.state_mode = o.state_mode;
+    }
     R.heavy = o.heavy_threshold > 0 ? o.heavy_threshold : kDefaultHeavy;
     return GA_OK;
 }
@@ -206,6 +228,13 @@ static ga_status dispatch(AttnParams &p, ga_dtype dtype, const ga_opts *opts, in
         p.workspace_bytes = opts->workspace_bytes;
     }
     ga_status st;
+    if (p.state.m) { // carried state: the edge kernel writes (m, l, o) per (row, head)
+        if (kernel != GA_KERNEL_AUTO && kernel != GA_KERNEL_EDGE) {
+            set_error("a carried state runs on the edge kernel (kernel AUTO or EDGE)");
+            return GA_ERR_UNSUPPORTED;
+        }
+        return launch_edge(p, dtype, s);
+    }
     if (p.mask.kind == GA_MASK_CSR) {
         const bool split = opts && opts->workspace && opts->workspace_bytes > 0;
         if (split) {
@@ -361,6 +390,15 @@ ga_status ga_attention_sharded(const void *Q, const void *K, const void *V, cons
         if (st != GA_OK) return st;
     }
     return comm_device_barrier(comm, s); // no rank changes its K/V while others still read it
+}
+
+ga_status ga_state_finalize(const ga_state *state, int64_t rows, int32_t heads, int32_t d, ga_dtype dtype, void *out,
+                            void *stream)
+{
+    if (!state || !state->l || !state->o || !out) { set_error("state (l, o) and out must be non-NULL"); return GA_ERR_INVALID_ARG; }
+    if (rows < 0 || heads < 1 || d < 1) { set_error("rows >= 0, heads >= 1, d >= 1"); return GA_ERR_INVALID_ARG; }
+    if (dtype != GA_F32 && dtype != GA_BF16 && dtype != GA_F16) { set_error("dtype invalid"); return GA_ERR_INVALID_ARG; }
+    return state_finalize(*state, rows, heads, d, dtype, out, reinterpret_cast<cudaStream_t>(stream));
 }
 
 ga_status ga_attention(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out, int64_t L,

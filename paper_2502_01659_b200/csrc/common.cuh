@@ -192,6 +192,9 @@ struct AttnParams {
     // optional caller workspace (ga_opts): CSR heavy-row split, LongNet block partials
     void *workspace;
     size_t workspace_bytes;
+    // carried (m, l, o) state (ga_opts.state; state.m == NULL: none)
+    ga_state state;
+    int32_t state_mode;
 };
 
 // Base address (head 0, element 0) of K and V token row j: the local buffer when j is in
@@ -230,5 +233,7 @@ ga_status mask_validate(const DevMask &M, cudaStream_t s, int *ok);
 ga_status scan_exclusive_i64(int64_t *data, int64_t n, cudaStream_t s);
 ga_status fill_inputs(void *dst, ga_dtype dt, int64_t n, uint64_t seed, int32_t tensor, int64_t e0, float shift,
                       cudaStream_t s);
+ga_status state_finalize(const ga_state &st, int64_t rows, int32_t H, int32_t d, ga_dtype dt, void *out,
+                         cudaStream_t s);
 
 } // namespace ga

@@ -236,6 +236,39 @@ template <typename T, int D, bool PROBE> struct EdgeAcc {
         }
     }
 
+    // carried state (ga_state): write or (+)-combine the merged (m, l, o) of this call's
+    // edges into the caller's buffers; with p.out also store the normalised row
+    __device__ __forceinline__ void store_state(const AttnParams &p, int64_t t, int h)
+    {
+        const size_t rh = (size_t)t * p.H + h;
+        float *so = p.state.o + rh * D + sub * PER;
+        float mm = m, ll = l;
+        if (g == 0 && p.state_mode == GA_STATE_ACCUMULATE) {
+            const float l2 = p.state.l[rh];
+            if (l2 > 0.f) { // l == 0 marks an empty state (its m is ignored)
+                const float m2 = p.state.m[rh];
+                const float mn = ll > 0.f ? fmaxf(mm, m2) : m2;
+                const float a = ll > 0.f ? ex2(mm - mn) : 0.f, b = ex2(m2 - mn);
+                ll = ll * a + l2 * b;
+#pragma unroll
+                for (int e = 0; e < PER; ++e) o[e] = o[e] * a + so[e] * b;
+                mm = mn;
+            }
+        }
+        __syncwarp(); // every lane has read the old state before any lane overwrites it
+        if (g != 0) return;
+        if (sub == 0) {
+            p.state.m[rh] = mm;
+            p.state.l[rh] = ll;
+        }
+#pragma unroll
+        for (int e = 0; e < PER; ++e) so[e] = o[e];
+        if (p.out) {
+            l = ll;
+            store(p, t, h);
+        }
+    }
+
     // warp totals of the probe counters (one lane per group counts)
     __device__ __forceinline__ void probe_totals(unsigned long long &ne, unsigned long long &sj,
                                                  unsigned long long &sh) const

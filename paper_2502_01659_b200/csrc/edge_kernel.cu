@@ -55,7 +55,8 @@ __global__ void __launch_bounds__(256) edge_kernel(AttnParams p)
             }
         }
     }
-    acc.store(p, t, h);
+    if (p.state.m) acc.store_state(p, t, h);
+    else acc.store(p, t, h);
 }
 
 template <typename T, int D>
@@ -83,6 +84,32 @@ static ga_status launch_edge_d(const AttnParams &p, cudaStream_t s)
     }
     set_error("d=%d unsupported (32, 64, 128)", p.d);
     return GA_ERR_UNSUPPORTED;
+}
+
+// out = o / l of a carried state (ga_state_finalize)
+template <typename T>
+__global__ void state_finalize_kernel(ga_state st, int64_t n, int32_t d, T *out)
+{
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        const float l = st.l[x / d];
+        out[x] = (T)(l > 0.f ? st.o[x] / l : 0.f);
+    }
+}
+
+ga_status state_finalize(const ga_state &st, int64_t rows, int32_t H, int32_t d, ga_dtype dt, void *out,
+                         cudaStream_t s)
+{
+    const int64_t n = rows * H * d;
+    if (n == 0) return GA_OK;
+    const unsigned blocks = (unsigned)imin((n + 255) / 256, 148 * 16);
+    switch (dt) {
+    case GA_F32: state_finalize_kernel<float><<<blocks, 256, 0, s>>>(st, n, d, (float *)out); break;
+    case GA_BF16: state_finalize_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(st, n, d, (__nv_bfloat16 *)out); break;
+    case GA_F16: state_finalize_kernel<__half><<<blocks, 256, 0, s>>>(st, n, d, (__half *)out); break;
+    default: set_error("unknown dtype"); return GA_ERR_INVALID_ARG;
+    }
+    GA_CHECK_LAUNCH("state_finalize_kernel");
+    return GA_OK;
 }
 
 ga_status launch_edge(const AttnParams &p, ga_dtype dt, cudaStream_t s)

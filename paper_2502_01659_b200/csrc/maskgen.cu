@@ -159,8 +159,11 @@ __global__ void fill_pieces_kernel(DevMask M, const int64_t *row_ptr, int32_t *c
     }
 }
 
-// BigBird: warp per row.  Global rows: lanes write 0..L-1.  Others: lane 0 draws the random
-// columns (reading R10), sorts them, and merges window U (G \ W) U R in ascending order.
+// BigBird: warp per row, columns ascending, restricted to the selected components
+// (bit 0 window W_i, bit 1 global rows/cols minus W_i, bit 2 random; reading R8-R10).
+// Global rows and rows whose complement of W_i U G is exhausted use a membership filter
+// over all j, warp-compacted in order; the others merge window, globals outside W_i and the
+// random columns drawn by lane 0 (reading R10), all ascending.
 static constexpr int MAX_RANDOM = 320;
 
 __global__ void fill_bigbird_kernel(DevMask M, const int64_t *row_ptr, int32_t *col_idx)
@@ -168,55 +171,71 @@ __global__ void fill_bigbird_kernel(DevMask M, const int64_t *row_ptr, int32_t *
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= M.L) return;
+    const int parts = M.parts ? M.parts : 7;
     int32_t *dst = col_idx + row_ptr[i];
-    if (bb_is_global(M, i)) {
-        for (int64_t j = lane; j < M.L; j += 32) dst[j] = (int32_t)j;
-        return;
-    }
-    int64_t lo, hi;
-    bb_window(M, i, lo, hi);
-    const int64_t comp = M.L - bb_wg(M, i);
-    if (comp <= M.nrand) { // complement exhausted: N(i) is every token
-        for (int64_t j = lane; j < M.L; j += 32) dst[j] = (int32_t)j;
+    const bool glob = bb_is_global(M, i);
+    const bool exhausted = !glob && M.L - bb_wg(M, i) <= M.nrand;
+    if (glob || exhausted) {
+        int64_t out = 0;
+        for (int64_t j0 = 0; j0 < M.L; j0 += 32) {
+            const int64_t j = j0 + lane;
+            bool inc = false;
+            if (j < M.L) {
+                const bool w = bb_in_window(M, i, j);
+                if (glob) inc = w ? (parts & 1) : (parts & 2);
+                else inc = w ? (parts & 1) : bb_is_global(M, j) ? (parts & 2) : (parts & 4);
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, inc);
+            if (inc) dst[out + __popc(bal & ((1u << lane) - 1u))] = (int32_t)j;
+            out += __popc(bal);
+        }
         return;
     }
     if (lane != 0) return;
     int64_t R[MAX_RANDOM];
     int n = 0;
-    const uint64_t base = splitmix64(M.seed);
-    for (uint64_t t = 0; n < M.nrand; ++t) {
-        const int64_t c = bb_candidate(M, base, i, t);
-        if (c >= lo && c <= hi) continue;
-        if (bb_is_global(M, c)) continue;
-        bool dup = false;
-        for (int q = 0; q < n; ++q)
-            if (R[q] == c) { dup = true; break; }
-        if (dup) continue;
-        // insertion keeps R sorted
-        int q = n++;
-        while (q > 0 && R[q - 1] > c) { R[q] = R[q - 1]; --q; }
-        R[q] = c;
+    if (parts & 4) {
+        const uint64_t base = splitmix64(M.seed);
+        for (uint64_t t = 0; n < M.nrand; ++t) {
+            const int64_t c = bb_candidate(M, base, i, t);
+            if (bb_in_window(M, i, c)) continue;
+            if (bb_is_global(M, c)) continue;
+            bool dup = false;
+            for (int q = 0; q < n; ++q)
+                if (R[q] == c) { dup = true; break; }
+            if (dup) continue;
+            // insertion keeps R sorted
+            int q = n++;
+            while (q > 0 && R[q - 1] > c) { R[q] = R[q - 1]; --q; }
+            R[q] = c;
+        }
     }
-    // 3-way merge: window [lo,hi], globals outside the window, random R
-    int64_t out = 0, wj = lo, gk = 0, rk = 0;
+    // 3-way merge: window W_i (step r), globals outside W_i, random R
+    int64_t wj = INT64_MAX, whi = -1;
+    if (parts & 1) {
+        wj = i - imin(i, M.w - 1) / M.r * M.r;
+        whi = i + imin(M.L - 1 - i, M.w - 1) / M.r * M.r;
+    }
+    int64_t out = 0, gk = 0, rk = 0;
     auto next_g = [&](int64_t &k) -> int64_t {
+        if (!(parts & 2)) return INT64_MAX;
         while (k < M.ng) {
             const int64_t gv = bb_global_at(M, k);
-            if (gv < lo || gv > hi) return gv;
+            if (!bb_in_window(M, i, gv)) return gv;
             ++k;
         }
         return INT64_MAX;
     };
     int64_t gv = next_g(gk);
     for (;;) {
-        const int64_t a = wj <= hi ? wj : INT64_MAX;
+        const int64_t a = wj <= whi ? wj : INT64_MAX;
         const int64_t r = rk < n ? R[rk] : INT64_MAX;
         int64_t v = a;
         if (gv < v) v = gv;
         if (r < v) v = r;
         if (v == INT64_MAX) break;
         dst[out++] = (int32_t)v;
-        if (v == a) ++wj;
+        if (v == a) wj += M.r;
         else if (v == gv) { ++gk; gv = next_g(gk); }
         else ++rk;
     }

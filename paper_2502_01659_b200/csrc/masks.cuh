@@ -39,7 +39,7 @@ enum PieceMode { P_AFFINE = 0, P_SKIPMUL = 1, P_CSR = 2 };
 
 struct DevMask {
     int32_t kind;
-    int32_t pad;
+    int32_t parts;        // BigBird components: bit 0 window, 1 global minus window, 2 random (0 = all)
     int64_t L;
     const int64_t *row_ptr;
     const int32_t *col_idx;
@@ -213,21 +213,43 @@ GA_HD void bb_window(const DevMask &M, int64_t i, int64_t &lo, int64_t &hi)
     hi = imin(M.L - 1, i + M.w - 1);
 }
 
-// |W_i U G| for a non-global row
-GA_HD int64_t bb_wg(const DevMask &M, int64_t i)
+// the BigBird window predicate: WINDOW(w, r) (r = 1 unless dilated)
+GA_HD bool bb_in_window(const DevMask &M, int64_t i, int64_t j)
+{
+    const int64_t d = i > j ? i - j : j - i;
+    return d < M.w && d % M.r == 0;
+}
+
+// |W_i| in closed form (the window rows inside [0, L))
+GA_HD int64_t bb_wsize(const DevMask &M, int64_t i)
+{
+    return 1 + imin(i, M.w - 1) / M.r + imin(M.L - 1 - i, M.w - 1) / M.r;
+}
+
+// globals inside W_i
+GA_HD int64_t bb_globals_in_window(const DevMask &M, int64_t i)
 {
     int64_t lo, hi;
     bb_window(M, i, lo, hi);
-    int64_t in_w = bb_count_below(M, hi + 1) - bb_count_below(M, lo);
-    return (hi - lo + 1) + (M.ng - in_w);
+    const int64_t a = bb_count_below(M, lo), b = bb_count_below(M, hi + 1);
+    if (M.r == 1) return b - a;
+    int64_t n = 0;
+    for (int64_t k = a; k < b; ++k) n += bb_in_window(M, i, bb_global_at(M, k)) ? 1 : 0;
+    return n;
 }
 
+// |W_i U G| for a non-global row
+GA_HD int64_t bb_wg(const DevMask &M, int64_t i) { return bb_wsize(M, i) + (M.ng - bb_globals_in_window(M, i)); }
+
+// degree of row i restricted to the selected components (window | global \ window | random)
 GA_HD int64_t bb_degree(const DevMask &M, int64_t i)
 {
-    if (bb_is_global(M, i)) return M.L;
-    int64_t wg = bb_wg(M, i);
-    int64_t comp = M.L - wg;
-    return wg + (comp < M.nrand ? comp : M.nrand);
+    const int parts = M.parts ? M.parts : 7;
+    const int64_t nw = bb_wsize(M, i);
+    if (bb_is_global(M, i)) return ((parts & 1) ? nw : 0) + ((parts & 2) ? M.L - nw : 0);
+    const int64_t gout = M.ng - bb_globals_in_window(M, i);
+    const int64_t comp = M.L - (nw + gout);
+    return ((parts & 1) ? nw : 0) + ((parts & 2) ? gout : 0) + ((parts & 4) ? imin(comp, M.nrand) : 0);
 }
 
 // candidate t of row i: floor((splitmix64(splitmix64(seed) ^ (i*2^20 + t)) >> 32) * L / 2^32)

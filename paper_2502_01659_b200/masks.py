@@ -64,21 +64,28 @@ class LongNet(Mask):
         return m
 
 
+BB_WINDOW, BB_GLOBAL, BB_RANDOM = _abi.GA_BB_WINDOW, _abi.GA_BB_GLOBAL, _abi.GA_BB_RANDOM
+
+
 @dataclass(frozen=True)
 class BigBird(Mask):
-    """Window(w) UNION global rows/cols UNION n_random random columns per non-global row
+    """Window(w, r) UNION global rows/cols UNION n_random random columns per non-global row
     (readings R8-R10).  `global_idx`: sorted int64 CUDA tensor or
-    None for the evenly spaced set {floor(k L / n_global)}."""
+    None for the evenly spaced set {floor(k L / n_global)}.  `parts` keeps only some of the
+    three disjoint components (BB_WINDOW | BB_GLOBAL | BB_RANDOM; 0 = all) — e.g. the
+    paper's "global minus local" kernel is parts=BB_GLOBAL (PAPER.md:235)."""
     w: int
     n_global: int
     n_random: int
     seed: int = 0xB16B12D
     global_idx: Optional[object] = None
+    r: int = 1
+    parts: int = 0
     kind = _abi.GA_MASK_BIGBIRD
 
     def to_c(self, L):
         m = self._base(L)
-        m.w, m.r = self.w, 1
+        m.w, m.r, m.parts = self.w, self.r, self.parts
         m.n_global, m.n_random, m.seed = self.n_global, self.n_random, self.seed & (2**64 - 1)
         if self.global_idx is not None:
             m.global_idx = self.global_idx.data_ptr()

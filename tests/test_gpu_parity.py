@@ -480,3 +480,72 @@ def test_cfg5_160M_window_sampled(ga, orc):
     got = out[torch.from_numpy(rows).cuda()].double().cpu().numpy()
     want, _ = orc.attention_seeded(seed, "bf16", orc.window(L, 128), H, d, rows=rows)
     assert np.abs(got - want).max() <= 2e-2
+
+
+# ---------------------------------------------------------------- composition API (f1)
+@pytest.mark.parametrize("L,w,ng,nr,r,parts", [(3000, 51, 3, 3, 1, 2), (3000, 51, 3, 3, 1, 4), (3000, 101, 3, 0, 2, 2),
+                                               (3000, 101, 3, 0, 2, 0), (2000, 51, 5, 7, 3, 1), (64, 30, 2, 50, 2, 4)])
+def test_bigbird_parts_csr_bit_exact(ga, orc, L, w, ng, nr, r, parts):
+    """ga_mask_to_csr of the BigBird components (and a dilated window) equals the oracle's
+    enumeration from the definitions, bit for bit."""
+    m = ga.mask_to_csr(ga.BigBird(w, ng, nr, seed=9, r=r, parts=parts), L)
+    rp, ci, _ = orc.mask_to_csr(orc.bigbird(L, w, ng, nr, 9, r=r, parts=parts))
+    assert np.array_equal(m.row_ptr.cpu().numpy(), rp)
+    assert np.array_equal(m.col_idx.cpu().numpy(), ci.astype(np.int32))
+
+
+@pytest.mark.parametrize("name", ["longformer", "longformer_dilated", "bigbird"])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_presets_compose_equals_union(ga, orc, name, dt):
+    """The paper's Fig. 5 patterns run as sequential component calls carrying
+    one (m, l, o) state equal one call over the union CSR, and the oracle."""
+    L, H, d = 4096, 2, 64
+    pre = getattr(ga.presets, name)(L)
+    cpu, f64 = _inputs(L, H, d, dt, 521, centred=True)
+    q, k, v = (x.cuda() for x in cpu)
+    comp = ga.compose(q, k, v, pre.components)
+    one = ga.attention(q, k, v, pre.union)
+    pm = pre.pattern
+    want, _ = orc.attention(*f64, orc.bigbird(L, pm.w, pm.n_global, pm.n_random, pm.seed, r=pm.r))
+    tol = TOL[dt]
+    assert np.abs(comp.double().cpu().numpy() - want).max() <= tol
+    assert np.abs(one.double().cpu().numpy() - want).max() <= tol
+    assert (comp.float() - one.float()).abs().max().item() <= (1e-5 if dt == "f32" else 2e-2)
+
+
+def test_state_api_semantics(ga, orc):
+    """WRITE overwrites, ACCUMULATE (+)-combines, an empty edge set leaves the state
+    unchanged, zero buffers are an empty state, and state + out are produced together."""
+    L, H, d = 1500, 2, 32
+    cpu, f64 = _inputs(L, H, d, "f32", 77, centred=True)
+    q, k, v = (x.cuda() for x in cpu)
+    st = ga.State.empty(L, H, d)
+    w = ga.Window(20)
+    ref = ga.attention(q, k, v, w)
+    ga.attention(q, k, v, w, state=st)  # write
+    assert torch.allclose(ga.state_finalize(st, torch.float32), ref, atol=1e-6)
+    ga.attention(q, k, v, w, state=st)  # write again: unchanged, not doubled
+    assert torch.allclose(ga.state_finalize(st, torch.float32), ref, atol=1e-6)
+    # split Window(20) into the band |i-j| < 5 and the rest (global-free BigBird parts)
+    st2 = ga.State.empty(L, H, d)
+    near = ga.Window(5)
+    far = ga.mask_to_csr(ga.BigBird(20, 0, 0, parts=ga.BB_WINDOW), L)  # = Window(20) as CSR
+    # far minus near as an explicit CSR built on the host from the two CSRs
+    near_csr = ga.mask_to_csr(ga.BigBird(5, 0, 0, parts=ga.BB_WINDOW), L)
+    rp_f, ci_f = far.row_ptr.cpu().numpy(), far.col_idx.cpu().numpy()
+    rp_n, ci_n = near_csr.row_ptr.cpu().numpy(), near_csr.col_idx.cpu().numpy()
+    rows = [np.setdiff1d(ci_f[rp_f[i]:rp_f[i + 1]], ci_n[rp_n[i]:rp_n[i + 1]]) for i in range(L)]
+    rp = np.concatenate([[0], np.cumsum([len(x) for x in rows])]).astype(np.int64)
+    ring = ga.CSR(torch.from_numpy(rp).cuda(), torch.from_numpy(np.concatenate(rows).astype(np.int32)).cuda())
+    out_near = ga.attention(q, k, v, near, state=st2, out=torch.empty_like(q))  # state + out together
+    assert torch.allclose(out_near, ga.attention(q, k, v, near), atol=1e-6)
+    ga.attention(q, k, v, ring, state=st2, accumulate=True)
+    assert torch.allclose(ga.state_finalize(st2, torch.float32), ref, atol=2e-6)
+    # an empty component (rows without edges) leaves the state as it was
+    empty = ga.CSR(torch.zeros(L + 1, dtype=torch.int64, device="cuda"), torch.zeros(0, dtype=torch.int32, device="cuda"))
+    before = ga.state_finalize(st2, torch.float32)
+    ga.attention(q, k, v, empty, state=st2, accumulate=True)
+    assert torch.equal(ga.state_finalize(st2, torch.float32), before)
+    # state needs the edge kernel
+    with pytest.raises(ga.GaError, match="UNSUPPORTED"):
+        ga.attention(q.bfloat16(), k.bfloat16(), v.bfloat16(), ga.Window(64), state=ga.State.empty(L, H, d), kernel="tiled")

@@ -69,21 +69,12 @@ def test_abi_struct_layout_matches_header():
     """ctypes mirrors of ga_mask / ga_opts have the C layout (checked with g++ offsetof)."""
     import paper_2502_01659_b200._abi as abi
 
-    src = r'''
-#include <cstdio>
-#include <cstddef>
-#include "ga.h"
-#define P(T, f) printf(#T "." #f " %zu\n", offsetof(T, f));
-int main() {
-  P(ga_mask, kind) P(ga_mask, L) P(ga_mask, row_ptr) P(ga_mask, col_idx) P(ga_mask, nnz) P(ga_mask, w)
-  P(ga_mask, r) P(ga_mask, w0) P(ga_mask, alpha) P(ga_mask, seg) P(ga_mask, global_idx) P(ga_mask, n_global)
-  P(ga_mask, n_random) P(ga_mask, seed)
-  P(ga_opts, q_begin) P(ga_opts, q_rows) P(ga_opts, kv_begin) P(ga_opts, kv_rows) P(ga_opts, workspace)
-  P(ga_opts, workspace_bytes) P(ga_opts, edge_counter) P(ga_opts, row_fingerprint) P(ga_opts, kernel)
-  P(ga_opts, heavy_threshold)
-  printf("sizeof.ga_mask %zu\nsizeof.ga_opts %zu\n", sizeof(ga_mask), sizeof(ga_opts));
-}
-'''
+    structs = ((abi.GaMask, "ga_mask"), (abi.GaOpts, "ga_opts"), (abi.GaState, "ga_state"))
+    probes = " ".join(f"P({c}, {f})" for cls, c in structs for f, _ in cls._fields_ if not f.startswith("reserved"))
+    sizes = " ".join(f'printf("sizeof.{c} %zu\\n", sizeof({c}));' for _, c in structs)
+    src = ('#include <cstdio>\n#include <cstddef>\n#include "ga.h"\n'
+           '#define P(T, f) printf(#T "." #f " %zu\\n", offsetof(T, f));\n'
+           f"int main() {{ {probes} {sizes} }}\n")
     import tempfile
     with tempfile.TemporaryDirectory() as td:
         p = os.path.join(td, "l.cpp")
@@ -91,7 +82,7 @@ int main() {
         subprocess.check_call(["g++", "-I", os.path.join(ROOT, "include"), "-o", p + ".bin", p])
         out = subprocess.check_output([p + ".bin"], text=True)
     got = dict(line.split() for line in out.splitlines())
-    for cls, cname in ((abi.GaMask, "ga_mask"), (abi.GaOpts, "ga_opts")):
+    for cls, cname in structs:
         for f, _ in cls._fields_:
             if f.startswith("reserved"):
                 continue
@@ -105,6 +96,9 @@ int main() {
     ("longnet", 4096, (64, 2)), ("longnet", 5000, (64, 2)), ("longnet", 2187, (27, 3)), ("longnet", 300, (512, 2)),
     ("longnet", 12345, (16, 4)), ("longnet", 5000, (100, 3)), ("longnet", 999, (7, 2)), ("longnet", 3000, (10, 4)),
     ("bigbird", 1024, (8, 4, 4)), ("bigbird", 3000, (64, 7, 20)), ("bigbird", 64, (30, 2, 50)),
+    # dilated window and single components (the composition API's parts)
+    ("bigbird", 3000, (101, 3, 0, 2, 0)), ("bigbird", 3000, (101, 3, 0, 2, 2)), ("bigbird", 3000, (51, 3, 3, 1, 4)),
+    ("bigbird", 2000, (51, 5, 7, 3, 1)), ("bigbird", 2000, (51, 5, 7, 3, 6)), ("bigbird", 64, (30, 2, 50, 2, 4)),
 ])
 def test_host_mask_count_equals_oracle(orc, spec):
     import paper_2502_01659_b200 as ga
@@ -117,7 +111,9 @@ def test_host_mask_count_equals_oracle(orc, spec):
     elif fam == "longnet":
         m, om = ga.LongNet(*a), orc.longnet(L, *a)
     else:
-        m, om = ga.BigBird(a[0], a[1], a[2], seed=5), orc.bigbird(L, a[0], a[1], a[2], 5)
+        r, parts = (a[3], a[4]) if len(a) > 3 else (1, 0)
+        m = ga.BigBird(a[0], a[1], a[2], seed=5, r=r, parts=parts)
+        om = orc.bigbird(L, a[0], a[1], a[2], 5, r=r, parts=parts)
     assert ga.mask_count(m, L) == orc.mask_to_csr(om, False)[2]
 
 

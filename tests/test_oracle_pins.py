@@ -357,3 +357,26 @@ def test_sparsity_schedule_paper_values():
         L, want = int(vals[0]), float(vals[1])
         got = 2730.0 / L
         assert float(f"{got:.2g}") == pytest.approx(want, rel=1e-9), (L, got, want)
+
+
+# ------------------------------------------------------------ composition components (f1)
+@pytest.mark.parametrize("L,w,ng,nr,r,gidx", [(300, 9, 3, 5, 1, None), (500, 21, 4, 6, 2, None),
+                                             (200, 15, 3, 2, 3, [0, 77, 199]), (40, 8, 2, 60, 1, None)])
+def test_bigbird_components_are_disjoint_and_cover_the_mask(orc, L, w, ng, nr, r, gidx):
+    """Window, global-minus-window and random parts partition the BigBird
+    mask: pairwise disjoint, union = the full definition, window part = WINDOW(w, r), and
+    the global part is exactly {(i, j) : (i in G or j in G) and j not in W_i}."""
+    full = orc.bigbird(L, w, ng, nr, 7, global_idx=gidx, r=r)
+    parts = {p: orc.bigbird(L, w, ng, nr, 7, global_idx=gidx, r=r, parts=p) for p in (1, 2, 4)}
+    G = set(gidx) if gidx is not None else {(k * L) // ng for k in range(ng)}
+    win = orc.window(L, w, r)
+    for i in range(L):
+        rows = {p: set(orc.neighbors(m, i).tolist()) for p, m in parts.items()}
+        assert not (rows[1] & rows[2]) and not (rows[1] & rows[4]) and not (rows[2] & rows[4])
+        assert rows[1] | rows[2] | rows[4] == set(orc.neighbors(full, i).tolist())
+        assert rows[1] == set(orc.neighbors(win, i).tolist())
+        W = rows[1]
+        want_g = {j for j in range(L) if (i in G or j in G) and j not in W}
+        assert rows[2] == want_g
+        if i in G:
+            assert not rows[4]
