@@ -25,6 +25,15 @@
 namespace ga {
 namespace band {
 
+#ifdef GA_BAND_PROF
+__device__ unsigned long long g_prof[8];
+#define PROF_T(var) const long long var = clock64()
+#define PROF_ADD(k, a, b) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_prof[k], (unsigned long long)((b) - (a))); } while (0)
+#else
+#define PROF_T(var)
+#define PROF_ADD(k, a, b)
+#endif
+
 constexpr int WARPS = 7; // 112 rows: two CTAs (28 KB Q + 94 KB band each) fit one SM at m=127
 constexpr int ROWS = 16 * WARPS;
 constexpr int THREADS = 32 * WARPS;
@@ -38,7 +47,10 @@ using tc::swz;
 using tc::cp_async16;
 
 constexpr int QBOX = 56; // rows per TMA box of the Q tile (2 boxes)
-constexpr int BBOX = 64; // rows per TMA box of the K/V band
+// TMA boxes of the K/V band: 64 rows (box * r <= 256 tokens up to r = 4; 32 rows beyond).
+// Few large boxes issue fastest (8- and 16-row boxes measured slower at cfg2; 128 rows no
+// faster than 64)
+__host__ __device__ constexpr int band_box_rows(int64_t r) { return r <= 4 ? 64 : 32; }
 
 struct BandParams {
     CUtensorMap tmQ, tmK, tmV; // TMA maps of one residue class x head (element stride r)
@@ -49,17 +61,21 @@ struct BandParams {
     int64_t edge_tiles; // tiles at each end whose band may be clipped (scheduled first)
     uint32_t smem_bytes;
     int32_t tma;        // 1: tiles whose band is local load through the tensor maps
+    int32_t bbox;       // rows per TMA box of the band (band_box_rows(r))
 };
 
 // band rows allocated: ROWS + 2m rounded up to whole TMA boxes (multiples of 16 rows, so the
 // V band starts on a swizzle period: 1024 B at d = 64, 512 B at d = 32)
-__host__ __device__ constexpr int64_t band_alloc_rows(int64_t m) { return (ROWS + 2 * m + BBOX - 1) / BBOX * BBOX; }
+__host__ __device__ constexpr int64_t band_alloc_rows(int64_t m, int64_t r)
+{
+    return (ROWS + 2 * m + band_box_rows(r) - 1) / band_box_rows(r) * band_box_rows(r);
+}
 
-template <int D> __host__ __device__ constexpr uint32_t band_smem(int64_t m)
+template <int D> __host__ __device__ constexpr uint32_t band_smem(int64_t m, int64_t r)
 {
     return (uint32_t)(1024                                           // alignment slack
                       + ROWS * Geo<D>::RB                            // Q tile (hand-off + output staging)
-                      + 2 * band_alloc_rows(m) * Geo<D>::RB + 64);   // K and V band, 2 mbarriers
+                      + 2 * band_alloc_rows(m, r) * Geo<D>::RB + 64); // K and V band, 2 mbarriers
 }
 
 // One CUDA-core edge: score of (q half, key half) -> full score via the lane pair.
@@ -107,6 +123,7 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
 
     // CTA geometry (32-bit divisions: the grid and r*H fit in 32 bits; 64-bit only for
     // sequences beyond 2^31 tokens)
+    PROF_T(t_start);
     const uint32_t rH = (uint32_t)(r * H), bid = blockIdx.x;
     const uint32_t ch = bid % rH;
     // tile order: the tiles at both sequence ends (clipped bands, predicated paths) run first
@@ -132,7 +149,8 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
     const bool interior = v_lo == a0 && v_hi == a0 + ROWS && a0 - m >= 0 && a0 + ROWS - 1 + m <= Nc - 1;
 
     const int64_t NB = ROWS + 2 * m; // band rows; band-local 0 = class row a0 - m
-    const int64_t NBA = band_alloc_rows(m);
+    const int64_t NBA = band_alloc_rows(m, r);
+    const int BBOX = bp.bbox;
     // 1024-byte aligned base: the 128B swizzle of TMA follows the address bits, tc::swz the row
     const uint32_t sraw = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t sbase = (sraw + 1023u) & ~1023u;
@@ -204,7 +222,8 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
         }
         __syncthreads();
         if (warp == 0) {
-            constexpr uint32_t QB = QBOX * G::RB, BB = BBOX * G::RB;
+            constexpr uint32_t QB = QBOX * G::RB;
+            const uint32_t BB = (uint32_t)BBOX * G::RB;
             if (lane == 0) {
                 tma::expect_tx(mb0, (uint32_t)(ROWS / QBOX) * QB + 2u * (uint32_t)(nbox - (s1 - s0)) * BB);
                 tma::expect_tx(mb1, 2u * (uint32_t)(s1 - s0) * BB);
@@ -244,6 +263,8 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
         __syncthreads();
     }
 
+    PROF_T(t_loaded);
+    PROF_ADD(0, t_start, t_loaded);
     const float sl2 = p.scale_log2;
 
     // A fragments of Q for the tensor-core phase, taken before the Q rows are reused
@@ -358,12 +379,16 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
             __syncwarp();
         }
     }
+    PROF_T(t_cuda);
+    PROF_ADD(1, t_loaded, t_cuda);
     if (use_tma) {
         umma::mbar_wait(mb1, 0); // dense rows landed
     } else {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads(); // dense rows landed
     }
+    PROF_T(t_dense);
+    PROF_ADD(2, t_cuda, t_dense);
     if (!warp_live) return; // no further CTA-wide barriers
 
     // ================= tensor-core phase: dense 16x16 blocks of F =================
@@ -386,6 +411,8 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
             st.block16x2(kaddr, vaddr, (uint32_t)(b * 16 * G::RB), (uint32_t)((b + 1) * 16 * G::RB), sl2);
         if (b < q16) st.block16(kaddr, vaddr, (uint32_t)(b * 16 * G::RB), sl2);
     }
+    PROF_T(t_mma);
+    PROF_ADD(3, t_dense, t_mma);
     // ---- finalise: l = quad sum, normalise, stage through this warp's Q rows, store
     rs.reduce_l();
     const float inv0 = lr[0] > 0.f ? 1.f / lr[0] : 0.f, inv1 = lr[1] > 0.f ? 1.f / lr[1] : 0.f;
@@ -408,6 +435,9 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) band_kernel(const 
         const int64_t i = c + xa * r;
         stg16(Og + (size_t)(i - p.q_begin) * row_bytes + cc * 16, lds16(sQ + swz<D>(w16 + row, cc)));
     }
+    PROF_T(t_end);
+    PROF_ADD(4, t_mma, t_end);
+    PROF_ADD(5, t_start, t_end);
 }
 
 static constexpr uint32_t kMaxSmem = 227 * 1024;
@@ -429,12 +459,21 @@ template <typename T, int D> static ga_status launch_t(const BandParams &bp, cud
 
 } // namespace band
 
-static uint32_t band_smem_for(int d, int64_t m)
+#ifdef GA_BAND_PROF
+extern "C" void ga_band_prof_read(unsigned long long *out)
+{
+    cudaMemcpyFromSymbol(out, band::g_prof, sizeof(unsigned long long) * 8);
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(band::g_prof, z, sizeof(z));
+}
+#endif
+
+static uint32_t band_smem_for(int d, int64_t m, int64_t r)
 {
     switch (d) {
-    case 32: return band::band_smem<32>(m);
-    case 64: return band::band_smem<64>(m);
-    default: return band::band_smem<128>(m);
+    case 32: return band::band_smem<32>(m, r);
+    case 64: return band::band_smem<64>(m, r);
+    default: return band::band_smem<128>(m, r);
     }
 }
 
@@ -444,7 +483,7 @@ bool window_tiled_supported(const AttnParams &p, ga_dtype dt)
 {
     if (p.mask.kind != K_WINDOW || (dt != GA_BF16 && dt != GA_F16)) return false;
     if (p.mask.m < 15) return false;
-    return band_smem_for(p.d, p.mask.m) <= band::kMaxSmem;
+    return band_smem_for(p.d, p.mask.m, p.mask.r) <= band::kMaxSmem;
 }
 
 ga_status launch_window_tiled(const AttnParams &p, ga_dtype dt, cudaStream_t s)
@@ -457,15 +496,16 @@ ga_status launch_window_tiled(const AttnParams &p, ga_dtype dt, cudaStream_t s)
     const int64_t per_class = (p.q_rows + bp.r - 1) / bp.r + 1;
     bp.tiles = (per_class + band::ROWS - 1) / band::ROWS + 1; // +1: grid anchored at ROWS multiples
     bp.edge_tiles = (bp.m + band::ROWS - 1) / band::ROWS + 2;
-    bp.smem_bytes = band_smem_for(p.d, bp.m);
+    bp.smem_bytes = band_smem_for(p.d, bp.m, bp.r);
+    bp.bbox = band::band_box_rows(bp.r);
     // TMA maps of Q (query rows) and K/V (key rows) with element stride r; d = 128 rows
     // (256 B) exceed one swizzle span and dilations above 8 exceed the traversal stride,
     // those keep the cp.async path
-    bp.tma = p.d <= 64 && band::BBOX * bp.r <= 256 && band::QBOX * bp.r <= 256 &&
-             band::band_alloc_rows(bp.m) / band::BBOX <= 32 &&
+    bp.tma = p.d <= 64 && (int64_t)bp.bbox * bp.r <= 256 && band::QBOX * bp.r <= 256 &&
+             band::band_alloc_rows(bp.m, bp.r) / bp.bbox <= 32 &&
              tma::encode_rows(&bp.tmQ, p.Q, p.q_rows, p.H, p.d, (int)bp.r, band::QBOX) &&
-             tma::encode_rows(&bp.tmK, p.K, p.kv_rows, p.H, p.d, (int)bp.r, band::BBOX) &&
-             tma::encode_rows(&bp.tmV, p.V, p.kv_rows, p.H, p.d, (int)bp.r, band::BBOX);
+             tma::encode_rows(&bp.tmK, p.K, p.kv_rows, p.H, p.d, (int)bp.r, bp.bbox) &&
+             tma::encode_rows(&bp.tmV, p.V, p.kv_rows, p.H, p.d, (int)bp.r, bp.bbox);
     if (bp.r * p.H * bp.tiles > (int64_t)INT32_MAX) {
         set_error("band kernel grid too large");
         return GA_ERR_UNSUPPORTED;
