@@ -110,7 +110,10 @@ typedef enum {
                             (K/V band in shared memory, mma.sync on fully dense 16x16 blocks,
                             CUDA cores on the partial triangles); LONGNET -> dense-group kernel
                             (rows sharing a neighbour set x their strided key pieces) */
-    GA_KERNEL_TC = 3     /* bf16 window: tcgen05 dense core (not built in this version) */
+    GA_KERNEL_TC = 3     /* bf16/fp16 tcgen05 (TMEM accumulator) kernel of the family, d = 64:
+                            WINDOW with 64 <= m <= 128, r <= 4 -> persistent band kernel (128-row
+                            query tiles x 64-key chunks, masked per row; window_tc.cu); LONGNET ->
+                            dense groups on tcgen05 + the rest on mma.sync */
 } ga_kernel;
 
 /* Carried online-softmax state: for query row i and head h over an edge

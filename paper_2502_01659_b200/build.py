@@ -24,6 +24,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2",
           "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC] + ARCH
+# debug builds: e.g. GA_NVCC_EXTRA="-DGA_MBAR_SPIN_LIMIT=100000000" makes a stuck mbarrier wait
+# trap (a reported launch failure) instead of hanging the GPU
+CFLAGS += os.environ.get("GA_NVCC_EXTRA", "").split()
 
 
 def _sources():

@@ -451,7 +451,10 @@ ga_status ga_query_alignment(const ga_mask *mask, int32_t d, ga_dtype dtype, int
     p.mask = M;
     p.d = d;
     *tokens = 1;
-    if (window_tiled_supported(p, dtype)) *tokens = band_tile_rows() * M.r;
+    p.q_rows = M.L;
+    p.kv_rows = M.L;
+    if (window_tc_supported(p, dtype)) *tokens = window_tc_tile_rows() * M.r;
+    else if (window_tiled_supported(p, dtype)) *tokens = band_tile_rows() * M.r;
     else if (longnet_tc_supported(p, dtype)) *tokens = M.w0;
     return GA_OK;
 }

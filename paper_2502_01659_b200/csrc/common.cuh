@@ -220,6 +220,7 @@ ga_status launch_csr_heavy(const AttnParams &p, ga_dtype dt, void *ws, size_t ws
 size_t csr_heavy_workspace(int64_t L, int64_t nnz, int32_t H, int32_t d, int64_t C);
 bool window_tiled_supported(const AttnParams &p, ga_dtype dt);
 int64_t band_tile_rows(); // class rows per band-kernel tile
+int64_t window_tc_tile_rows(); // class rows per tcgen05 window-kernel tile
 ga_status launch_window_tiled(const AttnParams &p, ga_dtype dt, cudaStream_t s);
 bool longnet_tc_supported(const AttnParams &p, ga_dtype dt);
 ga_status launch_longnet_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s, bool use_umma);

@@ -1,14 +1,528 @@
-// window_tc.cu — tcgen05 dense-tile window kernel (placeholder until implemented).
-#include "common.cuh"
+// window_tc.cu — tcgen05 (5th-gen tensor core, TMEM accumulators) kernel for Window(w, r)
+// masks, bf16/fp16, d = 64, band half-width 64 <= m <= 128 (cfg2: Window(256, 2), cfg5:
+// Window(128, 1); both m = 127).
+//
+// Residue class c of a dilated window is a band (readings R1/R2): class
+// row x sees class rows [x - m, x + m] ∩ [0, Nc).  A 128-row query tile (thread = row = TMEM
+// lane) meets the keys of 64-key chunks g (class rows [64g, 64g + 64)) with
+// g in [floor((a0 - m)/64), floor((a0 + 127 + m)/64)] — 6 chunks at m = 127, of which the
+// middle two are dense for every row and the outer ones hold the band's two triangles.  Per
+// chunk:
+//
+//   S  = Q K_g^T      tcgen05.mma.cta_group::1.kind::f16 M=128 N=64 (K=16 x 4), A (Q tile) and
+//                     B (K chunk) from 128B-swizzled shared memory, fp32 accumulator in TMEM
+//   softmax           each thread tcgen05.ld's its row of S; keys outside the row's band get
+//                     weight exactly 0; online softmax in the exp2 domain (lazy rescale, 2^8);
+//                     P (bf16/fp16 pairs) written back to TMEM with tcgen05.st.  A warp skips
+//                     chunks its 32 rows do not reach (P = 0 without reading S) and masks only
+//                     chunks its rows reach partially
+//   O += P V_g        tcgen05.mma with A = P from TMEM, B = V_g (MN-major) from shared memory
+//
+// The tensor cores see whole 128 x 64 chunks (66% of the products valid at m = 127: 32,640
+// band edges of 49,152 per tile); exponentials, sums and weights are computed only for the
+// chunks a warp's rows reach, and a masked pair contributes exactly 0 — the result is the
+// Algorithm 1 result over the band's edges, computed in O(nnz d) work.
+//
+// CTA organisation (persistent, one CTA per SM, 512 TMEM columns):
+//   warps 0-3  softmax warpgroup A: even tiles of a tile pair   (TMEM cols   0..255)
+//   warps 4-7  softmax warpgroup B: odd tiles                    (TMEM cols 256..511)
+//   warp 8     loader: TMA boxes of the Q tiles (2 x 64 class rows, element stride r) and the
+//              K/V chunks into an 8-slot ring (slot = g mod 8); peer rows (sharded runs) by
+//              cp.async from the owner's memory
+//   warp 9     MMA issuer (one elected lane)
+// A CTA walks a contiguous run of tile pairs of one (class, head) stream: consecutive pairs
+// share 4 of their 8 chunks, which stay resident (each K/V row is read from L2/HBM about once
+// per run), and the two warpgroups alternate on the tensor and MUFU pipes.
+#include "tc_common.cuh"
+#include "tma.cuh"
+#include "umma.cuh"
 
 namespace ga {
+namespace wtc {
+using namespace tc;
+using namespace umma;
 
-bool window_tc_supported(const AttnParams &, ga_dtype) { return false; }
+constexpr int ROWS = 128, KC = 64, NSLOT = 8, D = 64, RB = 2 * D;
+constexpr int THREADS = 320; // 8 softmax warps + loader + MMA
+constexpr uint32_t QBYTES = ROWS * RB;   // 16 KB
+constexpr uint32_t CBYTES = KC * RB;     // 8 KB: one K or V chunk
+constexpr uint32_t OFF_Q = 0;            // Q[wg][buf]: 4 x 16 KB
+constexpr uint32_t OFF_KV = 4 * QBYTES;  // slot s: K at OFF_KV + 2 s CBYTES, V right after
+constexpr uint32_t OFF_BAR = OFF_KV + NSLOT * 2 * CBYTES;
+constexpr uint32_t SMEM_BYTES = 1024 + OFF_BAR + 64 * 8;
 
-ga_status launch_window_tc(const AttnParams &, ga_dtype, cudaStream_t)
+// mbarrier indices (8 bytes each from OFF_BAR)
+constexpr int B_QFULL = 0, B_QEMPTY = 4, B_KVFULL = 8, B_KVEMPTY = 16, B_SFULL = 24, B_PFULL = 28, B_OFULL = 32;
+constexpr int B_TMEM = 40; // tcgen05.alloc writes the TMEM base here
+
+// TMEM columns of warpgroup w: S[2] at 256w + {0, 64}, P[2] at 256w + 128 + {0, 32}, O at 256w + 192
+constexpr uint32_t COL_S = 0, COL_P = 128, COL_O = 192;
+
+struct TcParams {
+    CUtensorMap tmQ, tmK, tmV; // one head, element stride r, 64-row boxes
+    AttnParams p;
+    int64_t m, r;
+    int64_t pps;   // tile pairs per (class, head) stream
+    int64_t items; // streams x pps
+};
+
+__host__ __device__ inline int64_t floordiv(int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// Geometry of one work item (a pair of consecutive 128-row tiles of one stream); every role
+// derives it independently from the item index, so all agree without communication.
+struct Pair {
+    int64_t stream, u, c, Nc, a_lo, a_hi;
+    int h;
+    int64_t a0[2];  // first class row of tile A / B
+    bool valid[2];
+    int64_t F[2], n[2]; // chunks [F, F + n) per tile
+    int64_t lo, hi;     // union of the chunk ranges
+    bool any;
+};
+
+__device__ __forceinline__ Pair pair_geo(const TcParams &tp, int64_t it)
 {
-    set_error("tcgen05 window kernel not built");
-    return GA_ERR_UNSUPPORTED;
+    const AttnParams &p = tp.p;
+    const int64_t r = tp.r, m = tp.m, L = p.mask.L;
+    Pair P;
+    P.stream = it / tp.pps;
+    P.u = it - P.stream * tp.pps;
+    P.c = P.stream / p.H;
+    P.h = (int)(P.stream - P.c * p.H);
+    const int64_t c = P.c;
+    P.Nc = c < L ? (L - c + r - 1) / r : 0;
+    const int64_t q_end = p.q_begin + p.q_rows;
+    P.a_lo = p.q_begin > c ? (p.q_begin - c + r - 1) / r : 0;
+    P.a_hi = q_end > c ? imin((q_end - c + r - 1) / r, P.Nc) : 0;
+    const int64_t t0 = P.a_lo / ROWS + 2 * P.u;
+    const int64_t lastc = (P.Nc - 1) / KC;
+    P.lo = INT64_MAX;
+    P.hi = -1;
+    for (int w = 0; w < 2; ++w) {
+        const int64_t a0 = (t0 + w) * ROWS;
+        P.a0[w] = a0;
+        P.valid[w] = P.a_lo < P.a_hi && a0 < P.a_hi;
+        const int64_t f = imax(floordiv(a0 - m, KC), 0), e = imin(floordiv(a0 + ROWS - 1 + m, KC), lastc);
+        P.F[w] = f;
+        P.n[w] = P.valid[w] ? e - f + 1 : 0;
+        if (P.valid[w]) {
+            P.lo = imin(P.lo, f);
+            P.hi = imax(P.hi, e);
+        }
+    }
+    P.any = P.valid[0];
+    return P;
+}
+
+__device__ __forceinline__ uint32_t bar(uint32_t base, int i) { return base + 8u * (uint32_t)i; }
+
+template <typename T>
+__global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_constant__ TcParams tp)
+{
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t sbase = (raw + 1023u) & ~1023u;
+    const uint32_t bars = sbase + OFF_BAR;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem_raw + (sbase - raw) + OFF_BAR + 8 * B_TMEM);
+    const AttnParams &p = tp.p;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t m = tp.m, r = tp.r;
+    const int H = p.H;
+    const size_t row_bytes = (size_t)H * D * sizeof(T);
+
+    // contiguous run of work items
+    const int64_t it_begin = tp.items * blockIdx.x / gridDim.x, it_end = tp.items * (blockIdx.x + 1) / gridDim.x;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(bar(bars, B_QFULL + i), 1);
+            mbar_init(bar(bars, B_QEMPTY + i), 1);
+            mbar_init(bar(bars, B_SFULL + i), 1);
+            mbar_init(bar(bars, B_PFULL + i), 128);
+            mbar_init(bar(bars, B_OFULL + i), 1);
+        }
+        for (int s = 0; s < NSLOT; ++s) {
+            mbar_init(bar(bars, B_KVFULL + s), 1);
+            mbar_init(bar(bars, B_KVEMPTY + s), 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 8) {
+        // ============================ loader ============================
+        int fills[NSLOT];
+#pragma unroll
+        for (int s = 0; s < NSLOT; ++s) fills[s] = 0;
+        int nq[2] = {0, 0};
+        int64_t prev_stream = -1, prev_u = -1, prev_hi = -1;
+        for (int64_t it = it_begin; it < it_end; ++it) {
+            const Pair P = pair_geo(tp, it);
+            if (!P.any) continue;
+            // Q tiles
+            for (int w = 0; w < 2; ++w) {
+                if (!P.valid[w]) continue;
+                const int b = nq[w] & 1;
+                if (nq[w] >= 2) mbar_wait(bar(bars, B_QEMPTY + 2 * w + b), ((nq[w] >> 1) - 1) & 1);
+                ++nq[w];
+                if (lane == 0) {
+                    const uint32_t fb = bar(bars, B_QFULL + 2 * w + b);
+                    tma::expect_tx(fb, QBYTES);
+                    const uint32_t dst = sbase + OFF_Q + (uint32_t)(2 * w + b) * QBYTES;
+                    const int tok = (int)(P.c + P.a0[w] * r - p.q_begin);
+                    tma::load_3d(dst, &tp.tmQ, 0, P.h, tok, fb);
+                    tma::load_3d(dst + QBYTES / 2, &tp.tmQ, 0, P.h, tok + 64 * (int)r, fb);
+                }
+            }
+            // K/V chunks not resident from the previous pair
+            const bool cont = P.stream == prev_stream && P.u == prev_u + 1;
+            for (int64_t g = P.lo; g <= P.hi; ++g) {
+                if (cont && g <= prev_hi) continue;
+                const int s = (int)(g & (NSLOT - 1));
+                if (fills[s] >= 1) mbar_wait(bar(bars, B_KVEMPTY + s), (fills[s] - 1) & 1);
+                ++fills[s];
+                const uint32_t fb = bar(bars, B_KVFULL + s);
+                const uint32_t dK = sbase + OFF_KV + (uint32_t)s * 2 * CBYTES, dV = dK + CBYTES;
+                const int64_t tok0 = P.c + g * KC * r;                       // first row's token
+                const int64_t tokL = P.c + imin(g * KC + KC - 1, P.Nc - 1) * r; // last in-range row
+                const bool local = p.k_peer == nullptr || (tok0 >= p.kv_begin && tokL < p.kv_begin + p.kv_rows);
+                if (local) {
+                    if (lane == 0) {
+                        tma::expect_tx(fb, 2 * CBYTES);
+                        tma::load_3d(dK, &tp.tmK, 0, P.h, (int)(tok0 - p.kv_begin), fb);
+                        tma::load_3d(dV, &tp.tmV, 0, P.h, (int)(tok0 - p.kv_begin), fb);
+                    }
+                } else {
+                    // rows owned by other ranks: 16-byte cp.async from the owner's buffer
+                    const size_t hoff = (size_t)P.h * D * sizeof(T);
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        const int row = lane + 32 * half;
+                        const int64_t kr = g * KC + row;
+                        if (kr < P.Nc) {
+                            const char *kp, *vp;
+                            kv_row(p, P.c + kr * r, row_bytes, kp, vp);
+#pragma unroll
+                            for (int cc = 0; cc < RB / 16; ++cc) {
+                                cp_async16(dK + swz<D>(row, cc), kp + hoff + cc * 16);
+                                cp_async16(dV + swz<D>(row, cc), vp + hoff + cc * 16);
+                            }
+                        } else {
+#pragma unroll
+                            for (int cc = 0; cc < RB / 16; ++cc) {
+                                sts_zero16(dK + swz<D>(row, cc));
+                                sts_zero16(dV + swz<D>(row, cc));
+                            }
+                        }
+                    }
+                    cp_async_wait<0>();
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(fb);
+                }
+                __syncwarp();
+            }
+            prev_stream = P.stream;
+            prev_u = P.u;
+            prev_hi = P.hi;
+        }
+    } else if (warp == 9) {
+        // ============================ MMA issuer ============================
+        const uint32_t idS = idesc<T>(ROWS, KC, false), idO = idesc<T>(ROWS, D, true);
+        int seen[NSLOT];
+#pragma unroll
+        for (int s = 0; s < NSLOT; ++s) seen[s] = 0;
+        int nq[2] = {0, 0};
+        int64_t cw[2] = {0, 0}; // running chunk counters per warpgroup (S/P/O buffer parity)
+        int64_t prev_stream = -1, prev_u = -1, prev_hi = -1;
+        for (int64_t it = it_begin; it < it_end; ++it) {
+            const Pair P = pair_geo(tp, it);
+            if (!P.any) continue;
+            const bool cont = P.stream == prev_stream && P.u == prev_u + 1;
+            // chunks kept for the next item: g >= keep_from
+            int64_t keep_from = INT64_MAX;
+            if (it + 1 < it_end) {
+                const Pair N = pair_geo(tp, it + 1);
+                if (N.any && N.stream == P.stream && N.u == P.u + 1) keep_from = N.lo;
+            }
+            uint32_t waited = 0; // chunks of this item whose fill we waited for
+            int qb[2];
+            for (int w = 0; w < 2; ++w) {
+                qb[w] = nq[w] & 1;
+                if (P.valid[w]) {
+                    mbar_wait(bar(bars, B_QFULL + 2 * w + qb[w]), (nq[w] >> 1) & 1);
+                    ++nq[w];
+                }
+            }
+            auto ensure = [&](int64_t g) {
+                if (cont && g <= prev_hi) return;
+                const uint32_t bit = 1u << (int)(g - P.lo);
+                if (waited & bit) return;
+                waited |= bit;
+                const int s = (int)(g & (NSLOT - 1));
+                mbar_wait(bar(bars, B_KVFULL + s), seen[s] & 1);
+                ++seen[s];
+            };
+            auto issue_S = [&](int w, int64_t j) {
+                const int64_t g = P.F[w] + j, c = cw[w] + j;
+                ensure(g);
+                if (lane == 0) {
+                    fence_after();
+                    const uint32_t bq = sbase + OFF_Q + (uint32_t)(2 * w + qb[w]) * QBYTES;
+                    const uint32_t bk = sbase + OFF_KV + (uint32_t)(g & (NSLOT - 1)) * 2 * CBYTES;
+                    const uint32_t dS = tmem + 256u * w + COL_S + (uint32_t)(c & 1) * KC;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        mma_ss(dS, sdesc_sw128(bq + kk * 32), sdesc_sw128(bk + kk * 32), idS, kk > 0);
+                    mma_commit(bar(bars, B_SFULL + 2 * w + (int)(c & 1)));
+                    if (j == P.n[w] - 1) mma_commit(bar(bars, B_QEMPTY + 2 * w + qb[w])); // Q tile read
+                }
+                __syncwarp();
+            };
+            auto issue_PV = [&](int w, int64_t j) {
+                const int64_t g = P.F[w] + j, c = cw[w] + j;
+                mbar_wait(bar(bars, B_PFULL + 2 * w + (int)(c & 1)), (uint32_t)((c >> 1) & 1));
+                if (lane == 0) {
+                    fence_after();
+                    const uint32_t bv = sbase + OFF_KV + (uint32_t)(g & (NSLOT - 1)) * 2 * CBYTES + CBYTES;
+                    const uint32_t tP = tmem + 256u * w + COL_P + (uint32_t)(c & 1) * (KC / 2);
+#pragma unroll
+                    for (int kk = 0; kk < KC / 16; ++kk) // 16 keys per MMA: 8 P columns, 16 V rows
+                        mma_ts(tmem + 256u * w + COL_O, tP + kk * 8, sdesc_sw128(bv + kk * 16 * RB), idO,
+                               (j > 0 || kk > 0));
+                    mma_commit(bar(bars, B_OFULL + 2 * w + (int)(c & 1)));
+                    // last reader of chunk g in this item: the P V of tile A on chunk g runs at
+                    // step g - F_A + 1, tile B's at step g - F_B + 1 (after A's within a step)
+                    const bool inA = g >= P.F[0] && g < P.F[0] + P.n[0];
+                    const bool inB = g >= P.F[1] && g < P.F[1] + P.n[1];
+                    const bool last = w == 0 ? (!inB || P.F[1] > P.F[0]) : (!inA || P.F[1] <= P.F[0]);
+                    if (last && g < keep_from) mma_commit(bar(bars, B_KVEMPTY + (int)(g & (NSLOT - 1))));
+                }
+                __syncwarp();
+            };
+            const int64_t jmax = imax(P.n[0], P.n[1]);
+            // step j: S of chunk j, then P V of chunk j - 1 (whose P the softmax is finishing)
+            for (int64_t j = 0; j <= jmax; ++j) {
+                for (int w = 0; w < 2; ++w)
+                    if (j < P.n[w]) issue_S(w, j);
+                if (j >= 1)
+                    for (int w = 0; w < 2; ++w)
+                        if (j - 1 < P.n[w]) issue_PV(w, j - 1);
+            }
+            cw[0] += P.n[0];
+            cw[1] += P.n[1];
+            prev_stream = P.stream;
+            prev_u = P.u;
+            prev_hi = P.hi;
+        }
+    } else {
+        // ============================ softmax warpgroups ============================
+        const int w = warp >> 2, q = warp & 3;
+        const uint32_t tl = tmem + 256u * w + ((uint32_t)(q * 32) << 16); // this warp's TMEM lanes
+        const float sl2 = p.scale_log2;
+        constexpr float kTau = 8.f;
+        int64_t cnt = 0; // running chunk counter (matches the MMA issuer's cw[w])
+        auto wait_O = [&](int64_t c) {
+            mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(c & 1)), (uint32_t)((c >> 1) & 1));
+            fence_after();
+        };
+        char *Og = reinterpret_cast<char *>(p.out);
+        for (int64_t it = it_begin; it < it_end; ++it) {
+            const Pair P = pair_geo(tp, it);
+            if (!P.valid[w]) continue;
+            const int64_t a0 = P.a0[w], xr0 = a0 + 32 * q, x = xr0 + lane;
+            // keys of this warp's rows: union [ulo, uhi], every row: [ilo, ihi]; this row: [klo, khi]
+            const int64_t ulo = imax(xr0 - m, 0), uhi = imin(xr0 + 31 + m, P.Nc - 1);
+            const int64_t ilo = imax(xr0 + 31 - m, 0), ihi = imin(xr0 + m, P.Nc - 1);
+            const int64_t klo = imax(x - m, 0), khi = imin(x + m, P.Nc - 1);
+            float m_run = -INFINITY, l_run = 0.f;
+            const int64_t n = P.n[w];
+            for (int64_t j = 0; j < n; ++j) {
+                const int64_t c = cnt + j, kmin = (P.F[w] + j) * KC;
+                const uint32_t tP = tl + COL_P + (uint32_t)(c & 1) * (KC / 2);
+                // S_c is waited for even when skipped: every phase of the S barriers is then
+                // observed in order (a parity wait cannot tell phase k from phase k + 2)
+                mbar_wait(bar(bars, B_SFULL + 2 * w + (int)(c & 1)), (uint32_t)((c >> 1) & 1));
+                fence_after();
+                if (kmin > uhi || kmin + KC - 1 < ulo) { // no row of this warp reaches the chunk
+                    if (c >= 2) wait_O(c - 2);
+                    uint32_t z[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) z[i] = 0u;
+                    tmem_st32(tP, z);
+                    tmem_wait_st();
+                    fence_before();
+                    mbar_arrive(bar(bars, B_PFULL + 2 * w + (int)(c & 1)));
+                    continue;
+                }
+                float sv[KC];
+                tmem_ld32(tl + COL_S + (uint32_t)(c & 1) * KC, sv);
+                tmem_ld32(tl + COL_S + (uint32_t)(c & 1) * KC + 32, sv + 32);
+                tmem_wait_ld();
+                if (!(kmin >= ilo && kmin + KC - 1 <= ihi)) { // partial: keep only this row's band
+                    const int il = (int)imax(klo - kmin, -1), ih = (int)imin(khi - kmin, KC);
+#pragma unroll
+                    for (int i = 0; i < KC; ++i) sv[i] = (i >= il && i <= ih) ? sv[i] : -INFINITY;
+                }
+                float lmx[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) lmx[i] = sv[i];
+#pragma unroll
+                for (int i = 8; i < KC; ++i) lmx[i & 7] = fmaxf(lmx[i & 7], sv[i]);
+                const float lm = fmaxf(fmaxf(fmaxf(lmx[0], lmx[1]), fmaxf(lmx[2], lmx[3])),
+                                       fmaxf(fmaxf(lmx[4], lmx[5]), fmaxf(lmx[6], lmx[7])));
+                const float lm2 = lm * sl2;
+                const bool need = lm2 > m_run + kTau;
+                if (__any_sync(0xffffffffu, need)) {
+                    if (j > 0) wait_O(c - 1); // O stable: P V of the previous chunk completed
+                    const float mn = fmaxf(m_run, lm2);
+                    const float a = m_run == -INFINITY ? 0.f : ex2(m_run - mn);
+                    if (__any_sync(0xffffffffu, j > 0 && a != 1.f)) {
+                        float ov[32];
+#pragma unroll
+                        for (int qq = 0; qq < D / 32; ++qq) {
+                            tmem_ld32(tl + COL_O + 32 * qq, ov);
+                            tmem_wait_ld();
+                            uint32_t ob[32];
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(ov[i] * a);
+                            tmem_st32(tl + COL_O + 32 * qq, ob);
+                        }
+                        tmem_wait_st();
+                    }
+                    l_run *= a;
+                    m_run = mn;
+                }
+                const float m_use = m_run == -INFINITY ? 0.f : m_run;
+                if (c >= 2) wait_O(c - 2); // P buffer last read by P V two chunks ago
+                uint32_t pk[KC / 2];
+                float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int i = 0; i < KC / 2; ++i) {
+                    float x0 = sv[2 * i], x1 = sv[2 * i + 1];
+                    ffma2_sm(x0, x1, sl2, -m_use);
+                    x0 = ex2(x0);
+                    x1 = ex2(x1);
+                    ls[i & 3] += x0 + x1;
+                    pk[i] = pack2<T>(x0, x1);
+                }
+                l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+                tmem_st32(tP, pk);
+                tmem_wait_st();
+                fence_before();
+                mbar_arrive(bar(bars, B_PFULL + 2 * w + (int)(c & 1)));
+            }
+            cnt += n;
+            // ---- epilogue: O row from TMEM, normalise, store
+            wait_O(cnt - 1);
+            float o[D];
+            tmem_ld32(tl + COL_O, o);
+            tmem_ld32(tl + COL_O + 32, o + 32);
+            tmem_wait_ld();
+            if (x >= P.a_lo && x < P.a_hi) {
+                const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+                const int64_t i = P.c + x * r;
+                char *orow = Og + (size_t)(i - p.q_begin) * row_bytes + (size_t)P.h * D * sizeof(T);
+#pragma unroll
+                for (int qq = 0; qq < D / 8; ++qq) {
+                    float r8[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) r8[e] = o[8 * qq + e] * inv;
+                    stg16(orow + qq * 16, pack<T>(r8));
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+static int sm_count()
+{
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
+// chunks spanned by a pair of tiles (the ring holds NSLOT)
+static int64_t pair_span(int64_t m) { return floordiv(2 * ROWS - 1 + m, KC) - floordiv(-m, KC) + 1; }
+
+template <typename T> static ga_status launch_t(const TcParams &tp, int64_t grid, cudaStream_t s)
+{
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(window_tc_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        if (e != cudaSuccess) return cuda_fail(e, "window_tc_kernel: set smem");
+        configured = true;
+    }
+    window_tc_kernel<T><<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(tp);
+    GA_CHECK_LAUNCH("window_tc_kernel");
+    return GA_OK;
+}
+
+} // namespace wtc
+
+int64_t window_tc_tile_rows() { return wtc::ROWS; }
+
+bool window_tc_supported(const AttnParams &p, ga_dtype dt)
+{
+    if (p.mask.kind != K_WINDOW || (dt != GA_BF16 && dt != GA_F16) || p.d != 64) return false;
+    const int64_t m = p.mask.m, r = p.mask.r;
+    if (m < 64 || m > 128 || r > 4 || wtc::pair_span(m) > wtc::NSLOT) return false;
+    if (p.mask.L >= ((int64_t)1 << 31) || p.q_rows <= 0) return false; // TMA coordinates are int32
+    // without peer memory the local K/V must hold every key the query range reaches
+    if (p.k_peer == nullptr && !(p.kv_begin == 0 && p.kv_rows == p.mask.L)) {
+        const int64_t reach = m * r; // farthest key token a query row reaches
+        if (p.kv_begin > imax(0, p.q_begin - reach) || p.kv_begin + p.kv_rows < imin(p.mask.L, p.q_begin + p.q_rows + reach))
+            return false;
+    }
+    return true;
+}
+
+ga_status launch_window_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s)
+{
+    wtc::TcParams tp;
+    tp.p = p;
+    tp.m = p.mask.m;
+    tp.r = p.mask.r;
+    const int64_t L = p.mask.L, r = tp.r, q_end = p.q_begin + p.q_rows;
+    int64_t pps = 0;
+    for (int64_t c = 0; c < r && c < L; ++c) {
+        const int64_t Nc = (L - c + r - 1) / r;
+        const int64_t a_lo = p.q_begin > c ? (p.q_begin - c + r - 1) / r : 0;
+        const int64_t a_hi = q_end > c ? imin((q_end - c + r - 1) / r, Nc) : 0;
+        if (a_hi <= a_lo) continue;
+        const int64_t tiles = (a_hi + wtc::ROWS - 1) / wtc::ROWS - a_lo / wtc::ROWS;
+        pps = imax(pps, (tiles + 1) / 2);
+    }
+    tp.pps = pps;
+    tp.items = pps * r * p.H;
+    if (tp.items == 0) return GA_OK;
+    if (!tma::encode_rows(&tp.tmQ, p.Q, p.q_rows, p.H, p.d, (int)r, 64) ||
+        !tma::encode_rows(&tp.tmK, p.K, p.kv_rows, p.H, p.d, (int)r, 64) ||
+        !tma::encode_rows(&tp.tmV, p.V, p.kv_rows, p.H, p.d, (int)r, 64)) {
+        set_error("tcgen05 window kernel: tensor-map encoding failed");
+        return GA_ERR_UNSUPPORTED;
+    }
+    const int64_t grid = imin(wtc::sm_count(), tp.items);
+    return dt == GA_BF16 ? wtc::launch_t<__nv_bfloat16>(tp, grid, s) : wtc::launch_t<__half>(tp, grid, s);
 }
 
 } // namespace ga

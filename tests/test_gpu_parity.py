@@ -128,12 +128,54 @@ def test_band_kernel_vs_oracle(ga, orc, w, r, dt, d):
     assert np.abs(got - want).max() <= TOL[dt]
 
 
+@pytest.mark.parametrize("L,w,r", [(3000, 65, 1), (3000, 128, 1), (3000, 129, 1), (3000, 256, 2), (3001, 200, 2),
+                                   (3000, 300, 3), (2999, 400, 4), (5000, 512, 4), (100, 128, 1), (1, 128, 1),
+                                   (700, 256, 2), (20000, 256, 2)])
+@pytest.mark.parametrize("dt", ["bf16", "f16"])
+def test_window_tc_vs_oracle(ga, orc, L, w, r, dt):
+    """tcgen05 window kernel (forced) against the oracle: m = floor((w-1)/r) from 64 to 128,
+    dilation 1-4, ragged L (partial tiles, partial chunks, sequences shorter than one tile),
+    tile pairs with one tile, several pairs per CTA run (L=20000)."""
+    H, d = 2, 64
+    cpu, f64 = _inputs(L, H, d, dt, w * 11 + r + L, centred=True)
+    want, _ = orc.attention(*f64, orc.window(L, w, r))
+    got = _run(ga, cpu, ga.Window(w, r), kernel="tc")
+    assert np.abs(got - want).max() <= TOL[dt]
+    # uncentred U[0,1) inputs (the paper's distribution, P:302): flat softmax, all weights alive
+    cpu2, f642 = _inputs(L, H, d, dt, w * 13 + r + L)
+    want2, _ = orc.attention(*f642, orc.window(L, w, r))
+    got2 = _run(ga, cpu2, ga.Window(w, r), kernel="tc")
+    assert np.abs(got2 - want2).max() <= TOL[dt]
+
+
+def test_window_tc_scaled_queries(ga, orc):
+    """Sharp softmax (queries x 8): the lazy rescale fires often; tcgen05 kernel vs oracle."""
+    L, H, d = 4096, 2, 64
+    q, k, v = synth.qkv(77, L, H, d, "bf16", centred=True)
+    q = (q.float() * 8).bfloat16()
+    f64 = tuple(synth.as_f64(x) for x in (q, k, v))
+    want, _ = orc.attention(*f64, orc.window(L, 256, 2))
+    got = _run(ga, (q, k, v), ga.Window(256, 2), kernel="tc")
+    assert np.abs(got - want).max() <= 2e-2
+
+
+def test_window_tc_unsupported(ga):
+    """The tcgen05 window kernel refuses what it does not implement (d != 64, fp32, m outside
+    [64, 128], r > 4) instead of computing something else."""
+    for shape, dt, mask in (((300, 1, 32), torch.bfloat16, ga.Window(128)), ((300, 1, 64), torch.float32, ga.Window(128)),
+                            ((300, 1, 64), torch.bfloat16, ga.Window(300)), ((300, 1, 64), torch.bfloat16, ga.Window(40)),
+                            ((3000, 1, 64), torch.bfloat16, ga.Window(600, 5))):
+        x = torch.zeros(shape, dtype=dt, device="cuda")
+        with pytest.raises(ga.GaError, match="UNSUPPORTED"):
+            ga.attention(x, x.clone(), x.clone(), mask, kernel="tc")
+
+
 def test_band_kernel_cfg2_shape(ga, orc):
     """cfg2 geometry (8 heads, Window(256, r=2), bf16) at L=8192: every row vs the oracle."""
     L, H, d = 8192, 8, 64
     cpu, f64 = _inputs(L, H, d, "bf16", 0x5EED0002)
     want, _ = orc.attention(*f64, orc.window(L, 256, 2))
-    for kernel in ("window", "edge"):
+    for kernel in ("window", "tc", "edge"):
         got = _run(ga, cpu, ga.Window(256, 2), kernel=kernel)
         assert np.abs(got - want).max() <= 2e-2, kernel
     with pytest.raises(ga.GaError, match="UNSUPPORTED"):
@@ -308,10 +350,12 @@ def test_sharded_offsets_bitwise(ga):
     q, k, v = ga.qkv_device(9, L, H, d, torch.bfloat16)
     m = ga.Window(256, 2)
     halo = 127 * 2
-    for kernel in ("edge", "auto"):
+    for kernel in ("edge", "window", "tc", "auto"):
         full = ga.attention(q, k, v, m, kernel=kernel)
-        # shard boundaries aligned to the band kernel's tile (112 class rows x r tokens)
-        for r0, r1 in ((0, 2240), (2240, 4480), (4480, 8192)):
+        # shard boundaries aligned to the kernel's tile (band kernel: 112 class rows x r tokens,
+        # tcgen05 kernel: 128 x r; auto: ga.query_alignment)
+        al = {"edge": 1, "window": 224, "tc": 256, "auto": ga.query_alignment(m, L, d, torch.bfloat16)}[kernel]
+        for r0, r1 in ((0, 10 * al), (10 * al, 20 * al), (20 * al, 8192)):
             k0, k1 = max(0, r0 - halo), min(L, r1 + halo)
             part = ga.attention(q[r0:r1].contiguous(), k[k0:k1].contiguous(), v[k0:k1].contiguous(), m, L=L,
                                 q_begin=r0, kv_begin=k0, kernel=kernel)
