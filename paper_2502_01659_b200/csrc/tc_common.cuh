@@ -93,6 +93,16 @@ __device__ __forceinline__ void ffma2_sm(float &x0, float &x1, float s, float ne
     asm("mov.b64 {%0, %1}, %2;" : "=f"(x0), "=f"(x1) : "l"(d));
 }
 
+// acc += (x0, x1) in one packed fp32 add (sm_100 add.f32x2)
+__device__ __forceinline__ void fadd2_acc(float2 &acc, float x0, float x1)
+{
+    unsigned long long a, b, d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(acc.x), "f"(acc.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(x0), "f"(x1));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(d));
+}
+
 // Running flash-attention state of one warp's 16 rows in the m16n8 accumulator layout:
 // lane (g = lane/4, t4 = lane%4) owns rows g and g+8 and dims 8j + 2*t4 + {0,1}.
 template <typename T, int D> struct MmaRows {

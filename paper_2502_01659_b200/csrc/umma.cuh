@@ -87,6 +87,27 @@ __device__ __forceinline__ bool mbar_try(uint32_t mbar, uint32_t phase)
     return ok != 0;
 }
 
+// one lane of the (converged) warp returns true
+__device__ __forceinline__ bool elect_one()
+{
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}\n" : "=r"(pred));
+    return pred != 0;
+}
+
+// non-blocking probe: has the phase with this parity completed?
+__device__ __forceinline__ bool mbar_test(uint32_t mbar, uint32_t phase)
+{
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred P1;\n\t"
+                 "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, P1;\n\t}\n"
+                 : "=r"(ok)
+                 : "r"(mbar), "r"(phase)
+                 : "memory");
+    return ok != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase)
 {
 #if GA_MBAR_SPIN_LIMIT > 0

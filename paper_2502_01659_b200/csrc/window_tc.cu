@@ -42,7 +42,7 @@ namespace wtc {
 using namespace tc;
 using namespace umma;
 
-constexpr int ROWS = 128, KC = 64, NSLOT = 8, D = 64, RB = 2 * D;
+constexpr int ROWS = 128, KC = 64, NSLOT = 10, D = 64, RB = 2 * D;
 constexpr int THREADS = 320; // 8 softmax warps + loader + MMA
 constexpr uint32_t QBYTES = ROWS * RB;   // 16 KB
 constexpr uint32_t CBYTES = KC * RB;     // 8 KB: one K or V chunk
@@ -52,8 +52,9 @@ constexpr uint32_t OFF_BAR = OFF_KV + NSLOT * 2 * CBYTES;
 constexpr uint32_t SMEM_BYTES = 1024 + OFF_BAR + 64 * 8;
 
 // mbarrier indices (8 bytes each from OFF_BAR)
-constexpr int B_QFULL = 0, B_QEMPTY = 4, B_KVFULL = 8, B_KVEMPTY = 16, B_SFULL = 24, B_PFULL = 28, B_OFULL = 32;
-constexpr int B_TMEM = 40; // tcgen05.alloc writes the TMEM base here
+constexpr int B_QFULL = 0, B_QEMPTY = 4, B_KVFULL = 8, B_KVEMPTY = 8 + NSLOT, B_SFULL = 8 + 2 * NSLOT,
+              B_PFULL = B_SFULL + 4, B_OFULL = B_PFULL + 4;
+constexpr int B_TMEM = B_OFULL + 4; // tcgen05.alloc writes the TMEM base here
 
 // TMEM columns of warpgroup w: S[2] at 256w + {0, 64}, P[2] at 256w + 128 + {0, 32}, O at 256w + 192
 constexpr uint32_t COL_S = 0, COL_P = 128, COL_O = 192;
@@ -82,27 +83,36 @@ struct Pair {
 
 __device__ __forceinline__ Pair pair_geo(const TcParams &tp, int64_t it)
 {
+    // 32-bit arithmetic throughout: L < 2^31 (window_tc_supported), so class rows, tiles and
+    // item indices fit; 64-bit division would cost hundreds of instructions per item
     const AttnParams &p = tp.p;
-    const int64_t r = tp.r, m = tp.m, L = p.mask.L;
+    const uint32_t r = (uint32_t)tp.r, L = (uint32_t)p.mask.L, H = (uint32_t)p.H, pps = (uint32_t)tp.pps;
+    const int32_t m = (int32_t)tp.m;
     Pair P;
-    P.stream = it / tp.pps;
-    P.u = it - P.stream * tp.pps;
-    P.c = P.stream / p.H;
-    P.h = (int)(P.stream - P.c * p.H);
-    const int64_t c = P.c;
-    P.Nc = c < L ? (L - c + r - 1) / r : 0;
-    const int64_t q_end = p.q_begin + p.q_rows;
-    P.a_lo = p.q_begin > c ? (p.q_begin - c + r - 1) / r : 0;
-    P.a_hi = q_end > c ? imin((q_end - c + r - 1) / r, P.Nc) : 0;
-    const int64_t t0 = P.a_lo / ROWS + 2 * P.u;
-    const int64_t lastc = (P.Nc - 1) / KC;
+    const uint32_t iu = (uint32_t)it, st = iu / pps;
+    P.stream = st;
+    P.u = iu - st * pps;
+    const uint32_t c = st / H;
+    P.c = c;
+    P.h = (int)(st - c * H);
+    const uint32_t Nc = c < L ? (L - c + r - 1) / r : 0;
+    P.Nc = Nc;
+    const uint32_t qb = (uint32_t)p.q_begin, qe = (uint32_t)(p.q_begin + p.q_rows);
+    const uint32_t a_lo = qb > c ? (qb - c + r - 1) / r : 0;
+    const uint32_t a_hi = qe > c ? min((qe - c + r - 1) / r, Nc) : 0;
+    P.a_lo = a_lo;
+    P.a_hi = a_hi;
+    const int32_t t0 = (int32_t)(a_lo / ROWS + 2 * (uint32_t)P.u);
+    const int32_t lastc = ((int32_t)Nc - 1) >> 6; // KC = 64
     P.lo = INT64_MAX;
     P.hi = -1;
+#pragma unroll
     for (int w = 0; w < 2; ++w) {
-        const int64_t a0 = (t0 + w) * ROWS;
+        const int32_t a0 = (t0 + w) * ROWS;
         P.a0[w] = a0;
-        P.valid[w] = P.a_lo < P.a_hi && a0 < P.a_hi;
-        const int64_t f = imax(floordiv(a0 - m, KC), 0), e = imin(floordiv(a0 + ROWS - 1 + m, KC), lastc);
+        P.valid[w] = a_lo < a_hi && (uint32_t)a0 < a_hi;
+        // floor((a0 - m) / 64) by arithmetic shift (exact for negative values too)
+        const int32_t f = max((a0 - m) >> 6, 0), e = min((a0 + ROWS - 1 + m) >> 6, lastc);
         P.F[w] = f;
         P.n[w] = P.valid[w] ? e - f + 1 : 0;
         if (P.valid[w]) {
@@ -115,6 +125,22 @@ __device__ __forceinline__ Pair pair_geo(const TcParams &tp, int64_t it)
 }
 
 __device__ __forceinline__ uint32_t bar(uint32_t base, int i) { return base + 8u * (uint32_t)i; }
+
+#ifdef GA_WTC_TRACE
+// debug timeline of CTA 0: (event << 48 | warp << 40 | (clock - t0)) per event
+constexpr int TRACE_N = 16384;
+__device__ unsigned long long g_trace[TRACE_N];
+__device__ unsigned int g_trace_n;
+// per-warp private slots (no atomics: a trace point costs one store)
+#define TRACE2(ev, val) do { if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && t_cnt < TRACE_N / 16) { \
+    g_trace[(threadIdx.x >> 5) * (TRACE_N / 16) + t_cnt++] = ((unsigned long long)((val) & 0xff) << 56) | \
+        ((unsigned long long)(ev) << 48) | ((unsigned long long)(threadIdx.x >> 5) << 40) | \
+        (unsigned long long)((clock64() - t_origin) & 0xffffffffffull); } } while (0)
+#define TRACE(ev) TRACE2(ev, 0)
+#else
+#define TRACE(ev)
+#define TRACE2(ev, val)
+#endif
 
 template <typename T>
 __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_constant__ TcParams tp)
@@ -157,6 +183,10 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_slot;
+#ifdef GA_WTC_TRACE
+    const long long t_origin = clock64();
+    int t_cnt = 0;
+#endif
 
     if (warp == 8) {
         // ============================ loader ============================
@@ -174,7 +204,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 const int b = nq[w] & 1;
                 if (nq[w] >= 2) mbar_wait(bar(bars, B_QEMPTY + 2 * w + b), ((nq[w] >> 1) - 1) & 1);
                 ++nq[w];
-                if (lane == 0) {
+                if (elect_one()) {
                     const uint32_t fb = bar(bars, B_QFULL + 2 * w + b);
                     tma::expect_tx(fb, QBYTES);
                     const uint32_t dst = sbase + OFF_Q + (uint32_t)(2 * w + b) * QBYTES;
@@ -187,8 +217,10 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             const bool cont = P.stream == prev_stream && P.u == prev_u + 1;
             for (int64_t g = P.lo; g <= P.hi; ++g) {
                 if (cont && g <= prev_hi) continue;
-                const int s = (int)(g & (NSLOT - 1));
+                const int s = (int)(g % NSLOT);
+                TRACE2(19, g);
                 if (fills[s] >= 1) mbar_wait(bar(bars, B_KVEMPTY + s), (fills[s] - 1) & 1);
+                TRACE2(20, g);
                 ++fills[s];
                 const uint32_t fb = bar(bars, B_KVFULL + s);
                 const uint32_t dK = sbase + OFF_KV + (uint32_t)s * 2 * CBYTES, dV = dK + CBYTES;
@@ -196,7 +228,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 const int64_t tokL = P.c + imin(g * KC + KC - 1, P.Nc - 1) * r; // last in-range row
                 const bool local = p.k_peer == nullptr || (tok0 >= p.kv_begin && tokL < p.kv_begin + p.kv_rows);
                 if (local) {
-                    if (lane == 0) {
+                    if (elect_one()) {
                         tma::expect_tx(fb, 2 * CBYTES);
                         tma::load_3d(dK, &tp.tmK, 0, P.h, (int)(tok0 - p.kv_begin), fb);
                         tma::load_3d(dV, &tp.tmV, 0, P.h, (int)(tok0 - p.kv_begin), fb);
@@ -237,89 +269,136 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         }
     } else if (warp == 9) {
         // ============================ MMA issuer ============================
+        // Warp-uniform control flow (the whole warp runs the schedule and the blocking waits;
+        // one elected lane issues), so descriptors and counters live in uniform registers.
+        // Per warpgroup w the schedule keeps S one chunk ahead of the softmax:
+        //     S_w(0), S_w(1); for j: [P_w(j)] P V_w(j), S_w(j+2)
+        // S_w(j+2) reuses S buffer j&1, which the softmax finished reading before P_w(j).  The
+        // two warpgroups interleave chunk by chunk; when one finishes its tile it starts the
+        // S MMAs of its next tile (chunks resident) while it runs its epilogue.
         const uint32_t idS = idesc<T>(ROWS, KC, false), idO = idesc<T>(ROWS, D, true);
+        // smem descriptors: constant high part | (address >> 4); the operand tiles stay below
+        // 256 KB so the 14-bit start field never carries
+        const uint64_t dbase = sdesc_sw128(0);
         int seen[NSLOT];
 #pragma unroll
         for (int s = 0; s < NSLOT; ++s) seen[s] = 0;
-        int nq[2] = {0, 0};
+        int nq[2] = {0, 0};     // Q tiles waited per warpgroup
         int64_t cw[2] = {0, 0}; // running chunk counters per warpgroup (S/P/O buffer parity)
+        int pre[2] = {0, 0};    // S MMAs of this item's tile already issued (end of the previous item)
+        bool preq[2] = {false, false};
         int64_t prev_stream = -1, prev_u = -1, prev_hi = -1;
+        Pair N = pair_geo(tp, it_begin);
         for (int64_t it = it_begin; it < it_end; ++it) {
-            const Pair P = pair_geo(tp, it);
+            const Pair P = N;
+            const bool has_next = it + 1 < it_end;
+            if (has_next) N = pair_geo(tp, it + 1);
             if (!P.any) continue;
             const bool cont = P.stream == prev_stream && P.u == prev_u + 1;
-            // chunks kept for the next item: g >= keep_from
-            int64_t keep_from = INT64_MAX;
-            if (it + 1 < it_end) {
-                const Pair N = pair_geo(tp, it + 1);
-                if (N.any && N.stream == P.stream && N.u == P.u + 1) keep_from = N.lo;
-            }
-            uint32_t waited = 0; // chunks of this item whose fill we waited for
-            int qb[2];
+            const bool next_cont = has_next && N.any && N.stream == P.stream && N.u == P.u + 1;
+            const int64_t keep_from = next_cont ? N.lo : INT64_MAX;
+            uint32_t readers = 0, ready = 0; // 4 bits per chunk g - lo; 1 bit per chunk
+            for (int w = 0; w < 2; ++w)
+                for (int64_t j = 0; j < P.n[w]; ++j) readers += 1u << (4 * (int)(P.F[w] + j - P.lo));
+            if (cont)
+                for (int64_t g = P.lo; g <= P.hi && g <= prev_hi; ++g) ready |= 1u << (int)(g - P.lo);
+            int qb[2] = {0, 0};
             for (int w = 0; w < 2; ++w) {
-                qb[w] = nq[w] & 1;
-                if (P.valid[w]) {
+                if (!P.valid[w]) continue;
+                if (preq[w]) {
+                    qb[w] = (nq[w] - 1) & 1;
+                } else {
+                    qb[w] = nq[w] & 1;
                     mbar_wait(bar(bars, B_QFULL + 2 * w + qb[w]), (nq[w] >> 1) & 1);
                     ++nq[w];
                 }
             }
-            auto ensure = [&](int64_t g) {
-                if (cont && g <= prev_hi) return;
-                const uint32_t bit = 1u << (int)(g - P.lo);
-                if (waited & bit) return;
-                waited |= bit;
-                const int s = (int)(g & (NSLOT - 1));
-                mbar_wait(bar(bars, B_KVFULL + s), seen[s] & 1);
-                ++seen[s];
+            fence_after();
+            auto chunk_ready = [&](int64_t g) {
+                const int gi = (int)(g - P.lo);
+                if ((ready >> gi) & 1u) return;
+                const int sl = (int)(g % NSLOT);
+                mbar_wait(bar(bars, B_KVFULL + sl), seen[sl] & 1);
+                ++seen[sl];
+                ready |= 1u << gi;
+                TRACE2(1, g);
+                fence_after();
             };
-            auto issue_S = [&](int w, int64_t j) {
-                const int64_t g = P.F[w] + j, c = cw[w] + j;
-                ensure(g);
-                if (lane == 0) {
-                    fence_after();
-                    const uint32_t bq = sbase + OFF_Q + (uint32_t)(2 * w + qb[w]) * QBYTES;
-                    const uint32_t bk = sbase + OFF_KV + (uint32_t)(g & (NSLOT - 1)) * 2 * CBYTES;
-                    const uint32_t dS = tmem + 256u * w + COL_S + (uint32_t)(c & 1) * KC;
+            auto issue_S = [&](int w, int64_t c, int64_t g, int qbuf, bool last) {
+                const uint32_t aq = sbase + OFF_Q + (uint32_t)(2 * w + qbuf) * QBYTES;
+                const uint32_t ak = sbase + OFF_KV + (uint32_t)(g % NSLOT) * 2 * CBYTES;
+                const uint32_t dS = tmem + 256u * w + COL_S + (uint32_t)(c & 1) * KC;
+                if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk)
-                        mma_ss(dS, sdesc_sw128(bq + kk * 32), sdesc_sw128(bk + kk * 32), idS, kk > 0);
+                        mma_ss(dS, dbase | ((aq + kk * 32) >> 4), dbase | ((ak + kk * 32) >> 4), idS, kk > 0);
                     mma_commit(bar(bars, B_SFULL + 2 * w + (int)(c & 1)));
-                    if (j == P.n[w] - 1) mma_commit(bar(bars, B_QEMPTY + 2 * w + qb[w])); // Q tile read
+                    if (last) mma_commit(bar(bars, B_QEMPTY + 2 * w + qbuf)); // Q tile read
                 }
                 __syncwarp();
+                TRACE2(6 + w, g);
             };
             auto issue_PV = [&](int w, int64_t j) {
-                const int64_t g = P.F[w] + j, c = cw[w] + j;
+                const int64_t c = cw[w] + j, g = P.F[w] + j;
                 mbar_wait(bar(bars, B_PFULL + 2 * w + (int)(c & 1)), (uint32_t)((c >> 1) & 1));
-                if (lane == 0) {
-                    fence_after();
-                    const uint32_t bv = sbase + OFF_KV + (uint32_t)(g & (NSLOT - 1)) * 2 * CBYTES + CBYTES;
-                    const uint32_t tP = tmem + 256u * w + COL_P + (uint32_t)(c & 1) * (KC / 2);
+                TRACE2(3 + w, g);
+                fence_after();
+                const int gi = (int)(g - P.lo), sl = (int)(g % NSLOT);
+                const uint32_t av = sbase + OFF_KV + (uint32_t)sl * 2 * CBYTES + CBYTES;
+                const uint32_t tP = tmem + 256u * w + COL_P + (uint32_t)(c & 1) * (KC / 2);
+                readers -= 1u << (4 * gi);
+                // the chunk's last reader: release its slot unless the next item keeps it
+                // (commit tracks every MMA this thread issued)
+                const bool release = ((readers >> (4 * gi)) & 15u) == 0 && g < keep_from;
+                if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < KC / 16; ++kk) // 16 keys per MMA: 8 P columns, 16 V rows
-                        mma_ts(tmem + 256u * w + COL_O, tP + kk * 8, sdesc_sw128(bv + kk * 16 * RB), idO,
+                        mma_ts(tmem + 256u * w + COL_O, tP + kk * 8, dbase | ((av + kk * 16 * RB) >> 4), idO,
                                (j > 0 || kk > 0));
                     mma_commit(bar(bars, B_OFULL + 2 * w + (int)(c & 1)));
-                    // last reader of chunk g in this item: the P V of tile A on chunk g runs at
-                    // step g - F_A + 1, tile B's at step g - F_B + 1 (after A's within a step)
-                    const bool inA = g >= P.F[0] && g < P.F[0] + P.n[0];
-                    const bool inB = g >= P.F[1] && g < P.F[1] + P.n[1];
-                    const bool last = w == 0 ? (!inB || P.F[1] > P.F[0]) : (!inA || P.F[1] <= P.F[0]);
-                    if (last && g < keep_from) mma_commit(bar(bars, B_KVEMPTY + (int)(g & (NSLOT - 1))));
+                    if (release) mma_commit(bar(bars, B_KVEMPTY + sl));
                 }
                 __syncwarp();
             };
+            // S of the first two chunks of each tile (unless issued early)
+            for (int w = 0; w < 2; ++w)
+                for (int64_t j = pre[w]; j < 2 && j < P.n[w]; ++j) {
+                    chunk_ready(P.F[w] + j);
+                    issue_S(w, cw[w] + j, P.F[w] + j, qb[w], j == P.n[w] - 1);
+                }
+            int npre[2] = {0, 0};
+            bool nqw[2] = {false, false};
             const int64_t jmax = imax(P.n[0], P.n[1]);
-            // step j: S of chunk j, then P V of chunk j - 1 (whose P the softmax is finishing)
-            for (int64_t j = 0; j <= jmax; ++j) {
-                for (int w = 0; w < 2; ++w)
-                    if (j < P.n[w]) issue_S(w, j);
-                if (j >= 1)
-                    for (int w = 0; w < 2; ++w)
-                        if (j - 1 < P.n[w]) issue_PV(w, j - 1);
+            for (int64_t j = 0; j < jmax; ++j) {
+                for (int w = 0; w < 2; ++w) {
+                    if (j >= P.n[w]) continue;
+                    issue_PV(w, j);
+                    if (j + 2 < P.n[w]) {
+                        chunk_ready(P.F[w] + j + 2);
+                        issue_S(w, cw[w] + j + 2, P.F[w] + j + 2, qb[w], j + 2 == P.n[w] - 1);
+                    } else if (j == P.n[w] - 1 && next_cont && N.valid[w]) {
+                        // tile done: start the next tile's first S MMAs (resident chunks)
+                        for (int64_t jn = 0; jn < 2 && jn < N.n[w]; ++jn) {
+                            const int64_t g = N.F[w] + jn;
+                            if (g > P.hi || !((ready >> (int)(g - P.lo)) & 1u)) break;
+                            if (!nqw[w]) {
+                                mbar_wait(bar(bars, B_QFULL + 2 * w + (nq[w] & 1)), (nq[w] >> 1) & 1);
+                                ++nq[w];
+                                nqw[w] = true;
+                                fence_after();
+                            }
+                            issue_S(w, cw[w] + P.n[w] + jn, g, (nq[w] - 1) & 1, jn == N.n[w] - 1);
+                            ++npre[w];
+                        }
+                    }
+                }
             }
             cw[0] += P.n[0];
             cw[1] += P.n[1];
+            pre[0] = npre[0];
+            pre[1] = npre[1];
+            preq[0] = nqw[0];
+            preq[1] = nqw[1];
             prev_stream = P.stream;
             prev_u = P.u;
             prev_hi = P.hi;
@@ -351,8 +430,10 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 const uint32_t tP = tl + COL_P + (uint32_t)(c & 1) * (KC / 2);
                 // S_c is waited for even when skipped: every phase of the S barriers is then
                 // observed in order (a parity wait cannot tell phase k from phase k + 2)
+                TRACE(10 + w);
                 mbar_wait(bar(bars, B_SFULL + 2 * w + (int)(c & 1)), (uint32_t)((c >> 1) & 1));
                 fence_after();
+                TRACE(12 + w);
                 if (kmin > uhi || kmin + KC - 1 < ulo) { // no row of this warp reaches the chunk
                     if (c >= 2) wait_O(c - 2);
                     uint32_t z[32];
@@ -370,8 +451,14 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 tmem_wait_ld();
                 if (!(kmin >= ilo && kmin + KC - 1 <= ihi)) { // partial: keep only this row's band
                     const int il = (int)imax(klo - kmin, -1), ih = (int)imin(khi - kmin, KC);
+                    if (__any_sync(0xffffffffu, il > 0)) { // left edge of the band inside the chunk
 #pragma unroll
-                    for (int i = 0; i < KC; ++i) sv[i] = (i >= il && i <= ih) ? sv[i] : -INFINITY;
+                        for (int i = 0; i < KC; ++i) sv[i] = i >= il ? sv[i] : -INFINITY;
+                    }
+                    if (__any_sync(0xffffffffu, ih < KC - 1)) { // right edge
+#pragma unroll
+                        for (int i = 0; i < KC; ++i) sv[i] = i <= ih ? sv[i] : -INFINITY;
+                    }
                 }
                 float lmx[8];
 #pragma unroll
@@ -380,46 +467,49 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 for (int i = 8; i < KC; ++i) lmx[i & 7] = fmaxf(lmx[i & 7], sv[i]);
                 const float lm = fmaxf(fmaxf(fmaxf(lmx[0], lmx[1]), fmaxf(lmx[2], lmx[3])),
                                        fmaxf(fmaxf(lmx[4], lmx[5]), fmaxf(lmx[6], lmx[7])));
+                // lazy rescale: a row moves its reference max only when the chunk's max exceeds
+                // it by more than kTau (weights stay <= 2^kTau); O needs rescaling only for rows
+                // that already hold weight (a row with m = -inf has O = 0 and l = 0)
                 const float lm2 = lm * sl2;
                 const bool need = lm2 > m_run + kTau;
-                if (__any_sync(0xffffffffu, need)) {
-                    if (j > 0) wait_O(c - 1); // O stable: P V of the previous chunk completed
-                    const float mn = fmaxf(m_run, lm2);
-                    const float a = m_run == -INFINITY ? 0.f : ex2(m_run - mn);
-                    if (__any_sync(0xffffffffu, j > 0 && a != 1.f)) {
-                        float ov[32];
+                const float a = (need && m_run != -INFINITY) ? ex2(m_run - lm2) : 1.f;
+                if (__any_sync(0xffffffffu, a != 1.f) && j > 0) {
+                    wait_O(c - 1); // O stable: P V of the previous chunk completed
+                    float ov[32];
 #pragma unroll
-                        for (int qq = 0; qq < D / 32; ++qq) {
-                            tmem_ld32(tl + COL_O + 32 * qq, ov);
-                            tmem_wait_ld();
-                            uint32_t ob[32];
+                    for (int qq = 0; qq < D / 32; ++qq) {
+                        tmem_ld32(tl + COL_O + 32 * qq, ov);
+                        tmem_wait_ld();
+                        uint32_t ob[32];
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(ov[i] * a);
-                            tmem_st32(tl + COL_O + 32 * qq, ob);
-                        }
-                        tmem_wait_st();
+                        for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(ov[i] * a);
+                        tmem_st32(tl + COL_O + 32 * qq, ob);
                     }
+                    tmem_wait_st();
+                }
+                if (need) {
                     l_run *= a;
-                    m_run = mn;
+                    m_run = lm2;
                 }
                 const float m_use = m_run == -INFINITY ? 0.f : m_run;
                 if (c >= 2) wait_O(c - 2); // P buffer last read by P V two chunks ago
                 uint32_t pk[KC / 2];
-                float ls[4] = {0.f, 0.f, 0.f, 0.f};
+                float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; // packed partial sums
 #pragma unroll
                 for (int i = 0; i < KC / 2; ++i) {
                     float x0 = sv[2 * i], x1 = sv[2 * i + 1];
                     ffma2_sm(x0, x1, sl2, -m_use);
                     x0 = ex2(x0);
                     x1 = ex2(x1);
-                    ls[i & 3] += x0 + x1;
+                    fadd2_acc(ls[i & 1], x0, x1);
                     pk[i] = pack2<T>(x0, x1);
                 }
-                l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+                l_run += (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
                 tmem_st32(tP, pk);
                 tmem_wait_st();
                 fence_before();
                 mbar_arrive(bar(bars, B_PFULL + 2 * w + (int)(c & 1)));
+                TRACE(14 + w);
             }
             cnt += n;
             // ---- epilogue: O row from TMEM, normalise, store
@@ -481,11 +571,22 @@ template <typename T> static ga_status launch_t(const TcParams &tp, int64_t grid
 
 int64_t window_tc_tile_rows() { return wtc::ROWS; }
 
+#ifdef GA_WTC_TRACE
+extern "C" int ga_wtc_trace_read(unsigned long long *out, int n)
+{
+    if (n < wtc::TRACE_N) return -1;
+    cudaMemcpyFromSymbol(out, wtc::g_trace, sizeof(unsigned long long) * wtc::TRACE_N);
+    static unsigned long long z[wtc::TRACE_N];
+    cudaMemcpyToSymbol(wtc::g_trace, z, sizeof(z));
+    return wtc::TRACE_N;
+}
+#endif
+
 bool window_tc_supported(const AttnParams &p, ga_dtype dt)
 {
     if (p.mask.kind != K_WINDOW || (dt != GA_BF16 && dt != GA_F16) || p.d != 64) return false;
     const int64_t m = p.mask.m, r = p.mask.r;
-    if (m < 64 || m > 128 || r > 4 || wtc::pair_span(m) > wtc::NSLOT) return false;
+    if (m < 64 || m > 128 || r > 4 || wtc::pair_span(m) > 8) return false; // 8 chunks per item (bitmasks)
     if (p.mask.L >= ((int64_t)1 << 31) || p.q_rows <= 0) return false; // TMA coordinates are int32
     // without peer memory the local K/V must hold every key the query range reaches
     if (p.k_peer == nullptr && !(p.kv_begin == 0 && p.kv_rows == p.mask.L)) {
