@@ -124,6 +124,37 @@ __device__ __forceinline__ Pair pair_geo(const TcParams &tp, int64_t it)
     return P;
 }
 
+// One warpgroup's tile of a work item (scalar fields: no dynamically indexed arrays, which
+// would live in local memory)
+struct Tile {
+    int32_t c, h, Nc, a_lo, a_hi, a0, F, n;
+    bool valid;
+};
+
+__device__ __forceinline__ Tile tile_geo(const TcParams &tp, int64_t it, int w)
+{
+    const AttnParams &p = tp.p;
+    const uint32_t r = (uint32_t)tp.r, L = (uint32_t)p.mask.L, H = (uint32_t)p.H, pps = (uint32_t)tp.pps;
+    const int32_t m = (int32_t)tp.m;
+    Tile T;
+    const uint32_t iu = (uint32_t)it, st = iu / pps, u = iu - st * pps;
+    const uint32_t c = st / H;
+    T.c = (int32_t)c;
+    T.h = (int32_t)(st - c * H);
+    const uint32_t Nc = c < L ? (L - c + r - 1) / r : 0;
+    const uint32_t qb = (uint32_t)p.q_begin, qe = (uint32_t)(p.q_begin + p.q_rows);
+    const uint32_t a_lo = qb > c ? (qb - c + r - 1) / r : 0;
+    const uint32_t a_hi = qe > c ? min((qe - c + r - 1) / r, Nc) : 0;
+    T.Nc = (int32_t)Nc;
+    T.a_lo = (int32_t)a_lo;
+    T.a_hi = (int32_t)a_hi;
+    T.a0 = (int32_t)((a_lo / ROWS + 2 * u + (uint32_t)w) * ROWS);
+    T.valid = a_lo < a_hi && (uint32_t)T.a0 < a_hi;
+    T.F = max((T.a0 - m) >> 6, 0);
+    T.n = T.valid ? min((T.a0 + ROWS - 1 + m) >> 6, ((int32_t)Nc - 1) >> 6) - T.F + 1 : 0;
+    return T;
+}
+
 __device__ __forceinline__ uint32_t bar(uint32_t base, int i) { return base + 8u * (uint32_t)i; }
 
 #ifdef GA_WTC_TRACE
@@ -190,15 +221,16 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
 
     if (warp == 8) {
         // ============================ loader ============================
-        int fills[NSLOT];
-#pragma unroll
-        for (int s = 0; s < NSLOT; ++s) fills[s] = 0;
+        // per slot: filled before (bit s of `used`), parity of the fill count (bit s of `par`);
+        // bitmasks, not arrays (a dynamically indexed array would live in local memory)
+        uint32_t used = 0, par = 0;
         int nq[2] = {0, 0};
         int64_t prev_stream = -1, prev_u = -1, prev_hi = -1;
         for (int64_t it = it_begin; it < it_end; ++it) {
             const Pair P = pair_geo(tp, it);
             if (!P.any) continue;
             // Q tiles
+#pragma unroll
             for (int w = 0; w < 2; ++w) {
                 if (!P.valid[w]) continue;
                 const int b = nq[w] & 1;
@@ -218,10 +250,12 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             for (int64_t g = P.lo; g <= P.hi; ++g) {
                 if (cont && g <= prev_hi) continue;
                 const int s = (int)(g % NSLOT);
-                TRACE2(19, g);
-                if (fills[s] >= 1) mbar_wait(bar(bars, B_KVEMPTY + s), (fills[s] - 1) & 1);
+                TRACE2(21, g);
+                // fill n of slot s waits for release n - 1 (parity of n - 1 = complement of n's)
+                if ((used >> s) & 1u) mbar_wait(bar(bars, B_KVEMPTY + s), ((par >> s) & 1u) ^ 1u);
                 TRACE2(20, g);
-                ++fills[s];
+                used |= 1u << s;
+                par ^= 1u << s;
                 const uint32_t fb = bar(bars, B_KVFULL + s);
                 const uint32_t dK = sbase + OFF_KV + (uint32_t)s * 2 * CBYTES, dV = dK + CBYTES;
                 const int64_t tok0 = P.c + g * KC * r;                       // first row's token
@@ -280,9 +314,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         // smem descriptors: constant high part | (address >> 4); the operand tiles stay below
         // 256 KB so the 14-bit start field never carries
         const uint64_t dbase = sdesc_sw128(0);
-        int seen[NSLOT];
-#pragma unroll
-        for (int s = 0; s < NSLOT; ++s) seen[s] = 0;
+        uint32_t seen = 0;      // parity of the fills waited for, bit per slot
         int nq[2] = {0, 0};     // Q tiles waited per warpgroup
         int64_t cw[2] = {0, 0}; // running chunk counters per warpgroup (S/P/O buffer parity)
         int pre[2] = {0, 0};    // S MMAs of this item's tile already issued (end of the previous item)
@@ -298,11 +330,13 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             const bool next_cont = has_next && N.any && N.stream == P.stream && N.u == P.u + 1;
             const int64_t keep_from = next_cont ? N.lo : INT64_MAX;
             uint32_t readers = 0, ready = 0; // 4 bits per chunk g - lo; 1 bit per chunk
+#pragma unroll
             for (int w = 0; w < 2; ++w)
                 for (int64_t j = 0; j < P.n[w]; ++j) readers += 1u << (4 * (int)(P.F[w] + j - P.lo));
             if (cont)
                 for (int64_t g = P.lo; g <= P.hi && g <= prev_hi; ++g) ready |= 1u << (int)(g - P.lo);
             int qb[2] = {0, 0};
+#pragma unroll
             for (int w = 0; w < 2; ++w) {
                 if (!P.valid[w]) continue;
                 if (preq[w]) {
@@ -318,8 +352,8 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 const int gi = (int)(g - P.lo);
                 if ((ready >> gi) & 1u) return;
                 const int sl = (int)(g % NSLOT);
-                mbar_wait(bar(bars, B_KVFULL + sl), seen[sl] & 1);
-                ++seen[sl];
+                mbar_wait(bar(bars, B_KVFULL + sl), (seen >> sl) & 1u);
+                seen ^= 1u << sl;
                 ready |= 1u << gi;
                 TRACE2(1, g);
                 fence_after();
@@ -361,6 +395,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 __syncwarp();
             };
             // S of the first two chunks of each tile (unless issued early)
+#pragma unroll
             for (int w = 0; w < 2; ++w)
                 for (int64_t j = pre[w]; j < 2 && j < P.n[w]; ++j) {
                     chunk_ready(P.F[w] + j);
@@ -370,6 +405,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             bool nqw[2] = {false, false};
             const int64_t jmax = imax(P.n[0], P.n[1]);
             for (int64_t j = 0; j < jmax; ++j) {
+#pragma unroll
                 for (int w = 0; w < 2; ++w) {
                     if (j >= P.n[w]) continue;
                     issue_PV(w, j);
@@ -409,29 +445,31 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         const uint32_t tl = tmem + 256u * w + ((uint32_t)(q * 32) << 16); // this warp's TMEM lanes
         const float sl2 = p.scale_log2;
         constexpr float kTau = 8.f;
-        int64_t cnt = 0; // running chunk counter (matches the MMA issuer's cw[w])
-        auto wait_O = [&](int64_t c) {
-            mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(c & 1)), (uint32_t)((c >> 1) & 1));
+        uint32_t cnt = 0; // running chunk counter (matches the MMA issuer's cw[w])
+        auto wait_O = [&](uint32_t c) {
+            mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(c & 1)), (c >> 1) & 1);
             fence_after();
         };
         char *Og = reinterpret_cast<char *>(p.out);
+        const int32_t mi = (int32_t)m;
         for (int64_t it = it_begin; it < it_end; ++it) {
-            const Pair P = pair_geo(tp, it);
-            if (!P.valid[w]) continue;
-            const int64_t a0 = P.a0[w], xr0 = a0 + 32 * q, x = xr0 + lane;
+            const Tile Tt = tile_geo(tp, it, w);
+            if (!Tt.valid) continue;
+            const int32_t xr0 = Tt.a0 + 32 * q, x = xr0 + lane;
             // keys of this warp's rows: union [ulo, uhi], every row: [ilo, ihi]; this row: [klo, khi]
-            const int64_t ulo = imax(xr0 - m, 0), uhi = imin(xr0 + 31 + m, P.Nc - 1);
-            const int64_t ilo = imax(xr0 + 31 - m, 0), ihi = imin(xr0 + m, P.Nc - 1);
-            const int64_t klo = imax(x - m, 0), khi = imin(x + m, P.Nc - 1);
+            const int32_t ulo = max(xr0 - mi, 0), uhi = min(xr0 + 31 + mi, Tt.Nc - 1);
+            const int32_t ilo = max(xr0 + 31 - mi, 0), ihi = min(xr0 + mi, Tt.Nc - 1);
+            const int32_t klo = max(x - mi, 0), khi = min(x + mi, Tt.Nc - 1);
             float m_run = -INFINITY, l_run = 0.f;
-            const int64_t n = P.n[w];
-            for (int64_t j = 0; j < n; ++j) {
-                const int64_t c = cnt + j, kmin = (P.F[w] + j) * KC;
-                const uint32_t tP = tl + COL_P + (uint32_t)(c & 1) * (KC / 2);
+            const int32_t n = Tt.n;
+            for (int32_t j = 0; j < n; ++j) {
+                const uint32_t c = cnt + (uint32_t)j;
+                const int32_t kmin = (Tt.F + j) * KC;
+                const uint32_t tP = tl + COL_P + (c & 1) * (KC / 2);
                 // S_c is waited for even when skipped: every phase of the S barriers is then
                 // observed in order (a parity wait cannot tell phase k from phase k + 2)
                 TRACE(10 + w);
-                mbar_wait(bar(bars, B_SFULL + 2 * w + (int)(c & 1)), (uint32_t)((c >> 1) & 1));
+                mbar_wait(bar(bars, B_SFULL + 2 * w + (int)(c & 1)), (c >> 1) & 1);
                 fence_after();
                 TRACE(12 + w);
                 if (kmin > uhi || kmin + KC - 1 < ulo) { // no row of this warp reaches the chunk
@@ -450,7 +488,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 tmem_ld32(tl + COL_S + (uint32_t)(c & 1) * KC + 32, sv + 32);
                 tmem_wait_ld();
                 if (!(kmin >= ilo && kmin + KC - 1 <= ihi)) { // partial: keep only this row's band
-                    const int il = (int)imax(klo - kmin, -1), ih = (int)imin(khi - kmin, KC);
+                    const int il = max(klo - kmin, -1), ih = min(khi - kmin, KC);
                     if (__any_sync(0xffffffffu, il > 0)) { // left edge of the band inside the chunk
 #pragma unroll
                         for (int i = 0; i < KC; ++i) sv[i] = i >= il ? sv[i] : -INFINITY;
@@ -513,15 +551,17 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             }
             cnt += n;
             // ---- epilogue: O row from TMEM, normalise, store
+            TRACE2(16 + w, 0);
             wait_O(cnt - 1);
+            TRACE2(18 + w, 0);
             float o[D];
             tmem_ld32(tl + COL_O, o);
             tmem_ld32(tl + COL_O + 32, o + 32);
             tmem_wait_ld();
-            if (x >= P.a_lo && x < P.a_hi) {
+            if (x >= Tt.a_lo && x < Tt.a_hi) {
                 const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-                const int64_t i = P.c + x * r;
-                char *orow = Og + (size_t)(i - p.q_begin) * row_bytes + (size_t)P.h * D * sizeof(T);
+                const int64_t i = (int64_t)Tt.c + (int64_t)x * r;
+                char *orow = Og + (size_t)(i - p.q_begin) * row_bytes + (size_t)Tt.h * D * sizeof(T);
 #pragma unroll
                 for (int qq = 0; qq < D / 8; ++qq) {
                     float r8[8];
