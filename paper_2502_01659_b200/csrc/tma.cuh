@@ -35,5 +35,20 @@ __device__ __forceinline__ void load_3d(uint32_t smem, const CUtensorMap *map, i
                  : "memory");
 }
 
+// shared memory -> box at coordinates (c0, c1, c2) (bulk-group completion); coordinates outside
+// the tensor are not written
+__device__ __forceinline__ void store_3d(const CUtensorMap *map, int c0, int c1, int c2, uint32_t smem)
+{
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(smem)
+                 : "memory");
+}
+
+__device__ __forceinline__ void store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+// the bulk stores committed so far have finished reading shared memory
+__device__ __forceinline__ void store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
 } // namespace tma
 } // namespace ga

@@ -52,15 +52,20 @@ constexpr uint32_t OFF_BAR = OFF_KV + NSLOT * 2 * CBYTES;
 constexpr uint32_t SMEM_BYTES = 1024 + OFF_BAR + 64 * 8;
 
 // mbarrier indices (8 bytes each from OFF_BAR)
+#ifndef GA_WTC_NSB
+#define GA_WTC_NSB 2
+#endif
+constexpr int NSB = GA_WTC_NSB; // S buffers per warpgroup (P is written over its S buffer)
 constexpr int B_QFULL = 0, B_QEMPTY = 4, B_KVFULL = 8, B_KVEMPTY = 8 + NSLOT, B_SFULL = 8 + 2 * NSLOT,
-              B_PFULL = B_SFULL + 4, B_OFULL = B_PFULL + 4;
+              B_PFULL = B_SFULL + 2 * NSB, B_OFULL = B_PFULL + 2 * NSB;
 constexpr int B_TMEM = B_OFULL + 4; // tcgen05.alloc writes the TMEM base here
 
-// TMEM columns of warpgroup w: S[2] at 256w + {0, 64}, P[2] at 256w + 128 + {0, 32}, O at 256w + 192
-constexpr uint32_t COL_S = 0, COL_P = 128, COL_O = 192;
+// TMEM columns of warpgroup w: S[3] at 256w + {0, 64, 128} (P of chunk c, 16-bit pairs, is written
+// over the first 32 columns of its S buffer), O at 256w + 192
+constexpr uint32_t COL_S = 0, COL_O = 192;
 
 struct TcParams {
-    CUtensorMap tmQ, tmK, tmV; // one head, element stride r, 64-row boxes
+    CUtensorMap tmQ, tmK, tmV, tmO; // one head, element stride r, 64-row boxes
     AttnParams p;
     int64_t m, r;
     int64_t pps;   // tile pairs per (class, head) stream
@@ -199,10 +204,12 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) {
             mbar_init(bar(bars, B_QFULL + i), 1);
-            mbar_init(bar(bars, B_QEMPTY + i), 1);
+            mbar_init(bar(bars, B_QEMPTY + i), 1); // the warpgroup's O store has read the buffer
+            mbar_init(bar(bars, B_OFULL + i), 1);
+        }
+        for (int i = 0; i < 2 * NSB; ++i) {
             mbar_init(bar(bars, B_SFULL + i), 1);
             mbar_init(bar(bars, B_PFULL + i), 128);
-            mbar_init(bar(bars, B_OFULL + i), 1);
         }
         for (int s = 0; s < NSLOT; ++s) {
             mbar_init(bar(bars, B_KVFULL + s), 1);
@@ -358,28 +365,29 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 TRACE2(1, g);
                 fence_after();
             };
-            auto issue_S = [&](int w, int64_t c, int64_t g, int qbuf, bool last) {
+            auto issue_S = [&](int w, int64_t c, int64_t g, int qbuf) {
                 const uint32_t aq = sbase + OFF_Q + (uint32_t)(2 * w + qbuf) * QBYTES;
                 const uint32_t ak = sbase + OFF_KV + (uint32_t)(g % NSLOT) * 2 * CBYTES;
-                const uint32_t dS = tmem + 256u * w + COL_S + (uint32_t)(c & 1) * KC;
+                const uint32_t sb = (uint32_t)(c % NSB);
+                const uint32_t dS = tmem + 256u * w + COL_S + sb * KC;
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk)
                         mma_ss(dS, dbase | ((aq + kk * 32) >> 4), dbase | ((ak + kk * 32) >> 4), idS, kk > 0);
-                    mma_commit(bar(bars, B_SFULL + 2 * w + (int)(c & 1)));
-                    if (last) mma_commit(bar(bars, B_QEMPTY + 2 * w + qbuf)); // Q tile read
+                    mma_commit(bar(bars, B_SFULL + NSB * w + (int)sb));
                 }
                 __syncwarp();
                 TRACE2(6 + w, g);
             };
             auto issue_PV = [&](int w, int64_t j) {
                 const int64_t c = cw[w] + j, g = P.F[w] + j;
-                mbar_wait(bar(bars, B_PFULL + 2 * w + (int)(c & 1)), (uint32_t)((c >> 1) & 1));
+                const uint32_t sb = (uint32_t)(c % NSB);
+                mbar_wait(bar(bars, B_PFULL + NSB * w + (int)sb), (uint32_t)((c / NSB) & 1));
                 TRACE2(3 + w, g);
                 fence_after();
                 const int gi = (int)(g - P.lo), sl = (int)(g % NSLOT);
                 const uint32_t av = sbase + OFF_KV + (uint32_t)sl * 2 * CBYTES + CBYTES;
-                const uint32_t tP = tmem + 256u * w + COL_P + (uint32_t)(c & 1) * (KC / 2);
+                const uint32_t tP = tmem + 256u * w + COL_S + sb * KC;
                 readers -= 1u << (4 * gi);
                 // the chunk's last reader: release its slot unless the next item keeps it
                 // (commit tracks every MMA this thread issued)
@@ -394,41 +402,54 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 }
                 __syncwarp();
             };
-            // S of the first two chunks of each tile (unless issued early)
+            // S of the first NSB chunks of each tile (unless issued early); S_w(j + NSB) reuses
+            // the buffer of chunk j, free once P V_w(j) is issued (the tensor pipe runs the MMAs
+            // in order, so the P V has read P before the next S overwrites it)
 #pragma unroll
             for (int w = 0; w < 2; ++w)
-                for (int64_t j = pre[w]; j < 2 && j < P.n[w]; ++j) {
+                for (int64_t j = pre[w]; j < NSB && j < P.n[w]; ++j) {
                     chunk_ready(P.F[w] + j);
-                    issue_S(w, cw[w] + j, P.F[w] + j, qb[w], j == P.n[w] - 1);
+                    issue_S(w, cw[w] + j, P.F[w] + j, qb[w]);
                 }
             int npre[2] = {0, 0};
             bool nqw[2] = {false, false};
+            auto prefetch = [&](int w, bool block) { // next tile's first S MMAs (resident chunks)
+                for (int64_t jn = 0; jn < NSB && jn < N.n[w]; ++jn) {
+                    const int64_t g = N.F[w] + jn;
+                    if (g > P.hi || !((ready >> (int)(g - P.lo)) & 1u)) break;
+                    if (!nqw[w]) {
+                        const uint32_t qf = bar(bars, B_QFULL + 2 * w + (nq[w] & 1));
+                        const uint32_t ph = (nq[w] >> 1) & 1;
+                        if (block) mbar_wait(qf, ph);
+                        else if (!mbar_test(qf, ph)) return;
+                        ++nq[w];
+                        nqw[w] = true;
+                        fence_after();
+                    }
+                    issue_S(w, cw[w] + P.n[w] + jn, g, (nq[w] - 1) & 1);
+                    ++npre[w];
+                }
+            };
             const int64_t jmax = imax(P.n[0], P.n[1]);
             for (int64_t j = 0; j < jmax; ++j) {
 #pragma unroll
                 for (int w = 0; w < 2; ++w) {
                     if (j >= P.n[w]) continue;
                     issue_PV(w, j);
-                    if (j + 2 < P.n[w]) {
-                        chunk_ready(P.F[w] + j + 2);
-                        issue_S(w, cw[w] + j + 2, P.F[w] + j + 2, qb[w], j + 2 == P.n[w] - 1);
+                    if (j + NSB < P.n[w]) {
+#ifdef GA_WTC_WAR_TEST
+                        { const int64_t cc = cw[w] + j; mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(cc & 1)), (uint32_t)((cc >> 1) & 1)); fence_after(); }
+#endif
+                        chunk_ready(P.F[w] + j + NSB);
+                        issue_S(w, cw[w] + j + NSB, P.F[w] + j + NSB, qb[w]);
                     } else if (j == P.n[w] - 1 && next_cont && N.valid[w]) {
-                        // tile done: start the next tile's first S MMAs (resident chunks)
-                        for (int64_t jn = 0; jn < 2 && jn < N.n[w]; ++jn) {
-                            const int64_t g = N.F[w] + jn;
-                            if (g > P.hi || !((ready >> (int)(g - P.lo)) & 1u)) break;
-                            if (!nqw[w]) {
-                                mbar_wait(bar(bars, B_QFULL + 2 * w + (nq[w] & 1)), (nq[w] >> 1) & 1);
-                                ++nq[w];
-                                nqw[w] = true;
-                                fence_after();
-                            }
-                            issue_S(w, cw[w] + P.n[w] + jn, g, (nq[w] - 1) & 1, jn == N.n[w] - 1);
-                            ++npre[w];
-                        }
+                        prefetch(w, false); // only if the next Q tile already landed
                     }
                 }
             }
+#pragma unroll
+            for (int w = 0; w < 2; ++w)
+                if (next_cont && N.valid[w] && npre[w] == 0) prefetch(w, true);
             cw[0] += P.n[0];
             cw[1] += P.n[1];
             pre[0] = npre[0];
@@ -450,7 +471,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(c & 1)), (c >> 1) & 1);
             fence_after();
         };
-        char *Og = reinterpret_cast<char *>(p.out);
+        uint32_t ntile = 0; // tiles of this warpgroup (Q / O staging buffer = ntile & 1)
         const int32_t mi = (int32_t)m;
         for (int64_t it = it_begin; it < it_end; ++it) {
             const Tile Tt = tile_geo(tp, it, w);
@@ -463,29 +484,28 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             float m_run = -INFINITY, l_run = 0.f;
             const int32_t n = Tt.n;
             for (int32_t j = 0; j < n; ++j) {
-                const uint32_t c = cnt + (uint32_t)j;
+                const uint32_t c = cnt + (uint32_t)j, sb = c % NSB, sph = (c / NSB) & 1;
                 const int32_t kmin = (Tt.F + j) * KC;
-                const uint32_t tP = tl + COL_P + (c & 1) * (KC / 2);
+                const uint32_t tS = tl + COL_S + sb * KC; // S of chunk c; P is written over it
                 // S_c is waited for even when skipped: every phase of the S barriers is then
                 // observed in order (a parity wait cannot tell phase k from phase k + 2)
                 TRACE(10 + w);
-                mbar_wait(bar(bars, B_SFULL + 2 * w + (int)(c & 1)), (c >> 1) & 1);
+                mbar_wait(bar(bars, B_SFULL + NSB * w + (int)sb), sph);
                 fence_after();
                 TRACE(12 + w);
                 if (kmin > uhi || kmin + KC - 1 < ulo) { // no row of this warp reaches the chunk
-                    if (c >= 2) wait_O(c - 2);
                     uint32_t z[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) z[i] = 0u;
-                    tmem_st32(tP, z);
+                    tmem_st32(tS, z);
                     tmem_wait_st();
                     fence_before();
-                    mbar_arrive(bar(bars, B_PFULL + 2 * w + (int)(c & 1)));
+                    mbar_arrive(bar(bars, B_PFULL + NSB * w + (int)sb));
                     continue;
                 }
                 float sv[KC];
-                tmem_ld32(tl + COL_S + (uint32_t)(c & 1) * KC, sv);
-                tmem_ld32(tl + COL_S + (uint32_t)(c & 1) * KC + 32, sv + 32);
+                tmem_ld32(tS, sv);
+                tmem_ld32(tS + 32, sv + 32);
                 tmem_wait_ld();
                 if (!(kmin >= ilo && kmin + KC - 1 <= ihi)) { // partial: keep only this row's band
                     const int il = max(klo - kmin, -1), ih = min(khi - kmin, KC);
@@ -530,7 +550,6 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     m_run = lm2;
                 }
                 const float m_use = m_run == -INFINITY ? 0.f : m_run;
-                if (c >= 2) wait_O(c - 2); // P buffer last read by P V two chunks ago
                 uint32_t pk[KC / 2];
                 float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; // packed partial sums
 #pragma unroll
@@ -543,33 +562,74 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     pk[i] = pack2<T>(x0, x1);
                 }
                 l_run += (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
-                tmem_st32(tP, pk);
+                tmem_st32(tS, pk);
                 tmem_wait_st();
                 fence_before();
-                mbar_arrive(bar(bars, B_PFULL + 2 * w + (int)(c & 1)));
+                mbar_arrive(bar(bars, B_PFULL + NSB * w + (int)sb));
                 TRACE(14 + w);
             }
             cnt += n;
             // ---- epilogue: O row from TMEM, normalise, store
             TRACE2(16 + w, 0);
+            // O final after P V of the tile's last chunk.  The O barriers alternate per chunk and
+            // a parity wait is exact only if the barrier's previous phase completed: P V(cnt-2)'s
+            // predecessor P V(cnt-4) ran before S(cnt-1) (observed), and P V(cnt-2) completing
+            // implies P V(cnt-3), the predecessor of P V(cnt-1)
+            if (cnt >= 2) wait_O(cnt - 2);
             wait_O(cnt - 1);
             TRACE2(18 + w, 0);
             float o[D];
             tmem_ld32(tl + COL_O, o);
             tmem_ld32(tl + COL_O + 32, o + 32);
             tmem_wait_ld();
-            if (x >= Tt.a_lo && x < Tt.a_hi) {
-                const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-                const int64_t i = (int64_t)Tt.c + (int64_t)x * r;
-                char *orow = Og + (size_t)(i - p.q_begin) * row_bytes + (size_t)Tt.h * D * sizeof(T);
+            // stage the normalised rows in this tile's Q buffer (its last reader, the last S MMA,
+            // completed before the last P V) in the TMA layout, then one thread stores the tile
+            // with two 64-row TMA boxes (rows outside the query range / sequence are clipped by
+            // the tensor map) and releases the buffer to the loader
+            const bool full_tile = Tt.a0 >= Tt.a_lo && Tt.a0 + ROWS <= Tt.a_hi;
+            if (!full_tile) { // tile cut by the query range / sequence end: plain stores of valid rows
+                if (x >= Tt.a_lo && x < Tt.a_hi) {
+                    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+                    const int64_t i = (int64_t)Tt.c + (int64_t)x * r;
+                    char *orow = reinterpret_cast<char *>(p.out) + (size_t)(i - p.q_begin) * row_bytes +
+                                 (size_t)Tt.h * D * sizeof(T);
 #pragma unroll
-                for (int qq = 0; qq < D / 8; ++qq) {
-                    float r8[8];
+                    for (int qq = 0; qq < D / 8; ++qq) {
+                        float r8[8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) r8[e] = o[8 * qq + e] * inv;
-                    stg16(orow + qq * 16, pack<T>(r8));
+                        for (int e = 0; e < 8; ++e) r8[e] = o[8 * qq + e] * inv;
+                        stg16(orow + qq * 16, pack<T>(r8));
+                    }
                 }
+                asm volatile("bar.sync %0, 128;" ::"r"(1 + w) : "memory");
+                if (q == 0 && lane == 0) mbar_arrive(bar(bars, B_QEMPTY + 2 * w + (int)(ntile & 1)));
+                ++ntile;
+                continue;
             }
+            const uint32_t sO = sbase + OFF_Q + (uint32_t)(2 * w + (ntile & 1)) * QBYTES;
+            const int xl = 32 * q + lane;
+            const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll
+            for (int qq = 0; qq < D / 8; ++qq) {
+                float r8[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) r8[e] = o[8 * qq + e] * inv;
+                const uint4 v = pack<T>(r8);
+                asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sO + swz<D>(xl, qq)), "r"(v.x), "r"(v.y),
+                             "r"(v.z), "r"(v.w)
+                             : "memory");
+            }
+            fence_proxy_async();
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + w) : "memory"); // the warpgroup's 128 rows staged
+            if (q == 0 && lane == 0) {
+                const int tok = (int)((int64_t)Tt.c + (int64_t)Tt.a0 * r - p.q_begin);
+                tma::store_3d(&tp.tmO, 0, Tt.h, tok, sO);
+                tma::store_3d(&tp.tmO, 0, Tt.h, tok + 64 * (int)r, sO + QBYTES / 2);
+                tma::store_commit();
+                tma::store_wait_read();
+                mbar_arrive(bar(bars, B_QEMPTY + 2 * w + (int)(ntile & 1)));
+            }
+            ++ntile;
         }
     }
     fence_before();
@@ -657,6 +717,7 @@ ga_status launch_window_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s)
     tp.items = pps * r * p.H;
     if (tp.items == 0) return GA_OK;
     if (!tma::encode_rows(&tp.tmQ, p.Q, p.q_rows, p.H, p.d, (int)r, 64) ||
+        !tma::encode_rows(&tp.tmO, p.out, p.q_rows, p.H, p.d, (int)r, 64) ||
         !tma::encode_rows(&tp.tmK, p.K, p.kv_rows, p.H, p.d, (int)r, 64) ||
         !tma::encode_rows(&tp.tmV, p.V, p.kv_rows, p.H, p.d, (int)r, 64)) {
         set_error("tcgen05 window kernel: tensor-map encoding failed");
