@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                             }
                         }
                     }
+                    cp_async_commit(); // wait_group only covers committed groups
                     cp_async_wait<0>();
                     fence_proxy_async();
                     __syncwarp();

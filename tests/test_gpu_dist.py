@@ -135,7 +135,9 @@ def _comm_case(rank, world, fam, kernel="auto"):
             out = comm.attention(q[b:e].contiguous(), ks[: e - b], vs[: e - b], mask, L, kernel=kernel)
             torch.cuda.synchronize()
             if exact:
-                assert torch.equal(out, full[b:e]), fam
+                diff = (out.float() - full[b:e].float()).abs().amax(dim=(1, 2))
+                bad = torch.nonzero(diff > 0).flatten()
+                assert bad.numel() == 0, (fam, rank, bad.numel(), bad[:8].tolist(), diff.max().item())
             else:
                 assert (out.float() - full[b:e].float()).abs().max().item() < 2e-2, fam
         assert not comm.timed_out()
