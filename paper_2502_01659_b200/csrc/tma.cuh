@@ -50,5 +50,8 @@ __device__ __forceinline__ void store_commit() { asm volatile("cp.async.bulk.com
 // the bulk stores committed so far have finished reading shared memory
 __device__ __forceinline__ void store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
+// every bulk store committed so far has completed (global writes done)
+__device__ __forceinline__ void store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 } // namespace tma
 } // namespace ga

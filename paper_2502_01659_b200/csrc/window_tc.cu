@@ -60,9 +60,10 @@ constexpr int B_QFULL = 0, B_QEMPTY = 4, B_KVFULL = 8, B_KVEMPTY = 8 + NSLOT, B_
               B_PFULL = B_SFULL + 2 * NSB, B_OFULL = B_PFULL + 2 * NSB;
 constexpr int B_TMEM = B_OFULL + 4; // tcgen05.alloc writes the TMEM base here
 
-// TMEM columns of warpgroup w: S[3] at 256w + {0, 64, 128} (P of chunk c, 16-bit pairs, is written
-// over the first 32 columns of its S buffer), O at 256w + 192
-constexpr uint32_t COL_S = 0, COL_O = 192;
+// TMEM columns of warpgroup w: S[NSB] at 256w + 64 b (P of chunk c, 16-bit pairs, is written over
+// the first 32 columns of its S buffer), O[2] (tile k accumulates in O[k & 1]) after them
+constexpr uint32_t COL_S = 0, COL_O = NSB * KC;
+static_assert(NSB * KC + 2 * D <= 256, "TMEM: 256 columns per warpgroup");
 
 struct TcParams {
     CUtensorMap tmQ, tmK, tmV, tmO; // one head, element stride r, 64-row boxes
@@ -77,16 +78,16 @@ __host__ __device__ inline int64_t floordiv(int64_t a, int64_t b) { return a >= 
 // Geometry of one work item (a pair of consecutive 128-row tiles of one stream); every role
 // derives it independently from the item index, so all agree without communication.
 struct Pair {
-    int64_t stream, u, c, Nc, a_lo, a_hi;
+    int32_t stream, u, c, Nc, a_lo, a_hi;
     int h;
-    int64_t a0[2];  // first class row of tile A / B
+    int32_t a0[2];  // first class row of tile A / B
     bool valid[2];
-    int64_t F[2], n[2]; // chunks [F, F + n) per tile
-    int64_t lo, hi;     // union of the chunk ranges
+    int32_t F[2], n[2]; // chunks [F, F + n) per tile
+    int32_t lo, hi;     // union of the chunk ranges
     bool any;
 };
 
-__device__ __forceinline__ Pair pair_geo(const TcParams &tp, int64_t it)
+__device__ __forceinline__ Pair pair_geo(const TcParams &tp, int32_t it)
 {
     // 32-bit arithmetic throughout: L < 2^31 (window_tc_supported), so class rows, tiles and
     // item indices fit; 64-bit division would cost hundreds of instructions per item
@@ -109,7 +110,7 @@ __device__ __forceinline__ Pair pair_geo(const TcParams &tp, int64_t it)
     P.a_hi = a_hi;
     const int32_t t0 = (int32_t)(a_lo / ROWS + 2 * (uint32_t)P.u);
     const int32_t lastc = ((int32_t)Nc - 1) >> 6; // KC = 64
-    P.lo = INT64_MAX;
+    P.lo = INT32_MAX;
     P.hi = -1;
 #pragma unroll
     for (int w = 0; w < 2; ++w) {
@@ -121,8 +122,8 @@ __device__ __forceinline__ Pair pair_geo(const TcParams &tp, int64_t it)
         P.F[w] = f;
         P.n[w] = P.valid[w] ? e - f + 1 : 0;
         if (P.valid[w]) {
-            P.lo = imin(P.lo, f);
-            P.hi = imax(P.hi, e);
+            P.lo = min(P.lo, f);
+            P.hi = max(P.hi, e);
         }
     }
     P.any = P.valid[0];
@@ -136,7 +137,7 @@ struct Tile {
     bool valid;
 };
 
-__device__ __forceinline__ Tile tile_geo(const TcParams &tp, int64_t it, int w)
+__device__ __forceinline__ Tile tile_geo(const TcParams &tp, int32_t it, int w)
 {
     const AttnParams &p = tp.p;
     const uint32_t r = (uint32_t)tp.r, L = (uint32_t)p.mask.L, H = (uint32_t)p.H, pps = (uint32_t)tp.pps;
@@ -193,7 +194,8 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
     const size_t row_bytes = (size_t)H * D * sizeof(T);
 
     // contiguous run of work items
-    const int64_t it_begin = tp.items * blockIdx.x / gridDim.x, it_end = tp.items * (blockIdx.x + 1) / gridDim.x;
+    const int32_t it_begin = (int32_t)(tp.items * blockIdx.x / gridDim.x),
+                  it_end = (int32_t)(tp.items * (blockIdx.x + 1) / gridDim.x);
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) {
             mbar_init(bar(bars, B_QFULL + i), 1);
-            mbar_init(bar(bars, B_QEMPTY + i), 1); // the warpgroup's O store has read the buffer
+            mbar_init(bar(bars, B_QEMPTY + i), 4); // each warp's O store has read its rows
             mbar_init(bar(bars, B_OFULL + i), 1);
         }
         for (int i = 0; i < 2 * NSB; ++i) {
@@ -232,8 +234,8 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         // bitmasks, not arrays (a dynamically indexed array would live in local memory)
         uint32_t used = 0, par = 0;
         int nq[2] = {0, 0};
-        int64_t prev_stream = -1, prev_u = -1, prev_hi = -1;
-        for (int64_t it = it_begin; it < it_end; ++it) {
+        int32_t prev_stream = -1, prev_u = -1, prev_hi = -1;
+        for (int32_t it = it_begin; it < it_end; ++it) {
             const Pair P = pair_geo(tp, it);
             if (!P.any) continue;
             // Q tiles
@@ -254,9 +256,9 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             }
             // K/V chunks not resident from the previous pair
             const bool cont = P.stream == prev_stream && P.u == prev_u + 1;
-            for (int64_t g = P.lo; g <= P.hi; ++g) {
+            for (int32_t g = P.lo; g <= P.hi; ++g) {
                 if (cont && g <= prev_hi) continue;
-                const int s = (int)(g % NSLOT);
+                const int s = (int)((uint32_t)g % NSLOT);
                 TRACE2(21, g);
                 // fill n of slot s waits for release n - 1 (parity of n - 1 = complement of n's)
                 if ((used >> s) & 1u) mbar_wait(bar(bars, B_KVEMPTY + s), ((par >> s) & 1u) ^ 1u);
@@ -265,8 +267,8 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 par ^= 1u << s;
                 const uint32_t fb = bar(bars, B_KVFULL + s);
                 const uint32_t dK = sbase + OFF_KV + (uint32_t)s * 2 * CBYTES, dV = dK + CBYTES;
-                const int64_t tok0 = P.c + g * KC * r;                       // first row's token
-                const int64_t tokL = P.c + imin(g * KC + KC - 1, P.Nc - 1) * r; // last in-range row
+                const int64_t tok0 = P.c + (int64_t)g * KC * r;                     // first row's token
+                const int64_t tokL = P.c + (int64_t)min(g * KC + KC - 1, P.Nc - 1) * r; // last in-range row
                 const bool local = p.k_peer == nullptr || (tok0 >= p.kv_begin && tokL < p.kv_begin + p.kv_rows);
                 if (local) {
                     if (elect_one()) {
@@ -280,10 +282,10 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {
                         const int row = lane + 32 * half;
-                        const int64_t kr = g * KC + row;
+                        const int32_t kr = g * KC + row;
                         if (kr < P.Nc) {
                             const char *kp, *vp;
-                            kv_row(p, P.c + kr * r, row_bytes, kp, vp);
+                            kv_row(p, P.c + (int64_t)kr * r, row_bytes, kp, vp);
 #pragma unroll
                             for (int cc = 0; cc < RB / 16; ++cc) {
                                 cp_async16(dK + swz<D>(row, cc), kp + hoff + cc * 16);
@@ -324,25 +326,25 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         const uint64_t dbase = sdesc_sw128(0);
         uint32_t seen = 0;      // parity of the fills waited for, bit per slot
         int nq[2] = {0, 0};     // Q tiles waited per warpgroup
-        int64_t cw[2] = {0, 0}; // running chunk counters per warpgroup (S/P/O buffer parity)
+        uint32_t cw[2] = {0, 0}; // running chunk counters per warpgroup (S/P/O buffer parity)
         int pre[2] = {0, 0};    // S MMAs of this item's tile already issued (end of the previous item)
         bool preq[2] = {false, false};
-        int64_t prev_stream = -1, prev_u = -1, prev_hi = -1;
+        int32_t prev_stream = -1, prev_u = -1, prev_hi = -1;
         Pair N = pair_geo(tp, it_begin);
-        for (int64_t it = it_begin; it < it_end; ++it) {
+        for (int32_t it = it_begin; it < it_end; ++it) {
             const Pair P = N;
             const bool has_next = it + 1 < it_end;
             if (has_next) N = pair_geo(tp, it + 1);
             if (!P.any) continue;
             const bool cont = P.stream == prev_stream && P.u == prev_u + 1;
             const bool next_cont = has_next && N.any && N.stream == P.stream && N.u == P.u + 1;
-            const int64_t keep_from = next_cont ? N.lo : INT64_MAX;
+            const int32_t keep_from = next_cont ? N.lo : INT32_MAX;
             uint32_t readers = 0, ready = 0; // 4 bits per chunk g - lo; 1 bit per chunk
 #pragma unroll
             for (int w = 0; w < 2; ++w)
-                for (int64_t j = 0; j < P.n[w]; ++j) readers += 1u << (4 * (int)(P.F[w] + j - P.lo));
+                for (int32_t j = 0; j < P.n[w]; ++j) readers += 1u << (4 * (P.F[w] + j - P.lo));
             if (cont)
-                for (int64_t g = P.lo; g <= P.hi && g <= prev_hi; ++g) ready |= 1u << (int)(g - P.lo);
+                for (int32_t g = P.lo; g <= P.hi && g <= prev_hi; ++g) ready |= 1u << (g - P.lo);
             int qb[2] = {0, 0};
 #pragma unroll
             for (int w = 0; w < 2; ++w) {
@@ -356,19 +358,19 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 }
             }
             fence_after();
-            auto chunk_ready = [&](int64_t g) {
+            auto chunk_ready = [&](int32_t g) {
                 const int gi = (int)(g - P.lo);
                 if ((ready >> gi) & 1u) return;
-                const int sl = (int)(g % NSLOT);
+                const int sl = (int)((uint32_t)g % NSLOT);
                 mbar_wait(bar(bars, B_KVFULL + sl), (seen >> sl) & 1u);
                 seen ^= 1u << sl;
                 ready |= 1u << gi;
                 TRACE2(1, g);
                 fence_after();
             };
-            auto issue_S = [&](int w, int64_t c, int64_t g, int qbuf) {
+            auto issue_S = [&](int w, uint32_t c, int32_t g, int qbuf) {
                 const uint32_t aq = sbase + OFF_Q + (uint32_t)(2 * w + qbuf) * QBYTES;
-                const uint32_t ak = sbase + OFF_KV + (uint32_t)(g % NSLOT) * 2 * CBYTES;
+                const uint32_t ak = sbase + OFF_KV + ((uint32_t)g % NSLOT) * 2 * CBYTES;
                 const uint32_t sb = (uint32_t)(c % NSB);
                 const uint32_t dS = tmem + 256u * w + COL_S + sb * KC;
                 if (elect_one()) {
@@ -380,13 +382,14 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 __syncwarp();
                 TRACE2(6 + w, g);
             };
-            auto issue_PV = [&](int w, int64_t j) {
-                const int64_t c = cw[w] + j, g = P.F[w] + j;
+            auto issue_PV = [&](int w, int32_t j) {
+                const uint32_t c = cw[w] + (uint32_t)j;
+                const int32_t g = P.F[w] + j;
                 const uint32_t sb = (uint32_t)(c % NSB);
                 mbar_wait(bar(bars, B_PFULL + NSB * w + (int)sb), (uint32_t)((c / NSB) & 1));
                 TRACE2(3 + w, g);
                 fence_after();
-                const int gi = (int)(g - P.lo), sl = (int)(g % NSLOT);
+                const int gi = (int)(g - P.lo), sl = (int)((uint32_t)g % NSLOT);
                 const uint32_t av = sbase + OFF_KV + (uint32_t)sl * 2 * CBYTES + CBYTES;
                 const uint32_t tP = tmem + 256u * w + COL_S + sb * KC;
                 readers -= 1u << (4 * gi);
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < KC / 16; ++kk) // 16 keys per MMA: 8 P columns, 16 V rows
-                        mma_ts(tmem + 256u * w + COL_O, tP + kk * 8, dbase | ((av + kk * 16 * RB) >> 4), idO,
+                        mma_ts(tmem + 256u * w + COL_O + (uint32_t)qb[w] * D, tP + kk * 8, dbase | ((av + kk * 16 * RB) >> 4), idO,
                                (j > 0 || kk > 0));
                     mma_commit(bar(bars, B_OFULL + 2 * w + (int)(c & 1)));
                     if (release) mma_commit(bar(bars, B_KVEMPTY + sl));
@@ -408,15 +411,15 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             // in order, so the P V has read P before the next S overwrites it)
 #pragma unroll
             for (int w = 0; w < 2; ++w)
-                for (int64_t j = pre[w]; j < NSB && j < P.n[w]; ++j) {
+                for (int32_t j = pre[w]; j < NSB && j < P.n[w]; ++j) {
                     chunk_ready(P.F[w] + j);
                     issue_S(w, cw[w] + j, P.F[w] + j, qb[w]);
                 }
             int npre[2] = {0, 0};
             bool nqw[2] = {false, false};
             auto prefetch = [&](int w, bool block) { // next tile's first S MMAs (resident chunks)
-                for (int64_t jn = 0; jn < NSB && jn < N.n[w]; ++jn) {
-                    const int64_t g = N.F[w] + jn;
+                for (int32_t jn = 0; jn < NSB && jn < N.n[w]; ++jn) {
+                    const int32_t g = N.F[w] + jn;
                     if (g > P.hi || !((ready >> (int)(g - P.lo)) & 1u)) break;
                     if (!nqw[w]) {
                         const uint32_t qf = bar(bars, B_QFULL + 2 * w + (nq[w] & 1));
@@ -431,15 +434,15 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     ++npre[w];
                 }
             };
-            const int64_t jmax = imax(P.n[0], P.n[1]);
-            for (int64_t j = 0; j < jmax; ++j) {
+            const int32_t jmax = max(P.n[0], P.n[1]);
+            for (int32_t j = 0; j < jmax; ++j) {
 #pragma unroll
                 for (int w = 0; w < 2; ++w) {
                     if (j >= P.n[w]) continue;
                     issue_PV(w, j);
                     if (j + NSB < P.n[w]) {
 #ifdef GA_WTC_WAR_TEST
-                        { const int64_t cc = cw[w] + j; mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(cc & 1)), (uint32_t)((cc >> 1) & 1)); fence_after(); }
+                        { const uint32_t cc = cw[w] + j; mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(cc & 1)), (uint32_t)((cc >> 1) & 1)); fence_after(); }
 #endif
                         chunk_ready(P.F[w] + j + NSB);
                         issue_S(w, cw[w] + j + NSB, P.F[w] + j + NSB, qb[w]);
@@ -463,6 +466,9 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         }
     } else {
         // ============================ softmax warpgroups ============================
+        // A tile's epilogue (O from TMEM, normalise, store) is deferred to the first chunk of the
+        // warpgroup's next tile: O is double-buffered in TMEM (tile k accumulates in O[k & 1]), so
+        // the softmax never waits for the last P V of a tile.
         const int w = warp >> 2, q = warp & 3;
         const uint32_t tl = tmem + 256u * w + ((uint32_t)(q * 32) << 16); // this warp's TMEM lanes
         const float sl2 = p.scale_log2;
@@ -472,12 +478,82 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(c & 1)), (c >> 1) & 1);
             fence_after();
         };
-        uint32_t ntile = 0; // tiles of this warpgroup (Q / O staging buffer = ntile & 1)
+        uint32_t ntile = 0; // tiles of this warpgroup (Q / O staging buffer and O buffer = index & 1)
+        // deferred epilogue of the previous tile
+        bool pend_epi = false, pend_rel = false;
+        int32_t p_it = 0; // previous tile's item (its geometry is recomputed: fewer live registers)
+        float l_prev = 0.f;
+        uint32_t cnt_prev = 0, tix_prev = 0;
+        auto release = [&]() { // the previous tile's O store has read its Q buffer: hand it back
+            if (lane == 0) {
+                tma::store_wait_read();
+                mbar_arrive(bar(bars, B_QEMPTY + 2 * w + (int)(tix_prev & 1)));
+            }
+            __syncwarp();
+            pend_rel = false;
+        };
+        auto epilogue = [&]() {
+            pend_epi = false;
+            // P V of the tile's last chunk completed.  The O barriers alternate per chunk and a
+            // parity wait is exact only if the barrier's previous phase completed: P V(e-2)'s
+            // predecessor P V(e-4) ran before S(e-1) (observed), and P V(e-2) completing implies
+            // P V(e-3), the predecessor of P V(e-1)
+            if (cnt_prev >= 2) wait_O(cnt_prev - 2);
+            wait_O(cnt_prev - 1);
+            TRACE2(18 + w, 0);
+            const uint32_t tO = tl + COL_O + (tix_prev & 1) * D;
+            const float inv = l_prev > 0.f ? 1.f / l_prev : 0.f;
+            const Tile Tq = tile_geo(tp, p_it, w);
+            const int32_t p_c = Tq.c, p_h = Tq.h, p_a0 = Tq.a0, p_alo = Tq.a_lo, p_ahi = Tq.a_hi;
+            const int32_t xr0 = p_a0 + 32 * q, x = xr0 + lane;
+            const bool cut = !(p_a0 >= p_alo && p_a0 + ROWS <= p_ahi);
+            // full tile: stage this warp's 32 rows in the tile's Q buffer (the tile's S MMAs
+            // completed) in the TMA layout and store them with one 32-row box, released to the
+            // loader later; tile cut by the query range / sequence end: plain stores of valid rows
+            const uint32_t sO = sbase + OFF_Q + (uint32_t)(2 * w + (tix_prev & 1)) * QBYTES;
+            char *orow = nullptr;
+            if (cut && x >= p_alo && x < p_ahi)
+                orow = reinterpret_cast<char *>(p.out) + (size_t)((int64_t)p_c + (int64_t)x * r - p.q_begin) * row_bytes +
+                       (size_t)p_h * D * sizeof(T);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) { // 32 columns at a time (register pressure)
+                float o[32];
+                tmem_ld32(tO + 32 * half, o);
+                tmem_wait_ld();
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                    float r8[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) r8[e] = o[8 * qq + e] * inv;
+                    const uint4 v = pack<T>(r8);
+                    if (!cut)
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sO + swz<D>(32 * q + lane, 4 * half + qq)),
+                                     "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                                     : "memory");
+                    else if (orow)
+                        stg16(orow + (4 * half + qq) * 16, v);
+                }
+            }
+            if (cut) {
+                if (lane == 0) mbar_arrive(bar(bars, B_QEMPTY + 2 * w + (int)(tix_prev & 1)));
+                __syncwarp();
+                return;
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                const int tok = (int)((int64_t)p_c + (int64_t)xr0 * r - p.q_begin);
+                tma::store_3d(&tp.tmO, 0, p_h, tok, sO + (uint32_t)q * (32 * RB));
+                tma::store_commit();
+            }
+            pend_rel = true;
+        };
         const int32_t mi = (int32_t)m;
-        for (int64_t it = it_begin; it < it_end; ++it) {
+        for (int32_t it = it_begin; it < it_end; ++it) {
             const Tile Tt = tile_geo(tp, it, w);
             if (!Tt.valid) continue;
             const int32_t xr0 = Tt.a0 + 32 * q, x = xr0 + lane;
+            const uint32_t tO = tl + COL_O + (ntile & 1) * D; // this tile's O accumulator
             // keys of this warp's rows: union [ulo, uhi], every row: [ilo, ihi]; this row: [klo, khi]
             const int32_t ulo = max(xr0 - mi, 0), uhi = min(xr0 + 31 + mi, Tt.Nc - 1);
             const int32_t ilo = max(xr0 + 31 - mi, 0), ihi = min(xr0 + mi, Tt.Nc - 1);
@@ -500,138 +576,102 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     for (int i = 0; i < 32; ++i) z[i] = 0u;
                     tmem_st32(tS, z);
                     tmem_wait_st();
+                    if (pend_epi) epilogue(); // see below
                     fence_before();
                     mbar_arrive(bar(bars, B_PFULL + NSB * w + (int)sb));
-                    continue;
-                }
-                float sv[KC];
-                tmem_ld32(tS, sv);
-                tmem_ld32(tS + 32, sv + 32);
-                tmem_wait_ld();
-                if (!(kmin >= ilo && kmin + KC - 1 <= ihi)) { // partial: keep only this row's band
-                    const int il = max(klo - kmin, -1), ih = min(khi - kmin, KC);
-                    if (__any_sync(0xffffffffu, il > 0)) { // left edge of the band inside the chunk
+                } else {
+                    float sv[KC];
+                    tmem_ld32(tS, sv);
+                    tmem_ld32(tS + 32, sv + 32);
+                    tmem_wait_ld();
+                    if (!(kmin >= ilo && kmin + KC - 1 <= ihi)) { // partial: keep only this row's band
+                        const int il = max(klo - kmin, -1), ih = min(khi - kmin, KC);
+                        if (__any_sync(0xffffffffu, il > 0)) { // left edge of the band inside the chunk
 #pragma unroll
-                        for (int i = 0; i < KC; ++i) sv[i] = i >= il ? sv[i] : -INFINITY;
+                            for (int i = 0; i < KC; ++i) sv[i] = i >= il ? sv[i] : -INFINITY;
+                        }
+                        if (__any_sync(0xffffffffu, ih < KC - 1)) { // right edge
+#pragma unroll
+                            for (int i = 0; i < KC; ++i) sv[i] = i <= ih ? sv[i] : -INFINITY;
+                        }
                     }
-                    if (__any_sync(0xffffffffu, ih < KC - 1)) { // right edge
+                    float lmx[8];
 #pragma unroll
-                        for (int i = 0; i < KC; ++i) sv[i] = i <= ih ? sv[i] : -INFINITY;
+                    for (int i = 0; i < 8; ++i) lmx[i] = sv[i];
+#pragma unroll
+                    for (int i = 8; i < KC; ++i) lmx[i & 7] = fmaxf(lmx[i & 7], sv[i]);
+                    const float lm = fmaxf(fmaxf(fmaxf(lmx[0], lmx[1]), fmaxf(lmx[2], lmx[3])),
+                                           fmaxf(fmaxf(lmx[4], lmx[5]), fmaxf(lmx[6], lmx[7])));
+                    // lazy rescale: a row moves its reference max only when the chunk's max exceeds
+                    // it by more than kTau (weights stay <= 2^kTau); O needs rescaling only for rows
+                    // that already hold weight (a row with m = -inf has O = 0 and l = 0)
+                    const float lm2 = lm * sl2;
+                    const bool need = lm2 > m_run + kTau;
+                    const float a = (need && m_run != -INFINITY) ? ex2(m_run - lm2) : 1.f;
+                    if (__any_sync(0xffffffffu, a != 1.f) && j > 0) {
+                        wait_O(c - 1); // O stable: P V of the previous chunk completed
+                        float ov[32];
+#pragma unroll
+                        for (int qq = 0; qq < D / 32; ++qq) {
+                            tmem_ld32(tO + 32 * qq, ov);
+                            tmem_wait_ld();
+                            uint32_t ob[32];
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(ov[i] * a);
+                            tmem_st32(tO + 32 * qq, ob);
+                        }
+                        tmem_wait_st();
                     }
-                }
-                float lmx[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) lmx[i] = sv[i];
-#pragma unroll
-                for (int i = 8; i < KC; ++i) lmx[i & 7] = fmaxf(lmx[i & 7], sv[i]);
-                const float lm = fmaxf(fmaxf(fmaxf(lmx[0], lmx[1]), fmaxf(lmx[2], lmx[3])),
-                                       fmaxf(fmaxf(lmx[4], lmx[5]), fmaxf(lmx[6], lmx[7])));
-                // lazy rescale: a row moves its reference max only when the chunk's max exceeds
-                // it by more than kTau (weights stay <= 2^kTau); O needs rescaling only for rows
-                // that already hold weight (a row with m = -inf has O = 0 and l = 0)
-                const float lm2 = lm * sl2;
-                const bool need = lm2 > m_run + kTau;
-                const float a = (need && m_run != -INFINITY) ? ex2(m_run - lm2) : 1.f;
-                if (__any_sync(0xffffffffu, a != 1.f) && j > 0) {
-                    wait_O(c - 1); // O stable: P V of the previous chunk completed
-                    float ov[32];
-#pragma unroll
-                    for (int qq = 0; qq < D / 32; ++qq) {
-                        tmem_ld32(tl + COL_O + 32 * qq, ov);
-                        tmem_wait_ld();
-                        uint32_t ob[32];
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(ov[i] * a);
-                        tmem_st32(tl + COL_O + 32 * qq, ob);
+                    if (need) {
+                        l_run *= a;
+                        m_run = lm2;
                     }
+                    const float m_use = m_run == -INFINITY ? 0.f : m_run;
+                    uint32_t pk[KC / 2];
+                    float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; // packed partial sums
+#pragma unroll
+                    for (int i = 0; i < KC / 2; ++i) {
+                        float x0 = sv[2 * i], x1 = sv[2 * i + 1];
+                        ffma2_sm(x0, x1, sl2, -m_use);
+                        x0 = ex2(x0);
+                        x1 = ex2(x1);
+                        fadd2_acc(ls[i & 1], x0, x1);
+                        pk[i] = pack2<T>(x0, x1);
+                    }
+                    l_run += (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
+                    tmem_st32(tS, pk);
                     tmem_wait_st();
+                    // the previous tile's epilogue with this tile's first chunk (its last P V has
+                    // long completed), BEFORE P of this chunk is released: P V of this chunk could
+                    // otherwise complete a second phase of the O barrier the epilogue waits on
+                    if (pend_epi) epilogue();
+                    fence_before();
+                    mbar_arrive(bar(bars, B_PFULL + NSB * w + (int)sb));
+                    TRACE(14 + w);
                 }
-                if (need) {
-                    l_run *= a;
-                    m_run = lm2;
-                }
-                const float m_use = m_run == -INFINITY ? 0.f : m_run;
-                uint32_t pk[KC / 2];
-                float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; // packed partial sums
-#pragma unroll
-                for (int i = 0; i < KC / 2; ++i) {
-                    float x0 = sv[2 * i], x1 = sv[2 * i + 1];
-                    ffma2_sm(x0, x1, sl2, -m_use);
-                    x0 = ex2(x0);
-                    x1 = ex2(x1);
-                    fadd2_acc(ls[i & 1], x0, x1);
-                    pk[i] = pack2<T>(x0, x1);
-                }
-                l_run += (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
-                tmem_st32(tS, pk);
-                tmem_wait_st();
-                fence_before();
-                mbar_arrive(bar(bars, B_PFULL + NSB * w + (int)sb));
-                TRACE(14 + w);
+                // the staging buffer goes back to the loader one chunk after the store
+                if (pend_rel && j > 0) release();
             }
-            cnt += n;
-            // ---- epilogue: O row from TMEM, normalise, store
-            TRACE2(16 + w, 0);
-            // O final after P V of the tile's last chunk.  The O barriers alternate per chunk and
-            // a parity wait is exact only if the barrier's previous phase completed: P V(cnt-2)'s
-            // predecessor P V(cnt-4) ran before S(cnt-1) (observed), and P V(cnt-2) completing
-            // implies P V(cnt-3), the predecessor of P V(cnt-1)
-            if (cnt >= 2) wait_O(cnt - 2);
-            wait_O(cnt - 1);
-            TRACE2(18 + w, 0);
-            float o[D];
-            tmem_ld32(tl + COL_O, o);
-            tmem_ld32(tl + COL_O + 32, o + 32);
-            tmem_wait_ld();
-            // stage the normalised rows in this tile's Q buffer (its last reader, the last S MMA,
-            // completed before the last P V) in the TMA layout, then one thread stores the tile
-            // with two 64-row TMA boxes (rows outside the query range / sequence are clipped by
-            // the tensor map) and releases the buffer to the loader
-            const bool full_tile = Tt.a0 >= Tt.a_lo && Tt.a0 + ROWS <= Tt.a_hi;
-            if (!full_tile) { // tile cut by the query range / sequence end: plain stores of valid rows
-                if (x >= Tt.a_lo && x < Tt.a_hi) {
-                    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-                    const int64_t i = (int64_t)Tt.c + (int64_t)x * r;
-                    char *orow = reinterpret_cast<char *>(p.out) + (size_t)(i - p.q_begin) * row_bytes +
-                                 (size_t)Tt.h * D * sizeof(T);
-#pragma unroll
-                    for (int qq = 0; qq < D / 8; ++qq) {
-                        float r8[8];
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) r8[e] = o[8 * qq + e] * inv;
-                        stg16(orow + qq * 16, pack<T>(r8));
-                    }
-                }
-                asm volatile("bar.sync %0, 128;" ::"r"(1 + w) : "memory");
-                if (q == 0 && lane == 0) mbar_arrive(bar(bars, B_QEMPTY + 2 * w + (int)(ntile & 1)));
-                ++ntile;
-                continue;
-            }
-            const uint32_t sO = sbase + OFF_Q + (uint32_t)(2 * w + (ntile & 1)) * QBYTES;
-            const int xl = 32 * q + lane;
-            const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-#pragma unroll
-            for (int qq = 0; qq < D / 8; ++qq) {
-                float r8[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) r8[e] = o[8 * qq + e] * inv;
-                const uint4 v = pack<T>(r8);
-                asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sO + swz<D>(xl, qq)), "r"(v.x), "r"(v.y),
-                             "r"(v.z), "r"(v.w)
-                             : "memory");
-            }
-            fence_proxy_async();
-            asm volatile("bar.sync %0, 128;" ::"r"(1 + w) : "memory"); // the warpgroup's 128 rows staged
-            if (q == 0 && lane == 0) {
-                const int tok = (int)((int64_t)Tt.c + (int64_t)Tt.a0 * r - p.q_begin);
-                tma::store_3d(&tp.tmO, 0, Tt.h, tok, sO);
-                tma::store_3d(&tp.tmO, 0, Tt.h, tok + 64 * (int)r, sO + QBYTES / 2);
-                tma::store_commit();
-                tma::store_wait_read();
-                mbar_arrive(bar(bars, B_QEMPTY + 2 * w + (int)(ntile & 1)));
-            }
+            if (pend_epi) epilogue(); // (n >= 1: not reached)
+            if (pend_rel) release();  // one-chunk tile
+            cnt += (uint32_t)n;
+            pend_epi = true;
+            p_it = it;
+            l_prev = l_run;
+            cnt_prev = cnt;
+            tix_prev = ntile;
             ++ntile;
+#ifndef GA_WTC_DEFER_EPILOGUE
+            // epilogue right away (measured faster than deferring it into the next tile, which
+            // needs more registers); O is still double-buffered, so the next tile's first P V
+            // never waits for these TMEM reads
+            epilogue();
+#endif
         }
+        if (pend_epi) epilogue();
+        if (pend_rel) release();
+        if (lane == 0) tma::store_wait_all(); // bulk stores complete before the CTA exits
+        __syncwarp();
     }
     fence_before();
     __syncthreads();
@@ -718,7 +758,7 @@ ga_status launch_window_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s)
     tp.items = pps * r * p.H;
     if (tp.items == 0) return GA_OK;
     if (!tma::encode_rows(&tp.tmQ, p.Q, p.q_rows, p.H, p.d, (int)r, 64) ||
-        !tma::encode_rows(&tp.tmO, p.out, p.q_rows, p.H, p.d, (int)r, 64) ||
+        !tma::encode_rows(&tp.tmO, p.out, p.q_rows, p.H, p.d, (int)r, 32) ||
         !tma::encode_rows(&tp.tmK, p.K, p.kv_rows, p.H, p.d, (int)r, 64) ||
         !tma::encode_rows(&tp.tmV, p.V, p.kv_rows, p.H, p.d, (int)r, 64)) {
         set_error("tcgen05 window kernel: tensor-map encoding failed");
