@@ -29,7 +29,8 @@ def launches(path):
 
 
 def ours(name):
-    return any(s in name for s in ("ga::", "lnet", "band_kernel", "edge_kernel", "heavy_", "longnet", "scan_"))
+    return any(s in name for s in ("ga::", "lnet", "band_kernel", "edge_kernel", "heavy_", "longnet", "scan_",
+                                   "window_tc", "csr_mma", "full_rows", "full_merge"))
 
 
 def main():
