@@ -237,14 +237,17 @@ static ga_status dispatch(AttnParams &p, ga_dtype dtype, const ga_opts *opts, in
     }
     if (p.mask.kind == GA_MASK_CSR) {
         const bool split = opts && opts->workspace && opts->workspace_bytes > 0;
+        // bf16/fp16: per-edge products on mma.sync (csr_mma.cu); fp32 and probes: edge kernel
+        const bool mma = !probe && (kernel == GA_KERNEL_AUTO || kernel == GA_KERNEL_TILED) && csr_mma_supported(p, dtype);
+        if (kernel == GA_KERNEL_TC) { set_error("no tcgen05 kernel for explicit CSR masks"); return GA_ERR_UNSUPPORTED; }
         if (split) {
             if (probe) { set_error("probes are not supported with the heavy-row split"); return GA_ERR_UNSUPPORTED; }
             p.heavy_threshold = heavy;
-            st = launch_edge(p, dtype, s); // light rows
+            st = mma ? launch_csr_mma(p, dtype, s) : launch_edge(p, dtype, s); // light rows
             if (st != GA_OK) return st;
             return launch_csr_heavy(p, dtype, opts->workspace, opts->workspace_bytes, s);
         }
-        return launch_edge(p, dtype, s);
+        return mma ? launch_csr_mma(p, dtype, s) : launch_edge(p, dtype, s);
     }
     if (!probe && (kernel == GA_KERNEL_TC || kernel == GA_KERNEL_AUTO) && window_tc_supported(p, dtype))
         return launch_window_tc(p, dtype, s);
@@ -293,7 +296,7 @@ ga_status ga_workspace_size(const ga_mask *mask, int64_t L, int32_t d, int32_t h
     }
     if (M.kind != GA_MASK_CSR) return GA_OK;
     int64_t C = opts && opts->heavy_threshold > 0 ? opts->heavy_threshold : kDefaultHeavy;
-    *bytes = csr_heavy_workspace(q_rows, mask->nnz, heads, d, C);
+    *bytes = csr_heavy_workspace(q_rows, L, mask->nnz, heads, d, C);
     return GA_OK;
 }
 

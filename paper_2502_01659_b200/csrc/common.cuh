@@ -217,7 +217,9 @@ __device__ __forceinline__ void kv_row(const AttnParams &p, int64_t j, size_t ro
 // launchers (defined in the kernel translation units)
 ga_status launch_edge(const AttnParams &p, ga_dtype dt, cudaStream_t s);
 ga_status launch_csr_heavy(const AttnParams &p, ga_dtype dt, void *ws, size_t ws_bytes, cudaStream_t s);
-size_t csr_heavy_workspace(int64_t L, int64_t nnz, int32_t H, int32_t d, int64_t C);
+bool csr_mma_supported(const AttnParams &p, ga_dtype dt);
+ga_status launch_csr_mma(const AttnParams &p, ga_dtype dt, cudaStream_t s);
+size_t csr_heavy_workspace(int64_t rows, int64_t Lmask, int64_t nnz, int32_t H, int32_t d, int64_t C);
 bool window_tiled_supported(const AttnParams &p, ga_dtype dt);
 int64_t band_tile_rows(); // class rows per band-kernel tile
 int64_t window_tc_tile_rows(); // class rows per tcgen05 window-kernel tile

@@ -38,6 +38,7 @@ struct Key {
 };
 
 static bool encode_uncached(CUtensorMap *map, const void *base, int64_t ntok, int H, int D, int r, int box_rows);
+static bool encode_gather_uncached(CUtensorMap *map, const void *base, int64_t ntok, int H, int D);
 
 // Encoding is host work on every launch; a small cache keyed by (buffer, shape, stride,
 // box) serves the repeated launches of a training / serving loop.
@@ -53,7 +54,8 @@ bool encode_rows(CUtensorMap *map, const void *base, int64_t ntok, int H, int D,
         for (int i = 0; i < n; ++i)
             if (keys[i] == k) { *map = maps[i]; return true; }
     }
-    if (!encode_uncached(map, base, ntok, H, D, r, box_rows)) return false;
+    if (!(r == 0 ? encode_gather_uncached(map, base, ntok, H, D) : encode_uncached(map, base, ntok, H, D, r, box_rows)))
+        return false;
     std::lock_guard<std::mutex> g(mu);
     keys[next] = k;
     maps[next] = *map;
@@ -79,6 +81,36 @@ static bool encode_uncached(CUtensorMap *map, const void *base, int64_t ntok, in
                            rb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return e == CUDA_SUCCESS;
+}
+
+} // namespace tma
+} // namespace ga
+
+namespace ga {
+namespace tma {
+
+// 2D view {H*D elements, ntok rows} with a {D, 1} box (one (token, head) row): the box of a
+// tile::gather4 load, which fetches 4 such rows at arbitrary token coordinates
+static bool encode_gather_uncached(CUtensorMap *map, const void *base, int64_t ntok, int H, int D)
+{
+    const int rb = D * 2;
+    if (rb != 128 || ntok <= 0 || ntok >= (int64_t)1 << 31) return false;
+    if ((reinterpret_cast<uintptr_t>(base) & 15u) != 0) return false;
+    EncodeTiled enc = encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)H * D, (cuuint64_t)ntok};
+    const cuuint64_t strides[1] = {(cuuint64_t)H * rb};
+    const cuuint32_t box[2] = {(cuuint32_t)D, 1u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult e = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void *>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return e == CUDA_SUCCESS;
+}
+
+bool encode_gather(CUtensorMap *map, const void *base, int64_t ntok, int H, int D)
+{
+    return encode_rows(map, base, ntok, H, D, 0, 0);
 }
 
 } // namespace tma

@@ -18,6 +18,20 @@ namespace tma {
 // r <= 8, D * 2 in {64, 128}).  Returns false if TMA cannot express it.
 bool encode_rows(CUtensorMap *map, const void *base, int64_t ntok, int H, int D, int r, int box_rows);
 
+// Host: 2D map {H*D, ntok} of a [ntok, H, D] 16-bit tensor with a one-row {D, 1} box,
+// 128B-swizzled (D = 64 only), for tile::gather4 loads of 4 arbitrary token rows of a head.
+bool encode_gather(CUtensorMap *map, const void *base, int64_t ntok, int H, int D);
+
+// 4 rows (tokens y0..y3, elements [x, x + D)) -> 4 consecutive 128-byte rows of shared memory
+__device__ __forceinline__ void gather4(uint32_t smem, const CUtensorMap *map, int x, int y0, int y1, int y2, int y3,
+                                        uint32_t mbar)
+{
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, "
+                 "{%2, %3, %4, %5, %6}], [%7];" ::"r"(smem),
+                 "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y0), "r"(y1), "r"(y2), "r"(y3), "r"(mbar)
+                 : "memory");
+}
+
 __device__ __forceinline__ void expect_tx(uint32_t mbar, uint32_t bytes)
 {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(mbar),

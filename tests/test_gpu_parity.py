@@ -256,6 +256,50 @@ def test_empty_rows_and_ragged_csr(ga, orc):
     assert np.abs(got - want).max() <= 1e-4
 
 
+@pytest.mark.parametrize("variant", ["", "GA_CSR_CPASYNC", "GA_CSR_LDG"])
+@pytest.mark.parametrize("dt", ["bf16", "f16"])
+@pytest.mark.parametrize("d", [32, 64, 128])
+def test_csr_mma_ragged_degrees(ga, orc, dt, d, variant, monkeypatch):
+    """Explicit CSR on the mma.sync path (csr_mma.cu; d = 64 staged by TMA gather4, or the
+    cp.async ring / direct loads when the variant flag is set): degrees 0, 1, 15, 16, 17,
+    31..33, 47, 48, 200 and a full row cover every 16-edge block tail, the stage ring and the
+    index ring; random sorted columns; centred inputs.  Same bar for the edge kernel."""
+    if variant:
+        monkeypatch.setenv(variant, "1")
+    L, H = 700, 2
+    rng = np.random.default_rng(d + (0 if dt == "bf16" else 1))
+    pattern = [0, 1, 15, 16, 17, 31, 32, 33, 47, 48, 200, 5, 64, 65, 700]
+    deg = np.array([pattern[i % len(pattern)] for i in range(L)])
+    rows = [np.sort(rng.choice(L, k, replace=False)) for k in deg]
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    ci = np.concatenate(rows).astype(np.int32)
+    cpu, f64 = _inputs(L, H, d, dt, 21 + d, centred=True)
+    want, _ = orc.attention(*f64, orc.csr(L, rp, ci))
+    m = ga.CSR(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+    for kernel in ("auto", "edge"):
+        got = _run(ga, cpu, m, kernel=kernel)
+        assert np.all(got[deg == 0] == 0), kernel
+        err = np.abs(got - want).max()
+        assert err <= TOL[dt], (kernel, err)
+
+
+def test_csr_mma_large_scores_rescale(ga, orc):
+    """Scores spanning many 2^8 rescale thresholds (queries scaled x40) on the mma CSR path."""
+    L, H, d = 512, 1, 64
+    rng = np.random.default_rng(5)
+    deg = rng.integers(1, 300, L)
+    rows = [np.sort(rng.choice(L, k, replace=False)) for k in deg]
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    ci = np.concatenate(rows).astype(np.int32)
+    (q, k, v), _ = _inputs(L, H, d, "bf16", 99, centred=True)
+    q = (q.float() * 40).bfloat16()
+    f64 = tuple(synth.as_f64(x) for x in (q, k, v))
+    want, _ = orc.attention(*f64, orc.csr(L, rp, ci))
+    m = ga.CSR(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+    got = _run(ga, (q, k, v), m)
+    assert np.abs(got - want).max() <= 2e-2
+
+
 # ---------------------------------------------------------------- work optimality (T4)
 @pytest.mark.parametrize("fam,L,args", [("window", 2000, (100, 3)), ("longnet", 4096, (64, 2)),
                                         ("block", 1000, (50, 4))])
