@@ -63,7 +63,11 @@ typedef enum {
        dilated window (readings R1, R2). */
     GA_MASK_WINDOW = 1,
     /* LongNet exponentially dilated: OR over k = 0..K of BLOCK_DILATED(w0*alpha^k, alpha^k),
-       K = max{k : w0*alpha^k <= L} (reading R11). */
+       K = max{k : w0*alpha^k <= L} (reading R11).  With
+       parts = GA_LONGNET_MULTISET: the multiset union instead — an edge in n levels' blocks
+       counts n times in the softmax (LongNet's own mixture); runs on the
+       edge kernel; its CSR (ga_mask_to_csr) repeats such columns (not strictly increasing,
+       so ga_mask_validate rejects it, while every attention kernel accepts it). */
     GA_MASK_LONGNET = 2,
     /* BigBird / Longformer: window(w) UNION global rows and columns UNION n_random random
        columns per non-global row (readings R8-R10).  Materialise with
@@ -79,13 +83,16 @@ typedef enum {
    window (the paper's "global minus local" kernel), the random columns.  They
    are disjoint and their union is the BigBird mask; Longformer = WINDOW + GLOBAL. */
 typedef enum { GA_BB_WINDOW = 1, GA_BB_GLOBAL = 2, GA_BB_RANDOM = 4 } ga_bigbird_part;
+/* LONGNET variant (ga_mask.parts): LongNet's multiset mixture (reading R11b). */
+enum { GA_LONGNET_MULTISET = 1 };
 
 /* Mask descriptor: the paper's "attention-specific parameters P_a" or explicit graph G
    (Algorithm 1 input).  Unused fields are ignored; zero-initialise. */
 typedef struct ga_mask {
     int32_t kind;              /* ga_mask_kind                                          */
     int32_t parts;             /* BIGBIRD components to include (ga_bigbird_part bits; 0 =
-                                  all): disjoint, so separate calls compose */
+                                  all): disjoint, so separate calls compose.
+                                  LONGNET: 0 = set union, GA_LONGNET_MULTISET = multiset */
     int64_t L;                 /* number of graph nodes (global sequence length)         */
     const int64_t *row_ptr;    /* CSR: DEVICE int64 [L+1], row_ptr[0]=0, nondecreasing     */
     const int32_t *col_idx;    /* CSR: DEVICE int32 [nnz], sorted strictly per row        */
@@ -221,6 +228,20 @@ ga_status ga_mask_count(const ga_mask *pattern, int64_t *nnz_out);
    col_idx: DEVICE int32 [nnz] with nnz from ga_mask_count.  The result equals the CPU
    enumeration bit for bit.  Temporary scan storage is stream-ordered (cudaMallocAsync). */
 ga_status ga_mask_to_csr(const ga_mask *pattern, int64_t *row_ptr, int32_t *col_idx, void *stream);
+
+/* COO input ("COO" mask storage): convert an edge list
+   (rows[e], cols[e]), e < n, in any order, to binary CSR on the device.  Duplicates are
+   counted once (a 0-1 mask, reading R7).  Method: keys row*L + col -> radix sort (CUB) ->
+   unique -> col_idx = key mod L, row_ptr[r] = lower_bound(keys, r*L).  The paper's COO
+   kernel searches the list per row; here COO is converted once, never searched.
+   rows, cols: DEVICE int32 [n]; row_ptr: DEVICE int64 [L+1] (written); col_idx: DEVICE
+   int32, capacity n (the first *nnz_out entries written, ascending per row); nnz_out: HOST,
+   the number of distinct edges (the call synchronises `stream` to read it).  Scratch is
+   stream-ordered (cudaMallocAsync).  Errors: GA_ERR_INVALID_ARG (L <= 0 or L > 2^31-1,
+   n < 0, NULL buffers), GA_ERR_MASK (an index outside [0, L); outputs then undefined),
+   GA_ERR_CUDA. */
+ga_status ga_coo_to_csr(int64_t L, const int32_t *rows, const int32_t *cols, int64_t n, int64_t *row_ptr,
+                        int32_t *col_idx, int64_t *nnz_out, void *stream);
 
 /* O(L + nnz) validity check of an explicit CSR (S:97-98 invariants).  Synchronises the
    stream.  *ok = 1 when valid; returns GA_ERR_MASK (and *ok = 0) otherwise. */

@@ -144,8 +144,10 @@ def block_dilated(L, seg, r=1):
     return Mask(BLOCK_DILATED, L, seg=seg, r=r)
 
 
-def longnet(L, w0, alpha=2):
-    return Mask(LONGNET, L, w0=w0, alpha=alpha)
+def longnet(L, w0, alpha=2, multiset=False):
+    """LongNet (reading R11); multiset=True: LongNet's own mixture, the multiset union of the
+    levels' blocks (reading R11b)."""
+    return Mask(LONGNET, L, w0=w0, alpha=alpha, parts=1 if multiset else 0)
 
 
 BB_WINDOW, BB_GLOBAL, BB_RANDOM = 1, 2, 4  # BigBird components (disjoint; union = full mask)
@@ -160,6 +162,24 @@ def bigbird(L, w, n_global, n_random, seed, global_idx=None, r=1, parts=0):
 
 def csr(L, row_ptr, col_idx):
     return Mask(CSR, L, row_ptr=np.asarray(row_ptr, np.int64), col_idx=np.asarray(col_idx, np.int32))
+
+
+def coo_to_csr(L: int, rows, cols):
+    """COO edge list -> binary CSR by the plain definition (reading R7: a 0-1
+    mask, so a repeated (i, j) is one edge): N(i) = sorted {cols[e] : rows[e] = i}.
+    Pure-Python sets: small cases only.  Returns (row_ptr int64 [L+1], col_idx int32)."""
+    nbrs = [set() for _ in range(L)]
+    for i, j in zip(np.asarray(rows).tolist(), np.asarray(cols).tolist()):
+        if not (0 <= i < L and 0 <= j < L):
+            raise ValueError(f"edge ({i}, {j}) outside [0, {L})")
+        nbrs[i].add(j)
+    row_ptr = np.zeros(L + 1, dtype=np.int64)
+    col_idx = []
+    for i in range(L):
+        cs = sorted(nbrs[i])
+        col_idx.extend(cs)
+        row_ptr[i + 1] = row_ptr[i] + len(cs)
+    return row_ptr, np.asarray(col_idx, dtype=np.int32)
 
 
 def splitmix64(x: int) -> int:

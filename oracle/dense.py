@@ -65,3 +65,35 @@ def masked_attention(q, k, v, mask):
         o[empty] = 0.0
         out[:, h, :] = o
     return out
+
+
+def longnet_multiplicity(L, w0, alpha=2):
+    """LongNet's multiset mixture (reading R11b): C[i, j] = number of levels k whose
+    BlockDilated(w0 alpha^k, alpha^k) block contains (i, j)."""
+    K = 0
+    while w0 * alpha ** (K + 1) <= L:
+        K += 1
+    c = np.zeros((L, L), dtype=np.int64)
+    for k in range(K + 1):
+        c += block_dilated_mask(L, w0 * alpha ** k, alpha ** k)
+    return c
+
+
+def weighted_attention(q, k, v, mult):
+    """Softmax over a multiset of neighbours: O_i = sum_j C_ij e^{s_ij} v_j / sum_j C_ij e^{s_ij}
+    (C = multiplicities; C = 0 masks the pair; rows with no neighbour -> 0)."""
+    L, H, d = q.shape
+    out = np.zeros((L, H, d), dtype=np.float64)
+    for h in range(H):
+        s = (q[:, h, :] @ k[:, h, :].T) / np.sqrt(d)
+        s = np.where(mult > 0, s, -np.inf)
+        mx = s.max(axis=1, keepdims=True)
+        empty = ~np.isfinite(mx[:, 0])
+        mx = np.where(np.isfinite(mx), mx, 0.0)
+        p = mult * np.exp(s - mx)
+        z = p.sum(axis=1, keepdims=True)
+        z = np.where(z > 0, z, 1.0)
+        o = (p / z) @ v[:, h, :]
+        o[empty] = 0.0
+        out[:, h, :] = o
+    return out

@@ -27,7 +27,9 @@
  *   BLOCK_DILATED(seg,r) floor(i/seg)==floor(j/seg) and (i mod seg) mod r == 0 and
  *                        (j mod seg) mod r == 0                      (reading R3)
  *   LONGNET(w0,alpha)    OR over k = 0..K of BLOCK_DILATED(w0*alpha^k, alpha^k),
- *                        K = max{k : w0*alpha^k <= L}                (reading R11)
+ *                        K = max{k : w0*alpha^k <= L}                (reading R11);
+ *                        parts = 1: the multiset union (a pair in n levels' blocks listed n
+ *                        times, so it weighs n times in the softmax; reading R11b)
  *   BIGBIRD(w,G,nr,seed) global rows/cols UNION window(w) UNION random
  *                        columns drawn by the counter hash of reading R10.
  *                        The window may be dilated (r: |i-j| < w and |i-j| mod r == 0, as
@@ -265,6 +267,10 @@ int64_t orc_row_neighbors(const orc_mask *m, int64_t i, int64_t *out)
                     if ((j % seg) % r == 0) out[n++] = j;
             seg *= m->alpha;
             r *= m->alpha;
+        }
+        if (m->parts == 1) { /* multiset union (LongNet's mixture, reading R11b): keep repeats */
+            if (n > 1) qsort(out, (size_t)n, sizeof(int64_t), cmp_i64);
+            return n;
         }
         return sort_unique(out, n);
     }

@@ -17,6 +17,7 @@ GA_F32, GA_BF16, GA_F16 = 0, 1, 2
 GA_MASK_CSR, GA_MASK_WINDOW, GA_MASK_LONGNET, GA_MASK_BIGBIRD, GA_MASK_BLOCK_DILATED = 0, 1, 2, 3, 4
 GA_KERNEL_AUTO, GA_KERNEL_EDGE, GA_KERNEL_TILED, GA_KERNEL_TC = 0, 1, 2, 3
 GA_BB_WINDOW, GA_BB_GLOBAL, GA_BB_RANDOM = 1, 2, 4
+GA_LONGNET_MULTISET = 1
 
 STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_INVALID_ARG", -2: "GA_ERR_UNSUPPORTED", -3: "GA_ERR_CUDA",
                 -4: "GA_ERR_COMM", -5: "GA_ERR_OOM", -6: "GA_ERR_MASK"}
@@ -63,6 +64,7 @@ SIGNATURES = [
     ("ga_mask_count", ctypes.c_int, [_PM, ctypes.POINTER(_I64)]),
     ("ga_query_alignment", ctypes.c_int, [_PM, _I32, ctypes.c_int, ctypes.POINTER(_I64)]),
     ("ga_mask_to_csr", ctypes.c_int, [_PM, _V, _V, _V]),
+    ("ga_coo_to_csr", ctypes.c_int, [ctypes.c_int64, _V, _V, ctypes.c_int64, _V, _V, ctypes.POINTER(ctypes.c_int64), _V]),
     ("ga_mask_validate", ctypes.c_int, [_PM, _V, ctypes.POINTER(ctypes.c_int)]),
     ("ga_fill_inputs", ctypes.c_int, [_V, ctypes.c_int, _I64, _U64, _I32, _I64, _F, _V]),
     ("ga_state_finalize", ctypes.c_int, [ctypes.POINTER(GaState), _I64, _I32, _I32, ctypes.c_int, _V, _V]),

@@ -174,6 +174,23 @@ def mask_to_csr(mask: Mask, L: int, device="cuda") -> CSR:
     return CSR(row_ptr, col_idx[:nnz])
 
 
+def coo_to_csr(rows: torch.Tensor, cols: torch.Tensor, L: int) -> CSR:
+    """COO edge list (int32 CUDA tensors, any order, duplicates counted once) -> device CSR
+    (sort + unique on the GPU; PAPER.md:227 COO storage)."""
+    n = rows.numel()
+    if cols.numel() != n:
+        raise ValueError("rows and cols must have the same length")
+    rows = rows.to(torch.int32).contiguous()
+    cols = cols.to(torch.int32).contiguous()
+    row_ptr = torch.empty(L + 1, dtype=torch.int64, device=rows.device)
+    col_idx = torch.empty(max(n, 1), dtype=torch.int32, device=rows.device)
+    nnz = ctypes.c_int64()
+    _abi.check(_abi.lib().ga_coo_to_csr(int(L), rows.data_ptr() if n else None, cols.data_ptr() if n else None, n,
+                                        row_ptr.data_ptr(), col_idx.data_ptr(), ctypes.byref(nnz),
+                                        _stream(rows.device)))
+    return CSR(row_ptr, col_idx[:nnz.value])
+
+
 def mask_validate(mask: CSR, L: int) -> bool:
     cm = mask.to_c(L)
     ok = ctypes.c_int()

@@ -75,6 +75,11 @@ static ga_status make_devmask(const ga_mask *m, int64_t L, DevMask &M)
         return GA_OK;
     case GA_MASK_LONGNET:
         if (m->w0 < 1 || m->alpha < 2) { set_error("LongNet needs w0 >= 1 and alpha >= 2"); return GA_ERR_INVALID_ARG; }
+        if (m->parts != 0 && m->parts != GA_LONGNET_MULTISET) {
+            set_error("LongNet parts must be 0 (set union) or GA_LONGNET_MULTISET");
+            return GA_ERR_INVALID_ARG;
+        }
+        M.parts = m->parts;
         M.w0 = m->w0;
         M.alpha = m->alpha;
         M.K = longnet_levels(m->w0, m->alpha, L);
@@ -498,6 +503,10 @@ ga_status ga_mask_count(const ga_mask *pattern, int64_t *nnz_out)
             for (int64_t s0 = 0; s0 < L; s0 += segw) {
                 const int64_t s1 = imin(L, s0 + segw);
                 const int64_t U = multiples(s0, s1, stp);
+                if (M.parts == GA_LONGNET_MULTISET) { // every level's block counted: U x U
+                    n += U * U;
+                    continue;
+                }
                 const int64_t gt = t < M.K ? multiples(s0, s1, stp * M.alpha) : 0;
                 const int64_t rx = (M.alpha - (s0 / stp) % M.alpha) % M.alpha; // excluded residue
                 const int64_t keep = U - (U > rx ? (U - 1 - rx) / M.alpha + 1 : 0);

@@ -39,7 +39,8 @@ enum PieceMode { P_AFFINE = 0, P_SKIPMUL = 1, P_CSR = 2 };
 
 struct DevMask {
     int32_t kind;
-    int32_t parts;        // BigBird components: bit 0 window, 1 global minus window, 2 random (0 = all)
+    int32_t parts;        // BigBird components: bit 0 window, 1 global minus window, 2 random (0 = all);
+                          // LongNet: GA_LONGNET_MULTISET = every level's block, duplicates kept
     int64_t L;
     const int64_t *row_ptr;
     const int32_t *col_idx;
@@ -135,7 +136,7 @@ GA_HD Piece get_piece(const DevMask &M, int64_t i, int pc)
         int64_t U = ceil_div(s1 - s0, stp); // multiples of alpha^t in the segment
         P.base = s0;
         P.step = stp;
-        if (pc < s) {
+        if (pc < s && M.parts != 1) { // parts 1 = GA_LONGNET_MULTISET: every level keeps all multiples
             // keep j = s0 + a^t u with nu(j) == t exactly, i.e. (s0/a^t + u) mod a != 0:
             // exclude the residue u == -(s0/a^t) (mod a)  (s0 is a multiple of a^t, and of
             // a^(t+1) only when a | w0 * (segment index))

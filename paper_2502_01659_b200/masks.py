@@ -53,14 +53,17 @@ class BlockDilated(Mask):
 @dataclass(frozen=True)
 class LongNet(Mask):
     """Union over k = 0..K of BlockDilated(w0 alpha^k, alpha^k), K = max{k: w0 alpha^k <= L}
-    ("alpha = 2 and w0 = 2048"; reading R11)."""
+    ("alpha = 2 and w0 = 2048"; reading R11); multiset=True keeps repeats
+    (reading R11b)."""
     w0: int
     alpha: int = 2
+    multiset: bool = False  # LongNet's mixture: a pair in n levels' blocks weighs n times (f4)
     kind = _abi.GA_MASK_LONGNET
 
     def to_c(self, L):
         m = self._base(L)
         m.w0, m.alpha = self.w0, self.alpha
+        m.parts = _abi.GA_LONGNET_MULTISET if self.multiset else 0
         return m
 
 

@@ -1,6 +1,6 @@
 // Host build of the product's neighbour enumerator (paper_2502_01659_b200/csrc/masks.cuh)
 // so tests can compare it with the oracle on the CPU.  Prints, for each row, the sorted
-// union of its pieces and whether the pieces were disjoint.
+// union of its pieces (repeats kept) and whether the pieces were disjoint.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -15,6 +15,7 @@ int main(int argc, char **argv)
     M.kind = atoi(argv[1]);
     M.L = atoll(argv[2]);
     long long a = atoll(argv[3]), b = atoll(argv[4]);
+    M.parts = atoi(argv[5]); // LongNet: 1 = multiset mixture
     if (M.kind == ga::K_WINDOW) { M.w = a; M.r = b; M.m = (a - 1) / b; }
     if (M.kind == ga::K_BLOCK_DILATED) { M.seg = a; M.r = b; }
     if (M.kind == ga::K_LONGNET) {
@@ -30,7 +31,8 @@ int main(int argc, char **argv)
         }
         size_t n = v.size();
         std::sort(v.begin(), v.end());
-        bool disjoint = std::unique(v.begin(), v.end()) == v.end();
+        std::vector<int64_t> u = v;
+        bool disjoint = std::unique(u.begin(), u.end()) == u.end();
         if (ga::degree(M, i) != (int64_t)n) disjoint = false;
         printf("%lld %d", (long long)i, disjoint ? 1 : 0);
         for (auto j : v) printf(" %lld", (long long)j);

@@ -300,6 +300,63 @@ def test_csr_mma_large_scores_rescale(ga, orc):
     assert np.abs(got - want).max() <= 2e-2
 
 
+@pytest.mark.parametrize("L,n", [(1, 0), (1, 5), (97, 2000), (5000, 200_000)])
+def test_coo_to_csr_bit_exact(ga, orc, L, n):
+    """ga_coo_to_csr (device sort + unique) == the oracle's set-based conversion, bit for bit,
+    for shuffled edge lists with duplicates; attention over the result equals attention over
+    the same CSR built on the host."""
+    rng = np.random.default_rng(L + n)
+    rows = rng.integers(0, L, n).astype(np.int32)
+    cols = rng.integers(0, L, n).astype(np.int32)
+    rows = np.concatenate([rows, rows[: n // 4]])
+    cols = np.concatenate([cols, cols[: n // 4]])
+    perm = rng.permutation(len(rows))
+    rows, cols = rows[perm], cols[perm]
+    rp, ci = orc.coo_to_csr(L, rows, cols)
+    csr = ga.coo_to_csr(torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda(), L)
+    assert np.array_equal(csr.row_ptr.cpu().numpy(), rp)
+    assert np.array_equal(csr.col_idx.cpu().numpy(), ci)
+    if 0 < n <= 2000:
+        H, d = 1, 64
+        cpu, f64 = _inputs(L, H, d, "bf16", 31)
+        want, _ = orc.attention(*f64, orc.csr(L, rp, ci))
+        got = _run(ga, cpu, csr)
+        assert np.abs(got - want).max() <= 2e-2
+
+
+def test_coo_to_csr_errors(ga):
+    r = torch.tensor([0, 5], dtype=torch.int32, device="cuda")
+    c = torch.tensor([1, 1], dtype=torch.int32, device="cuda")
+    with pytest.raises(ga.GaError):
+        ga.coo_to_csr(r, c, 4)
+    with pytest.raises(ga.GaError):
+        ga.coo_to_csr(r, -c, 8)
+
+
+@pytest.mark.parametrize("L,w0,alpha", [(2048, 64, 2), (1800, 27, 3)])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_longnet_multiset_vs_oracle(ga, orc, L, w0, alpha, dt):
+    """LongNet multiset mixture (reading R11b): implicit (edge kernel) and
+    as device CSR with repeated columns (bit-exact with the oracle's CSR; CSR kernels)."""
+    H, d = 2, 64
+    cpu, f64 = _inputs(L, H, d, dt, 41, centred=True)
+    m = ga.LongNet(w0, alpha, multiset=True)
+    om = orc.longnet(L, w0, alpha, multiset=True)
+    want, _ = orc.attention(*f64, om)
+    got = _run(ga, cpu, m)
+    assert np.abs(got - want).max() <= TOL[dt]
+    rp, ci, nnz = orc.mask_to_csr(om)
+    assert ga.mask_count(m, L) == nnz
+    csr = ga.mask_to_csr(m, L)
+    assert np.array_equal(csr.row_ptr.cpu().numpy(), rp)
+    assert np.array_equal(csr.col_idx.cpu().numpy(), ci)
+    got2 = _run(ga, cpu, csr)
+    assert np.abs(got2 - want).max() <= TOL[dt]
+    # differs from the set union (repeats weigh twice)
+    want_set, _ = orc.attention(*f64, orc.longnet(L, w0, alpha))
+    assert np.abs(want - want_set).max() > 1e-4
+
+
 # ---------------------------------------------------------------- work optimality (T4)
 @pytest.mark.parametrize("fam,L,args", [("window", 2000, (100, 3)), ("longnet", 4096, (64, 2)),
                                         ("block", 1000, (50, 4))])

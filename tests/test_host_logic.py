@@ -20,8 +20,8 @@ def enum_bin(tmp_path_factory):
     return out
 
 
-def _run_enum(binary, kind, L, a, b):
-    txt = subprocess.check_output([binary, str(kind), str(L), str(a), str(b), "0"], text=True)
+def _run_enum(binary, kind, L, a, b, parts=0):
+    txt = subprocess.check_output([binary, str(kind), str(L), str(a), str(b), str(parts)], text=True)
     rows = []
     for line in txt.splitlines():
         f = [int(x) for x in line.split()]
@@ -48,6 +48,17 @@ def test_enumerator_matches_oracle(orc, enum_bin, kind, L, a, b):
     assert len(rows) == L
     for i, (disjoint, nb) in enumerate(rows):
         assert disjoint == 1, f"row {i}: pieces overlap or degree() disagrees"
+        assert np.array_equal(nb, ci[rp[i]:rp[i + 1]]), f"row {i}"
+
+
+@pytest.mark.parametrize("L,w0,alpha", [(256, 16, 2), (243, 9, 3), (5000, 100, 3), (999, 7, 2)])
+def test_enumerator_multiset_matches_oracle(orc, enum_bin, L, w0, alpha):
+    """LongNet multiset mixture (f4): the product's pieces (all multiples at every level)
+    list exactly the oracle's neighbour multiset, repeats included."""
+    rp, ci, nnz = orc.mask_to_csr(orc.longnet(L, w0, alpha, multiset=True))
+    rows = _run_enum(enum_bin, 2, L, w0, alpha, parts=1)
+    assert len(rows) == L
+    for i, (_, nb) in enumerate(rows):
         assert np.array_equal(nb, ci[rp[i]:rp[i + 1]]), f"row {i}"
 
 
@@ -125,6 +136,8 @@ def test_closed_form_counts_at_bench_sizes():
     assert ga.mask_count(ga.Window(256, 2), 65536) * 8 == 133_433_344
     assert ga.mask_count(ga.Window(128), 160_000_000) == 40_799_983_744
     assert ga.mask_count(ga.LongNet(2048, 2), 2 ** 24) == 51_537_510_400
+    # multiset mixture (f4): w0 L (2 - 2^-13) = 68,715,282,432
+    assert ga.mask_count(ga.LongNet(2048, 2, multiset=True), 2 ** 24) == 68_715_282_432
     assert ga.mask_count(ga.BigBird(128, 64, 64), 2 ** 20) == 468_656_702
 
 

@@ -380,3 +380,67 @@ def test_bigbird_components_are_disjoint_and_cover_the_mask(orc, L, w, ng, nr, r
         assert rows[2] == want_g
         if i in G:
             assert not rows[4]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_coo_to_csr_matches_dense_brute_force(orc, seed):
+    """oracle.coo_to_csr (sets) against a dense 0-1 matrix built from the edge list and read
+    back row-major by np.nonzero — an independent route to the same unique sorted CSR.
+    Duplicates, shuffled order, empty rows and a full row are present."""
+    rng = np.random.default_rng(seed)
+    L = [1, 7, 64, 300][seed]
+    n = [3, 40, 900, 5000][seed]
+    rows = rng.integers(0, L, n)
+    cols = rng.integers(0, L, n)
+    if L > 2:
+        rows = np.concatenate([rows, np.full(L, L - 1), rows[: n // 3]])  # full last row + duplicates
+        cols = np.concatenate([cols, np.arange(L), cols[: n // 3]])
+    perm = rng.permutation(len(rows))
+    rows, cols = rows[perm], cols[perm]
+    rp, ci = orc.coo_to_csr(L, rows, cols)
+    dense = np.zeros((L, L), dtype=bool)
+    dense[rows, cols] = True
+    r2, c2 = np.nonzero(dense)
+    assert np.array_equal(ci, c2.astype(np.int32))
+    assert np.array_equal(rp, np.concatenate([[0], np.cumsum(dense.sum(1))]))
+    if L > 2:
+        assert rp[L] - rp[L - 1] == L
+
+
+def test_coo_to_csr_rejects_out_of_range(orc):
+    with pytest.raises(ValueError):
+        orc.coo_to_csr(4, [0, 4], [1, 1])
+
+
+@pytest.mark.parametrize("L,w0,alpha", [(256, 16, 2), (300, 7, 3), (512, 64, 2), (100, 200, 2)])
+def test_longnet_multiset_against_weighted_dense(orc, L, w0, alpha):
+    """LongNet's multiset mixture (reading R11b): the oracle's neighbour lists with repeats
+    reproduce the dense multiplicity matrix (each level's BlockDilated block added), and its
+    attention equals the weighted dense softmax within 1e-12; with one level (w0 >= L) it is
+    the set version."""
+    from oracle import dense
+
+    om = orc.longnet(L, w0, alpha, multiset=True)
+    C = dense.longnet_multiplicity(L, w0, alpha)
+    rp, ci, nnz = orc.mask_to_csr(om)
+    assert nnz == C.sum()
+    for i in range(0, L, max(1, L // 37)):
+        want = np.repeat(np.arange(L), C[i])
+        assert np.array_equal(ci[rp[i]:rp[i + 1]], want)
+    q, k, v = orc.inputs(0x5EED0004, L, 1, 16, "f32")
+    got, _ = orc.attention(q, k, v, om)
+    assert np.abs(got - dense.weighted_attention(q, k, v, C)).max() < 1e-12
+    if w0 >= L:
+        want_set, _ = orc.attention(q, k, v, orc.longnet(L, w0, alpha))
+        assert np.abs(got - want_set).max() < 1e-12
+    else:  # repeats exist and change the result
+        assert C.max() > 1
+        want_set, _ = orc.attention(q, k, v, orc.longnet(L, w0, alpha))
+        assert np.abs(got - want_set).max() > 1e-6
+
+
+def test_longnet_multiset_closed_form_count(orc):
+    """Full segments: level k holds L / alpha^k lattice points, each meeting w0 of them, so
+    nnz = L w0 sum_k alpha^-k — at L = 2^12, w0 = 16: 16 * 4096 * (2 - 2^-8) = 130,816."""
+    rp, _, nnz = orc.mask_to_csr(orc.longnet(4096, 16, 2, multiset=True), with_cols=False)
+    assert nnz == 130_816

@@ -30,7 +30,7 @@ def launches(path):
 
 def ours(name):
     return any(s in name for s in ("ga::", "lnet", "band_kernel", "edge_kernel", "heavy_", "longnet", "scan_",
-                                   "window_tc", "csr_mma", "full_rows", "full_merge"))
+                                   "window_tc", "csr_mma", "csr_tma", "full_rows", "full_merge", "coo_"))
 
 
 def main():
