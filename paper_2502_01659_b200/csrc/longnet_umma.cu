@@ -217,30 +217,40 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
         }
         fence_proxy_async();
         cp_async_mbar_arrive(mbQ);
-        // chunk c -> stage c % STAGES: 32 lanes x 2 keys, whole K and V rows per lane
-        // (16-byte cp.async); keys past the last whole 16-key block are zeroed (masked)
+        // chunk c -> stage c % STAGES.  Lane l resolves the token rows of keys l and l + 32
+        // (piece cursor + piece_at + kv_row, once per key); the copies then go 8 lanes per
+        // 128-byte row, 4 rows per instruction (coalesced), the row addresses passed by shuffle.
+        // Keys past the last whole 16-key block are zeroed (masked).
+        static_assert(RB / 16 == 8 && KC == 64, "8 lanes per 128-byte row, 2 keys per lane");
+        const int cc = lane & 7;
         int cur_t = 0;
         for (int c = 0; c < nchunks; ++c) {
             const int st = c % STAGES;
             if (c >= STAGES) mbar_wait(mbEmpty0 + 8 * st, ((c / STAGES) - 1) & 1);
+            const char *kr2[2], *vr2[2];
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
-                const int kl = lane + 32 * half, k = c * KC + kl;
+                const int k = c * KC + lane + 32 * half;
+                kr2[half] = vr2[half] = nullptr;
                 if (k < nblk * 16) {
                     while (cur_t + 1 < np && pstart[cur_t + 1] <= k) ++cur_t;
-                    const char *kr, *vr;
-                    kv_row(p, piece_at(spiece[cur_t], k - pstart[cur_t]), row_bytes, kr, vr);
+                    kv_row(p, piece_at(spiece[cur_t], k - pstart[cur_t]), row_bytes, kr2[half], vr2[half]);
+                }
+            }
 #pragma unroll
-                    for (int cc = 0; cc < RB / 16; ++cc) {
-                        cp_async16(sK0 + st * KC * RB + swz<D>(kl, cc), kr + hoff + cc * 16);
-                        cp_async16(sV0 + st * KC * RB + swz<D>(kl, cc), vr + hoff + cc * 16);
-                    }
+            for (int it = 0; it < KC / 4; ++it) {
+                const int kl = 4 * it + (lane >> 3); // half = it >= 8 (warp-uniform)
+                const int src = kl & 31;
+                const char *kr = reinterpret_cast<const char *>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(kr2[it >= 8]), src));
+                const char *vr = reinterpret_cast<const char *>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(vr2[it >= 8]), src));
+                if (kr != nullptr) {
+                    cp_async16(sK0 + st * KC * RB + swz<D>(kl, cc), kr + hoff + cc * 16);
+                    cp_async16(sV0 + st * KC * RB + swz<D>(kl, cc), vr + hoff + cc * 16);
                 } else {
-#pragma unroll
-                    for (int cc = 0; cc < RB / 16; ++cc) {
-                        sts_zero16(sK0 + st * KC * RB + swz<D>(kl, cc));
-                        sts_zero16(sV0 + st * KC * RB + swz<D>(kl, cc));
-                    }
+                    sts_zero16(sK0 + st * KC * RB + swz<D>(kl, cc));
+                    sts_zero16(sV0 + st * KC * RB + swz<D>(kl, cc));
                 }
             }
             fence_proxy_async();
@@ -583,7 +593,10 @@ ga_status launch_longnet_umma(const AttnParams &p, ga_dtype dt, int64_t seg0, in
         int n = 0;
         int64_t stp = 1;
         for (int t = 0; t <= s_max; ++t) {
-            const int64_t cnt = (M.w0 + stp - 1) / stp; // most multiples of a^t in a w0 segment
+            // most rows with min(nu(i), K) == t in a w0 segment: multiples of a^t (at most
+            // ceil(w0/a^t)) minus those of a^(t+1) (at least floor(w0/a^(t+1))) for t < K;
+            // +1 covers a shorter range (last segment, shard cut), whose ceil can round up once
+            const int64_t cnt = (M.w0 + stp - 1) / stp - (t < (int)M.K ? M.w0 / (stp * M.alpha) : 0) + 1;
             const int64_t tiles = (cnt + lnet_umma::ROWS - 1) / lnet_umma::ROWS;
             for (int64_t k = 0; k < tiles; ++k) {
                 if (n >= lnet_umma::MAX_ITEMS) { set_error("LongNet tcgen05: too many items"); return GA_ERR_UNSUPPORTED; }
