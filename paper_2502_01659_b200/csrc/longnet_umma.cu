@@ -223,34 +223,63 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
         // Keys past the last whole 16-key block are zeroed (masked).
         static_assert(RB / 16 == 8 && KC == 64, "8 lanes per 128-byte row, 2 keys per lane");
         const int cc = lane & 7;
+        const char *kloc = reinterpret_cast<const char *>(p.K) + hoff + cc * 16;
+        const ptrdiff_t vdelta = reinterpret_cast<const char *>(p.V) - reinterpret_cast<const char *>(p.K);
         int cur_t = 0;
         for (int c = 0; c < nchunks; ++c) {
             const int st = c % STAGES;
             if (c >= STAGES) mbar_wait(mbEmpty0 + 8 * st, ((c / STAGES) - 1) & 1);
-            const char *kr2[2], *vr2[2];
+            if (p.k_peer == nullptr && p.kv_rows < INT32_MAX) { // local K/V: pass the row index (one shuffle)
+                int jr[2];
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const int k = c * KC + lane + 32 * half;
-                kr2[half] = vr2[half] = nullptr;
-                if (k < nblk * 16) {
-                    while (cur_t + 1 < np && pstart[cur_t + 1] <= k) ++cur_t;
-                    kv_row(p, piece_at(spiece[cur_t], k - pstart[cur_t]), row_bytes, kr2[half], vr2[half]);
+                for (int half = 0; half < 2; ++half) {
+                    const int k = c * KC + lane + 32 * half;
+                    jr[half] = -1;
+                    if (k < nblk * 16) {
+                        while (cur_t + 1 < np && pstart[cur_t + 1] <= k) ++cur_t;
+                        jr[half] = (int)(piece_at(spiece[cur_t], k - pstart[cur_t]) - p.kv_begin);
+                    }
                 }
-            }
 #pragma unroll
-            for (int it = 0; it < KC / 4; ++it) {
-                const int kl = 4 * it + (lane >> 3); // half = it >= 8 (warp-uniform)
-                const int src = kl & 31;
-                const char *kr = reinterpret_cast<const char *>(
-                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(kr2[it >= 8]), src));
-                const char *vr = reinterpret_cast<const char *>(
-                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(vr2[it >= 8]), src));
-                if (kr != nullptr) {
-                    cp_async16(sK0 + st * KC * RB + swz<D>(kl, cc), kr + hoff + cc * 16);
-                    cp_async16(sV0 + st * KC * RB + swz<D>(kl, cc), vr + hoff + cc * 16);
-                } else {
-                    sts_zero16(sK0 + st * KC * RB + swz<D>(kl, cc));
-                    sts_zero16(sV0 + st * KC * RB + swz<D>(kl, cc));
+                for (int it = 0; it < KC / 4; ++it) {
+                    const int kl = 4 * it + (lane >> 3); // half = it >= 8 (warp-uniform)
+                    const int j = __shfl_sync(0xffffffffu, jr[it >= 8], kl & 31);
+                    const uint32_t so = st * KC * RB + swz<D>(kl, cc);
+                    if (j >= 0) {
+                        const char *kr = kloc + (int64_t)j * (int64_t)row_bytes;
+                        cp_async16(sK0 + so, kr);
+                        cp_async16(sV0 + so, kr + vdelta);
+                    } else {
+                        sts_zero16(sK0 + so);
+                        sts_zero16(sV0 + so);
+                    }
+                }
+            } else { // sharded: rows may live in a peer's buffer (kv_row), pass both pointers
+                const char *kr2[2], *vr2[2];
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const int k = c * KC + lane + 32 * half;
+                    kr2[half] = vr2[half] = nullptr;
+                    if (k < nblk * 16) {
+                        while (cur_t + 1 < np && pstart[cur_t + 1] <= k) ++cur_t;
+                        kv_row(p, piece_at(spiece[cur_t], k - pstart[cur_t]), row_bytes, kr2[half], vr2[half]);
+                    }
+                }
+#pragma unroll
+                for (int it = 0; it < KC / 4; ++it) {
+                    const int kl = 4 * it + (lane >> 3); // half = it >= 8 (warp-uniform)
+                    const int src = kl & 31;
+                    const char *kr = reinterpret_cast<const char *>(
+                        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(kr2[it >= 8]), src));
+                    const char *vr = reinterpret_cast<const char *>(
+                        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(vr2[it >= 8]), src));
+                    if (kr != nullptr) {
+                        cp_async16(sK0 + st * KC * RB + swz<D>(kl, cc), kr + hoff + cc * 16);
+                        cp_async16(sV0 + st * KC * RB + swz<D>(kl, cc), vr + hoff + cc * 16);
+                    } else {
+                        sts_zero16(sK0 + st * KC * RB + swz<D>(kl, cc));
+                        sts_zero16(sV0 + st * KC * RB + swz<D>(kl, cc));
+                    }
                 }
             }
             fence_proxy_async();
@@ -350,17 +379,17 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
             // P_c into P[c&1] (last read by P V_{c-2})
             if (c >= 2) wait_O(c - 2);
             uint32_t pk[KC / 2];
-            float ls[4] = {0.f, 0.f, 0.f, 0.f}; // independent partial sums
+            float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; // packed partial sums
 #pragma unroll
             for (int i = 0; i < KC / 2; ++i) {
                 float x0 = sv[2 * i], x1 = sv[2 * i + 1];
                 ffma2_sm(x0, x1, sl2, -m_run);
                 x0 = ex2(x0);
                 x1 = ex2(x1);
-                ls[i & 3] += x0 + x1;
+                fadd2_acc(ls[i & 1], x0, x1);
                 pk[i] = pack2<T>(x0, x1);
             }
-            l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+            l_run += (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
             tmem_st32(tlane + COL_P + (c & 1) * (KC / 2), pk);
             tmem_wait_st();
             fence_before();
