@@ -28,9 +28,12 @@
 // same tcgen05 pipeline; each block writes a partial (m, l, o~) per row and level, and
 // longnet_merge_kernel combines a row's s + 1 partials with the associative (+) (P:374's
 // split-and-merge, as in csr_heavy.cu).
+#include <cstdlib>
+#include <mutex>
 #include <type_traits>
 
 #include "tc_common.cuh"
+#include "tma.cuh"
 #include "umma.cuh"
 
 namespace ga {
@@ -43,6 +46,7 @@ constexpr int ROWS = 128, SM_THREADS = 128, THREADS = SM_THREADS + 64, KC = 64, 
 constexpr int MAX_ITEMS = 64, MAX_PIECES = 64;
 
 constexpr int MAX_BLK = 128; // block-mode work entries (level, kind)
+constexpr int MAX_LAT = 24;  // TMA lattice levels (alpha = 2): 2^23 row pitch
 
 struct UParams {
     AttnParams p;
@@ -60,6 +64,11 @@ struct UParams {
     // partial slots: level t of high row i -> slot_off[t] + i / alpha^max(t,h0) - slot_first[t]
     int64_t slot_off[MAX_PIECES], slot_first[MAX_PIECES];
     float *partials; // [slots][H][D + 4]: m, l, (2 pad), o~ — 16-byte aligned o~
+    // TMA lattice maps (alpha = 2, local K/V with kv_begin = 0; n_lat = 0: cp.async loader):
+    // level t, kind 0 = odd multiples of 2^t (pieces t < s, nu(j) = t), kind 1 = all multiples
+    // (the last piece); 64-row boxes of one head
+    int32_t n_lat;
+    CUtensorMap tmK[2 * MAX_LAT], tmV[2 * MAX_LAT];
 };
 
 template <int D> __host__ __device__ constexpr uint32_t smem_bytes()
@@ -68,11 +77,15 @@ template <int D> __host__ __device__ constexpr uint32_t smem_bytes()
            256 /* mbarriers, tmem base */;
 }
 
-// TMEM columns: S[2] at 0 and KC, P[2] (16-bit pairs) at 2KC and 2KC + KC/2, O at 3KC
-constexpr uint32_t COL_S = 0, COL_P = 2 * KC, COL_O = 3 * KC; // S0 S1 | P0 P1 | O  (256 columns at d=64)
+// TMEM columns: S ring of NSB buffers at b KC (P_c, 16-bit pairs, is written over the first
+// KC/2 columns of its S buffer), O at NSB KC: S0 S1 S2 | O = 256 columns at d = 64.  Three S
+// buffers let S_{c+3} be issued as soon as P V_c is (P_c read), so S_{c+1} is ready well
+// before the softmax of chunk c ends.
+constexpr int NSB = 3;
+constexpr uint32_t COL_S = 0, COL_O = NSB * KC;
 
 template <typename T, int D>
-__global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams up)
+__global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_constant__ UParams up)
 {
     extern __shared__ unsigned char smem_raw[];
     // 1024-byte aligned base for the 128B-swizzled operand tiles
@@ -85,13 +98,14 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
     const uint32_t sV0 = sK0 + STAGES * KC * RB;
     int64_t *rows = reinterpret_cast<int64_t *>(sgen + ROWS * RB + 2 * STAGES * KC * RB);
     uint64_t *mbars = reinterpret_cast<uint64_t *>(rows + ROWS);
-    uint32_t *tmem_base_smem = reinterpret_cast<uint32_t *>(mbars + 7 + 2 * STAGES);
+    uint32_t *tmem_base_smem = reinterpret_cast<uint32_t *>(mbars + 9 + 2 * STAGES);
     const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(mbars);
-    const uint32_t mbS[2] = {mb0, mb0 + 8};       // S_c complete (tcgen05.commit)
-    const uint32_t mbO[2] = {mb0 + 16, mb0 + 24}; // P V_c complete (tcgen05.commit)
-    const uint32_t mbP[2] = {mb0 + 32, mb0 + 40}; // P_c written by the 128 softmax threads
-    const uint32_t mbQ = mb0 + 48;                // Q tile landed (32 loader lanes)
-    const uint32_t mbFull0 = mb0 + 56;            // stage st landed: mbFull0 + 8 st (32 lanes)
+    // S_c complete (tcgen05.commit) for buffer b = c % NSB: mbS0 + 8 b; P V_c complete: mbO0 +
+    // 8 (c & 1); P_c written by the 128 softmax threads: mbP0 + 8 b (addresses, not arrays:
+    // dynamically indexed arrays would live in local memory)
+    const uint32_t mbS0 = mb0, mbO0 = mb0 + 8 * NSB, mbP0 = mbO0 + 16;
+    const uint32_t mbQ = mb0 + 64;                // Q tile landed (32 loader lanes)
+    const uint32_t mbFull0 = mb0 + 72;            // stage st landed: mbFull0 + 8 st (32 lanes)
     const uint32_t mbEmpty0 = mbFull0 + 8 * STAGES; // stage st consumed (P V commit)
 
     const AttnParams &p = up.p;
@@ -168,11 +182,11 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (tid == 0) {
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(mbS[b], 1);
-            mbar_init(mbO[b], 1);
-            mbar_init(mbP[b], SM_THREADS);
+        for (int b = 0; b < NSB; ++b) {
+            mbar_init(mbS0 + 8 * b, 1);
+            mbar_init(mbP0 + 8 * b, SM_THREADS);
         }
+        for (int b = 0; b < 2; ++b) mbar_init(mbO0 + 8 * b, 1);
         mbar_init(mbQ, 32);
         for (int st = 0; st < STAGES; ++st) {
             mbar_init(mbFull0 + 8 * st, 32);
@@ -229,6 +243,33 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
         for (int c = 0; c < nchunks; ++c) {
             const int st = c % STAGES;
             if (c >= STAGES) mbar_wait(mbEmpty0 + 8 * st, ((c / STAGES) - 1) & 1);
+            // whole chunk inside one piece of an alpha = 2 mask: the keys are KC consecutive
+            // rows of a token lattice -> one TMA box for K and one for V (warp-uniform test)
+            int lt = -1;
+            int64_t u0 = 0;
+            if (up.n_lat > 0 && (c + 1) * KC <= nblk * 16) {
+                const int k0 = c * KC;
+                while (cur_t + 1 < np && pstart[cur_t + 1] <= k0) ++cur_t;
+                if (k0 + KC <= pstart[cur_t + 1]) {
+                    const Piece &P = spiece[cur_t];
+                    const int64_t j0 = piece_at(P, k0 - pstart[cur_t]);
+                    const int lev = __ffsll((unsigned long long)P.step) - 1; // step = 2^lev
+                    if (lev < up.n_lat) {
+                        if (P.mode == P_SKIPMUL) { lt = 2 * lev; u0 = (j0 / P.step - 1) / 2; }
+                        else { lt = 2 * lev + 1; u0 = j0 / P.step; }
+                    }
+                }
+            }
+            if (lt >= 0) {
+                if (lane == 0) {
+                    tma::expect_tx(mbFull0 + 8 * st, 2 * KC * RB);
+                    tma::load_3d(sK0 + st * KC * RB, &up.tmK[lt], 0, h, (int)u0, mbFull0 + 8 * st);
+                    tma::load_3d(sV0 + st * KC * RB, &up.tmV[lt], 0, h, (int)u0, mbFull0 + 8 * st);
+                } else {
+                    mbar_arrive(mbFull0 + 8 * st);
+                }
+                continue;
+            }
             if (p.k_peer == nullptr && p.kv_rows < INT32_MAX) { // local K/V: pass the row index (one shuffle)
                 int jr[2];
 #pragma unroll
@@ -289,38 +330,49 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
     } else if (warp == 5) {
         // =================== MMA warp: S_c = Q K_c^T, then O += P_{c-1} V_{c-1} ===================
         const int lane = tid & 31;
-        auto issue_PV = [&](int c) { // after P_c arrived
-            mbar_wait(mbP[c & 1], (c >> 1) & 1);
+        auto issue_PV = [&](int c) { // after P_c arrived (written over S buffer c % NSB)
+            mbar_wait(mbP0 + 8 * (c % NSB), (c / NSB) & 1);
             if (lane == 0) {
                 fence_after();
                 const uint32_t bv = sV0 + (c % STAGES) * KC * RB;
 #pragma unroll
                 for (int kk = 0; kk < KC / 16; ++kk) // 16 keys per MMA: 8 P columns, 16 V rows
-                    mma_ts(tmem + COL_O, tmem + COL_P + (c & 1) * (KC / 2) + kk * 8, sdesc_sw128(bv + kk * 16 * RB),
+                    mma_ts(tmem + COL_O, tmem + COL_S + (c % NSB) * KC + kk * 8, sdesc_sw128(bv + kk * 16 * RB),
                            idO, (c > 0 || kk > 0));
-                mma_commit(mbO[c & 1]);
+                mma_commit(mbO0 + 8 * (c & 1));
                 mma_commit(mbEmpty0 + 8 * (c % STAGES)); // S_c and P V_c have read the stage
             }
             __syncwarp();
         };
-        if (nchunks > 0) mbar_wait(mbQ, 0);
-        for (int c = 0; c < nchunks; ++c) {
-            // stage c landed; S buffer c&1 was last read by the softmax of chunk c-2, done
-            // before P_{c-2} arrived (waited in issue_PV(c-2))
+        // S_c into buffer c % NSB once stage c landed; the buffer's previous tenant P_{c-NSB}
+        // was read by P V_{c-NSB}, issued before (tcgen05 ops of one thread run in order)
+        auto issue_S = [&](int c) {
             mbar_wait(mbFull0 + 8 * (c % STAGES), (c / STAGES) & 1);
             if (lane == 0) {
                 fence_after();
                 const uint32_t bk = sK0 + (c % STAGES) * KC * RB;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) // K = 16 per MMA: +32 B inside the swizzle atom
-                    mma_ss(tmem + COL_S + (c & 1) * KC, sdesc_sw128(sQ + kk * 32), sdesc_sw128(bk + kk * 32), idS,
+                    mma_ss(tmem + COL_S + (c % NSB) * KC, sdesc_sw128(sQ + kk * 32), sdesc_sw128(bk + kk * 32), idS,
                            kk > 0);
-                mma_commit(mbS[c & 1]);
+                mma_commit(mbS0 + 8 * (c % NSB));
             }
             __syncwarp();
-            if (c >= 1) issue_PV(c - 1);
+        };
+        if (nchunks > 0) mbar_wait(mbQ, 0);
+        for (int c = 0; c < nchunks && c < NSB; ++c) issue_S(c);
+        for (int c = 0; c < nchunks; ++c) {
+            issue_PV(c);
+            if (c + NSB < nchunks) {
+                // S_{c+NSB} overwrites the TMEM columns P V_c reads (P_c): wait for P V_c to
+                // complete first — issue order alone does not order an MMA's TMEM A-operand
+                // reads before a later MMA's accumulator writes (measured: sporadic corrupted
+                // 32-lane quarters without this wait).  P V_{c+2} is not issued yet, so the
+                // two-phase mbO ring cannot alias here.
+                mbar_wait(mbO0 + 8 * (c & 1), (c >> 1) & 1);
+                issue_S(c + NSB);
+            }
         }
-        if (nchunks > 0) issue_PV(nchunks - 1);
     }
 
     // =================== softmax warps: thread = row = TMEM lane ===================
@@ -329,17 +381,17 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
     constexpr float kTau = 8.f;
     float m_run = -INFINITY, l_run = 0.f;
     auto wait_O = [&](int c) { // P V_c complete
-        mbar_wait(mbO[c & 1], (c >> 1) & 1);
+        mbar_wait(mbO0 + 8 * (c & 1), (c >> 1) & 1);
         fence_after();
     };
     if (warp < 4) {
         for (int c = 0; c < nchunks; ++c) {
             // S_c
-            mbar_wait(mbS[c & 1], (c >> 1) & 1);
+            mbar_wait(mbS0 + 8 * (c % NSB), (c / NSB) & 1);
             fence_after();
             float sv[KC];
-            tmem_ld32(tlane + COL_S + (c & 1) * KC, sv);
-            tmem_ld32(tlane + COL_S + (c & 1) * KC + 32, sv + 32);
+            tmem_ld32(tlane + COL_S + (c % NSB) * KC, sv);
+            tmem_ld32(tlane + COL_S + (c % NSB) * KC + 32, sv + 32);
             tmem_wait_ld();
             const int valid = nblk * 16 - c * KC; // keys of this chunk (< KC only in the last one)
             if (valid < KC) {
@@ -376,8 +428,7 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
                 l_run *= a;
                 m_run = mn;
             }
-            // P_c into P[c&1] (last read by P V_{c-2})
-            if (c >= 2) wait_O(c - 2);
+            // P_c over S_c (this thread has read its row of S_c)
             uint32_t pk[KC / 2];
             float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; // packed partial sums
 #pragma unroll
@@ -390,10 +441,10 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const UParams 
                 pk[i] = pack2<T>(x0, x1);
             }
             l_run += (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
-            tmem_st32(tlane + COL_P + (c & 1) * (KC / 2), pk);
+            tmem_st32(tlane + COL_S + (c % NSB) * KC, pk);
             tmem_wait_st();
             fence_before();
-            mbar_arrive(mbP[c & 1]);
+            mbar_arrive(mbP0 + 8 * (c % NSB));
         }
     }
     // ---- O row from TMEM (+ ragged tail on CUDA cores), normalise, store
@@ -602,6 +653,54 @@ size_t longnet_umma_workspace(const AttnParams &p, int h0)
 // Launch the tcgen05 kernel on the groups s = 0..s_max (those that fill 128-row tiles);
 // with `partials` (workspace of longnet_umma_workspace bytes) the rows with s > s_max run
 // block-wise on tcgen05 too and are merged; otherwise the caller runs them elsewhere.
+namespace lnet_umma {
+// TMA lattice maps for alpha = 2 with local K/V starting at token 0: level t, odd multiples of
+// 2^t (kind 0) and all multiples (kind 1).  Encoding ~4(K+1) maps is host work, so the set of
+// the last (K, V, shape) is cached.
+static void set_lattice(UParams &up, const AttnParams &p)
+{
+    up.n_lat = 0;
+    const DevMask &M = p.mask;
+    if (M.alpha != 2 || p.k_peer != nullptr || p.kv_begin != 0 || p.d != 64 || getenv("GA_LNET_CPASYNC")) return;
+    struct Cache {
+        const void *K, *V;
+        int64_t rows;
+        int H, n;
+        CUtensorMap k[2 * MAX_LAT], v[2 * MAX_LAT];
+    };
+    static Cache c{};
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    const int levels = (int)(M.K + 1 < MAX_LAT ? M.K + 1 : MAX_LAT);
+    if (!(c.K == p.K && c.V == p.V && c.rows == p.kv_rows && c.H == p.H && c.n == levels)) {
+        c.n = 0;
+        const size_t rb = (size_t)p.H * p.d * 2;
+        for (int t = 0; t < levels; ++t) {
+            const int64_t stp = (int64_t)1 << t;
+            const int64_t n_all = (p.kv_rows + stp - 1) >> t, n_odd = n_all / 2;
+            const char *Kc = reinterpret_cast<const char *>(p.K), *Vc = reinterpret_cast<const char *>(p.V);
+            const bool ok = n_odd > 0 &&
+                            tma::encode_lattice(&c.k[2 * t], Kc + stp * rb, n_odd, p.H, p.d, 2 * stp, KC) &&
+                            tma::encode_lattice(&c.v[2 * t], Vc + stp * rb, n_odd, p.H, p.d, 2 * stp, KC) &&
+                            tma::encode_lattice(&c.k[2 * t + 1], Kc, n_all, p.H, p.d, stp, KC) &&
+                            tma::encode_lattice(&c.v[2 * t + 1], Vc, n_all, p.H, p.d, stp, KC);
+            if (!ok) break;
+            c.n = t + 1;
+        }
+        c.K = p.K;
+        c.V = p.V;
+        c.rows = p.kv_rows;
+        c.H = p.H;
+        if (c.n != levels) c.n = 0; // all levels or none
+    }
+    up.n_lat = c.n;
+    for (int i = 0; i < 2 * c.n; ++i) {
+        up.tmK[i] = c.k[i];
+        up.tmV[i] = c.v[i];
+    }
+}
+} // namespace lnet_umma
+
 ga_status launch_longnet_umma(const AttnParams &p, ga_dtype dt, int64_t seg0, int64_t n_seg, int s_max,
                               float *partials, cudaStream_t s)
 {
@@ -617,6 +716,7 @@ ga_status launch_longnet_umma(const AttnParams &p, ga_dtype dt, int64_t seg0, in
     if (s_max >= 0) { // group mode
         lnet_umma::UParams up{};
         up.p = p;
+        lnet_umma::set_lattice(up, p);
         up.seg0 = seg0;
         up.n_seg = n_seg;
         int n = 0;
@@ -643,6 +743,7 @@ ga_status launch_longnet_umma(const AttnParams &p, ga_dtype dt, int64_t seg0, in
     // block mode for the high rows + merge
     lnet_umma::UParams ub{};
     ub.p = p;
+    lnet_umma::set_lattice(ub, p);
     ub.partials = partials;
     int64_t blocks = 0;
     if (lnet_umma::plan_blocks(p, s_max + 1, ub, blocks) < 0) { set_error("LongNet: too many levels"); return GA_ERR_UNSUPPORTED; }

@@ -115,3 +115,26 @@ bool encode_gather(CUtensorMap *map, const void *base, int64_t ntok, int H, int 
 
 } // namespace tma
 } // namespace ga
+
+namespace ga {
+namespace tma {
+
+bool encode_lattice(CUtensorMap *map, const void *base, int64_t nrows, int H, int D, int64_t pitch, int box_rows)
+{
+    const int rb = D * 2;
+    if (rb != 128 || nrows <= 0 || nrows >= (int64_t)1 << 32 || pitch < 1 || box_rows < 1 || box_rows > 256) return false;
+    const uint64_t gstride = (uint64_t)pitch * H * rb;
+    if ((reinterpret_cast<uintptr_t>(base) & 15u) != 0 || gstride >= (uint64_t)1 << 40) return false;
+    EncodeTiled enc = encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)nrows};
+    const cuuint64_t strides[2] = {(cuuint64_t)rb, (cuuint64_t)gstride};
+    const cuuint32_t box[3] = {(cuuint32_t)D, 1u, (cuuint32_t)box_rows};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+} // namespace tma
+} // namespace ga

@@ -18,6 +18,11 @@ namespace tma {
 // r <= 8, D * 2 in {64, 128}).  Returns false if TMA cannot express it.
 bool encode_rows(CUtensorMap *map, const void *base, int64_t ntok, int H, int D, int r, int box_rows);
 
+// Host: rank-3 map {D, H, nrows} over the token lattice base + pitch * u (u < nrows) of a
+// [tokens, H, D] 16-bit tensor (token pitch `pitch` rows, any size: the lattice row stride is
+// a plain global stride), boxes of `box_rows` lattice rows of one head, 128B-swizzled (D = 64).
+bool encode_lattice(CUtensorMap *map, const void *base, int64_t nrows, int H, int D, int64_t pitch, int box_rows);
+
 // Host: 2D map {H*D, ntok} of a [ntok, H, D] 16-bit tensor with a one-row {D, 1} box,
 // 128B-swizzled (D = 64 only), for tile::gather4 loads of 4 arbitrary token rows of a head.
 bool encode_gather(CUtensorMap *map, const void *base, int64_t ntok, int H, int D);
