@@ -407,8 +407,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 __syncwarp();
             };
             // S of the first NSB chunks of each tile (unless issued early); S_w(j + NSB) reuses
-            // the buffer of chunk j, free once P V_w(j) is issued (the tensor pipe runs the MMAs
-            // in order, so the P V has read P before the next S overwrites it)
+            // the buffer of chunk j, free once P V_w(j) has completed (waited below)
 #pragma unroll
             for (int w = 0; w < 2; ++w)
                 for (int32_t j = pre[w]; j < NSB && j < P.n[w]; ++j) {
@@ -441,7 +440,11 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     if (j >= P.n[w]) continue;
                     issue_PV(w, j);
                     if (j + NSB < P.n[w]) {
-#ifdef GA_WTC_WAR_TEST
+#ifndef GA_WTC_NO_WAR_WAIT
+                        // S_w(j + NSB) overwrites the TMEM columns P V_w(j) reads (P over S): wait
+                        // for P V_w(j) to complete — issue order alone did not keep the A-operand
+                        // reads ahead of a later MMA's accumulator writes in the LongNet kernel
+                        // (tools/lnet_stress.py); costs ~1-2% here (tools/ab_war.sh)
                         { const uint32_t cc = cw[w] + j; mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(cc & 1)), (uint32_t)((cc >> 1) & 1)); fence_after(); }
 #endif
                         chunk_ready(P.F[w] + j + NSB);
