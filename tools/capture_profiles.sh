@@ -13,7 +13,7 @@ done
 [ -n "${NO_FULL:-}" ] && exit 0
 full="ncu --set full --import-source on --clock-control none"
 timeout 900 $full -k regex:window_tc -s 3 -c 1 -o $out/full_cfg2_wtc $B --config cfg2 > /dev/null 2>&1
-timeout 900 $full -k regex:edge_kernel -s 3 -c 1 -o $out/full_cfg3_edge $B --config cfg3 > /dev/null 2>&1
+timeout 900 $full -k regex:csr_tma -s 1 -c 1 -o $out/full_cfg3_csrtma $B --config cfg3 > /dev/null 2>&1
 timeout 900 $full -k regex:longnet_umma -s 6 -c 2 -o $out/full_cfg4_umma $B --config cfg4 > /dev/null 2>&1
 timeout 900 $full -k regex:window_tc -s 3 -c 1 -o $out/full_cfg5_wtc $B --config cfg5 > /dev/null 2>&1
 ls -la $out
