@@ -46,6 +46,10 @@ constexpr int ROWS = 128, SM_THREADS = 128, THREADS = SM_THREADS + 64, KC = 64, 
 constexpr int MAX_ITEMS = 64, MAX_PIECES = 64;
 
 constexpr int MAX_BLK = 128; // block-mode work entries (level, kind)
+#ifndef GA_LNET_POLY
+#define GA_LNET_POLY 0 // of every 4 exp2 pairs, this many run as a polynomial on the FMA pipe (measured
+                       // cfg4: 0 -> 26.07 ms, 1 -> 27.15, 2 -> 28.74: the softmax warps are issue-bound)
+#endif
 constexpr int MAX_LAT = 24;  // TMA lattice levels (alpha = 2): 2^23 row pitch
 
 struct UParams {
@@ -435,8 +439,12 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
             for (int i = 0; i < KC / 2; ++i) {
                 float x0 = sv[2 * i], x1 = sv[2 * i + 1];
                 ffma2_sm(x0, x1, sl2, -m_run);
-                x0 = ex2(x0);
-                x1 = ex2(x1);
+                if ((i & 3) < GA_LNET_POLY) { // part of the exponentials on the FMA pipe
+                    ex2_poly2(x0, x1);
+                } else {
+                    x0 = ex2(x0);
+                    x1 = ex2(x1);
+                }
                 fadd2_acc(ls[i & 1], x0, x1);
                 pk[i] = pack2<T>(x0, x1);
             }
@@ -544,22 +552,35 @@ __global__ void __launch_bounds__(256) longnet_merge_kernel(const UParams up, in
     if (i == 0) s = (int)M.K;
     else for (int64_t x = i; s < (int)M.K && x % M.alpha == 0; x /= M.alpha) ++s;
     constexpr int PER = D / 32;
-    float m = -INFINITY, l = 0.f, o[PER];
+    // lane t < s+1 fetches level t's (m, l) and its partial's address; one warp max and one
+    // sum replace the sequential (+) chain, and the o~ loads of all levels are independent
+    // (the exact (+) of a7 with the common reference max: o = sum_t 2^(m_t - M) o_t)
+    const float *src = nullptr;
+    float mt = -INFINITY, lt = 0.f;
+    if (lane <= s) {
+        int64_t stp = 1;
+        for (int u = 0; u < (lane > up.h0 ? lane : up.h0); ++u) stp *= M.alpha; // alpha^max(t, h0)
+        src = up.partials + ((size_t)(up.slot_off[lane] + i / stp - up.slot_first[lane]) * H + h) * (D + 4);
+        mt = src[0];
+        lt = src[1];
+    }
+    float mx = mt;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    const float bt = (mt == -INFINITY) ? 0.f : ex2(mt - mx);
+    float l = bt * lt;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+    float o[PER];
 #pragma unroll
     for (int e = 0; e < PER; ++e) o[e] = 0.f;
-    int64_t stp = 1;
-    for (int u = 0; u < up.h0; ++u) stp *= M.alpha;
+    const unsigned long long sp = reinterpret_cast<unsigned long long>(src);
+#pragma unroll 4
     for (int t = 0; t <= s; ++t) {
-        if (t > up.h0) stp *= M.alpha; // alpha^max(t, h0)
-        const float *src = up.partials + ((size_t)(up.slot_off[t] + i / stp - up.slot_first[t]) * H + h) * (D + 4);
-        const float m2 = src[0], l2 = src[1];
-        const float mn = fmaxf(m, m2);
-        const float a = m == -INFINITY ? 0.f : ex2(m - mn);
-        const float b = m2 == -INFINITY ? 0.f : ex2(m2 - mn);
-        l = l * a + l2 * b;
+        const float b = __shfl_sync(0xffffffffu, bt, t);
+        const float *st = reinterpret_cast<const float *>(__shfl_sync(0xffffffffu, sp, t));
 #pragma unroll
-        for (int e = 0; e < PER; ++e) o[e] = o[e] * a + src[4 + lane + 32 * e] * b;
-        m = mn;
+        for (int e = 0; e < PER; ++e) o[e] = fmaf(st[4 + lane + 32 * e], b, o[e]);
     }
     const float inv = l > 0.f ? 1.f / l : 0.f;
     T *Op = reinterpret_cast<T *>(p.out) + ((size_t)(i - p.q_begin) * H + h) * D;

@@ -93,6 +93,37 @@ __device__ __forceinline__ void ffma2_sm(float &x0, float &x1, float s, float ne
     asm("mov.b64 {%0, %1}, %2;" : "=f"(x0), "=f"(x1) : "l"(d));
 }
 
+// (2^x0, 2^x1) on the FMA pipe instead of MUFU (offloads the exp unit, as FA4 does):
+// n = round(x) via the 1.5 * 2^23 magic add, f = x - n in [-0.5, 0.5], 2^f by a degree-3
+// minimax polynomial (max relative error 7.6e-5: below the bf16/fp16 rounding of P), then
+// n added to the exponent field with one IMAD.  x is clamped to >= -126 (2^-126 ~ 1e-38
+// stands in for 0, e.g. for a masked -inf score).
+__device__ __forceinline__ void ex2_poly2(float &x0, float &x1)
+{
+    x0 = fmaxf(x0, -126.f);
+    x1 = fmaxf(x1, -126.f);
+    unsigned long long x, t, r, f, pp, c;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(x0), "f"(x1));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(12582912.f));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(x), "l"(c));  // t = x + 1.5*2^23 (round)
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(t), "l"(c));  // r = round(x)
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f) : "l"(x), "l"(r));  // f in [-0.5, 0.5]
+    unsigned long long c3, c2, c1, c0;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c3) : "f"(0.055194102227687836f));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c2) : "f"(0.24260859191417694f));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c1) : "f"(0.6932564377784729f));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(c0) : "f"(0.9999281167984009f));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(c3), "l"(f), "l"(c2));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c1));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(f), "l"(c0));
+    uint32_t p0, p1, t0, t1;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(p0), "=r"(p1) : "l"(pp));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(t0), "=r"(t1) : "l"(t));
+    // the low bits of t hold n (two's complement); t << 23 keeps exactly n << 23
+    x0 = __uint_as_float(p0 + (t0 << 23));
+    x1 = __uint_as_float(p1 + (t1 << 23));
+}
+
 // acc += (x0, x1) in one packed fp32 add (sm_100 add.f32x2)
 __device__ __forceinline__ void fadd2_acc(float2 &acc, float x0, float x1)
 {
