@@ -402,53 +402,71 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
 #pragma unroll
                 for (int i = 0; i < KC; ++i) sv[i] = i < valid ? sv[i] : -INFINITY;
             }
-            float lmx[8]; // 8 independent max chains
-#pragma unroll
-            for (int j = 0; j < 8; ++j) lmx[j] = sv[j];
-#pragma unroll
-            for (int i = 8; i < KC; ++i) lmx[i & 7] = fmaxf(lmx[i & 7], sv[i]);
-            const float lm = fmaxf(fmaxf(fmaxf(lmx[0], lmx[1]), fmaxf(lmx[2], lmx[3])),
-                                   fmaxf(fmaxf(lmx[4], lmx[5]), fmaxf(lmx[6], lmx[7])));
-            // lazy rescale, voted per warp (each warp owns its 32 TMEM lanes of O); O is
-            // stable once P V_{c-1} completed (P V_c is not issued before our P_c arrives)
-            const bool need = lm * sl2 > m_run + kTau;
-            if (__any_sync(0xffffffffu, need)) {
-                if (c > 0) wait_O(c - 1);
-                const float mn = fmaxf(m_run, lm * sl2);
-                const float a = ex2(m_run - mn);
-                if (__any_sync(0xffffffffu, c > 0 && a != 1.f)) { // tcgen05.ld/st: warp-uniform
-                    float ov[32];
-#pragma unroll
-                    for (int q = 0; q < D / 32; ++q) {
-                        tmem_ld32(tlane + COL_O + 32 * q, ov);
-                        tmem_wait_ld();
-                        uint32_t ob[32];
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(ov[i] * a);
-                        tmem_st32(tlane + COL_O + 32 * q, ob);
-                    }
-                    tmem_wait_st();
-                }
-                l_run *= a;
-                m_run = mn;
-            }
             // P_c over S_c (this thread has read its row of S_c)
             uint32_t pk[KC / 2];
-            float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; // packed partial sums
+            auto exps = [&]() -> float { // pk = P_c (input type), returns the row's chunk sum
+                float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; // packed partial sums
 #pragma unroll
-            for (int i = 0; i < KC / 2; ++i) {
-                float x0 = sv[2 * i], x1 = sv[2 * i + 1];
-                ffma2_sm(x0, x1, sl2, -m_run);
-                if ((i & 3) < GA_LNET_POLY) { // part of the exponentials on the FMA pipe
-                    ex2_poly2(x0, x1);
-                } else {
-                    x0 = ex2(x0);
-                    x1 = ex2(x1);
+                for (int i = 0; i < KC / 2; ++i) {
+                    float x0 = sv[2 * i], x1 = sv[2 * i + 1];
+                    ffma2_sm(x0, x1, sl2, -m_run);
+                    if ((i & 3) < GA_LNET_POLY) { // part of the exponentials on the FMA pipe
+                        ex2_poly2(x0, x1);
+                    } else {
+                        x0 = ex2(x0);
+                        x1 = ex2(x1);
+                    }
+                    fadd2_acc(ls[i & 1], x0, x1);
+                    pk[i] = pack2<T>(x0, x1);
                 }
-                fadd2_acc(ls[i & 1], x0, x1);
-                pk[i] = pack2<T>(x0, x1);
+                return (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
+            };
+            // Fast path (c > 0, reference max set): exponentials against the current reference
+            // first; the lazy rescale is needed iff some weight exceeds 2^kTau, which a chunk
+            // sum <= 2^kTau rules out — then the chunk max is never computed.  Otherwise the
+            // careful path below (max, vote, rescale, exponentials again) gives exactly the
+            // result it always gave, so both paths are bit-identical to it.
+            bool fast = false;
+            if (c > 0) {
+                const float lsum = exps();
+                if (!__any_sync(0xffffffffu, !(lsum <= 256.f))) { // 2^kTau; NaN/inf -> careful
+                    l_run += lsum;
+                    fast = true;
+                }
             }
-            l_run += (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
+            if (!fast) {
+                float lmx[8]; // 8 independent max chains
+#pragma unroll
+                for (int j = 0; j < 8; ++j) lmx[j] = sv[j];
+#pragma unroll
+                for (int i = 8; i < KC; ++i) lmx[i & 7] = fmaxf(lmx[i & 7], sv[i]);
+                const float lm = fmaxf(fmaxf(fmaxf(lmx[0], lmx[1]), fmaxf(lmx[2], lmx[3])),
+                                       fmaxf(fmaxf(lmx[4], lmx[5]), fmaxf(lmx[6], lmx[7])));
+                // lazy rescale, voted per warp (each warp owns its 32 TMEM lanes of O); O is
+                // stable once P V_{c-1} completed (P V_c is not issued before our P_c arrives)
+                const bool need = lm * sl2 > m_run + kTau;
+                if (__any_sync(0xffffffffu, need)) {
+                    if (c > 0) wait_O(c - 1);
+                    const float mn = fmaxf(m_run, lm * sl2);
+                    const float a = ex2(m_run - mn);
+                    if (__any_sync(0xffffffffu, c > 0 && a != 1.f)) { // tcgen05.ld/st: warp-uniform
+                        float ov[32];
+#pragma unroll
+                        for (int q = 0; q < D / 32; ++q) {
+                            tmem_ld32(tlane + COL_O + 32 * q, ov);
+                            tmem_wait_ld();
+                            uint32_t ob[32];
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(ov[i] * a);
+                            tmem_st32(tlane + COL_O + 32 * q, ob);
+                        }
+                        tmem_wait_st();
+                    }
+                    l_run *= a;
+                    m_run = mn;
+                }
+                l_run += exps();
+            }
             tmem_st32(tlane + COL_S + (c % NSB) * KC, pk);
             tmem_wait_st();
             fence_before();
