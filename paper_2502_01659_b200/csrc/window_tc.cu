@@ -598,50 +598,67 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                             for (int i = 0; i < KC; ++i) sv[i] = i <= ih ? sv[i] : -INFINITY;
                         }
                     }
-                    float lmx[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) lmx[i] = sv[i];
-#pragma unroll
-                    for (int i = 8; i < KC; ++i) lmx[i & 7] = fmaxf(lmx[i & 7], sv[i]);
-                    const float lm = fmaxf(fmaxf(fmaxf(lmx[0], lmx[1]), fmaxf(lmx[2], lmx[3])),
-                                           fmaxf(fmaxf(lmx[4], lmx[5]), fmaxf(lmx[6], lmx[7])));
-                    // lazy rescale: a row moves its reference max only when the chunk's max exceeds
-                    // it by more than kTau (weights stay <= 2^kTau); O needs rescaling only for rows
-                    // that already hold weight (a row with m = -inf has O = 0 and l = 0)
-                    const float lm2 = lm * sl2;
-                    const bool need = lm2 > m_run + kTau;
-                    const float a = (need && m_run != -INFINITY) ? ex2(m_run - lm2) : 1.f;
-                    if (__any_sync(0xffffffffu, a != 1.f) && j > 0) {
-                        wait_O(c - 1); // O stable: P V of the previous chunk completed
-                        float ov[32];
-#pragma unroll
-                        for (int qq = 0; qq < D / 32; ++qq) {
-                            tmem_ld32(tO + 32 * qq, ov);
-                            tmem_wait_ld();
-                            uint32_t ob[32];
-#pragma unroll
-                            for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(ov[i] * a);
-                            tmem_st32(tO + 32 * qq, ob);
-                        }
-                        tmem_wait_st();
-                    }
-                    if (need) {
-                        l_run *= a;
-                        m_run = lm2;
-                    }
-                    const float m_use = m_run == -INFINITY ? 0.f : m_run;
                     uint32_t pk[KC / 2];
-                    float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; // packed partial sums
+                    auto exps = [&]() -> float { // pk = P (input type); returns the row's chunk sum
+                        const float m_use = m_run == -INFINITY ? 0.f : m_run;
+                        float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; // packed partial sums
 #pragma unroll
-                    for (int i = 0; i < KC / 2; ++i) {
-                        float x0 = sv[2 * i], x1 = sv[2 * i + 1];
-                        ffma2_sm(x0, x1, sl2, -m_use);
-                        x0 = ex2(x0);
-                        x1 = ex2(x1);
-                        fadd2_acc(ls[i & 1], x0, x1);
-                        pk[i] = pack2<T>(x0, x1);
+                        for (int i = 0; i < KC / 2; ++i) {
+                            float x0 = sv[2 * i], x1 = sv[2 * i + 1];
+                            ffma2_sm(x0, x1, sl2, -m_use);
+                            x0 = ex2(x0);
+                            x1 = ex2(x1);
+                            fadd2_acc(ls[i & 1], x0, x1);
+                            pk[i] = pack2<T>(x0, x1);
+                        }
+                        return (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
+                    };
+                    // fast path once every row of the warp holds a reference max: weights against
+                    // it first; a rescale is needed iff some weight exceeds 2^kTau, which a chunk
+                    // sum <= 2^kTau rules out (then the chunk max is never computed); otherwise the
+                    // careful path repeats the chunk exactly as before (bit-identical results)
+                    bool fast = false;
+                    if (__all_sync(0xffffffffu, m_run != -INFINITY)) {
+                        const float lsum = exps();
+                        if (!__any_sync(0xffffffffu, !(lsum <= 256.f))) { // 2^kTau; NaN/inf -> careful
+                            l_run += lsum;
+                            fast = true;
+                        }
                     }
-                    l_run += (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
+                    if (!fast) {
+                        float lmx[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) lmx[i] = sv[i];
+#pragma unroll
+                        for (int i = 8; i < KC; ++i) lmx[i & 7] = fmaxf(lmx[i & 7], sv[i]);
+                        const float lm = fmaxf(fmaxf(fmaxf(lmx[0], lmx[1]), fmaxf(lmx[2], lmx[3])),
+                                               fmaxf(fmaxf(lmx[4], lmx[5]), fmaxf(lmx[6], lmx[7])));
+                        // lazy rescale: a row moves its reference max only when the chunk's max exceeds
+                        // it by more than kTau (weights stay <= 2^kTau); O needs rescaling only for rows
+                        // that already hold weight (a row with m = -inf has O = 0 and l = 0)
+                        const float lm2 = lm * sl2;
+                        const bool need = lm2 > m_run + kTau;
+                        const float a = (need && m_run != -INFINITY) ? ex2(m_run - lm2) : 1.f;
+                        if (__any_sync(0xffffffffu, a != 1.f) && j > 0) {
+                            wait_O(c - 1); // O stable: P V of the previous chunk completed
+                            float ov[32];
+#pragma unroll
+                            for (int qq = 0; qq < D / 32; ++qq) {
+                                tmem_ld32(tO + 32 * qq, ov);
+                                tmem_wait_ld();
+                                uint32_t ob[32];
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(ov[i] * a);
+                                tmem_st32(tO + 32 * qq, ob);
+                            }
+                            tmem_wait_st();
+                        }
+                        if (need) {
+                            l_run *= a;
+                            m_run = lm2;
+                        }
+                        l_run += exps();
+                    }
                     tmem_st32(tS, pk);
                     tmem_wait_st();
                     // the previous tile's epilogue with this tile's first chunk (its last P V has

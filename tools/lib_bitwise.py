@@ -8,6 +8,7 @@ import tempfile
 
 CASES = {
     "longnet": [("longnet", 65536, 2048, 2, 2), ("longnet", 2 ** 20, 2048, 2, 1), ("longnet", 5000, 300, 2, 2)],
+    "window": [("window", 65536, 256, 2, 8), ("window", 1 << 22, 128, 1, 1), ("window", 50000, 400, 4, 2)],
 }
 
 
@@ -16,9 +17,10 @@ def child(out_path, fam):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import paper_2502_01659_b200 as ga
     res = {}
-    for (f, L, w0, alpha, H) in CASES[fam]:
+    for (f, L, a, b, H) in CASES[fam]:
         q, k, v = ga.qkv_device(L + 7, L, H, 64, torch.bfloat16)
-        res[(L, w0, alpha, H)] = ga.attention(q, k, v, ga.LongNet(w0, alpha)).cpu()
+        m = ga.LongNet(a, b) if f == "longnet" else ga.Window(a, b)
+        res[(L, a, b, H)] = ga.attention(q, k, v, m).cpu()
     torch.save(res, out_path)
 
 
