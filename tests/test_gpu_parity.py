@@ -357,6 +357,25 @@ def test_longnet_multiset_vs_oracle(ga, orc, L, w0, alpha, dt):
     assert np.abs(want - want_set).max() > 1e-4
 
 
+@pytest.mark.parametrize("L,w0", [(65536, 2048), (5000, 300), (8192, 256)])
+def test_longnet_tma_lattice_loader_bitwise(ga, L, w0, monkeypatch):
+    """The LongNet tcgen05 kernel's two K/V loaders — TMA boxes from per-level lattice tensor
+    maps (alpha = 2, default) and per-row cp.async (GA_LNET_CPASYNC=1) — stage the same bytes,
+    so the outputs are bit-identical, for a whole run and a query sub-range, repeated (the
+    repeats also catch races such as the TMEM WAR hazard of DESIGN.md K5)."""
+    H, d = 2, 64
+    q, k, v = ga.qkv_device(L + 3, L, H, d, torch.bfloat16)
+    m = ga.LongNet(w0, 2)
+    r0 = (L // 3 // w0) * w0
+    monkeypatch.setenv("GA_LNET_CPASYNC", "1")
+    ref = ga.attention(q, k, v, m, kernel="tc")
+    ref_part = ga.attention(q[r0:].contiguous(), k, v, m, L=L, q_begin=r0, kernel="tc")
+    monkeypatch.delenv("GA_LNET_CPASYNC")
+    for _ in range(5):
+        assert torch.equal(ga.attention(q, k, v, m, kernel="tc"), ref)
+        assert torch.equal(ga.attention(q[r0:].contiguous(), k, v, m, L=L, q_begin=r0, kernel="tc"), ref_part)
+
+
 # ---------------------------------------------------------------- work optimality (T4)
 @pytest.mark.parametrize("fam,L,args", [("window", 2000, (100, 3)), ("longnet", 4096, (64, 2)),
                                         ("block", 1000, (50, 4))])
