@@ -358,6 +358,9 @@ def roofline_for(args, cfg, kind, head_edges, L_local, H, d, nnz, per_step):
         "lower_bound_us": {"hbm": round(t_mem * 1e6, 2), "flops": round(t_fl * 1e6, 2)},
         "tensor_tflops_achieved": round(flops_alg / s / 1e12, 2),
         "kernel_ms_median": round(kernel_ms, 4)})
+    if traffic:  # measured DRAM bytes of the step (ncu, profiles/traffic.json) over this run's time
+        roof["dram_GBps_measured_traffic"] = round(traffic / s / 1e9, 1)
+        roof["dram_frac_measured_traffic"] = round(traffic / s / 1e9 / hbm, 4)
     gbe = 2 * d * e + (4 if kind == "bigbird" else 0)
     ggbs = head_edges * gbe / s / 1e9
     gather = {"bytes_per_edge": gbe, "GBps": round(ggbs, 1), "frac_of_8TBps": round(ggbs / 8000.0, 3),
