@@ -42,7 +42,10 @@ using namespace tc;
 using namespace umma;
 
 // warps 0-3: softmax (thread = row = TMEM lane); warp 4: loader (cp.async ring); warp 5: MMA
-constexpr int ROWS = 128, SM_THREADS = 128, THREADS = SM_THREADS + 64, KC = 64, STAGES = 4;
+#ifndef GA_LNET_STAGES
+#define GA_LNET_STAGES 4 // K/V ring depth (5 fits twice per SM too; measured equal: the ring is fed at the L2 rate)
+#endif
+constexpr int ROWS = 128, SM_THREADS = 128, THREADS = SM_THREADS + 64, KC = 64, STAGES = GA_LNET_STAGES;
 constexpr int MAX_ITEMS = 64, MAX_PIECES = 64;
 
 constexpr int MAX_BLK = 128; // block-mode work entries (level, kind)
@@ -88,6 +91,19 @@ template <int D> __host__ __device__ constexpr uint32_t smem_bytes()
 constexpr int NSB = 3;
 constexpr uint32_t COL_S = 0, COL_O = NSB * KC;
 
+#ifdef GA_LNET_TRACE
+// debug timeline of one group-mode CTA (blockIdx.x == LNET_TRACE_CTA): per warp, lane 0
+// records (val << 56 | event << 48 | warp << 40 | clock - t0)
+constexpr int LT_N = 8192, LT_PER = LT_N / 8, LNET_TRACE_CTA = 2853; // item 3 (an s = 0 tile) of segment 150 at w0 = 2048, H = 1
+__device__ unsigned long long g_ltrace[LT_N];
+#define LTRACE(ev, val) do { if (lt_on && (threadIdx.x & 31) == 0 && lt_cnt < LT_PER) { \
+    g_ltrace[(threadIdx.x >> 5) * LT_PER + lt_cnt++] = ((unsigned long long)((val) & 0xff) << 56) | \
+        ((unsigned long long)(ev) << 48) | ((unsigned long long)(threadIdx.x >> 5) << 40) | \
+        (unsigned long long)((clock64() - lt_t0) & 0xffffffffffull); } } while (0)
+#else
+#define LTRACE(ev, val)
+#endif
+
 template <typename T, int D>
 __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_constant__ UParams up)
 {
@@ -116,6 +132,12 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
     const DevMask &M = p.mask;
     const int tid = threadIdx.x, warp = tid >> 5;
     const int H = p.H;
+#ifdef GA_LNET_TRACE
+    const bool lt_on = !up.blocked && blockIdx.x == LNET_TRACE_CTA;
+    const long long lt_t0 = clock64();
+    int lt_cnt = 0;
+    LTRACE(0, 0);
+#endif
 
     // ---- work item -> (segment [S0, S1), row progression, key pieces)
     int64_t S0, S1, seg_len, row_step; // rows: candidates (f0 + q) * row_step in [lo, hi)
@@ -247,6 +269,7 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
         for (int c = 0; c < nchunks; ++c) {
             const int st = c % STAGES;
             if (c >= STAGES) mbar_wait(mbEmpty0 + 8 * st, ((c / STAGES) - 1) & 1);
+            LTRACE(20, c);
             // whole chunk inside one piece of an alpha = 2 mask: the keys are KC consecutive
             // rows of a token lattice -> one TMA box for K and one for V (warp-uniform test)
             int lt = -1;
@@ -336,6 +359,7 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
         const int lane = tid & 31;
         auto issue_PV = [&](int c) { // after P_c arrived (written over S buffer c % NSB)
             mbar_wait(mbP0 + 8 * (c % NSB), (c / NSB) & 1);
+            LTRACE(3, c);
             if (lane == 0) {
                 fence_after();
                 const uint32_t bv = sV0 + (c % STAGES) * KC * RB;
@@ -352,6 +376,7 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
         // was read by P V_{c-NSB}, issued before (tcgen05 ops of one thread run in order)
         auto issue_S = [&](int c) {
             mbar_wait(mbFull0 + 8 * (c % STAGES), (c / STAGES) & 1);
+            LTRACE(1, c);
             if (lane == 0) {
                 fence_after();
                 const uint32_t bk = sK0 + (c % STAGES) * KC * RB;
@@ -365,16 +390,20 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
         };
         if (nchunks > 0) mbar_wait(mbQ, 0);
         for (int c = 0; c < nchunks && c < NSB; ++c) issue_S(c);
+        static_assert(NSB == 3, "S_{c+2} reuses the buffer of P_{c-1}");
         for (int c = 0; c < nchunks; ++c) {
             issue_PV(c);
-            if (c + NSB < nchunks) {
-                // S_{c+NSB} overwrites the TMEM columns P V_c reads (P_c): wait for P V_c to
-                // complete first — issue order alone does not order an MMA's TMEM A-operand
+            if (c >= 1 && c + 2 < nchunks) {
+                // S_{c+2} overwrites the TMEM columns P V_{c-1} read (P_{c-1}): wait for P V_{c-1}
+                // to complete first — issue order alone does not order an MMA's TMEM A-operand
                 // reads before a later MMA's accumulator writes (measured: sporadic corrupted
-                // 32-lane quarters without this wait).  P V_{c+2} is not issued yet, so the
-                // two-phase mbO ring cannot alias here.
-                mbar_wait(mbO0 + 8 * (c & 1), (c >> 1) & 1);
-                issue_S(c + NSB);
+                // 32-lane quarters without this wait).  Waiting for the PREVIOUS P V (issued an
+                // iteration ago, normally complete) keeps the MMA warp off the P V latency
+                // (tools/lnet_trace.py).  P V_{c+1} is not issued yet, so the two-phase mbO ring
+                // cannot alias here.
+                mbar_wait(mbO0 + 8 * ((c - 1) & 1), ((c - 1) >> 1) & 1);
+                LTRACE(7, c);
+                issue_S(c + 2);
             }
         }
     }
@@ -391,7 +420,9 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
     if (warp < 4) {
         for (int c = 0; c < nchunks; ++c) {
             // S_c
+            LTRACE(10, c);
             mbar_wait(mbS0 + 8 * (c % NSB), (c / NSB) & 1);
+            LTRACE(12, c);
             fence_after();
             float sv[KC];
             tmem_ld32(tlane + COL_S + (c % NSB) * KC, sv);
@@ -471,6 +502,7 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
             tmem_wait_st();
             fence_before();
             mbar_arrive(mbP0 + 8 * (c % NSB));
+            LTRACE(14, c);
         }
     }
     // ---- O row from TMEM (+ ragged tail on CUDA cores), normalise, store
@@ -543,6 +575,7 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
             stg16(Og + q * 16, pack<T>(r8));
         }
     }
+    LTRACE(99, 0);
     fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -692,6 +725,17 @@ size_t longnet_umma_workspace(const AttnParams &p, int h0)
 // Launch the tcgen05 kernel on the groups s = 0..s_max (those that fill 128-row tiles);
 // with `partials` (workspace of longnet_umma_workspace bytes) the rows with s > s_max run
 // block-wise on tcgen05 too and are merged; otherwise the caller runs them elsewhere.
+#ifdef GA_LNET_TRACE
+extern "C" int ga_lnet_trace_read(unsigned long long *out, int n)
+{
+    if (n < lnet_umma::LT_N) return -1;
+    cudaMemcpyFromSymbol(out, lnet_umma::g_ltrace, sizeof(unsigned long long) * lnet_umma::LT_N);
+    static unsigned long long z[lnet_umma::LT_N];
+    cudaMemcpyToSymbol(lnet_umma::g_ltrace, z, sizeof(z));
+    return lnet_umma::LT_N;
+}
+#endif
+
 namespace lnet_umma {
 // TMA lattice maps for alpha = 2 with local K/V starting at token 0: level t, odd multiples of
 // 2^t (kind 0) and all multiples (kind 1).  Encoding ~4(K+1) maps is host work, so the set of
