@@ -94,7 +94,8 @@ static_assert(PD < IR, "a slot is refilled only after its pair was issued");
 
 struct TmaParams {
     AttnParams p;
-    CUtensorMap tmK, tmV;
+    CUtensorMap tmK, tmV;   // gather4: one-row boxes
+    CUtensorMap tbK, tbV;   // 16 consecutive rows (a contiguous block of columns)
 };
 
 __device__ __forceinline__ uint4 lds128(uint32_t a)
@@ -289,14 +290,31 @@ __global__ void __launch_bounds__(TW * 32, 2) csr_tma_kernel(const __grid_consta
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d + 2048), "l"(ka + vdelta) : "memory");
             }
             umma::cp_async_mbar_arrive(bar);
-        } else if (lane == 0) { // 4 K and 4 V tile::gather4 loads of 4 rows each
+        } else if (lane == 0) {
             tma::expect_tx(bar, STAGE);
+            // a block of 16 consecutive columns (e.g. the window run of a BigBird row) is one
+            // 16-row box for K and one for V; otherwise 4 + 4 tile::gather4 loads.  Every
+            // column is checked (duplicate columns of a multiset CSR can span 15 too).
+            uint4 jq[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint4 j = lds128(src + 16 * q);
-                const int j0 = (int)j.x - kv0, j1 = (int)j.y - kv0, j2 = (int)j.z - kv0, j3 = (int)j.w - kv0;
-                tma::gather4(dst + q * 512, &tp.tmK, h * D, j0, j1, j2, j3, bar);
-                tma::gather4(dst + 2048 + q * 512, &tp.tmV, h * D, j0, j1, j2, j3, bar);
+            for (int q = 0; q < 4; ++q) jq[q] = lds128(src + 16 * q);
+            const int jb = (int)jq[0].x;
+            bool run = true;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                run = run && (int)jq[q].x == jb + 4 * q && (int)jq[q].y == jb + 4 * q + 1 &&
+                      (int)jq[q].z == jb + 4 * q + 2 && (int)jq[q].w == jb + 4 * q + 3;
+            if (run) {
+                tma::load_3d(dst, &tp.tbK, 0, h, jb - kv0, bar);
+                tma::load_3d(dst + 2048, &tp.tbV, 0, h, jb - kv0, bar);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 j = jq[q];
+                    const int j0 = (int)j.x - kv0, j1 = (int)j.y - kv0, j2 = (int)j.z - kv0, j3 = (int)j.w - kv0;
+                    tma::gather4(dst + q * 512, &tp.tmK, h * D, j0, j1, j2, j3, bar);
+                    tma::gather4(dst + 2048 + q * 512, &tp.tmV, h * D, j0, j1, j2, j3, bar);
+                }
             }
         }
         if (n & 1) { // pair n/2 retires: every lane's reads of its slot are done before the refill
@@ -372,7 +390,9 @@ template <typename T> static ga_status launch_tma(const AttnParams &p, cudaStrea
     tp.p = p;
     const bool g4 = !getenv_flag("GA_CSR_CPASYNC");
     if (g4 && (!tma::encode_gather(&tp.tmK, p.K, p.kv_rows, p.H, 64) ||
-               !tma::encode_gather(&tp.tmV, p.V, p.kv_rows, p.H, 64)))
+               !tma::encode_gather(&tp.tmV, p.V, p.kv_rows, p.H, 64) ||
+               !tma::encode_block(&tp.tbK, p.K, p.kv_rows, p.H, 64, 16) ||
+               !tma::encode_block(&tp.tbV, p.V, p.kv_rows, p.H, 64, 16)))
         return GA_OK;
     const int64_t warps = p.q_rows * p.H;
     done = true;

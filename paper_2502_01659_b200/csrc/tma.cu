@@ -54,8 +54,10 @@ bool encode_rows(CUtensorMap *map, const void *base, int64_t ntok, int H, int D,
         for (int i = 0; i < n; ++i)
             if (keys[i] == k) { *map = maps[i]; return true; }
     }
-    if (!(r == 0 ? encode_gather_uncached(map, base, ntok, H, D) : encode_uncached(map, base, ntok, H, D, r, box_rows)))
-        return false;
+    const bool ok = r == 0  ? encode_gather_uncached(map, base, ntok, H, D)
+                    : r < 0 ? encode_lattice(map, base, ntok, H, D, 1, -r) // contiguous rows, box -r
+                            : encode_uncached(map, base, ntok, H, D, r, box_rows);
+    if (!ok) return false;
     std::lock_guard<std::mutex> g(mu);
     keys[next] = k;
     maps[next] = *map;
@@ -111,6 +113,11 @@ static bool encode_gather_uncached(CUtensorMap *map, const void *base, int64_t n
 bool encode_gather(CUtensorMap *map, const void *base, int64_t ntok, int H, int D)
 {
     return encode_rows(map, base, ntok, H, D, 0, 0);
+}
+
+bool encode_block(CUtensorMap *map, const void *base, int64_t ntok, int H, int D, int box_rows)
+{
+    return encode_rows(map, base, ntok, H, D, -box_rows, 0);
 }
 
 } // namespace tma

@@ -27,6 +27,10 @@ bool encode_lattice(CUtensorMap *map, const void *base, int64_t nrows, int H, in
 // 128B-swizzled (D = 64 only), for tile::gather4 loads of 4 arbitrary token rows of a head.
 bool encode_gather(CUtensorMap *map, const void *base, int64_t ntok, int H, int D);
 
+// Host: rank-3 map {D, H, ntok} with {D, 1, box_rows} boxes of consecutive token rows of one
+// head, 128B-swizzled (D = 64): the same shared layout as box_rows / 4 gather4 loads (cached).
+bool encode_block(CUtensorMap *map, const void *base, int64_t ntok, int H, int D, int box_rows);
+
 // 4 rows (tokens y0..y3, elements [x, x + D)) -> 4 consecutive 128-byte rows of shared memory
 __device__ __forceinline__ void gather4(uint32_t smem, const CUtensorMap *map, int x, int y0, int y1, int y2, int y3,
                                         uint32_t mbar)

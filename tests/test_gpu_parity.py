@@ -376,6 +376,39 @@ def test_longnet_tma_lattice_loader_bitwise(ga, L, w0, monkeypatch):
         assert torch.equal(ga.attention(q[r0:].contiguous(), k, v, m, L=L, q_begin=r0, kernel="tc"), ref_part)
 
 
+@pytest.mark.parametrize("variant", ["", "GA_CSR_CPASYNC"])
+def test_csr_contiguous_blocks_and_duplicate_traps(ga, orc, variant, monkeypatch):
+    """Explicit CSR rows made of 16-column runs (loaded as one 16-row TMA box each) next to
+    blocks that only look like runs: repeated columns spanning exactly 15 (a multiset row),
+    a run shifted by one, a run cut by the row end.  Repeats weigh twice, as in the oracle."""
+    if variant:
+        monkeypatch.setenv(variant, "1")
+    L, H, d = 600, 2, 64
+    rows = []
+    for i in range(L):
+        b = (i * 7) % (L - 64)
+        k = i % 5
+        if k == 0:
+            r = list(range(b, b + 48))                                  # three whole runs
+        elif k == 1:
+            r = [b, b + 1, b + 1] + list(range(b + 3, b + 16))           # span 15, one column repeated
+        elif k == 2:
+            r = list(range(b, b + 16)) + [b + 20] + list(range(b + 21, b + 37))  # run, then shifted run
+        elif k == 3:
+            r = list(range(b, b + 23))                                  # run + ragged tail
+        else:
+            r = sorted(set(range(b, b + 40, 2)))                        # strided: never a run
+        rows.append(np.array(sorted(r), dtype=np.int32))
+    deg = np.array([len(r) for r in rows])
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    ci = np.concatenate(rows).astype(np.int32)
+    cpu, f64 = _inputs(L, H, d, "bf16", 77, centred=True)
+    want, _ = orc.attention(*f64, orc.csr(L, rp, ci))
+    m = ga.CSR(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+    got = _run(ga, cpu, m)
+    assert np.abs(got - want).max() <= 2e-2
+
+
 # ---------------------------------------------------------------- work optimality (T4)
 @pytest.mark.parametrize("fam,L,args", [("window", 2000, (100, 3)), ("longnet", 4096, (64, 2)),
                                         ("block", 1000, (50, 4))])
