@@ -808,7 +808,11 @@ ga_status launch_longnet_umma(const AttnParams &p, ga_dtype dt, int64_t seg0, in
             // most rows with min(nu(i), K) == t in a w0 segment: multiples of a^t (at most
             // ceil(w0/a^t)) minus those of a^(t+1) (at least floor(w0/a^(t+1))) for t < K;
             // +1 covers a shorter range (last segment, shard cut), whose ceil can round up once
-            const int64_t cnt = (M.w0 + stp - 1) / stp - (t < (int)M.K ? M.w0 / (stp * M.alpha) : 0) + 1;
+            // exact when every segment is whole and alpha^(t+1) | w0 (then no tile is empty)
+            const bool whole = M.L % M.w0 == 0 && p.q_begin % M.w0 == 0 && (p.q_begin + p.q_rows) % M.w0 == 0;
+            const int64_t cnt = (whole && t < (int)M.K && M.w0 % (stp * M.alpha) == 0)
+                                    ? M.w0 / stp - M.w0 / (stp * M.alpha)
+                                    : (M.w0 + stp - 1) / stp - (t < (int)M.K ? M.w0 / (stp * M.alpha) : 0) + 1;
             const int64_t tiles = (cnt + lnet_umma::ROWS - 1) / lnet_umma::ROWS;
             for (int64_t k = 0; k < tiles; ++k) {
                 if (n >= lnet_umma::MAX_ITEMS) { set_error("LongNet tcgen05: too many items"); return GA_ERR_UNSUPPORTED; }
