@@ -695,7 +695,14 @@ static int64_t plan_blocks(const AttnParams &p, int h0, UParams &up, int64_t &bl
             if (kind == 0 && t >= K) continue; // B: t < K
             if (kind == 1 && t < h0) continue; // A: levels of the high rows' last piece
             const int ex = kind == 0 ? (t + 1 > h0 ? t + 1 : h0) : t;
-            const int64_t qs = ipow(M.alpha, ex), rows_max = (W + qs - 1) / qs; // most multiples in W tokens
+            const int64_t qs = ipow(M.alpha, ex);
+            // most rows per level-t segment: multiples of alpha^ex in W tokens; A rows (kind 1,
+            // t < K) have valuation exactly t, which for whole segments with alpha^(t+1) | W is
+            // exactly W/alpha^t - W/alpha^(t+1) (no empty tiles)
+            const bool whole = M.L % W == 0 && qb % W == 0 && qe % W == 0;
+            const int64_t rows_max = (kind == 1 && t < K && whole && W % (qs * M.alpha) == 0)
+                                         ? W / qs - W / (qs * M.alpha)
+                                         : (W + qs - 1) / qs;
             if (e >= MAX_BLK) return -1;
             up.blk_t[e] = (int16_t)t;
             up.blk_kind[e] = (int16_t)kind;
