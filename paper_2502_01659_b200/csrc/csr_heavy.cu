@@ -179,11 +179,13 @@ __global__ void __launch_bounds__(FULL_THREADS) full_rows_kernel(const __grid_co
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int H = p.H;
     const int64_t nfull = cnt_scanned[p.q_rows] >> 40;
-    const int64_t tile = blockIdx.x % ntiles;
-    const int64_t ch = blockIdx.x / ntiles; // chunk-major: a chunk's tiles share its keys in L2
+    const int64_t ch = blockIdx.x; // one CTA per (key chunk, head) walks the tiles of full rows
     const int h = (int)(blockIdx.y);
+    (void)ntiles;
+    // (a grid sized by the host's bound on the full-row count would launch mostly empty CTAs)
+    for (int64_t tile = 0; tile * FULL_ROWS < nfull; ++tile) {
     const int nrows = (int)imin(FULL_ROWS, nfull - tile * FULL_ROWS);
-    if (nrows <= 0) return;
+    if (tile > 0) __syncthreads(); // the previous tile's shared buffers are free
     const int64_t NCH = full_chunks(p.mask.L);
     const int64_t k0 = ch * FULL_KCH, nkeys = imin((int64_t)FULL_KCH, p.mask.L - k0); // multiple of 16
 
@@ -261,6 +263,7 @@ __global__ void __launch_bounds__(FULL_THREADS) full_rows_kernel(const __grid_co
             dst[2 + 8 * j + 2 * t4 + 1] = st.o[j][2 * hr + 1];
         }
     }
+    }
 }
 
 // one warp per (full row, head): (+)-merge its NCH chunk partials, normalise, store
@@ -317,8 +320,8 @@ static ga_status launch_full_t(const AttnParams &p, const int64_t *cnt, const in
         cudaFuncSetAttribute(full_rows_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    full_rows_kernel<T, D><<<dim3((unsigned)(ntiles * NCH), (unsigned)p.H), FULL_THREADS, smem, s>>>(p, cnt, full_row,
-                                                                                                     ntiles, fpart);
+    full_rows_kernel<T, D><<<dim3((unsigned)NCH, (unsigned)p.H), FULL_THREADS, smem, s>>>(p, cnt, full_row, ntiles,
+                                                                                          fpart);
     GA_CHECK_LAUNCH("full_rows_kernel");
     full_merge_kernel<T, D><<<(unsigned)((F * p.H + 7) / 8), 256, 0, s>>>(p, cnt, full_row, fpart);
     GA_CHECK_LAUNCH("full_merge_kernel");
