@@ -415,6 +415,97 @@ ga_status ga_attention(const void *Q, const void *K, const void *V, const ga_mas
     return ga_attention_ex(Q, K, V, mask, out, L, d, heads, dtype, nullptr, stream);
 }
 
+// Host-buffer path for Window masks: the query range is cut into kHostPipeChunks aligned
+// chunks (ga_query_alignment, so every row is computed exactly as by one launch).  Chunk c
+// needs Q rows [b, e) and K/V rows up to e + w (|i - j| < w), so its launch starts as soon
+// as those rows are in; H2D of the next chunk, the launch and D2H of the previous output
+// overlap on two copy streams forked from and joined back to the caller's stream.
+static const int kHostPipeChunks = 8;
+static const int64_t kHostPipeMinRows = 4096;
+
+static ga_status host_copy_streams(cudaStream_t *h2d, cudaStream_t *d2h)
+{
+    static std::mutex mu;
+    static cudaStream_t tab[64][2] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess || dev < 0 || dev >= 64) return cuda_fail(e, "ga_attention_host: cudaGetDevice");
+    std::lock_guard<std::mutex> g(mu);
+    for (int k = 0; k < 2; ++k)
+        if (!tab[dev][k] && (e = cudaStreamCreateWithFlags(&tab[dev][k], cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "ga_attention_host: copy stream");
+    *h2d = tab[dev][0];
+    *d2h = tab[dev][1];
+    return GA_OK;
+}
+
+static ga_status host_window_pipeline(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out,
+                                      int64_t L, int32_t d, int32_t heads, ga_dtype dtype, cudaStream_t s, char *dq,
+                                      char *dk, char *dv, char *dout)
+{
+    cudaStream_t sh, so;
+    ga_status st = host_copy_streams(&sh, &so);
+    if (st != GA_OK) return st;
+    int64_t align = 1;
+    if ((st = ga_query_alignment(mask, d, dtype, &align)) != GA_OK) return st;
+    if (align < 1) align = 1;
+    const size_t rb = (size_t)heads * d * dtype_bytes(dtype);
+    int64_t per = (L + kHostPipeChunks - 1) / kHostPipeChunks;
+    per = (per + align - 1) / align * align;
+    const int nc = (int)((L + per - 1) / per);
+    std::vector<cudaEvent_t> ev(2 * nc + 2, nullptr);
+    cudaError_t e = cudaSuccess;
+    for (auto &x : ev)
+        if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) break;
+    if (e != cudaSuccess) {
+        for (auto x : ev)
+            if (x) cudaEventDestroy(x);
+        return cuda_fail(e, "ga_attention_host: events");
+    }
+    cudaEvent_t fork = ev[2 * nc], join = ev[2 * nc + 1];
+    // fork: the copy streams start after the caller's prior work and the allocations
+    cudaEventRecord(fork, s);
+    cudaStreamWaitEvent(sh, fork, 0);
+    cudaStreamWaitEvent(so, fork, 0);
+    const char *hq = (const char *)Q, *hk = (const char *)K, *hv = (const char *)V;
+    int64_t kv_done = 0;
+    for (int c = 0; c < nc && st == GA_OK; ++c) {
+        const int64_t b = (int64_t)c * per, n = imin(L, b + per) - b;
+        const int64_t need = imin(L, b + n + mask->w);
+        if ((e = cudaMemcpyAsync(dq + b * rb, hq + b * rb, n * rb, cudaMemcpyHostToDevice, sh)) != cudaSuccess ||
+            (need > kv_done &&
+             ((e = cudaMemcpyAsync(dk + kv_done * rb, hk + kv_done * rb, (need - kv_done) * rb,
+                                   cudaMemcpyHostToDevice, sh)) != cudaSuccess ||
+              (e = cudaMemcpyAsync(dv + kv_done * rb, hv + kv_done * rb, (need - kv_done) * rb,
+                                   cudaMemcpyHostToDevice, sh)) != cudaSuccess))) {
+            st = cuda_fail(e, "ga_attention_host: H2D");
+            break;
+        }
+        kv_done = need;
+        cudaEventRecord(ev[2 * c], sh);
+        cudaStreamWaitEvent(s, ev[2 * c], 0);
+        ga_opts o{};
+        o.q_begin = b;
+        o.q_rows = n;
+        o.kv_begin = 0;
+        o.kv_rows = L;
+        st = ga_attention_ex(dq + b * rb, dk, dv, mask, dout + b * rb, L, d, heads, dtype, &o, s);
+        if (st != GA_OK) break;
+        cudaEventRecord(ev[2 * c + 1], s);
+        cudaStreamWaitEvent(so, ev[2 * c + 1], 0);
+        if ((e = cudaMemcpyAsync((char *)out + b * rb, dout + b * rb, n * rb, cudaMemcpyDeviceToHost, so)) !=
+            cudaSuccess)
+            st = cuda_fail(e, "ga_attention_host: D2H");
+    }
+    // join: the caller's stream (and the frees enqueued on it) wait for both copy streams
+    cudaEventRecord(join, so);
+    cudaStreamWaitEvent(s, join, 0);
+    cudaEventRecord(ev[2 * nc - 2], sh); // reuse: H2D tail (covers an early break)
+    cudaStreamWaitEvent(s, ev[2 * nc - 2], 0);
+    for (auto x : ev) cudaEventDestroy(x);
+    return st;
+}
+
 ga_status ga_attention_host(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out, int64_t L,
                             int32_t d, int32_t heads, ga_dtype dtype, void *stream)
 {
@@ -434,6 +525,15 @@ ga_status ga_attention_host(const void *Q, const void *K, const void *V, const g
         return GA_ERR_OOM;
     }
     ga_status st = GA_OK;
+    if (mask && mask->kind == GA_MASK_WINDOW && mask->w >= 1 && L >= 2 * kHostPipeMinRows) {
+        st = host_window_pipeline(Q, K, V, mask, out, L, d, heads, dtype, s, (char *)dq, (char *)dk, (char *)dv,
+                                  (char *)dout);
+        cudaFreeAsync(dq, s);
+        cudaFreeAsync(dk, s);
+        cudaFreeAsync(dv, s);
+        cudaFreeAsync(dout, s);
+        return st;
+    }
     if ((e = cudaMemcpyAsync(dq, Q, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
         (e = cudaMemcpyAsync(dk, K, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
         (e = cudaMemcpyAsync(dv, V, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) {

@@ -586,11 +586,18 @@ def test_uniform_attention_is_neighbour_mean(ga, orc, fam, L, args, kernel):
     assert np.abs(got - want).max() <= 1e-3
 
 
-def test_host_entry_point_matches_device(ga):
-    L, H, d = 2048, 8, 64
-    cpu = synth.qkv(21, L, H, d, "bf16")
+@pytest.mark.parametrize("L,H,dt,win", [
+    (2048, 8, "bf16", (256, 2)),      # below the pipelining threshold: one launch
+    (65536, 8, "bf16", (256, 2)),     # cfg2 shape: 8 aligned chunks, copies overlapped
+    (20011, 2, "bf16", (128, 1)),     # ragged last chunk
+    (9000, 1, "f32", (33, 3)),        # fp32 edge kernel, chunked
+    (12289, 3, "f16", (1, 1)),        # w = 1: no halo
+])
+def test_host_entry_point_matches_device(ga, L, H, dt, win):
+    d = 64
+    cpu = synth.qkv(21, L, H, d, dt)
     q, k, v = (x.cuda() for x in cpu)
-    m = ga.Window(256, 2)
+    m = ga.Window(*win)
     dev = ga.attention(q, k, v, m)
     pinned = [x.pin_memory() for x in cpu]
     out = torch.empty_like(pinned[0]).pin_memory()
