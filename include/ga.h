@@ -195,7 +195,9 @@ ga_status ga_attention_ex(const void *Q, const void *K, const void *V, const ga_
    runs the attention, copies out back to host `out`, all enqueued on `stream` using the
    stream-ordered allocator (cudaMallocAsync).  Host buffers should be pinned for
    asynchronous copies; `out` is valid after the caller synchronises `stream`.  CSR arrays
-   in `mask` must already be DEVICE pointers. */
+   in `mask` must already be DEVICE pointers.  For WINDOW and CSR masks with L >= 8192 the
+   query range runs as 8 aligned chunks whose H2D, launch and D2H overlap on two internal
+   copy streams forked from and joined back to `stream` (results identical to one call). */
 ga_status ga_attention_host(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out,
                             int64_t L, int32_t d, int32_t heads, ga_dtype dtype, void *stream);
 

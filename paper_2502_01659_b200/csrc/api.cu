@@ -415,11 +415,12 @@ ga_status ga_attention(const void *Q, const void *K, const void *V, const ga_mas
     return ga_attention_ex(Q, K, V, mask, out, L, d, heads, dtype, nullptr, stream);
 }
 
-// Host-buffer path for Window masks: the query range is cut into kHostPipeChunks aligned
-// chunks (ga_query_alignment, so every row is computed exactly as by one launch).  Chunk c
-// needs Q rows [b, e) and K/V rows up to e + w (|i - j| < w), so its launch starts as soon
-// as those rows are in; H2D of the next chunk, the launch and D2H of the previous output
-// overlap on two copy streams forked from and joined back to the caller's stream.
+// Host-buffer path for Window and CSR masks: the query range is cut into kHostPipeChunks
+// aligned chunks (ga_query_alignment, so every row is computed exactly as by one launch).
+// Chunk c needs Q rows [b, e) and K/V rows up to e + w (Window: |i - j| < w; CSR: all of
+// K/V, copied with chunk 0), so its launch starts as soon as those rows are in; H2D of the
+// next chunk, the launch and D2H of the previous output overlap on two copy streams forked
+// from and joined back to the caller's stream.
 static const int kHostPipeChunks = 8;
 static const int64_t kHostPipeMinRows = 4096;
 
@@ -471,7 +472,7 @@ static ga_status host_window_pipeline(const void *Q, const void *K, const void *
     int64_t kv_done = 0;
     for (int c = 0; c < nc && st == GA_OK; ++c) {
         const int64_t b = (int64_t)c * per, n = imin(L, b + per) - b;
-        const int64_t need = imin(L, b + n + mask->w);
+        const int64_t need = mask->kind == GA_MASK_CSR ? L : imin(L, b + n + mask->w);
         if ((e = cudaMemcpyAsync(dq + b * rb, hq + b * rb, n * rb, cudaMemcpyHostToDevice, sh)) != cudaSuccess ||
             (need > kv_done &&
              ((e = cudaMemcpyAsync(dk + kv_done * rb, hk + kv_done * rb, (need - kv_done) * rb,
@@ -525,7 +526,8 @@ ga_status ga_attention_host(const void *Q, const void *K, const void *V, const g
         return GA_ERR_OOM;
     }
     ga_status st = GA_OK;
-    if (mask && mask->kind == GA_MASK_WINDOW && mask->w >= 1 && L >= 2 * kHostPipeMinRows) {
+    if (mask && ((mask->kind == GA_MASK_WINDOW && mask->w >= 1) || mask->kind == GA_MASK_CSR) &&
+        L >= 2 * kHostPipeMinRows) {
         st = host_window_pipeline(Q, K, V, mask, out, L, d, heads, dtype, s, (char *)dq, (char *)dk, (char *)dv,
                                   (char *)dout);
         cudaFreeAsync(dq, s);

@@ -592,12 +592,13 @@ def test_uniform_attention_is_neighbour_mean(ga, orc, fam, L, args, kernel):
     (20011, 2, "bf16", (128, 1)),     # ragged last chunk
     (9000, 1, "f32", (33, 3)),        # fp32 edge kernel, chunked
     (12289, 3, "f16", (1, 1)),        # w = 1: no halo
+    (20011, 2, "bf16", "csr"),        # CSR (BigBird without globals): K/V with chunk 0
 ])
 def test_host_entry_point_matches_device(ga, L, H, dt, win):
     d = 64
     cpu = synth.qkv(21, L, H, d, dt)
     q, k, v = (x.cuda() for x in cpu)
-    m = ga.Window(*win)
+    m = ga.mask_to_csr(ga.BigBird(64, 0, 8, seed=3), L) if win == "csr" else ga.Window(*win)
     dev = ga.attention(q, k, v, m)
     pinned = [x.pin_memory() for x in cpu]
     out = torch.empty_like(pinned[0]).pin_memory()
