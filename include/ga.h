@@ -153,9 +153,9 @@ typedef struct ga_opts {
     int64_t kv_begin, kv_rows;
     /* Device workspace, size from ga_workspace_size: needed by CSR inputs with rows above
        the heavy-row threshold; optional for LONGNET bf16/fp16 d=64 (partial states of the
-       tcgen05 block path — without it the library takes stream-ordered scratch with
-       cudaMallocAsync from the device's default pool, whose release threshold it raises so
-       freed blocks stay cached). */
+       tcgen05 block path — without it the library takes stream-ordered scratch from its
+       private per-device memory pool (cudaMallocFromPoolAsync; freed blocks stay cached in
+       that pool, the device's default pool is not modified)). */
     void *workspace;
     size_t workspace_bytes;
     /* Debug / work-optimality probes ("probe build").  When non-NULL a slower
@@ -193,7 +193,7 @@ ga_status ga_attention_ex(const void *Q, const void *K, const void *V, const ga_
 
 /* End-to-end variant on HOST buffers: copies Q,K,V (host, [L,heads,d]) to the device,
    runs the attention, copies out back to host `out`, all enqueued on `stream` using the
-   stream-ordered allocator (cudaMallocAsync).  Host buffers should be pinned for
+   stream-ordered allocator (libga's private pool, cudaMallocFromPoolAsync).  Host buffers should be pinned for
    asynchronous copies; `out` is valid after the caller synchronises `stream`.  CSR arrays
    in `mask` must already be DEVICE pointers.  For WINDOW and CSR masks with L >= 8192 the
    query range runs as 8 aligned chunks whose H2D, launch and D2H overlap on two internal
@@ -228,7 +228,7 @@ ga_status ga_mask_count(const ga_mask *pattern, int64_t *nnz_out);
 /* Materialise an implicit pattern as binary CSR on the device:
    degrees -> exclusive scan -> fill, columns ascending.  row_ptr: DEVICE int64 [L+1];
    col_idx: DEVICE int32 [nnz] with nnz from ga_mask_count.  The result equals the CPU
-   enumeration bit for bit.  Temporary scan storage is stream-ordered (cudaMallocAsync). */
+   enumeration bit for bit.  Temporary scan storage is stream-ordered (libga's private pool). */
 ga_status ga_mask_to_csr(const ga_mask *pattern, int64_t *row_ptr, int32_t *col_idx, void *stream);
 
 /* COO input ("COO" mask storage): convert an edge list
@@ -239,7 +239,7 @@ ga_status ga_mask_to_csr(const ga_mask *pattern, int64_t *row_ptr, int32_t *col_
    rows, cols: DEVICE int32 [n]; row_ptr: DEVICE int64 [L+1] (written); col_idx: DEVICE
    int32, capacity n (the first *nnz_out entries written, ascending per row); nnz_out: HOST,
    the number of distinct edges (the call synchronises `stream` to read it).  Scratch is
-   stream-ordered (cudaMallocAsync).  Errors: GA_ERR_INVALID_ARG (L <= 0 or L > 2^31-1,
+   stream-ordered (libga's private pool).  Errors: GA_ERR_INVALID_ARG (L <= 0 or L > 2^31-1,
    n < 0, NULL buffers), GA_ERR_MASK (an index outside [0, L); outputs then undefined),
    GA_ERR_CUDA. */
 ga_status ga_coo_to_csr(int64_t L, const int32_t *rows, const int32_t *cols, int64_t n, int64_t *row_ptr,
@@ -276,8 +276,9 @@ ga_status ga_comm_get_unique_id(void *id128);
 /* Collective over `world` processes: connect to rank 0 through the id, then (device >= 0)
    allocate the device barrier flags on CUDA device `device`.  device = -1 creates a
    host-only comm (bootstrap and ga_comm_host_allgather only).  Blocks until every rank has
-   joined (timeout 120 s -> GA_ERR_COMM).  *comm is owned by the caller until
-   ga_comm_destroy. */
+   joined (timeout 120 s -> GA_ERR_COMM).  Every pair of distinct devices must have peer
+   access (cudaDeviceCanAccessPeer; the kernels load peer rows over NVLink): otherwise every
+   rank returns GA_ERR_COMM.  *comm is owned by the caller until ga_comm_destroy. */
 ga_status ga_comm_create(int32_t world, int32_t rank, const void *id128, int32_t device, ga_comm **comm);
 
 /* Collective: allocate `bytes` (same on every rank) of DEVICE memory whose copies on all
@@ -298,7 +299,9 @@ ga_status ga_comm_barrier(ga_comm *comm, void *stream);
    (small control data; also the CPU test hook of the bootstrap). */
 ga_status ga_comm_host_allgather(ga_comm *comm, const void *mine, size_t bytes, void *all);
 
-/* *timed_out = 1 if a device barrier of this comm gave up waiting for a peer (synchronous). */
+/* *timed_out = 1 if a device barrier of this comm gave up waiting for a peer.  The flag lives
+   in device-mapped pinned host memory: no synchronisation, but it reflects only barriers that
+   have already executed (synchronise the stream first for a definite answer). */
 ga_status ga_comm_status(ga_comm *comm, int *timed_out);
 
 /* Sharded attention: this rank's query rows [row_begin, row_end) of a length-L sequence.
@@ -311,7 +314,9 @@ ga_status ga_comm_status(ga_comm *comm, int *timed_out);
    the entry barrier makes every rank's K/V visible, the exit barrier keeps them unchanged
    until every rank has finished reading.  opts: kernel choice, CSR workspace, probes (its
    q_/kv_ ranges are ignored).  Shards that are multiples of ga_query_alignment produce
-   rows bit-identical to ga_attention on one GPU. */
+   rows bit-identical to ga_attention on one GPU.  Failure of a peer: if either barrier
+   times out, this rank's `out` is overwritten with NaN (0xff bytes) on the stream, and every
+   later call on the comm returns GA_ERR_COMM without enqueuing anything. */
 ga_status ga_attention_sharded(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out,
                                int64_t L, int64_t row_begin, int64_t row_end, int32_t d, int32_t heads,
                                ga_dtype dtype, const ga_opts *opts, ga_comm *comm, void *stream);

@@ -90,6 +90,8 @@ class Comm:
         return [out.raw[i * n:(i + 1) * n] for i in range(self.world)]
 
     def timed_out(self) -> bool:
+        """True if a device barrier gave up waiting for a peer (reflects barriers that have
+        executed: synchronise first for a definite answer)."""
         t = ctypes.c_int()
         _abi.check(_abi.lib().ga_comm_status(self._h, ctypes.byref(t)))
         return bool(t.value)
@@ -112,6 +114,13 @@ class Comm:
                                                    out.data_ptr(), L, b, e, d, H, dtype_code(q.dtype),
                                                    ctypes.byref(o), self._h, _stream(q.device)))
         return out
+
+    def check(self) -> None:
+        """Synchronise this rank's device and raise if any barrier timed out (the sharded
+        output was then poisoned with NaN)."""
+        torch.cuda.synchronize(self.device)
+        if self.timed_out():
+            raise _abi.GaError(_abi.GA_ERR_COMM, "a device barrier timed out: a peer stalled; outputs are NaN")
 
     def close(self) -> None:
         if self._h is not None:

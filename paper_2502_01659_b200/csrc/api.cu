@@ -110,25 +110,44 @@ static ga_status make_devmask(const ga_mask *m, int64_t L, DevMask &M)
 
 static size_t dtype_bytes(ga_dtype dt) { return dt == GA_F32 ? 4 : 2; }
 
-// Stream-ordered scratch (cudaMallocAsync) comes from the current device's default pool;
-// keep freed blocks there between calls instead of returning them to the OS each
-// synchronisation (the default release threshold is 0), so repeated calls do not re-map
-// memory.  Once per device.
-void keep_stream_pool()
+// Stream-ordered scratch comes from a libga-private memory pool per device (cudaMemPoolCreate),
+// whose release threshold is raised so freed blocks stay cached between calls (no re-mapping
+// on every synchronisation).  The device's DEFAULT pool is left untouched, so other
+// allocators in the process (PyTorch's caching allocator, libraries using cudaMallocAsync)
+// see the usual behaviour; ga_scratch_trim() hands the cached blocks back.
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pool[64] = {};
+
+static cudaMemPool_t scratch_pool(int dev)
 {
-    static std::mutex mu;
-    static bool done[64] = {};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
-    std::lock_guard<std::mutex> g(mu);
-    if (done[dev]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    if (!g_pool[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        g_pool[dev] = pool;
     }
-    done[dev] = true;
+    return g_pool[dev];
 }
+
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t s)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    cudaMemPool_t pool = scratch_pool(dev);
+    if (!pool) return cudaErrorMemoryAllocation;
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+cudaError_t scratch_free(void *p, cudaStream_t s) { return p ? cudaFreeAsync(p, s) : cudaSuccess; }
 
 static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -172,10 +191,6 @@ static ga_status resolve(const void *Q, const void *K, const void *V, const ga_m
     DevMask M;
     ga_status st = make_devmask(mask, L, M);
     if (st != GA_OK) return st;
-    if (M.kind == GA_MASK_BIGBIRD) {
-        set_error("BIGBIRD masks are materialised with ga_mask_to_csr and run as CSR");
-        return GA_ERR_UNSUPPORTED;
-    }
     ga_opts o{};
     if (opts) o = *opts;
     if (o.q_begin < 0 || o.q_begin > L || o.q_rows < 0 || o.q_begin + o.q_rows > L) {
@@ -195,6 +210,14 @@ static ga_status resolve(const void *Q, const void *K, const void *V, const ga_m
         const char *vb = (const char *)V, *ve = vb + (size_t)o.kv_rows * row_bytes;
         if ((ob < ke && kb < oe) || (ob < ve && vb < oe)) {
             set_error("out must not alias K or V");
+            return GA_ERR_INVALID_ARG;
+        }
+        // out may BE Q (every launch sequence reads a row's Q before any launch writes that
+        // row's O: tests/test_gpu_contracts.py), but a shifted overlap would overwrite other
+        // rows' queries before they are read
+        const char *qb = (const char *)Q, *qe = qb + (size_t)o.q_rows * row_bytes;
+        if (ob != qb && ob < qe && qb < oe) {
+            set_error("out overlaps Q at a different offset (only out == Q is allowed)");
             return GA_ERR_INVALID_ARG;
         }
     }
@@ -220,6 +243,7 @@ static ga_status resolve(const void *Q, const void *K, const void *V, const ga_m
         p.state_mode = o.state_mode;
     }
     R.heavy = o.heavy_threshold > 0 ? o.heavy_threshold : kDefaultHeavy;
+    if (M.kind == GA_MASK_BIGBIRD) return bigbird_check(p);
     return GA_OK;
 }
 
@@ -233,11 +257,18 @@ static ga_status dispatch(AttnParams &p, ga_dtype dtype, const ga_opts *opts, in
         p.workspace_bytes = opts->workspace_bytes;
     }
     ga_status st;
-    if (p.state.m) { // carried state: the edge kernel writes (m, l, o) per (row, head)
-        if (kernel != GA_KERNEL_AUTO && kernel != GA_KERNEL_EDGE) {
-            set_error("a carried state runs on the edge kernel (kernel AUTO or EDGE)");
+    if (p.mask.kind == GA_MASK_BIGBIRD) { // implicit BigBird / Longformer (bigbird.cu)
+        if (probe) { set_error("probes are not supported for implicit BIGBIRD masks (run its CSR)"); return GA_ERR_UNSUPPORTED; }
+        if (kernel == GA_KERNEL_TILED) { set_error("no mma.sync band kernel for implicit BIGBIRD masks"); return GA_ERR_UNSUPPORTED; }
+        return launch_bigbird(p, dtype, s);
+    }
+    if (p.state.m) { // carried state: (m, l, o) per (row, head) from the tcgen05 window kernel or the edge kernel
+        if (kernel != GA_KERNEL_AUTO && kernel != GA_KERNEL_EDGE && kernel != GA_KERNEL_TC) {
+            set_error("a carried state runs on the tcgen05 window kernel or the edge kernel (kernel AUTO, TC or EDGE)");
             return GA_ERR_UNSUPPORTED;
         }
+        if (kernel != GA_KERNEL_EDGE && !probe && window_tc_supported(p, dtype)) return launch_window_tc(p, dtype, s);
+        if (kernel == GA_KERNEL_TC) { set_error("tcgen05 path does not support this (mask, dtype, d) with a state"); return GA_ERR_UNSUPPORTED; }
         return launch_edge(p, dtype, s);
     }
     if (p.mask.kind == GA_MASK_CSR) {
@@ -299,6 +330,15 @@ ga_status ga_workspace_size(const ga_mask *mask, int64_t L, int32_t d, int32_t h
         if (s_umma >= 0 && s_umma < (int)M.K) *bytes = longnet_umma_workspace(p, s_umma + 1);
         return GA_OK;
     }
+    if (M.kind == GA_MASK_BIGBIRD) { // window-part state + full-row partials (bigbird.cu)
+        AttnParams p{};
+        p.mask = M;
+        p.d = d;
+        p.H = heads;
+        p.q_rows = q_rows;
+        *bytes = bigbird_workspace(p, dtype);
+        return GA_OK;
+    }
     if (M.kind != GA_MASK_CSR) return GA_OK;
     int64_t C = opts && opts->heavy_threshold > 0 ? opts->heavy_threshold : kDefaultHeavy;
     *bytes = csr_heavy_workspace(q_rows, L, mask->nnz, heads, d, C);
@@ -328,10 +368,6 @@ ga_status ga_attention_sharded(const void *Q, const void *K, const void *V, cons
                   (long long)b, (long long)e, (long long)L, (long long)row_begin, (long long)row_end);
         return GA_ERR_INVALID_ARG;
     }
-    if (mask->kind == GA_MASK_BIGBIRD) {
-        set_error("BIGBIRD masks are materialised with ga_mask_to_csr and run as CSR");
-        return GA_ERR_UNSUPPORTED;
-    }
     DeviceGuard dg(comm->device);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int64_t rows = e - b;
@@ -343,13 +379,17 @@ ga_status ga_attention_sharded(const void *Q, const void *K, const void *V, cons
         set_error("K/V shard overruns its ga_comm_alloc buffer");
         return GA_ERR_INVALID_ARG;
     }
+    if (comm->timed_out_host && *comm->timed_out_host) {
+        set_error("a device barrier of this comm timed out earlier (a peer stalled): the comm is unusable");
+        return GA_ERR_COMM;
+    }
     ga_opts o{};
     if (opts) o = *opts;
     ga_status st = comm_device_barrier(comm, s); // every rank's K/V shard is complete
     if (st != GA_OK) return st;
     if (rows > 0) {
-        if (mask->kind == GA_MASK_CSR) {
-            // unstructured columns: all-gather K and V (copy engines, peer -> local), then a
+        if (mask->kind == GA_MASK_CSR || mask->kind == GA_MASK_BIGBIRD) {
+            // unstructured columns (explicit CSR, BigBird's random columns): all-gather K and V (copy engines, peer -> local), then a
             // local launch over the full-length buffers
             const size_t full = (size_t)L * row_bytes;
             if (comm->gather_bytes < full) {
@@ -397,7 +437,11 @@ ga_status ga_attention_sharded(const void *Q, const void *K, const void *V, cons
         }
         if (st != GA_OK) return st;
     }
-    return comm_device_barrier(comm, s); // no rank changes its K/V while others still read it
+    st = comm_device_barrier(comm, s); // no rank changes its K/V while others still read it
+    // a peer that missed either barrier may have left its K/V rows unwritten: poison this
+    // rank's output (NaN) instead of returning silently wrong rows
+    if (st == GA_OK && out) st = comm_poison_on_timeout(comm, out, (size_t)rows * row_bytes, s);
+    return st;
 }
 
 ga_status ga_state_finalize(const ga_state *state, int64_t rows, int32_t heads, int32_t d, ga_dtype dtype, void *out,
@@ -472,7 +516,9 @@ static ga_status host_window_pipeline(const void *Q, const void *K, const void *
     int64_t kv_done = 0;
     for (int c = 0; c < nc && st == GA_OK; ++c) {
         const int64_t b = (int64_t)c * per, n = imin(L, b + per) - b;
-        const int64_t need = mask->kind == GA_MASK_CSR ? L : imin(L, b + n + mask->w);
+        // K/V rows [0, need) are on the device once this chunk's copies land (saturating:
+        // a huge w must not overflow b + n + w)
+        const int64_t need = mask->kind == GA_MASK_CSR || mask->w >= L - (b + n) ? L : b + n + mask->w;
         if ((e = cudaMemcpyAsync(dq + b * rb, hq + b * rb, n * rb, cudaMemcpyHostToDevice, sh)) != cudaSuccess ||
             (need > kv_done &&
              ((e = cudaMemcpyAsync(dk + kv_done * rb, hk + kv_done * rb, (need - kv_done) * rb,
@@ -488,8 +534,11 @@ static ga_status host_window_pipeline(const void *Q, const void *K, const void *
         ga_opts o{};
         o.q_begin = b;
         o.q_rows = n;
+        // the launch sees only the rows copied so far: tile loads past `need` (whole 64-key
+        // chunks) are zero-filled by TMA instead of reading rows still in flight on the copy
+        // stream or uninitialised pool memory (NaN x 0 = NaN)
         o.kv_begin = 0;
-        o.kv_rows = L;
+        o.kv_rows = need;
         st = ga_attention_ex(dq + b * rb, dk, dv, mask, dout + b * rb, L, d, heads, dtype, &o, s);
         if (st != GA_OK) break;
         cudaEventRecord(ev[2 * c + 1], s);
@@ -512,17 +561,16 @@ ga_status ga_attention_host(const void *Q, const void *K, const void *V, const g
 {
     if (!Q || !K || !V || !out) { set_error("host buffers must be non-NULL"); return GA_ERR_INVALID_ARG; }
     if (dtype != GA_F32 && dtype != GA_BF16 && dtype != GA_F16) { set_error("dtype invalid"); return GA_ERR_INVALID_ARG; }
-    keep_stream_pool();
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const size_t bytes = (size_t)L * heads * d * dtype_bytes(dtype);
     void *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
     cudaError_t e;
-    if ((e = cudaMallocAsync(&dq, bytes, s)) != cudaSuccess || (e = cudaMallocAsync(&dk, bytes, s)) != cudaSuccess ||
-        (e = cudaMallocAsync(&dv, bytes, s)) != cudaSuccess || (e = cudaMallocAsync(&dout, bytes, s)) != cudaSuccess) {
+    if ((e = scratch_alloc(&dq, bytes, s)) != cudaSuccess || (e = scratch_alloc(&dk, bytes, s)) != cudaSuccess ||
+        (e = scratch_alloc(&dv, bytes, s)) != cudaSuccess || (e = scratch_alloc(&dout, bytes, s)) != cudaSuccess) {
         if (dq) cudaFreeAsync(dq, s);
         if (dk) cudaFreeAsync(dk, s);
         if (dv) cudaFreeAsync(dv, s);
-        set_error("ga_attention_host: cudaMallocAsync: %s", cudaGetErrorString(e));
+        set_error("ga_attention_host: scratch allocation: %s", cudaGetErrorString(e));
         return GA_ERR_OOM;
     }
     ga_status st = GA_OK;
@@ -563,6 +611,10 @@ ga_status ga_query_alignment(const ga_mask *mask, int32_t d, ga_dtype dtype, int
     *tokens = 1;
     p.q_rows = M.L;
     p.kv_rows = M.L;
+    if (M.kind == GA_MASK_BIGBIRD) { // its window part runs on the window kernels
+        p.mask.kind = GA_MASK_WINDOW;
+        p.mask.m = (M.w - 1) / M.r;
+    }
     if (window_tc_supported(p, dtype)) *tokens = window_tc_tile_rows() * M.r;
     else if (window_tiled_supported(p, dtype)) *tokens = band_tile_rows() * M.r;
     else if (longnet_tc_supported(p, dtype)) *tokens = M.w0;

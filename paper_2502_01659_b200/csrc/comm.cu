@@ -171,7 +171,10 @@ __global__ void comm_barrier_kernel(uint64_t *const *peer_flags, uint64_t *my_fl
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my_flags + q) : "memory");
             if (v >= gen) break;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > kBarrierTimeoutNs) { atomicExch(timed_out, 1); break; }
+            if (t - t0 > kBarrierTimeoutNs) { // mapped host flag: a plain system-scope store
+                asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(timed_out), "r"(1) : "memory");
+                break;
+            }
             __nanosleep(200);
         }
     }
@@ -188,10 +191,25 @@ ga_status comm_device_barrier(ga_comm *c, cudaStream_t s)
     if (st != GA_OK) return st;
     ++c->gen;
     uint64_t *mine = reinterpret_cast<uint64_t *>(c->flag_alloc->local);
-    int *timed_out = reinterpret_cast<int *>(mine + c->world);
     comm_barrier_kernel<<<1, 32, 0, s>>>((uint64_t *const *)tbl, mine,
-                                         c->rank, c->world, c->gen, timed_out);
+                                         c->rank, c->world, c->gen, c->timed_out_dev);
     GA_CHECK_LAUNCH("comm_barrier_kernel");
+    return GA_OK;
+}
+
+__global__ void comm_poison_kernel(const int *timed_out, uint4 *out, size_t n16)
+{
+    if (*(const volatile int *)timed_out == 0) return; // the common case: one load per CTA
+    const uint4 nan = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = nan;
+}
+
+ga_status comm_poison_on_timeout(ga_comm *c, void *out, size_t bytes, cudaStream_t s)
+{
+    if (c->world == 1 || !c->timed_out_dev || !out || bytes < 16) return GA_OK;
+    comm_poison_kernel<<<64, 256, 0, s>>>(c->timed_out_dev, reinterpret_cast<uint4 *>(out), bytes / 16);
+    GA_CHECK_LAUNCH("comm_poison_kernel");
     return GA_OK;
 }
 
@@ -324,9 +342,43 @@ ga_status ga_comm_create(int32_t world, int32_t rank, const void *id128, int32_t
     } else if (lfd >= 0) {
         close(lfd);
     }
-    if (device >= 0) { // barrier flags: uint64 [world] + int timed_out, zeroed before use
+    if (device >= 0) { // barrier flags: uint64 [world], zeroed before use; timeout flag in mapped host memory
         void *flags = nullptr;
-        ga_status st = ga_comm_alloc(c, sizeof(uint64_t) * world + 64, &flags);
+        ga_status st = GA_OK;
+        {
+            DeviceGuard dg(device);
+            // every pair of devices must reach each other's memory (the kernels load peer rows
+            // over NVLink); ranks sharing one device need no peer access
+            int ndev = 0;
+            cudaGetDeviceCount(&ndev);
+            std::vector<int> devs(world);
+            st = host_allgather(c, &device, sizeof(int), devs.data());
+            for (int q = 0; st == GA_OK && q < world; ++q) {
+                if (devs[q] == device) continue;
+                int can = 0;
+                if (devs[q] < 0 || devs[q] >= ndev || cudaDeviceCanAccessPeer(&can, device, devs[q]) != cudaSuccess ||
+                    !can) {
+                    set_error("comm: device %d cannot access peer device %d (cudaDeviceCanAccessPeer)", device, devs[q]);
+                    st = GA_ERR_COMM;
+                }
+            }
+            int ok_all = st == GA_OK, all[64] = {};
+            if (world <= 64 && host_allgather(c, &ok_all, sizeof(int), all) == GA_OK)
+                for (int q = 0; q < world; ++q)
+                    if (!all[q] && st == GA_OK) { set_error("comm: peer access missing on rank %d", q); st = GA_ERR_COMM; }
+            void *h = nullptr;
+            if (st == GA_OK) {
+                cudaError_t e = cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable);
+                if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->timed_out_dev), h, 0);
+                if (e != cudaSuccess) st = cuda_fail(e, "comm: timeout flag");
+                else {
+                    c->timed_out_host = static_cast<volatile int *>(h);
+                    *c->timed_out_host = 0;
+                }
+            }
+        }
+        if (st != GA_OK) { ga_comm_destroy(c); return st; }
+        st = ga_comm_alloc(c, sizeof(uint64_t) * world + 64, &flags);
         if (st == GA_OK) {
             DeviceGuard dg(device);
             cudaError_t e = cudaMemset(flags, 0, sizeof(uint64_t) * world + 64);
@@ -425,12 +477,8 @@ ga_status ga_comm_host_allgather(ga_comm *c, const void *mine, size_t bytes, voi
 ga_status ga_comm_status(ga_comm *c, int *timed_out)
 {
     if (!c || !timed_out) { set_error("NULL argument"); return GA_ERR_INVALID_ARG; }
-    *timed_out = 0;
-    if (!c->flag_alloc) return GA_OK;
-    DeviceGuard dg(c->device);
-    const int *p = reinterpret_cast<const int *>(reinterpret_cast<uint64_t *>(c->flag_alloc->local) + c->world);
-    cudaError_t e = cudaMemcpy(timed_out, p, sizeof(int), cudaMemcpyDeviceToHost);
-    return e == cudaSuccess ? GA_OK : cuda_fail(e, "ga_comm_status");
+    *timed_out = c->timed_out_host ? *c->timed_out_host : 0;
+    return GA_OK;
 }
 
 ga_status ga_comm_destroy(ga_comm *c)
@@ -446,6 +494,7 @@ ga_status ga_comm_destroy(ga_comm *c)
         }
         if (c->gather_k) cudaFree(c->gather_k);
         if (c->gather_v) cudaFree(c->gather_v);
+        if (c->timed_out_host) cudaFreeHost(const_cast<int *>(c->timed_out_host));
     }
     c->allocs.clear();
     close_fds(c);

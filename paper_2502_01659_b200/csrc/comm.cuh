@@ -24,6 +24,11 @@ struct ga_comm {
     // device barrier state: flags[q] (in the first symmetric allocation) is written by rank q
     GaSymAlloc *flag_alloc = nullptr;
     uint64_t gen = 0;
+    // set to 1 by a device barrier that gave up waiting for a peer: pinned, device-mapped host
+    // memory, so the host reads it without synchronising (ga_comm_status, and the entry check
+    // of ga_attention_sharded)
+    volatile int *timed_out_host = nullptr;
+    int *timed_out_dev = nullptr;
     // CSR / BigBird all-gather scratch: full-length K and V (grown on demand)
     void *gather_k = nullptr, *gather_v = nullptr;
     size_t gather_bytes = 0;
@@ -35,6 +40,9 @@ GaSymAlloc *comm_find(ga_comm *c, const void *p);
 // DEVICE table of the peers' copies of `p` (same offset in every rank's allocation)
 ga_status comm_peer_table(ga_comm *c, const void *p, const char *const **table);
 ga_status comm_device_barrier(ga_comm *c, cudaStream_t s);
+// after a sharded call: if any barrier of this comm timed out, overwrite `bytes` of `out` with
+// 0xff (NaN in fp32 / bf16 / fp16) so a stalled peer cannot yield silently wrong rows
+ga_status comm_poison_on_timeout(ga_comm *c, void *out, size_t bytes, cudaStream_t s);
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev)

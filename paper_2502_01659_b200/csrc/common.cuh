@@ -14,7 +14,9 @@ namespace ga {
 void set_error(const char *fmt, ...);
 ga_status cuda_fail(cudaError_t e, const char *where);
 void note_launches(int n); // telemetry: kernels launched by the library (ga_launch_count)
-void keep_stream_pool();   // default mem pool keeps freed blocks (cudaMallocAsync scratch)
+// stream-ordered scratch from libga's private per-device pool (freed blocks stay cached there)
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t s);
+cudaError_t scratch_free(void *p, cudaStream_t s);
 
 #define GA_CHECK_LAUNCH(where)                                                     \
     do {                                                                           \
@@ -230,6 +232,12 @@ int longnet_umma_levels(const AttnParams &p, ga_dtype dt);
 size_t longnet_umma_workspace(const AttnParams &p, int h0);
 bool window_tc_supported(const AttnParams &p, ga_dtype dt);
 ga_status launch_window_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s);
+size_t full_rows_partials_bytes(int64_t F, int64_t Lm, int32_t H, int32_t d);
+ga_status launch_full_rows(const AttnParams &p, ga_dtype dt, const int64_t *nfull_packed, const int64_t *full_row,
+                           float *fpart, int64_t F, cudaStream_t s);
+ga_status bigbird_check(const AttnParams &p);
+size_t bigbird_workspace(const AttnParams &p, ga_dtype dt);
+ga_status launch_bigbird(const AttnParams &p, ga_dtype dt, cudaStream_t s);
 
 ga_status maskgen_to_csr(const DevMask &M, int64_t *row_ptr, int32_t *col_idx, cudaStream_t s);
 ga_status mask_validate(const DevMask &M, cudaStream_t s, int *ok);

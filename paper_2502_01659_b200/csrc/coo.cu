@@ -73,10 +73,9 @@ extern "C" ga_status ga_coo_to_csr(int64_t L, const int32_t *rows, const int32_t
     cub::DeviceSelect::Unique(nullptr, uniq_bytes, (const int64_t *)nullptr, (int64_t *)nullptr, (int64_t *)nullptr,
                               n1, s);
     const size_t tmp_bytes = sort_bytes > uniq_bytes ? sort_bytes : uniq_bytes;
-    keep_stream_pool();
     char *buf = nullptr;
     const size_t kb = (size_t)n1 * sizeof(int64_t);
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&buf), 2 * kb + 256 + tmp_bytes, s);
+    cudaError_t e = scratch_alloc(reinterpret_cast<void **>(&buf), 2 * kb + 256 + tmp_bytes, s);
     if (e != cudaSuccess) return cuda_fail(e, "ga_coo_to_csr scratch");
     int64_t *keys = reinterpret_cast<int64_t *>(buf), *sorted = reinterpret_cast<int64_t *>(buf + kb);
     int64_t *nsel = reinterpret_cast<int64_t *>(buf + 2 * kb);
@@ -114,7 +113,7 @@ extern "C" ga_status ga_coo_to_csr(int64_t L, const int32_t *rows, const int32_t
             break;
         }
     } while (0);
-    cudaFreeAsync(buf, s);
+    scratch_free(buf, s);
     if (st != GA_OK) return st;
     if (h_bad) {
         set_error("ga_coo_to_csr: an edge index lies outside [0, L)");

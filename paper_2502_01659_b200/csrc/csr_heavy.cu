@@ -171,14 +171,14 @@ __global__ void __launch_bounds__(256) heavy_merge_kernel(AttnParams p, const in
 // the partial (m, l, o~) of each (row, chunk) in natural dim order.
 template <typename T, int D>
 __global__ void __launch_bounds__(FULL_THREADS) full_rows_kernel(const __grid_constant__ AttnParams p,
-                                                                 const int64_t *cnt_scanned, const int64_t *full_row,
+                                                                 const int64_t *nfull_packed, const int64_t *full_row,
                                                                  int64_t ntiles, float *fpart)
 {
     using G = tc::Geo<D>;
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int H = p.H;
-    const int64_t nfull = cnt_scanned[p.q_rows] >> 40;
+    const int64_t nfull = *nfull_packed >> 40;
     const int64_t ch = blockIdx.x; // one CTA per (key chunk, head) walks the tiles of full rows
     const int h = (int)(blockIdx.y);
     (void)ntiles;
@@ -269,13 +269,13 @@ __global__ void __launch_bounds__(FULL_THREADS) full_rows_kernel(const __grid_co
 // one warp per (full row, head): (+)-merge its NCH chunk partials, normalise, store
 template <typename T, int D>
 __global__ void __launch_bounds__(256) full_merge_kernel(const __grid_constant__ AttnParams p,
-                                                         const int64_t *cnt_scanned, const int64_t *full_row,
+                                                         const int64_t *nfull_packed, const int64_t *full_row,
                                                          const float *fpart)
 {
     const int lane = threadIdx.x & 31;
     const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int H = p.H;
-    const int64_t nfull = cnt_scanned[p.q_rows] >> 40;
+    const int64_t nfull = *nfull_packed >> 40;
     if (gw >= nfull * H) return;
     const int64_t f = gw / H;
     const int h = (int)(gw - f * H);
@@ -307,8 +307,11 @@ __global__ void __launch_bounds__(256) full_merge_kernel(const __grid_constant__
     }
 }
 
+// nfull_packed: DEVICE int64 whose bits 40-63 hold the number of full rows (the last entry of
+// the scanned heavy-row counts, or a count written by the BigBird prep kernel); full_row:
+// their local query rows; F: a host upper bound on that number
 template <typename T, int D>
-static ga_status launch_full_t(const AttnParams &p, const int64_t *cnt, const int64_t *full_row, float *fpart,
+static ga_status launch_full_t(const AttnParams &p, const int64_t *nfull_packed, const int64_t *full_row, float *fpart,
                                int64_t F, cudaStream_t s)
 {
     if (F == 0) return GA_OK;
@@ -320,10 +323,10 @@ static ga_status launch_full_t(const AttnParams &p, const int64_t *cnt, const in
         cudaFuncSetAttribute(full_rows_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    full_rows_kernel<T, D><<<dim3((unsigned)NCH, (unsigned)p.H), FULL_THREADS, smem, s>>>(p, cnt, full_row, ntiles,
-                                                                                          fpart);
+    full_rows_kernel<T, D><<<dim3((unsigned)NCH, (unsigned)p.H), FULL_THREADS, smem, s>>>(p, nfull_packed, full_row,
+                                                                                          ntiles, fpart);
     GA_CHECK_LAUNCH("full_rows_kernel");
-    full_merge_kernel<T, D><<<(unsigned)((F * p.H + 7) / 8), 256, 0, s>>>(p, cnt, full_row, fpart);
+    full_merge_kernel<T, D><<<(unsigned)((F * p.H + 7) / 8), 256, 0, s>>>(p, nfull_packed, full_row, fpart);
     GA_CHECK_LAUNCH("full_merge_kernel");
     return GA_OK;
 }
@@ -334,7 +337,7 @@ static ga_status launch_heavy_t(const AttnParams &p, int64_t *cnt, int64_t *item
                                 cudaStream_t s)
 {
     if constexpr (sizeof(T) == 2) {
-        const ga_status st = launch_full_t<T, D>(p, cnt, full_row, fpart, F, s);
+        const ga_status st = launch_full_t<T, D>(p, cnt + p.q_rows, full_row, fpart, F, s);
         if (st != GA_OK) return st;
     }
     const int64_t warps = I * p.H;
@@ -354,6 +357,30 @@ static ga_status launch_heavy_d(const AttnParams &p, int64_t *cnt, int64_t *ir, 
     case 32: return launch_heavy_t<T, 32>(p, cnt, ir, ic, part, I, fr, fp, F, s);
     case 64: return launch_heavy_t<T, 64>(p, cnt, ir, ic, part, I, fr, fp, F, s);
     case 128: return launch_heavy_t<T, 128>(p, cnt, ir, ic, part, I, fr, fp, F, s);
+    }
+    set_error("d=%d unsupported", p.d);
+    return GA_ERR_UNSUPPORTED;
+}
+
+size_t full_rows_partials_bytes(int64_t F, int64_t Lm, int32_t H, int32_t d)
+{
+    return sizeof(float) * (size_t)F * full_chunks(Lm) * H * (d + 2);
+}
+
+ga_status launch_full_rows(const AttnParams &p, ga_dtype dt, const int64_t *nfull_packed, const int64_t *full_row,
+                           float *fpart, int64_t F, cudaStream_t s)
+{
+    if (dt == GA_F32 || p.mask.L % 16 != 0) {
+        set_error("full-row tiles need bf16/fp16 and L %% 16 == 0");
+        return GA_ERR_UNSUPPORTED;
+    }
+    switch (p.d) {
+    case 32: return dt == GA_BF16 ? launch_full_t<__nv_bfloat16, 32>(p, nfull_packed, full_row, fpart, F, s)
+                                  : launch_full_t<__half, 32>(p, nfull_packed, full_row, fpart, F, s);
+    case 64: return dt == GA_BF16 ? launch_full_t<__nv_bfloat16, 64>(p, nfull_packed, full_row, fpart, F, s)
+                                  : launch_full_t<__half, 64>(p, nfull_packed, full_row, fpart, F, s);
+    case 128: return dt == GA_BF16 ? launch_full_t<__nv_bfloat16, 128>(p, nfull_packed, full_row, fpart, F, s)
+                                   : launch_full_t<__half, 128>(p, nfull_packed, full_row, fpart, F, s);
     }
     set_error("d=%d unsupported", p.d);
     return GA_ERR_UNSUPPORTED;

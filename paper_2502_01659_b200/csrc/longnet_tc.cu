@@ -420,15 +420,14 @@ ga_status launch_longnet_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s, bo
                 partials = reinterpret_cast<float *>(p.workspace);
             } else {
                 void *w = nullptr;
-                keep_stream_pool();
-                cudaError_t e = cudaMallocAsync(&w, need, s);
-                if (e != cudaSuccess) return cuda_fail(e, "LongNet partials: cudaMallocAsync");
+                cudaError_t e = scratch_alloc((void **)&w, need, s);
+                if (e != cudaSuccess) return cuda_fail(e, "LongNet partials: scratch allocation");
                 partials = reinterpret_cast<float *>(w);
                 owned = true;
             }
         }
         ga_status st = launch_longnet_umma(p, dt, lp.seg0, lp.n_seg, s_umma, partials, s);
-        if (owned) cudaFreeAsync(partials, s);
+        if (owned) scratch_free(partials, s);
         if (st != GA_OK) return st;
         s_done = (int)M.K;
     }

@@ -102,12 +102,12 @@ ga_status scan_exclusive_i64(int64_t *data, int64_t n, cudaStream_t s)
     if (n <= 0) return GA_OK;
     const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
     int64_t *sums = nullptr;
-    cudaError_t e = cudaMallocAsync(&sums, sizeof(int64_t) * nb, s);
-    if (e != cudaSuccess) return cuda_fail(e, "scan: cudaMallocAsync");
+    cudaError_t e = scratch_alloc((void **)&sums, sizeof(int64_t) * nb, s);
+    if (e != cudaSuccess) return cuda_fail(e, "scan: scratch allocation");
     scan_reduce_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(data, n, sums);
     scan_sums_kernel<<<1, SCAN_THREADS, 0, s>>>(sums, nb);
     scan_apply_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(data, n, sums);
-    e = cudaFreeAsync(sums, s);
+    e = scratch_free(sums, s);
     if (e != cudaSuccess) return cuda_fail(e, "scan: cudaFreeAsync");
     note_launches(2); // + 1 below: three scan kernels
     GA_CHECK_LAUNCH("scan kernels");
@@ -288,14 +288,14 @@ __global__ void validate_kernel(DevMask M, int *bad)
 ga_status mask_validate(const DevMask &M, cudaStream_t s, int *ok)
 {
     int *bad = nullptr;
-    cudaError_t e = cudaMallocAsync(&bad, sizeof(int), s);
-    if (e != cudaSuccess) return cuda_fail(e, "validate: cudaMallocAsync");
+    cudaError_t e = scratch_alloc((void **)&bad, sizeof(int), s);
+    if (e != cudaSuccess) return cuda_fail(e, "validate: scratch allocation");
     cudaMemsetAsync(bad, 0, sizeof(int), s);
     validate_kernel<<<(unsigned)((M.L + 1 + 255) / 256), 256, 0, s>>>(M, bad);
     GA_CHECK_LAUNCH("validate_kernel");
     int h = 1;
     cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
-    cudaFreeAsync(bad, s);
+    scratch_free(bad, s);
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, "validate: sync");
     *ok = h == 0;

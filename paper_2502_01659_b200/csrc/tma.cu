@@ -40,13 +40,15 @@ struct Key {
 static bool encode_uncached(CUtensorMap *map, const void *base, int64_t ntok, int H, int D, int r, int box_rows);
 static bool encode_gather_uncached(CUtensorMap *map, const void *base, int64_t ntok, int H, int D);
 
-// Encoding is host work on every launch; a small cache keyed by (buffer, shape, stride,
-// box) serves the repeated launches of a training / serving loop.
+// Encoding is host work on every launch; a cache keyed by (buffer, shape, stride, box)
+// serves the repeated launches of a training / serving loop.  64 entries: the host pipeline
+// (8 chunks x Q/out maps + K/V) and a few device-path callers fit without evicting each other.
+static const int kCache = 64;
 bool encode_rows(CUtensorMap *map, const void *base, int64_t ntok, int H, int D, int r, int box_rows)
 {
     static std::mutex mu;
-    static Key keys[16];
-    static CUtensorMap maps[16];
+    static Key keys[kCache];
+    static CUtensorMap maps[kCache];
     static int n = 0, next = 0;
     const Key k{base, ntok, H, D, r, box_rows};
     {
@@ -61,8 +63,8 @@ bool encode_rows(CUtensorMap *map, const void *base, int64_t ntok, int H, int D,
     std::lock_guard<std::mutex> g(mu);
     keys[next] = k;
     maps[next] = *map;
-    next = (next + 1) % 16;
-    if (n < 16) ++n;
+    next = (next + 1) % kCache;
+    if (n < kCache) ++n;
     return true;
 }
 

@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         // deferred epilogue of the previous tile
         bool pend_epi = false, pend_rel = false;
         int32_t p_it = 0; // previous tile's item (its geometry is recomputed: fewer live registers)
-        float l_prev = 0.f;
+        float l_prev = 0.f, m_prev = -INFINITY;
         uint32_t cnt_prev = 0, tix_prev = 0;
         auto release = [&]() { // the previous tile's O store has read its Q buffer: hand it back
             if (lane == 0) {
@@ -494,6 +494,64 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             }
             __syncwarp();
             pend_rel = false;
+        };
+        // carried-state epilogue (ga_opts.state): this row's (m, l, o~) in the
+        // log2 domain, written or (+)-combined into the caller's fp32 buffers (m is the row's
+        // softmax reference: its running max, or within 2^kTau of it after a lazy rescale —
+        // any reference combines exactly); with p.out also the normalised row
+        auto state_epilogue = [&](uint32_t tO, int32_t c, int32_t h, int32_t x, int32_t alo, int32_t ahi) {
+            const bool valid = x >= alo && x < ahi;
+            const int64_t t = (int64_t)c + (int64_t)x * r - p.q_begin; // local query row
+            const size_t rh = valid ? (size_t)t * H + h : 0;
+            float mm = m_prev, ll = l_prev, a = 1.f, b = 0.f;
+            bool mix = false;
+            if (valid && p.state_mode == GA_STATE_ACCUMULATE) {
+                const float l2 = p.state.l[rh];
+                if (l2 > 0.f) { // l == 0 marks an empty state (its m is ignored)
+                    const float m2 = p.state.m[rh];
+                    const float mn = ll > 0.f ? fmaxf(mm, m2) : m2;
+                    a = ll > 0.f ? ex2(mm - mn) : 0.f;
+                    b = ex2(m2 - mn);
+                    ll = ll * a + l2 * b;
+                    mm = mn;
+                    mix = true;
+                }
+            }
+            const float inv = ll > 0.f ? 1.f / ll : 0.f;
+            float4 *so = reinterpret_cast<float4 *>(p.state.o + rh * D);
+            char *orow = p.out ? reinterpret_cast<char *>(p.out) + (size_t)t * row_bytes + (size_t)h * D * sizeof(T)
+                               : nullptr;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                float o[32];
+                tmem_ld32(tO + 32 * half, o); // warp-collective: every lane
+                tmem_wait_ld();
+                if (!valid) continue;
+#pragma unroll
+                for (int qq = 0; qq < 8; ++qq) {
+                    float4 v = make_float4(o[4 * qq], o[4 * qq + 1], o[4 * qq + 2], o[4 * qq + 3]);
+                    if (mix) {
+                        const float4 u = so[8 * half + qq];
+                        v.x = v.x * a + u.x * b;
+                        v.y = v.y * a + u.y * b;
+                        v.z = v.z * a + u.z * b;
+                        v.w = v.w * a + u.w * b;
+                    }
+                    so[8 * half + qq] = v;
+                    o[4 * qq] = v.x * inv;
+                    o[4 * qq + 1] = v.y * inv;
+                    o[4 * qq + 2] = v.z * inv;
+                    o[4 * qq + 3] = v.w * inv;
+                }
+                if (orow) {
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) stg16(orow + (4 * half + qq) * 16, pack<T>(o + 8 * qq));
+                }
+            }
+            if (valid) {
+                p.state.m[rh] = mm;
+                p.state.l[rh] = ll;
+            }
         };
         auto epilogue = [&]() {
             pend_epi = false;
@@ -513,6 +571,12 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             // full tile: stage this warp's 32 rows in the tile's Q buffer (the tile's S MMAs
             // completed) in the TMA layout and store them with one 32-row box, released to the
             // loader later; tile cut by the query range / sequence end: plain stores of valid rows
+            if (p.state.m) { // carried state (ga_state): fp32 (m, l, o~) per row, plain stores
+                state_epilogue(tO, p_c, p_h, x, p_alo, p_ahi);
+                if (lane == 0) mbar_arrive(bar(bars, B_QEMPTY + 2 * w + (int)(tix_prev & 1)));
+                __syncwarp();
+                return;
+            }
             const uint32_t sO = sbase + OFF_Q + (uint32_t)(2 * w + (tix_prev & 1)) * QBYTES;
             char *orow = nullptr;
             if (cut && x >= p_alo && x < p_ahi)
@@ -678,6 +742,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             pend_epi = true;
             p_it = it;
             l_prev = l_run;
+            m_prev = m_run;
             cnt_prev = cnt;
             tix_prev = ntile;
             ++ntile;

@@ -612,8 +612,8 @@ def test_errors_are_reported(ga):
     q, k, v = ga.qkv_device(1, L, H, d, torch.bfloat16)
     with pytest.raises(ga.GaError, match="INVALID_ARG"):
         ga.attention(q, k, v, ga.Window(8), out=k)
-    with pytest.raises(ga.GaError, match="UNSUPPORTED"):
-        ga.attention(q, k, v, ga.BigBird(8, 2, 2))
+    with pytest.raises(ga.GaError, match="UNSUPPORTED"):  # implicit BigBird needs its window part
+        ga.attention(q, k, v, ga.BigBird(8, 2, 2, parts=ga.BB_GLOBAL))
     q48 = torch.zeros(L, 1, 48, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ga.GaError, match="UNSUPPORTED"):
         ga.attention(q48, q48.clone(), q48.clone(), ga.Window(8))
