@@ -1,15 +1,21 @@
 #!/usr/bin/env python
 """bench.py — graph-view masked attention (arXiv 2502.01659) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg4]
+                    [--scaling weak|strong] [--no-per-config] [--max-context]
 
 One "step" is one pass of the whole hot path (neighbour enumeration, scores, online
 softmax, aggregation — one ga_attention call, or one ga_attention_sharded call per rank at N>1)
-over the configuration's full synthetic input.  Default workload: BASELINE.json configs[1]
-(L=65536, 8 heads, d=64, bf16, dilated window w=256 r=2) on one B200.  N>1 (torchrun,
-one process per GPU) is weak scaling: every rank owns L query rows of an N*L-token
-sequence; its K/V shard sits in a symmetric CUDA-IPC buffer and the kernels read the halo /
-long-range rows they need from the other ranks' HBM over NVLink (CSR: K/V all-gather).
+over the configuration's full synthetic input.  Default workload: the largest single-GPU
+configuration of BASELINE.json, configs[3] (cfg4: L=2^24, d=64, bf16, LongNet(w0=2048,
+alpha=2) implicit).  At N=1 the line also carries `per_config`: cfg2, cfg3 (explicit CSR, as
+BASELINE.json names it), cfg3i (the same BigBird mask as an implicit descriptor) and cfg5
+(L=160M, Window(128)), each with its own time, edges/s and roofline.
+
+N>1 (torchrun, one process per GPU): --scaling weak (default) gives every rank L query rows
+of an N*L-token sequence; --scaling strong cuts one L-token sequence into N shards.  K/V
+shards sit in symmetric CUDA-IPC buffers and the kernels read the halo / long-range rows they
+need from the other ranks' HBM over NVLink (CSR / BigBird: K/V all-gather).
 
 metric: attention edges/s = (mask nnz x heads) / step time, whole job.
 """
@@ -33,10 +39,13 @@ CONFIGS = {
     "cfg1": dict(L=1024, H=1, d=64, dtype="f32", mask=("window", 32, 1)),
     "cfg2": dict(L=65536, H=8, d=64, dtype="bf16", mask=("window", 256, 2)),
     "cfg3": dict(L=2 ** 20, H=1, d=64, dtype="bf16", mask=("bigbird", 128, 64, 64)),
+    "cfg3i": dict(L=2 ** 20, H=1, d=64, dtype="bf16", mask=("bigbird_implicit", 128, 64, 64)),
     "cfg4": dict(L=2 ** 24, H=1, d=64, dtype="bf16", mask=("longnet", 2048, 2)),
     "cfg5": dict(L=160_000_000, H=1, d=64, dtype="bf16", mask=("window", 128, 1)),
 }
-SEEDS = {"cfg1": 0x5EED0001, "cfg2": 0x5EED0002, "cfg3": 0x5EED0003, "cfg4": 0x5EED0004, "cfg5": 0x5EED0005}
+SEEDS = {"cfg1": 0x5EED0001, "cfg2": 0x5EED0002, "cfg3": 0x5EED0003, "cfg3i": 0x5EED0003, "cfg4": 0x5EED0004,
+         "cfg5": 0x5EED0005}
+PER_CONFIG = ("cfg2", "cfg3", "cfg3i", "cfg5")  # extra N=1 lines next to the headline
 BIGBIRD_SEED = 0xB16B12D
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 
@@ -47,6 +56,8 @@ def mask_desc(cfg):
         return f"Window(w={a[0]}, r={a[1]})"
     if kind == "bigbird":
         return f"BigBird(window={a[0]}, globals={a[1]} evenly spaced, random={a[2]}/row) as explicit CSR"
+    if kind == "bigbird_implicit":
+        return f"BigBird(window={a[0]}, globals={a[1]} evenly spaced, random={a[2]}/row) implicit descriptor"
     return f"LongNet(w0={a[0]}, alpha={a[1]}) implicit"
 
 
@@ -131,6 +142,7 @@ def oracle_rate(cfg_name, budget_s=15.0, max_rows=None):
     kind, *a = cfg["mask"]
     om = {"window": lambda: oracle.window(L, a[0], a[1]),
           "bigbird": lambda: oracle.bigbird(L, a[0], a[1], a[2], BIGBIRD_SEED),
+          "bigbird_implicit": lambda: oracle.bigbird(L, a[0], a[1], a[2], BIGBIRD_SEED),
           "longnet": lambda: oracle.longnet(L, a[0], a[1])}[kind]()
     arrays = 3 * L * H * d * 8 <= 4 << 30
     if arrays:
@@ -161,6 +173,165 @@ def oracle_rate(cfg_name, budget_s=15.0, max_rows=None):
     return e / t, oracle.num_threads(), sample, e, t
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline_line(cfg_name, budget_s):
+    """The oracle as it stands on the host cores (all threads), plus a 1-thread rate on a
+    smaller sample; rows are sampled uniformly, so the full-workload time is extrapolated."""
+    import oracle
+
+    rate, cores, sample, e, t = oracle_rate(cfg_name, budget_s)
+    nthreads = oracle.num_threads()
+    oracle.set_num_threads(1)
+    try:
+        rate1, _, sample1, e1, t1 = oracle_rate(cfg_name, max(2.0, budget_s / 4))
+    finally:
+        oracle.set_num_threads(nthreads)
+    cfg = CONFIGS[cfg_name]
+    return {"value": rate, "unit": "edges/s", "cores": cores, "kind": "oracle", "sample": sample,
+            "cpu_model": cpu_model(), "host_logical_cpus": os.cpu_count(),
+            "rate_1thread": rate1, "sample_1thread": sample1,
+            "full_workload_s_extrapolated": None if not rate else round(
+                _nnz_host(cfg_name) * cfg["H"] / rate, 1),
+            "note": "fp64 oracle (oracle/oracle.c, OpenMP over rows), timed on sampled query rows; "
+                    "full-workload time extrapolated from the per-edge rate"}
+
+
+def _nnz_host(cfg_name):
+    import paper_2502_01659_b200 as ga
+
+    cfg = CONFIGS[cfg_name]
+    kind, *a = cfg["mask"]
+    m = {"window": lambda: ga.Window(a[0], a[1]), "longnet": lambda: ga.LongNet(a[0], a[1]),
+         "bigbird": lambda: ga.BigBird(a[0], a[1], a[2], seed=BIGBIRD_SEED),
+         "bigbird_implicit": lambda: ga.BigBird(a[0], a[1], a[2], seed=BIGBIRD_SEED)}[kind]()
+    return ga.mask_count(m, cfg["L"])
+
+
+class Workload:
+    """Inputs resident in HBM and the step function of one configuration on this rank."""
+
+    def __init__(self, ga, torch, name, dev, world, rank, kernel, scaling):
+        cfg = CONFIGS[name]
+        self.name, self.cfg = name, cfg
+        self.kind, *a = cfg["mask"]
+        self.H, self.d = cfg["H"], cfg["d"]
+        L0 = cfg["L"]
+        if scaling == "strong" and world > 1:
+            self.L = L0
+            S = -(-L0 // world)
+            self.r0, self.r1 = min(L0, rank * S), min(L0, (rank + 1) * S)
+        else:
+            self.L = L0 * world
+            self.r0, self.r1 = rank * L0, (rank + 1) * L0
+        self.L_local = self.r1 - self.r0
+        tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[cfg["dtype"]]
+        seed = SEEDS[name]
+        L, H, d = self.L, self.H, self.d
+        self.ws = None
+        if self.kind == "window":
+            self.mask = ga.Window(a[0], a[1])
+            self.nnz = ga.mask_count(self.mask, L)
+        elif self.kind == "bigbird":
+            self.mask = ga.mask_to_csr(ga.BigBird(a[0], a[1], a[2], seed=BIGBIRD_SEED), L)
+            self.nnz = self.mask.nnz
+            self.ws = torch.empty(ga.workspace_size(self.mask, L, d, H, tdt, q_begin=self.r0, q_rows=self.L_local),
+                                  dtype=torch.uint8, device=dev)
+        elif self.kind == "bigbird_implicit":
+            self.mask = ga.BigBird(a[0], a[1], a[2], seed=BIGBIRD_SEED)
+            self.nnz = ga.mask_count(self.mask, L)
+            self.ws = torch.empty(ga.workspace_size(self.mask, L, d, H, tdt, q_begin=self.r0, q_rows=self.L_local),
+                                  dtype=torch.uint8, device=dev)
+        else:
+            self.mask = ga.LongNet(a[0], a[1])
+            self.nnz = ga.mask_count(self.mask, L)
+            wsb = ga.workspace_size(self.mask, L, d, H, tdt, q_begin=self.r0, q_rows=self.L_local)
+            self.ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
+        self.q = torch.empty((self.L_local, H, d), dtype=tdt, device=dev)
+        ga.fill_inputs(self.q, seed, 0, self.r0 * H * d)
+        self.comm = None
+        if world > 1:
+            from paper_2502_01659_b200.comm import Comm
+
+            self.comm = Comm()
+            S = -(-L // world)  # symmetric buffers: every rank allocates the largest shard
+            self.k = self.comm.empty((S, H, d), tdt)[:self.L_local]
+            self.v = self.comm.empty((S, H, d), tdt)[:self.L_local]
+        else:
+            self.k = torch.empty((self.L_local, H, d), dtype=tdt, device=dev)
+            self.v = torch.empty_like(self.k)
+        ga.fill_inputs(self.k, seed, 1, self.r0 * H * d)
+        ga.fill_inputs(self.v, seed, 2, self.r0 * H * d)
+        self.out = torch.empty_like(self.q)
+        self.ga, self.kernel = ga, kernel
+        self.edges_total = self.nnz * H  # all ranks together (one global mask)
+
+    def step(self):
+        if self.comm is not None:
+            self.comm.attention(self.q, self.k, self.v, self.mask, self.L, out=self.out, kernel=self.kernel,
+                                workspace=self.ws)
+        else:
+            self.ga.attention(self.q, self.k, self.v, self.mask, self.out, kernel=self.kernel, workspace=self.ws)
+
+    def close(self):
+        if self.comm is not None:
+            self.comm.check()
+            self.comm.close()
+            self.comm = None
+        self.q = self.k = self.v = self.out = self.ws = self.mask = None
+
+
+def time_steps(torch, dist, world, wl, steps, warmup, flush, sampler=None):
+    """W untimed steps; K timed steps, each bracketed by CUDA events on the launching stream
+    with an L2 flush before it (outside the events); max over ranks."""
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(warmup):
+        wl.step()
+    barrier()
+    if sampler is not None:
+        sampler.start()
+    lib = wl.ga._abi.lib()
+    launches0 = lib.ga_launch_count()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    barrier()
+    for s in range(steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        if world > 1:
+            dist.barrier()
+        starts[s].record()
+        wl.step()
+        ends[s].record()
+    barrier()
+    launches = lib.ga_launch_count() - launches0
+    clocks = sampler.stop() if sampler is not None else None
+    per_step = [st.elapsed_time(en) for st, en in zip(starts, ends)]
+    total_ms = torch.tensor([sum(per_step)], dtype=torch.float64, device=flush.device)
+    if world > 1:
+        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+    return total_ms.item() / steps, per_step, launches, clocks
+
+
+def workload_desc(wl, world, scaling):
+    cfg = wl.cfg
+    shard = (f"L={wl.L_local}x{world}" if scaling == "weak" else f"L={wl.L} over {world} shards") if world > 1 \
+        else f"L={wl.L}"
+    return f"{wl.name}: {shard} tokens, {wl.H} heads, d={wl.d}, {cfg['dtype']}, {mask_desc(cfg)}"
+
+
 # ------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
@@ -168,8 +339,10 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg4")
     ap.add_argument("--kernel", default="auto", choices=["auto", "edge", "tiled", "window", "tc"])
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--no-per-config", action="store_true", help="skip the extra per-config lines at N=1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -196,172 +369,130 @@ def main():
     import paper_2502_01659_b200 as ga
 
     dev = _init_dist(torch, dist, world, local_rank)
-    L_local, H, d = cfg["L"], cfg["H"], cfg["d"]
-    L = L_local * world
-    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[cfg["dtype"]]
-    seed = SEEDS[args.config]
-    kind, *a = cfg["mask"]
-    r0, r1 = rank * L_local, (rank + 1) * L_local
-
-    # ---- inputs (resident in HBM before timing) and the step function
-    ws = None
-    if kind == "window":
-        mask = ga.Window(a[0], a[1])
-        nnz = ga.mask_count(mask, L)
-    elif kind == "bigbird":
-        mask = ga.mask_to_csr(ga.BigBird(a[0], a[1], a[2], seed=BIGBIRD_SEED), L)
-        nnz = mask.nnz
-        ws = torch.empty(ga.workspace_size(mask, L, d, H, tdt, q_begin=r0, q_rows=L_local), dtype=torch.uint8,
-                         device=dev)
-    else:
-        mask = ga.LongNet(a[0], a[1])
-        nnz = ga.mask_count(mask, L)
-        wsb = ga.workspace_size(mask, L, d, H, tdt, q_begin=r0, q_rows=L_local)  # tcgen05 block partials
-        ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
-    q = torch.empty((L_local, H, d), dtype=tdt, device=dev)
-    ga.fill_inputs(q, seed, 0, r0 * H * d)
-    comm = None
-    if world > 1:
-        # weak scaling: rank owns rows [r0, r1) of an N*L sequence; its K/V shard lives in a
-        # symmetric buffer the other ranks read over NVLink (ga_attention_sharded)
-        from paper_2502_01659_b200.comm import Comm
-
-        comm = Comm()
-        k = comm.empty((L_local, H, d), tdt)
-        v = comm.empty((L_local, H, d), tdt)
-    else:
-        k = torch.empty((L_local, H, d), dtype=tdt, device=dev)
-        v = torch.empty_like(k)
-    ga.fill_inputs(k, seed, 1, r0 * H * d)
-    ga.fill_inputs(v, seed, 2, r0 * H * d)
-    out = torch.empty_like(q)
-
-    def step():
-        if comm is not None:
-            comm.attention(q, k, v, mask, L, out=out, kernel=args.kernel, workspace=ws)
-        else:
-            ga.attention(q, k, v, mask, out, kernel=args.kernel, workspace=ws)
-    e2e_targets = [q, k, v]
-
-    edges_total = nnz * H  # all ranks together (global mask over the N*L sequence)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    for _ in range(args.warmup):
-        step()
-    barrier()
-
+    wl = Workload(ga, torch, args.config, dev, world, rank, args.kernel, args.scaling)
     sampler = ClockSampler(local_rank)
-    sampler.start()
-    lib = ga._abi.lib()
-    launches0 = lib.ga_launch_count()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    barrier()
-    for s in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps (outside the events)
-        if world > 1:
-            dist.barrier()
-        starts[s].record()
-        step()
-        ends[s].record()
-    barrier()
-    launches = lib.ga_launch_count() - launches0
-    clocks = sampler.stop()
-    per_step = [st.elapsed_time(en) for st, en in zip(starts, ends)]
-    total_ms = torch.tensor([sum(per_step)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
-    ms = total_ms.item() / args.steps
-    value = edges_total / (ms / 1e3)
-
-    # ---- roofline for the dominant kernel (the attention kernel; one launch per step at N=1)
-    roofline, gather = roofline_for(args, cfg, kind, edges_total // world, L_local, H, d, nnz, per_step)
+    ms, per_step, launches, clocks = time_steps(torch, dist, world, wl, args.steps, args.warmup, flush, sampler)
+    value = wl.edges_total / (ms / 1e3)
+    # ---- roofline for the dominant kernel (per rank's share of the work)
+    roofline, gather = roofline_for(args.config, args.kernel, cfg, wl.kind, wl.edges_total * wl.L_local // wl.L,
+                                    wl.L_local, wl.H, wl.d, wl.nnz * wl.L_local // wl.L, per_step)
     # ---- end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
         c_abi = None
-        if world == 1 and kind != "bigbird":
-            c_abi = (mask, q.cpu().pin_memory(), e2e_targets[1].cpu().pin_memory(), e2e_targets[2].cpu().pin_memory())
-        e2e = measure_e2e(args, ga, world, dev, edges_total, e2e_targets, step, out, c_abi)
+        if world == 1 and wl.kind != "bigbird":
+            c_abi = (wl.mask, wl.q.cpu().pin_memory(), wl.k.cpu().pin_memory(), wl.v.cpu().pin_memory())
+        e2e = measure_e2e(args, ga, world, dev, wl.edges_total, [wl.q, wl.k, wl.v], wl.step, wl.out, c_abi)
+        c_abi = None
+    workload = workload_desc(wl, world, args.scaling)
+    conf = {"workload": workload, "L": wl.L, "heads": wl.H, "d": wl.d, "mask": mask_desc(cfg), "nnz": wl.nnz,
+            "kernel": args.kernel,
+            "parallelism": f"query-range shards x{world}" + (
+                ", ga_attention_sharded (remote K/V rows read over NVLink peer memory"
+                + (", K/V all-gather" if wl.kind.startswith("bigbird") else "") + ")" if world > 1 else ""),
+            "l2": "flushed between timed steps (256 MiB write outside the events); inputs > L2"}
+    wl.close()
+    wl = None
+    torch.cuda.empty_cache()
+
+    # ---- the other BASELINE.json configurations at N=1
+    per_config = None
+    if world == 1 and not args.no_per_config:
+        per_config = {}
+        for name in PER_CONFIG:
+            if name == args.config:
+                continue
+            w2 = Workload(ga, torch, name, dev, 1, 0, "auto", "weak")
+            ms2, ps2, _, _ = time_steps(torch, dist, 1, w2, max(3, min(args.steps, 10)), 3, flush)
+            roof2, _ = roofline_for(name, "auto", w2.cfg, w2.kind, w2.edges_total, w2.L_local, w2.H, w2.d, w2.nnz, ps2)
+            per_config[name] = {"workload": workload_desc(w2, 1, "weak"), "value": w2.edges_total / (ms2 / 1e3),
+                                "unit": "edges/s", "ms_per_step": ms2, "steps": max(3, min(args.steps, 10)),
+                                "warmup": 3, "nnz": w2.nnz, "roofline": roof2}
+            w2.close()
+            w2 = None
+            torch.cuda.empty_cache()
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, cores, sample, _, _ = oracle_rate(args.config, args.cpu_budget)
-        cpu = {"value": rate, "unit": "edges/s", "cores": cores, "kind": "oracle", "sample": sample}
+        cpu = cpu_baseline_line(args.config, args.cpu_budget)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if (world == 1 or args.scaling == "weak") else "strong",
             "vs_baseline": None, "dtype": cfg["dtype"], "accum": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config}: L={L_local}{'x' + str(world) if world > 1 else ''} tokens, "
-                                   f"{H} heads, d={d}, {cfg['dtype']}, {mask_desc(cfg)}",
-                       "L": L, "heads": H, "d": d, "mask": mask_desc(cfg), "nnz": nnz,
-                       "kernel": args.kernel, "parallelism": f"query-range shards x{world}" + (
-                           ", ga_attention_sharded (remote K/V rows read over NVLink peer memory"
-                           + (", CSR K/V all-gather" if kind == "bigbird" else "") + ")" if world > 1 else ""),
-                       "l2": "flushed between timed steps (256 MiB write outside the events); inputs > L2"},
-            "clocks": clocks, "roofline": roofline, "gather_model": gather, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches,
+            "config": conf, "clocks": clocks, "roofline": roofline, "gather_model": gather, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": launches, "per_config": per_config,
         }
         print(json.dumps(line), flush=True)
-    if comm is not None:
-        comm.close()
     if world > 1:
         dist.destroy_process_group()
 
 
-def roofline_for(args, cfg, kind, head_edges, L_local, H, d, nnz, per_step):
-    """Roofline of the attention kernel.
+MUFU_EX2_PER_CLK_SM = 15.7  # measured, profiles/r01_microbench.txt (tools/microbench.cu)
+SMS = 148
 
-    Algorithmic bytes per launch = Q, K, V read once + O written once (+ row_ptr and col_idx
-    for explicit CSR): no implementation can move less.  Algorithmic flops = 4d per
-    head-edge (2d for q.k, 2d for p*v).  The bound is whichever resource's
-    lower-bound time is larger at the measured peaks (HBM copy GB/s vs bf16 tensor TFLOP/s;
-    fp32 inputs use the FP32 FMA pipe).  The north-star "gather model" (every edge pulls
-    K_j and V_j from memory) is reported separately."""
+
+def roofline_for(cfg_name, kernel, cfg, kind, head_edges, L_local, H, d, nnz, per_step):
+    """Roofline of the attention step: the binding resource is whichever
+    lower-bound time is largest at the measured peaks.
+
+    * HBM: algorithmic bytes per launch = Q, K, V read once + O written once (+ row_ptr and
+      col_idx for explicit CSR) — no implementation can move less — at MEASURED_PEAKS hbm_gbs.
+    * tensor: algorithmic flops = 4d per head-edge (2d for q.k, 2d for p*v) at the
+      measured dense bf16 peak (fp32 inputs: the FP32 FMA pipe, 148 x 128 x 2 x clock).
+    * alu (MUFU): one exp2 per head-edge — the online softmax's weight 2^(s - m) — at the
+      measured MUFU.EX2 rate (15.7 /clk/SM x 148 SMs x max clock).
+    The north-star "gather model" (every edge pulls K_j and V_j) is reported separately."""
     peaks, peak_src = load_peaks()
     kernel_ms = statistics.median(per_step)
     e = eb(cfg["dtype"])
-    bytes_alg = 4 * L_local * H * d * e + ((L_local + 1) * 8 + nnz * 4 if kind == "bigbird" else 0)
+    csr = kind == "bigbird"
+    bytes_alg = 4 * L_local * H * d * e + ((L_local + 1) * 8 + nnz * 4 if csr else 0)
     flops_alg = 4 * d * head_edges
     hbm = peaks["hbm_gbs"]
+    clk = peaks.get("sm_max_mhz", 1965.0) * 1e6
     if cfg["dtype"] == "f32":
-        fpeak, funit = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, "fp32 FMA pipe (derived)"
+        fpeak, funit = SMS * 128 * 2 * clk / 1e12, "fp32 FMA pipe (derived: 148 SMs x 128 FMA/clk x max clock)"
     else:
-        fpeak, funit = peaks["bf16_tflops"], f"bf16 dense tensor ({peak_src})"
-    t_mem, t_fl = bytes_alg / (hbm * 1e9), flops_alg / (fpeak * 1e12)
+        fpeak, funit = peaks["bf16_tflops"], f"bf16 dense tensor ({peak_src} MEASURED_PEAKS.json)"
+    xpeak = MUFU_EX2_PER_CLK_SM * SMS * clk  # exp2 / s
+    t_mem, t_fl, t_ex = bytes_alg / (hbm * 1e9), flops_alg / (fpeak * 1e12), head_edges / xpeak
     s = kernel_ms / 1e3
-    if t_mem >= t_fl:
+    bound = max((t_mem, "hbm"), (t_fl, "tensor"), (t_ex, "alu"))[1]
+    if bound == "hbm":
         ach = bytes_alg / s / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
                 "peak_source": f"hbm_gbs, {peak_src} MEASURED_PEAKS.json (copy bandwidth)"}
-    else:
+    elif bound == "tensor":
         ach = flops_alg / s / 1e12
         roof = {"bound": "tensor" if cfg["dtype"] != "f32" else "alu", "achieved": round(ach, 2), "peak": fpeak,
                 "unit": "TFLOP/s", "frac": round(ach / fpeak, 4), "peak_source": funit}
+    else:
+        ach = head_edges / s / 1e9
+        roof = {"bound": "alu", "achieved": round(ach, 1), "peak": round(xpeak / 1e9, 1), "unit": "Gexp2/s",
+                "frac": round(ach * 1e9 / xpeak, 4),
+                "peak_source": "MUFU.EX2: 15.7/clk/SM measured (profiles/r01_microbench.txt) x 148 SMs x "
+                               f"{clk / 1e6:.0f} MHz; one exp2 per head-edge"}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(f"{args.config}:{args.kernel}")
+            traffic = json.load(f).get(f"{cfg_name}:{kernel}")
     roof.update({
         "traffic": traffic,
-        "algorithmic": f"{bytes_alg} B (Q,K,V,O once{' + CSR' if kind == 'bigbird' else ''}) and {flops_alg} flop "
-                       f"(4d x {head_edges} head-edges) per launch",
-        "lower_bound_us": {"hbm": round(t_mem * 1e6, 2), "flops": round(t_fl * 1e6, 2)},
-        "tensor_tflops_achieved": round(flops_alg / s / 1e12, 2),
+        "algorithmic": f"{bytes_alg} B (Q,K,V,O once{' + CSR' if csr else ''}), {flops_alg} flop "
+                       f"(4d x {head_edges} head-edges) and {head_edges} exp2 per launch",
+        "lower_bound_us": {"hbm": round(t_mem * 1e6, 2), "tensor": round(t_fl * 1e6, 2), "mufu": round(t_ex * 1e6, 2)},
+        "frac_hbm": round(t_mem / s, 4), "frac_tensor": round(t_fl / s, 4), "frac_mufu": round(t_ex / s, 4),
         "kernel_ms_median": round(kernel_ms, 4)})
     if traffic:  # measured DRAM bytes of the step (ncu, profiles/traffic.json) over this run's time
         roof["dram_GBps_measured_traffic"] = round(traffic / s / 1e9, 1)
         roof["dram_frac_measured_traffic"] = round(traffic / s / 1e9 / hbm, 4)
-    gbe = 2 * d * e + (4 if kind == "bigbird" else 0)
+    gbe = 2 * d * e + (4 if csr else 0)
     ggbs = head_edges * gbe / s / 1e9
     gather = {"bytes_per_edge": gbe, "GBps": round(ggbs, 1), "frac_of_8TBps": round(ggbs / 8000.0, 3),
               "frac_of_measured_hbm": round(ggbs / hbm, 3),
@@ -454,7 +585,7 @@ def max_context(args, world, rank, local_rank):
     row = H * d * 2
     reserve = 2 << 30  # context, runtime workspace, clocks
     L_local = int((free - reserve) // (3 * row))
-    L_local = (L_local // 224) * 224  # band-kernel tile multiple (112 rows x r=1) x 2
+    L_local = (L_local // 256) * 256  # tcgen05 window-kernel tile pairs (2 x 128 rows), shard-aligned
     L = L_local * world
     r0, r1 = rank * L_local, (rank + 1) * L_local
     comm = None

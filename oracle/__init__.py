@@ -91,6 +91,10 @@ def lib():
             fn.restype = ctypes.c_int64
             fn.argtypes = [ctypes.POINTER(_OrcInputs), ctypes.POINTER(_OrcMask), ctypes.c_int64,
                            ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.orc_attention_backward.restype = ctypes.c_int64
+        L.orc_attention_backward.argtypes = [ctypes.POINTER(_OrcInputs), ctypes.POINTER(_OrcMask), ctypes.c_int64,
+                                             ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_void_p]
         L.orc_num_threads.restype = ctypes.c_int
         L.orc_set_num_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -256,6 +260,24 @@ def attention(q, k, v, mask: Mask, rows: Optional[Sequence[int]] = None):
 def attention_seeded(seed, dtype, mask: Mask, H, d, rows: Optional[Sequence[int]] = None):
     """Two-pass fp64 oracle regenerating Q/K/V rows from the counter hash (reading R22)."""
     return _run(lib().orc_attention, None, None, None, mask, H, d, rows, seed, dtype)
+
+
+def attention_backward(q, k, v, mask: Mask, dout):
+    """fp64 gradients (dQ, dK, dV) of the masked attention for upstream dO (oracle.c
+    orc_attention_backward: the chain rule per edge, serial).  Returns (dq, dk, dv, edges)."""
+    L, H, d = q.shape
+    cm = mask.c()
+    inp = _OrcInputs()
+    keep = []
+    for name, a in (("q", q), ("k", k), ("v", v)):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        keep.append(a)
+        setattr(inp, name, a.ctypes.data)
+    g = np.ascontiguousarray(dout, dtype=np.float64)
+    dq, dk, dv = (np.empty((L, H, d), dtype=np.float64) for _ in range(3))
+    edges = lib().orc_attention_backward(ctypes.byref(inp), ctypes.byref(cm), H, d, g.ctypes.data, dq.ctypes.data,
+                                         dk.ctypes.data, dv.ctypes.data)
+    return dq, dk, dv, edges
 
 
 def attention_alg1(q, k, v, mask: Mask, rows=None):

@@ -452,6 +452,74 @@ int64_t orc_attention_alg1(const orc_inputs *in, const orc_mask *m, int64_t H, i
     return edges;
 }
 
+/* Backward pass (the training use case of PAPER.md:555) — the chain rule of
+ * O_i = sum_{e in N(i)} P_e V_{j_e}, P_e = softmax_e(S_e), S_e = Q_i.K_{j_e} / sqrt(d), written
+ * out per edge e = (i, j) of the (multi)set N(i) in fp64, for upstream gradients dO [L,H,d]:
+ *     dV_j += P_e dO_i                       dP_e = dO_i . V_j
+ *     D_i   = sum_e P_e dP_e                 dS_e = P_e (dP_e - D_i)      (softmax Jacobian)
+ *     dQ_i += dS_e K_j / sqrt(d)             dK_j += dS_e Q_i / sqrt(d)
+ * Serial over rows (dK, dV are scattered): small cases only.  dq, dk, dv: [L,H,d], zeroed
+ * here.  Empty rows contribute nothing (their O is the constant 0, reading R6).  Returns the
+ * number of edges x H.  PARITY PINS: central finite differences of orc_attention and torch
+ * autograd of the dense masked softmax (tests/test_oracle_pins.py). */
+int64_t orc_attention_backward(const orc_inputs *in, const orc_mask *m, int64_t H, int64_t d, const double *dout,
+                               double *dq, double *dk, double *dv)
+{
+    const int64_t L = m->L, cap = orc_max_degree(m);
+    const double inv_sqrt_d = 1.0 / sqrt((double)d);
+    int64_t edges = 0;
+    int64_t *nb = (int64_t *)malloc(sizeof(int64_t) * (size_t)(cap + 1));
+    double *P = (double *)malloc(sizeof(double) * (size_t)(cap + 1));
+    double *dP = (double *)malloc(sizeof(double) * (size_t)(cap + 1));
+    double *q = (double *)malloc(sizeof(double) * (size_t)d);
+    double *kv = (double *)malloc(sizeof(double) * (size_t)d);
+    memset(dq, 0, sizeof(double) * (size_t)(L * H * d));
+    memset(dk, 0, sizeof(double) * (size_t)(L * H * d));
+    memset(dv, 0, sizeof(double) * (size_t)(L * H * d));
+    for (int64_t i = 0; i < L; ++i) {
+        const int64_t n = orc_row_neighbors(m, i, nb);
+        if (n == 0) continue;
+        for (int64_t h = 0; h < H; ++h) {
+            const size_t ri = ((size_t)i * (size_t)H + (size_t)h) * (size_t)d;
+            const double *g = dout + ri;
+            load_row(in, 0, i, h, H, d, q);
+            double mx = -INFINITY;
+            for (int64_t e = 0; e < n; ++e) { /* scores S_e, kept in P */
+                load_row(in, 1, nb[e], h, H, d, kv);
+                double acc = 0.0;
+                for (int64_t c = 0; c < d; ++c) acc += q[c] * kv[c];
+                P[e] = acc * inv_sqrt_d;
+                if (P[e] > mx) mx = P[e];
+            }
+            double z = 0.0;
+            for (int64_t e = 0; e < n; ++e) { P[e] = exp(P[e] - mx); z += P[e]; }
+            double D = 0.0;
+            for (int64_t e = 0; e < n; ++e) {
+                P[e] /= z;
+                load_row(in, 2, nb[e], h, H, d, kv);
+                double acc = 0.0;
+                for (int64_t c = 0; c < d; ++c) acc += g[c] * kv[c];
+                dP[e] = acc;
+                D += P[e] * dP[e];
+                double *dvj = dv + ((size_t)nb[e] * (size_t)H + (size_t)h) * (size_t)d;
+                for (int64_t c = 0; c < d; ++c) dvj[c] += P[e] * g[c];
+            }
+            for (int64_t e = 0; e < n; ++e) {
+                const double dS = P[e] * (dP[e] - D);
+                load_row(in, 1, nb[e], h, H, d, kv);
+                double *dkj = dk + ((size_t)nb[e] * (size_t)H + (size_t)h) * (size_t)d;
+                for (int64_t c = 0; c < d; ++c) {
+                    dq[ri + (size_t)c] += dS * kv[c] * inv_sqrt_d;
+                    dkj[c] += dS * q[c] * inv_sqrt_d;
+                }
+            }
+            edges += n;
+        }
+    }
+    free(nb); free(P); free(dP); free(q); free(kv);
+    return edges;
+}
+
 int orc_num_threads(void)
 {
 #ifdef _OPENMP

@@ -121,3 +121,37 @@ def test_cfg3_bigbird_implicit_full_size_sampled(ga, orc):
     rows = np.array(rows, dtype=np.int64)
     want, _ = orc.attention_seeded(seed, "bf16", orc.bigbird(L, 128, 64, 64, 0xB16B12D), H, d, rows=rows)
     assert np.abs(out[rows] - want).max() <= 2e-2
+
+
+@pytest.mark.parametrize("with_out", [False, True])
+def test_window_tc_carried_state(ga, orc, with_out):
+    """The tcgen05 window kernel's state epilogue (ga_opts.state): WRITE gives the row's
+    (m, l, o~) — same softmax mass l 2^m as the edge kernel's state — and ACCUMULATE (+)s
+    into a state from another component: window (tcgen05) + CSR(global | random) composed
+    equals the BigBird oracle (PAPER.md:521 sequential composition)."""
+    L, H, d, seed = 5000, 2, 64, 0xB16B12D
+    cpu = synth.qkv(12, L, H, d, "bf16", centred=True)
+    q, k, v = (x.cuda() for x in cpu)
+    f64 = tuple(synth.as_f64(x) for x in cpu)
+    st_tc = ga.State.empty(L, H, d)
+    st_ed = ga.State.empty(L, H, d)
+    out = torch.empty_like(q) if with_out else None
+    ga.attention(q, k, v, ga.Window(128), out, state=st_tc, kernel="tc")
+    ga.attention(q, k, v, ga.Window(128), state=st_ed, kernel="edge")
+    torch.cuda.synchronize()
+    z_tc = st_tc.l.double() * torch.exp2(st_tc.m.double())
+    z_ed = st_ed.l.double() * torch.exp2(st_ed.m.double())
+    assert ((z_tc - z_ed).abs() / z_ed).max().item() < 5e-3
+    want_w, _ = orc.attention(*f64, orc.window(L, 128))
+    fin = ga.state_finalize(st_tc, torch.bfloat16).double().cpu().numpy()
+    assert np.abs(fin - want_w).max() <= 2e-2
+    if with_out:
+        assert np.abs(out.double().cpu().numpy() - want_w).max() <= 2e-2
+    # composition: CSR of the global + random components first (edge kernel), then the window
+    rest = ga.mask_to_csr(ga.BigBird(128, 5, 16, seed=seed, parts=ga.BB_GLOBAL | ga.BB_RANDOM), L)
+    st = ga.State.empty(L, H, d)
+    ga.attention(q, k, v, rest, state=st, accumulate=True)
+    ga.attention(q, k, v, ga.Window(128), state=st, accumulate=True, kernel="tc")
+    got = ga.state_finalize(st, torch.bfloat16).double().cpu().numpy()
+    want, _ = orc.attention(*f64, orc.bigbird(L, 128, 5, 16, seed))
+    assert np.abs(got - want).max() <= 2e-2

@@ -148,3 +148,20 @@ def test_invalid_arguments_rejected_without_gpu():
         ga.mask_count(ga.Window(0), 10)
     with pytest.raises(ga.GaError, match="INVALID_ARG"):
         ga.mask_count(ga.LongNet(16, 1), 10)
+
+
+def test_bench_roofline_picks_binding_bound():
+    """bench.py reports the resource with the largest lower-bound time: HBM for
+    the window configs and explicit CSR, MUFU exp2 for LongNet and implicit BigBird (cfg4: 5.15e10 exp2 ~ 11 ms
+    against 7.8 ms of tensor flops and 1.3 ms of compulsory HBM traffic)."""
+    import bench
+
+    cases = {"cfg2": (133433344, 65536 * 8, "hbm"), "cfg4": (51537510400, 2 ** 24, "alu"),
+             "cfg5": (40799983744, 160_000_000, "hbm"), "cfg3": (468656702, 2 ** 20, "hbm"),
+             "cfg3i": (468656702, 2 ** 20, "alu")}  # implicit: no CSR bytes, 4.7e8 exp2 > 0.54 GB of QKVO
+    for name, (edges, rows, bound) in cases.items():
+        cfg = bench.CONFIGS[name]
+        roof, _ = bench.roofline_for(name, "auto", cfg, cfg["mask"][0], edges, cfg["L"], cfg["H"], cfg["d"],
+                                     edges // cfg["H"], [50.0])
+        assert roof["bound"] == bound, (name, roof)
+        assert 0 < roof["frac"] < 1

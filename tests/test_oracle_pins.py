@@ -444,3 +444,69 @@ def test_longnet_multiset_closed_form_count(orc):
     nnz = L w0 sum_k alpha^-k — at L = 2^12, w0 = 16: 16 * 4096 * (2 - 2^-8) = 130,816."""
     rp, _, nnz = orc.mask_to_csr(orc.longnet(4096, 16, 2, multiset=True), with_cols=False)
     assert nnz == 130_816
+
+
+# ---------------------------------------------------------------- backward (SURVEY §8(f) f3)
+def _bwd_inputs(L, H, d, seed):
+    rng = np.random.default_rng(seed)
+    return tuple(rng.standard_normal((L, H, d)) for _ in range(4))  # q, k, v, dO
+
+
+@pytest.mark.parametrize("fam", ["window", "longnet_multiset", "csr_empty_rows", "bigbird"])
+def test_backward_matches_finite_differences(orc, fam):
+    """orc_attention_backward against central differences of orc_attention (an independent
+    route: only the forward definition is used) for the scalar loss sum(dO * O)."""
+    L, H, d = 12, 2, 4
+    q, k, v, g = _bwd_inputs(L, H, d, 7)
+    if fam == "window":
+        om = orc.window(L, 3, 1)
+    elif fam == "longnet_multiset":
+        om = orc.longnet(L, 2, 2, multiset=True)  # repeated columns: weights count twice
+    elif fam == "bigbird":
+        om = orc.bigbird(L, 2, 1, 2, 5)
+    else:
+        rp = np.array([0, 2, 2, 5, 6, 6, 8, 9, 9, 12, 13, 13, 16], dtype=np.int64)  # rows 1, 4, 7, 10 empty
+        ci = np.array([0, 5, 1, 2, 11, 3, 4, 9, 6, 7, 8, 10, 11, 0, 5, 11], dtype=np.int32)
+        om = orc.csr(L, rp, ci)
+    dq, dk, dv, _ = orc.attention_backward(q, k, v, om, g)
+
+    def loss(q_, k_, v_):
+        return float((orc.attention(q_, k_, v_, om)[0] * g).sum())
+
+    h = 1e-6
+    for name, x, grad in (("q", q, dq), ("k", k, dk), ("v", v, dv)):
+        num = np.zeros_like(x)
+        for idx in np.ndindex(*x.shape):
+            xp, xm = x.copy(), x.copy()
+            xp[idx] += h
+            xm[idx] -= h
+            args_p = {"q": q, "k": k, "v": v}
+            args_m = dict(args_p)
+            args_p[name], args_m[name] = xp, xm
+            num[idx] = (loss(**{a + "_": b for a, b in args_p.items()}) -
+                        loss(**{a + "_": b for a, b in args_m.items()})) / (2 * h)
+        np.testing.assert_allclose(grad, num, rtol=1e-6, atol=1e-8, err_msg=f"d{name} ({fam})")
+
+
+@pytest.mark.parametrize("fam,L,args", [("window", 64, (9, 2)), ("longnet", 64, (8, 2)), ("block", 60, (12, 3))])
+def test_backward_matches_torch_autograd_dense(orc, fam, L, args):
+    """Library routine: torch.autograd (fp64) through the dense masked softmax of
+    oracle/dense.py's predicate grid (shares no code with oracle.c)."""
+    from oracle import dense
+
+    H, d = 2, 8
+    q, k, v, g = _bwd_inputs(L, H, d, 11)
+    grid = {"window": dense.window_mask, "longnet": dense.longnet_mask, "block": dense.block_dilated_mask}[fam](L, *args)
+    om = {"window": orc.window, "longnet": orc.longnet, "block": orc.block_dilated}[fam](L, *args)
+    tq, tk, tv = (torch.tensor(x, requires_grad=True) for x in (q, k, v))
+    mask = torch.tensor(grid)
+    s = torch.einsum("ihc,jhc->hij", tq, tk) / math.sqrt(d)
+    s = s.masked_fill(~mask, float("-inf"))
+    p = torch.softmax(s, dim=-1)
+    p = torch.nan_to_num(p, nan=0.0)  # empty rows (none here)
+    o = torch.einsum("hij,jhc->ihc", p, tv)
+    (o * torch.tensor(g)).sum().backward()
+    dq, dk, dv, edges = orc.attention_backward(q, k, v, om, g)
+    assert edges == int(grid.sum()) * H
+    for got, want in ((dq, tq.grad), (dk, tk.grad), (dv, tv.grad)):
+        np.testing.assert_allclose(got, want.numpy(), rtol=1e-10, atol=1e-12)
