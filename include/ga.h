@@ -175,8 +175,18 @@ typedef struct ga_opts {
        split (no workspace). */
     ga_state state;
     int32_t state_mode;      /* ga_state_mode */
-    int32_t reserved1;
+    /* ga_attention_sharded with an explicit CSR mask: how K/V reach the ranks (SURVEY §8(e),
+       §8(f) f2).  GA_EXCHANGE_ALLGATHER (0): every rank gathers the full [L, heads, d] K and V
+       (memory 2 L per rank: the context cap does not grow with the rank count).
+       GA_EXCHANGE_RING (1): the key dimension is cut into the ranks' shards; rank r streams
+       shard (r + s) mod world for s = 0..world-1 through two staging buffers (peer -> local
+       copy of the next shard overlapped with the current one's compute), each step computing
+       its rows' edges into that shard's key range only and (+)-merging the carried state
+       (memory ~6 L / world per rank).  Ignored elsewhere. */
+    int32_t exchange;
 } ga_opts;
+
+enum { GA_EXCHANGE_ALLGATHER = 0, GA_EXCHANGE_RING = 1 };
 
 /* The north-star entry point: O = masked-softmax attention of (Q,K,V) over mask.
    Q,K,V,out: DEVICE [L, heads, d] in `dtype`.  `out` must not alias K or V; it may alias
@@ -200,6 +210,23 @@ ga_status ga_attention_ex(const void *Q, const void *K, const void *V, const ga_
    copy streams forked from and joined back to `stream` (results identical to one call). */
 ga_status ga_attention_host(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out,
                             int64_t L, int32_t d, int32_t heads, ga_dtype dtype, void *stream);
+
+/* Backward pass (training): gradients of O = attention(Q, K,
+   V, mask) for the upstream gradient dO, by the chain rule per edge (i, j) of the mask:
+       P_ij = softmax_j(q_i.k_j / sqrt(d)),  dP_ij = dO_i.v_j,  D_i = dO_i.O_i,
+       dS_ij = P_ij (dP_ij - D_i),  dQ_i = sum_j dS_ij k_j / sqrt(d),
+       dK_j = sum_i dS_ij q_i / sqrt(d),  dV_j = sum_i P_ij dO_i.
+   Q, K, V, O (the forward output), dO: DEVICE [L, heads, d] in `dtype`; dQ, dK, dV: DEVICE fp32
+   [L, heads, d], overwritten (they must not overlap any input).  lse: optional DEVICE fp32
+   [L, heads], the forward's log2-sum-exp2 of the row scores, lse_i = log2 sum_j 2^(s_ij log2 e)
+   (= m + log2 l of a carried state, ga_state); NULL recomputes it (one extra pass over the
+   edges).  Masks: CSR (a transposed CSR is built on the device; repeated columns keep their
+   multiplicity), WINDOW, LONGNET, BLOCK_DILATED (symmetric: N^T(j) = N(j)).  BIGBIRD (implicit)
+   returns GA_ERR_UNSUPPORTED: pass its ga_mask_to_csr.  Two launches (row pass: lse, D, dQ;
+   column pass: dK, dV), no atomics: deterministic.  Scratch is stream-ordered (libga's pool). */
+ga_status ga_attention_backward(const void *Q, const void *K, const void *V, const void *O, const void *dO,
+                                const ga_mask *mask, const float *lse, float *dQ, float *dK, float *dV, int64_t L,
+                                int32_t d, int32_t heads, ga_dtype dtype, void *stream);
 
 /* out = o / l of a carried state (0 where l = 0), rounded to `dtype`: rows x heads x d.
    Composition: run the disjoint component masks of a pattern (e.g. WINDOW + BIGBIRD with

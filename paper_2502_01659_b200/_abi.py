@@ -11,6 +11,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 # GA_LIB overrides the library path (A/B timing of two builds); default: the in-tree build
 LIB_PATH = os.environ.get("GA_LIB") or os.path.join(_PKG, "libga.so")
 
+GA_EXCHANGE_ALLGATHER, GA_EXCHANGE_RING = 0, 1
 GA_OK, GA_ERR_INVALID_ARG, GA_ERR_UNSUPPORTED, GA_ERR_CUDA, GA_ERR_COMM, GA_ERR_OOM, GA_ERR_MASK = 0, -1, -2, -3, -4, -5, -6
 GA_COMM_ID_BYTES = 128
 GA_F32, GA_BF16, GA_F16 = 0, 1, 2
@@ -49,7 +50,7 @@ class GaOpts(ctypes.Structure):
         ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
         ("edge_counter", ctypes.c_void_p), ("row_fingerprint", ctypes.c_void_p),
         ("kernel", ctypes.c_int32), ("heavy_threshold", ctypes.c_int32),
-        ("state", GaState), ("state_mode", ctypes.c_int32), ("reserved1", ctypes.c_int32),
+        ("state", GaState), ("state_mode", ctypes.c_int32), ("exchange", ctypes.c_int32),
     ]
 
 
@@ -68,6 +69,8 @@ SIGNATURES = [
     ("ga_mask_validate", ctypes.c_int, [_PM, _V, ctypes.POINTER(ctypes.c_int)]),
     ("ga_fill_inputs", ctypes.c_int, [_V, ctypes.c_int, _I64, _U64, _I32, _I64, _F, _V]),
     ("ga_state_finalize", ctypes.c_int, [ctypes.POINTER(GaState), _I64, _I32, _I32, ctypes.c_int, _V, _V]),
+    ("ga_attention_backward", ctypes.c_int, [_V, _V, _V, _V, _V, ctypes.POINTER(GaMask), _V, _V, _V, _V, _I64, _I32,
+                                             _I32, ctypes.c_int, _V]),
     ("ga_comm_get_unique_id", ctypes.c_int, [_V]),
     ("ga_comm_create", ctypes.c_int, [_I32, _I32, _V, _I32, ctypes.POINTER(_V)]),
     ("ga_comm_alloc", ctypes.c_int, [_V, _SZ, ctypes.POINTER(_V)]),

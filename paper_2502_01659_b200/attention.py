@@ -112,6 +112,44 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: Mask, out
     return out
 
 
+def attention_backward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor, dout: torch.Tensor,
+                       mask: Mask, lse: Optional[torch.Tensor] = None):
+    """Gradients (dq, dk, dv) — fp32 CUDA tensors [L, H, d] — of out = attention(q, k, v, mask)
+    for the upstream gradient dout (ga_attention_backward).  lse: optional
+    fp32 [L, H] log2-sum-exp2 of the forward's row scores (recomputed when None)."""
+    for t in (q, k, v, out, dout):
+        if not t.is_cuda or not t.is_contiguous() or t.dtype != q.dtype or t.shape != q.shape:
+            raise ValueError("q, k, v, out, dout: contiguous CUDA tensors of one shape and dtype")
+    L, H, d = q.shape
+    dq, dk, dv = (torch.empty((L, H, d), dtype=torch.float32, device=q.device) for _ in range(3))
+    cm = mask.to_c(L)
+    _abi.check(_abi.lib().ga_attention_backward(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                                dout.data_ptr(), ctypes.byref(cm),
+                                                lse.data_ptr() if lse is not None else None, dq.data_ptr(),
+                                                dk.data_ptr(), dv.data_ptr(), L, d, H, dtype_code(q.dtype),
+                                                _stream(q.device)))
+    return dq, dk, dv
+
+
+class GraphAttention(torch.autograd.Function):
+    """torch.autograd wrapper: forward = ga_attention_ex, backward = ga_attention_backward
+    (gradients returned in the input dtype)."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, mask):
+        out = attention(q.contiguous(), k.contiguous(), v.contiguous(), mask)
+        ctx.save_for_backward(q, k, v, out)
+        ctx.mask = mask
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        q, k, v, out = ctx.saved_tensors
+        dq, dk, dv = attention_backward(q.contiguous(), k.contiguous(), v.contiguous(), out,
+                                        dout.contiguous().to(q.dtype), ctx.mask)
+        return dq.to(q.dtype), dk.to(k.dtype), dv.to(v.dtype), None
+
+
 def state_finalize(state: State, dtype=torch.bfloat16, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """out = o / l of a carried state (ga_state_finalize)."""
     rows, H, d = state.o.shape

@@ -99,9 +99,12 @@ class Comm:
     # ---------------------------------------------------------------- attention
     def attention(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: Mask, L: int,
                   out: Optional[torch.Tensor] = None, *, kernel: str = "auto",
-                  workspace: Optional[torch.Tensor] = None, heavy_threshold: int = 0) -> torch.Tensor:
+                  workspace: Optional[torch.Tensor] = None, heavy_threshold: int = 0,
+                  exchange: str = "allgather") -> torch.Tensor:
         """This rank's rows of attention over the whole sequence (ga_attention_sharded).
-        q: local query rows [rows, H, d]; k, v: this rank's shard, views of empty() tensors."""
+        q: local query rows [rows, H, d]; k, v: this rank's shard, views of empty() tensors.
+        exchange (explicit CSR only): "allgather" (full-length K/V per rank) or "ring" (K/V
+        shards streamed through two staging buffers, partial states merged)."""
         rows, H, d = q.shape
         b, e = shard_rows(L, self.world, self.rank)
         if rows != e - b:
@@ -110,6 +113,7 @@ class Comm:
             out = torch.empty_like(q)
         cm = mask.to_c(L)
         o = _opts(0, 0, 0, 0, workspace, None, None, kernel, heavy_threshold)
+        o.exchange = {"allgather": _abi.GA_EXCHANGE_ALLGATHER, "ring": _abi.GA_EXCHANGE_RING}[exchange]
         _abi.check(_abi.lib().ga_attention_sharded(q.data_ptr(), k.data_ptr(), v.data_ptr(), ctypes.byref(cm),
                                                    out.data_ptr(), L, b, e, d, H, dtype_code(q.dtype),
                                                    ctypes.byref(o), self._h, _stream(q.device)))

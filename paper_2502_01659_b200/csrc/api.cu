@@ -354,6 +354,105 @@ ga_status ga_attention_ex(const void *Q, const void *K, const void *V, const ga_
     return dispatch(R.p, dtype, opts, R.heavy, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// Ring exchange of K/V for explicit CSR (GA_EXCHANGE_RING): the key
+// dimension is cut into the ranks' shards; step s computes this rank's rows against shard
+// q = (rank + s) mod world only (edge kernel, kv_clip: each row's slice of sorted columns in
+// that range) into a carried state, while the copy stream brings shard q + 1 from its owner
+// into the other staging buffer.  Memory per rank: 2 staging buffers of one K + V shard and
+// the fp32 state of the local rows, instead of the full-length K and V.
+static ga_status sharded_ring(ga_comm *c, const void *Q, const void *K, const void *V, const ga_mask *mask, void *out,
+                              int64_t L, int64_t b, int64_t rows, int64_t S, int32_t d, int32_t heads, ga_dtype dtype,
+                              const GaSymAlloc *ak, const GaSymAlloc *av, cudaStream_t s)
+{
+    const size_t rb = (size_t)heads * d * dtype_bytes(dtype);
+    const size_t blk = (size_t)S * rb; // K (or V) of one shard
+    cudaError_t e = cudaSuccess;
+    if (c->ring_bytes < 2 * blk) {
+        for (int i = 0; i < 2; ++i) {
+            if (c->ring_kv[i]) cudaFree(c->ring_kv[i]);
+            c->ring_kv[i] = nullptr;
+        }
+        c->ring_bytes = 0;
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&c->ring_kv[i], 2 * blk);
+        if (e != cudaSuccess) { set_error("ring staging buffers (%zu B): %s", 4 * blk, cudaGetErrorString(e)); return GA_ERR_OOM; }
+        c->ring_bytes = 2 * blk;
+    }
+    const size_t rh = (size_t)rows * heads, a256 = (sizeof(float) * rh + 255) & ~size_t(255);
+    const size_t st_bytes = 2 * a256 + sizeof(float) * rh * d;
+    if (c->ring_state_bytes < st_bytes) {
+        if (c->ring_state) cudaFree(c->ring_state);
+        c->ring_state = nullptr;
+        c->ring_state_bytes = 0;
+        if ((e = cudaMalloc(&c->ring_state, st_bytes)) != cudaSuccess) { set_error("ring state (%zu B): %s", st_bytes, cudaGetErrorString(e)); return GA_ERR_OOM; }
+        c->ring_state_bytes = st_bytes;
+    }
+    if (!c->ring_stream) {
+        e = cudaStreamCreateWithFlags(&c->ring_stream, cudaStreamNonBlocking);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            e = cudaEventCreateWithFlags(&c->ring_ready[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ring_done[i], cudaEventDisableTiming);
+        }
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ring_start, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ring_end, cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "ring stream / events");
+    }
+    char *sb = reinterpret_cast<char *>(c->ring_state);
+    ga_state stt{reinterpret_cast<float *>(sb), reinterpret_cast<float *>(sb + a256), reinterpret_cast<float *>(sb + 2 * a256)};
+    const size_t koff = (size_t)((const char *)K - ak->local), voff = (size_t)((const char *)V - av->local);
+    // the copy stream starts after the entry barrier (every shard complete)
+    cudaEventRecord(c->ring_start, s);
+    cudaStreamWaitEvent(c->ring_stream, c->ring_start, 0);
+    auto shard = [&](int step, int64_t &qb, int64_t &qn) {
+        const int q = (c->rank + step) % c->world;
+        qb = imin(L, (int64_t)q * S);
+        qn = imin(L, qb + S) - qb;
+        return q;
+    };
+    auto prefetch = [&](int step) -> cudaError_t {
+        int64_t qb, qn;
+        const int q = shard(step, qb, qn);
+        if (qn <= 0) return cudaSuccess;
+        const int bi = step & 1;
+        cudaStreamWaitEvent(c->ring_stream, c->ring_done[bi], 0); // step - 2 finished reading this buffer
+        char *dk = static_cast<char *>(c->ring_kv[bi]), *dv = dk + blk;
+        cudaError_t ce = cudaMemcpyAsync(dk, ak->peers[q] + koff, (size_t)qn * rb, cudaMemcpyDefault, c->ring_stream);
+        if (ce == cudaSuccess) ce = cudaMemcpyAsync(dv, av->peers[q] + voff, (size_t)qn * rb, cudaMemcpyDefault, c->ring_stream);
+        if (ce == cudaSuccess) ce = cudaEventRecord(c->ring_ready[bi], c->ring_stream);
+        return ce;
+    };
+    ga_status st = GA_OK;
+    for (int step = 0; step < c->world && st == GA_OK; ++step) {
+        if (step + 1 < c->world && (e = prefetch(step + 1)) != cudaSuccess) { st = cuda_fail(e, "ring copy"); break; }
+        int64_t qb, qn;
+        shard(step, qb, qn);
+        if (qn <= 0) continue;
+        const char *kb = (const char *)K, *vb = (const char *)V;
+        if (step > 0) {
+            kb = static_cast<const char *>(c->ring_kv[step & 1]);
+            vb = kb + blk;
+            cudaStreamWaitEvent(s, c->ring_ready[step & 1], 0);
+        }
+        ga_opts oo{};
+        oo.q_begin = b;
+        oo.q_rows = rows;
+        oo.kv_begin = qb;
+        oo.kv_rows = qn;
+        oo.state = stt;
+        oo.state_mode = step == 0 ? GA_STATE_WRITE : GA_STATE_ACCUMULATE;
+        Resolved R;
+        st = resolve(Q, kb, vb, mask, nullptr, L, d, heads, dtype, &oo, R);
+        if (st != GA_OK) break;
+        R.p.kv_clip = 1;
+        st = launch_edge(R.p, dtype, s);
+        cudaEventRecord(c->ring_done[step & 1], s);
+    }
+    // join the copy stream (its reads of the peers' shards precede the exit barrier)
+    cudaEventRecord(c->ring_end, c->ring_stream);
+    cudaStreamWaitEvent(s, c->ring_end, 0);
+    if (st == GA_OK) st = state_finalize(stt, rows, heads, d, dtype, out, s);
+    return st;
+}
+
 ga_status ga_attention_sharded(const void *Q, const void *K, const void *V, const ga_mask *mask, void *out, int64_t L,
                                int64_t row_begin, int64_t row_end, int32_t d, int32_t heads, ga_dtype dtype,
                                const ga_opts *opts, ga_comm *comm, void *stream)
@@ -388,7 +487,10 @@ ga_status ga_attention_sharded(const void *Q, const void *K, const void *V, cons
     ga_status st = comm_device_barrier(comm, s); // every rank's K/V shard is complete
     if (st != GA_OK) return st;
     if (rows > 0) {
-        if (mask->kind == GA_MASK_CSR || mask->kind == GA_MASK_BIGBIRD) {
+        if (mask->kind == GA_MASK_CSR && o.exchange == GA_EXCHANGE_RING && comm->world > 1) {
+            if (!out) { set_error("ring exchange needs out"); return GA_ERR_INVALID_ARG; }
+            st = sharded_ring(comm, Q, K, V, mask, out, L, b, rows, S, d, heads, dtype, ak, av, s);
+        } else if (mask->kind == GA_MASK_CSR || mask->kind == GA_MASK_BIGBIRD) {
             // unstructured columns (explicit CSR, BigBird's random columns): all-gather K and V (copy engines, peer -> local), then a
             // local launch over the full-length buffers
             const size_t full = (size_t)L * row_bytes;
@@ -442,6 +544,44 @@ ga_status ga_attention_sharded(const void *Q, const void *K, const void *V, cons
     // rank's output (NaN) instead of returning silently wrong rows
     if (st == GA_OK && out) st = comm_poison_on_timeout(comm, out, (size_t)rows * row_bytes, s);
     return st;
+}
+
+ga_status ga_attention_backward(const void *Q, const void *K, const void *V, const void *O, const void *dO,
+                                const ga_mask *mask, const float *lse, float *dQ, float *dK, float *dV, int64_t L,
+                                int32_t d, int32_t heads, ga_dtype dtype, void *stream)
+{
+    if (dtype != GA_F32 && dtype != GA_BF16 && dtype != GA_F16) { set_error("dtype %d invalid", (int)dtype); return GA_ERR_INVALID_ARG; }
+    if (d != 32 && d != 64 && d != 128) { set_error("d=%d unsupported (32, 64, 128)", d); return GA_ERR_UNSUPPORTED; }
+    if (heads < 1) { set_error("heads must be >= 1"); return GA_ERR_INVALID_ARG; }
+    if (!Q || !K || !V || !O || !dO || !dQ || !dK || !dV) { set_error("Q, K, V, O, dO, dQ, dK, dV must be non-NULL"); return GA_ERR_INVALID_ARG; }
+    for (const void *x : {Q, K, V, O, dO, (const void *)dQ, (const void *)dK, (const void *)dV})
+        if (!aligned16(x)) { set_error("all tensors must be 16-byte aligned"); return GA_ERR_INVALID_ARG; }
+    if (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)) { set_error("lse must be 4-byte aligned"); return GA_ERR_INVALID_ARG; }
+    DevMask M;
+    ga_status st = make_devmask(mask, L, M);
+    if (st != GA_OK) return st;
+    if (M.kind == GA_MASK_BIGBIRD) {
+        set_error("backward of an implicit BIGBIRD mask: materialise it with ga_mask_to_csr");
+        return GA_ERR_UNSUPPORTED;
+    }
+    const size_t bytes = (size_t)L * heads * d;
+    const char *gb[3] = {(const char *)dQ, (const char *)dK, (const char *)dV};
+    for (int a = 0; a < 3; ++a) // the gradients are written while every input is still read
+        for (const void *x : {Q, K, V, O, dO}) {
+            const char *xb = (const char *)x, *xe = xb + bytes * dtype_bytes(dtype);
+            if (gb[a] < xe && xb < gb[a] + bytes * 4) { set_error("dQ, dK, dV must not overlap the inputs"); return GA_ERR_INVALID_ARG; }
+        }
+    AttnParams p{};
+    p.Q = Q;
+    p.K = K;
+    p.V = V;
+    p.mask = M;
+    p.q_rows = p.kv_rows = L;
+    p.H = heads;
+    p.d = d;
+    p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+    p.nnz = M.kind == GA_MASK_CSR ? mask->nnz : 0;
+    return attention_backward(p, dtype, O, dO, lse, dQ, dK, dV, reinterpret_cast<cudaStream_t>(stream));
 }
 
 ga_status ga_state_finalize(const ga_state *state, int64_t rows, int32_t heads, int32_t d, ga_dtype dtype, void *out,

@@ -39,33 +39,70 @@ struct Args {
 
 __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
+// The mask's geometry in 32-bit arithmetic (L < 2^31 for BIGBIRD) with the sorted global list
+// staged in shared memory once per CTA: membership tests are a binary search over shared
+// memory instead of 64-bit divisions (the evenly spaced default G = {floor(k L / g)}).
+struct View {
+    const int32_t *G; // shared, ascending
+    int32_t ng, L, w, r;
+    __device__ __forceinline__ bool in_window(int32_t i, int32_t j) const
+    {
+        const int32_t d = i > j ? i - j : j - i;
+        return d < w && (r == 1 || d % r == 0);
+    }
+    __device__ __forceinline__ int32_t count_below(int32_t x) const // globals < x
+    {
+        int32_t lo = 0, hi = ng;
+        while (lo < hi) {
+            const int32_t mid = (lo + hi) >> 1;
+            if (G[mid] < x) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    }
+    __device__ __forceinline__ bool is_global(int32_t j) const
+    {
+        const int32_t k = count_below(j);
+        return k < ng && G[k] == j;
+    }
+    // |W_i U G| (reading R10's exclusion set)
+    __device__ __forceinline__ int32_t wg(int32_t i) const
+    {
+        const int32_t wlo = i - min(i, w - 1), whi = i + min(L - 1 - i, w - 1);
+        const int32_t nw = 1 + min(i, w - 1) / r + min(L - 1 - i, w - 1) / r;
+        const int32_t a = count_below(wlo), b = count_below(whi + 1);
+        int32_t in = b - a;
+        if (r > 1) {
+            in = 0;
+            for (int32_t k = a; k < b; ++k) in += in_window(i, G[k]) ? 1 : 0;
+        }
+        return nw + (ng - in);
+    }
+};
+
 // Extra columns of non-global row i — (G \ W_i) if parts has GA_BB_GLOBAL, R_i if it has
 // GA_BB_RANDOM — into buf (warp-collective; returns the warp-uniform count).
-__device__ int extras(const DevMask &M, int parts, int64_t i, int32_t *buf, int lane)
+__device__ int extras(const DevMask &M, const View &V, int parts, int32_t i, int32_t *buf, int lane)
 {
     int n = 0;
     if (parts & 2) {
-        for (int64_t k0 = 0; k0 < M.ng; k0 += 32) {
-            const int64_t k = k0 + lane;
-            int64_t gv = 0;
-            bool keep = false;
-            if (k < M.ng) {
-                gv = bb_global_at(M, k);
-                keep = !bb_in_window(M, i, gv);
-            }
+        for (int32_t k0 = 0; k0 < V.ng; k0 += 32) {
+            const int32_t k = k0 + lane;
+            const int32_t gv = k < V.ng ? V.G[k] : 0;
+            const bool keep = k < V.ng && !V.in_window(i, gv);
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
-            if (keep) buf[n + __popc(bal & lanemask_lt(lane))] = (int32_t)gv;
+            if (keep) buf[n + __popc(bal & lanemask_lt(lane))] = gv;
             n += __popc(bal);
         }
     }
     if ((parts & 4) && M.nrand > 0) {
-        const int64_t comp = M.L - bb_wg(M, i); // |complement of W_i U G|
-        if (comp <= M.nrand) {                  // exhausted: all of the complement (R10)
-            for (int64_t j0 = 0; j0 < M.L; j0 += 32) {
-                const int64_t j = j0 + lane;
-                const bool keep = j < M.L && !bb_in_window(M, i, j) && !bb_is_global(M, j);
+        const int32_t comp = V.L - V.wg(i); // |complement of W_i U G|
+        if (comp <= M.nrand) {              // exhausted: all of the complement (R10)
+            for (int32_t j0 = 0; j0 < V.L; j0 += 32) {
+                const int32_t j = j0 + lane;
+                const bool keep = j < V.L && !V.in_window(i, j) && !V.is_global(j);
                 const unsigned bal = __ballot_sync(0xffffffffu, keep);
-                if (keep) buf[n + __popc(bal & lanemask_lt(lane))] = (int32_t)j;
+                if (keep) buf[n + __popc(bal & lanemask_lt(lane))] = j;
                 n += __popc(bal);
             }
         } else {
@@ -80,19 +117,19 @@ __device__ int extras(const DevMask &M, int parts, int64_t i, int32_t *buf, int 
             int32_t *R = buf + n;
             int got = 0;
             for (uint64_t t0 = 0; got < target; t0 += 32) {
-                const int64_t c = bb_candidate(M, base, i, t0 + (uint64_t)lane);
-                bool valid = !bb_in_window(M, i, c) && !bb_is_global(M, c);
+                const int32_t c = (int32_t)bb_candidate(M, base, i, t0 + (uint64_t)lane);
+                bool valid = !V.in_window(i, c) && !V.is_global(c);
                 for (int q = 0; valid && q < got; ++q)
-                    if (R[q] == (int32_t)c) valid = false;
+                    if (R[q] == c) valid = false;
                 const unsigned vm = __ballot_sync(0xffffffffu, valid);
                 bool first = false;
                 if (valid) {
-                    const unsigned same = __match_any_sync(vm, (int32_t)c);
+                    const unsigned same = __match_any_sync(vm, c);
                     first = (same & lanemask_lt(lane)) == 0u;
                 }
                 const unsigned fm = __ballot_sync(0xffffffffu, first);
                 const int rank = __popc(fm & lanemask_lt(lane));
-                if (first && got + rank < target) R[got + rank] = (int32_t)c;
+                if (first && got + rank < target) R[got + rank] = c;
                 __syncwarp();
                 got = min(target, got + __popc(fm));
             }
@@ -107,16 +144,21 @@ template <typename T, int D>
 __global__ void __launch_bounds__(WARPS * 32) extras_kernel(const __grid_constant__ AttnParams p, const Args a)
 {
     __shared__ int32_t cols[WARPS][CAP];
+    __shared__ int32_t sG[CAP];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const DevMask &M = p.mask;
+    for (int k = threadIdx.x; k < M.ng; k += WARPS * 32) sG[k] = (int32_t)bb_global_at(M, k);
+    __syncthreads();
+    // |i - j| < L always, so w and r above L act as L (keeps them in 32 bits)
+    const View V{sG, (int32_t)M.ng, (int32_t)M.L, (int32_t)imin(M.w, M.L), (int32_t)imin(M.r, M.L)};
     const int64_t gw = (int64_t)blockIdx.x * WARPS + wib;
     const int H = p.H;
     if (gw >= p.q_rows * H) return;
     const int64_t t = gw / H;
     const int h = (int)(gw - t * H);
-    const int64_t i = p.q_begin + t;
-    const DevMask &M = p.mask;
+    const int32_t i = (int32_t)(p.q_begin + t);
     const int parts = M.parts ? M.parts : 7;
-    const bool glob = M.ng > 0 && bb_is_global(M, i);
+    const bool glob = M.ng > 0 && V.is_global(i);
     if (glob && a.full_rows) return;
 
     EdgeAcc<T, D, false> acc;
@@ -135,7 +177,7 @@ __global__ void __launch_bounds__(WARPS * 32) extras_kernel(const __grid_constan
             with_window = false;
         } // else: window only (random columns are drawn for non-global rows, R10)
     } else {
-        const int n = extras(M, parts, i, cols[wib], lane);
+        const int n = extras(M, V, parts, i, cols[wib], lane);
         acc.template run_csr<csr_depth<T, D>()>(cols[wib], 0, n);
     }
     acc.merge_groups();

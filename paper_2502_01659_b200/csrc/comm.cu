@@ -495,6 +495,15 @@ ga_status ga_comm_destroy(ga_comm *c)
         if (c->gather_k) cudaFree(c->gather_k);
         if (c->gather_v) cudaFree(c->gather_v);
         if (c->timed_out_host) cudaFreeHost(const_cast<int *>(c->timed_out_host));
+        for (int b = 0; b < 2; ++b) {
+            if (c->ring_kv[b]) cudaFree(c->ring_kv[b]);
+            if (c->ring_ready[b]) cudaEventDestroy(c->ring_ready[b]);
+            if (c->ring_done[b]) cudaEventDestroy(c->ring_done[b]);
+        }
+        if (c->ring_state) cudaFree(c->ring_state);
+        if (c->ring_start) cudaEventDestroy(c->ring_start);
+        if (c->ring_end) cudaEventDestroy(c->ring_end);
+        if (c->ring_stream) cudaStreamDestroy(c->ring_stream);
     }
     c->allocs.clear();
     close_fds(c);

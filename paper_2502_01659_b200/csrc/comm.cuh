@@ -32,6 +32,15 @@ struct ga_comm {
     // CSR / BigBird all-gather scratch: full-length K and V (grown on demand)
     void *gather_k = nullptr, *gather_v = nullptr;
     size_t gather_bytes = 0;
+    // ring exchange (GA_EXCHANGE_RING): two staging buffers for one shard of K and of V, the
+    // fp32 carried state of the local rows, a copy stream and its events (grown on demand)
+    void *ring_kv[2] = {nullptr, nullptr};
+    size_t ring_bytes = 0; // per staging buffer (K and V of one shard)
+    float *ring_state = nullptr;
+    size_t ring_state_bytes = 0;
+    cudaStream_t ring_stream = nullptr;
+    cudaEvent_t ring_ready[2] = {nullptr, nullptr}, ring_done[2] = {nullptr, nullptr}, ring_start = nullptr,
+                ring_end = nullptr;
 };
 
 namespace ga {

@@ -197,6 +197,10 @@ struct AttnParams {
     // carried (m, l, o) state (ga_opts.state; state.m == NULL: none)
     ga_state state;
     int32_t state_mode;
+    // explicit CSR on the edge kernel: edges whose key lies outside [kv_begin, kv_begin +
+    // kv_rows) are skipped (a row's sorted columns in that range are one contiguous slice,
+    // found by binary search) — one key block of the ring exchange (ga_opts.exchange)
+    int32_t kv_clip;
 };
 
 // Base address (head 0, element 0) of K and V token row j: the local buffer when j is in
@@ -238,6 +242,8 @@ ga_status launch_full_rows(const AttnParams &p, ga_dtype dt, const int64_t *nful
 ga_status bigbird_check(const AttnParams &p);
 size_t bigbird_workspace(const AttnParams &p, ga_dtype dt);
 ga_status launch_bigbird(const AttnParams &p, ga_dtype dt, cudaStream_t s);
+ga_status attention_backward(const AttnParams &p, ga_dtype dt, const void *O, const void *dO, const float *lse_in,
+                             float *dQ, float *dK, float *dV, cudaStream_t s);
 
 ga_status maskgen_to_csr(const DevMask &M, int64_t *row_ptr, int32_t *col_idx, cudaStream_t s);
 ga_status mask_validate(const DevMask &M, cudaStream_t s, int *ok);

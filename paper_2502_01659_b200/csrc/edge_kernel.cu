@@ -37,8 +37,24 @@ __global__ void __launch_bounds__(256) edge_kernel(AttnParams p)
     const int np = num_pieces(p.mask, i);
     for (int pc = 0; pc < np; ++pc) {
         const Piece P = get_piece(p.mask, i, pc);
-        if (P.mode == P_CSR)
-            acc.template run_csr<csr_depth<T, D>()>(P.cols + P.base, 0, P.count);
+        if (P.mode == P_CSR) {
+            int64_t kb = 0, ke = P.count;
+            if (p.kv_clip) { // this key block's slice of the row's ascending columns
+                const int32_t *c = P.cols + P.base;
+                auto lower = [&](int64_t x) {
+                    int64_t lo = 0, hi = P.count;
+                    while (lo < hi) {
+                        const int64_t mid = (lo + hi) >> 1;
+                        if ((int64_t)c[mid] < x) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    return lo;
+                };
+                kb = lower(p.kv_begin);
+                ke = lower(p.kv_begin + p.kv_rows);
+            }
+            acc.template run_csr<csr_depth<T, D>()>(P.cols + P.base, kb, ke);
+        }
         else
             acc.run(P, 0, P.count);
     }

@@ -104,25 +104,41 @@ def test_sharded_longnet_two_ranks():
 # ------------------------------------------------------------ C-ABI comm over IPC peer memory
 def _comm_case(rank, world, fam, kernel="auto"):
     """ga_attention_sharded: K/V shards in symmetric (IPC-mapped) buffers, remote rows read
-    in-kernel from the other rank's memory (window halo, LongNet strided rows) or
-    all-gathered (CSR).  Both ranks share cuda:0 here; across GPUs the same mappings go over
-    NVLink."""
+    in-kernel from the other rank's memory (window halo, LongNet strided rows), all-gathered
+    (CSR, implicit BigBird) or ring-streamed (CSR, GA_EXCHANGE_RING).  Both ranks share cuda:0
+    here; across GPUs the same mappings go over NVLink.  Checked against the 1-GPU output
+    (bitwise where the shards are tile-aligned) AND against the fp64 oracle on sampled rows,
+    including every row within reach + 256 of each shard boundary."""
+    import numpy as np
+
+    import oracle
     import paper_2502_01659_b200 as ga
     from paper_2502_01659_b200.comm import Comm, shard_rows
 
     comm = Comm()
+    exchange = "allgather"
     try:
         if fam == "window":
             H, d, L, mask, exact = 8, 64, 224 * 40 * world, ga.Window(256, 2), True
+            om, reach = oracle.window(L, 256, 2), 254
         elif fam == "window_unaligned":
             H, d, L, mask, exact = 2, 64, 10001, ga.Window(300, 3), False
+            om, reach = oracle.window(L, 300, 3), 297
         elif fam == "longnet":
             H, d, L, mask, exact = 1, 64, 2 ** 16, ga.LongNet(256, 2), True
+            om, reach = oracle.longnet(L, 256, 2), 256
         elif fam == "longnet_a3":
             H, d, L, mask, exact = 2, 32, 9000, ga.LongNet(100, 3), False
-        else:  # BigBird materialised as CSR: K/V all-gather path
-            H, d, L, exact = 2, 64, 8192, True
+            om, reach = oracle.longnet(L, 100, 3), 100
+        elif fam == "bigbird_implicit":  # implicit descriptor: K/V all-gather, window on tcgen05
+            H, d, L, exact = 2, 64, 8192, False
+            mask, om, reach = ga.BigBird(128, 8, 16, 7), oracle.bigbird(L, 128, 8, 16, 7), 127
+        else:  # BigBird materialised as CSR: K/V all-gather or ring
+            H, d, L, exact = 2, 64, 8192, fam == "bigbird_csr"
             mask = ga.mask_to_csr(ga.BigBird(64, 8, 16, 7), L)
+            om, reach = oracle.bigbird(L, 64, 8, 16, 7), 63
+            if fam == "bigbird_csr_ring":
+                exchange = "ring"
         q, k, v = ga.qkv_device(17, L, H, d, torch.bfloat16)
         full = ga.attention(q, k, v, mask, kernel=kernel)
         b, e = shard_rows(L, world, rank)
@@ -132,7 +148,8 @@ def _comm_case(rank, world, fam, kernel="auto"):
         ks[: e - b].copy_(k[b:e])
         vs[: e - b].copy_(v[b:e])
         for _ in range(2):  # reuse of the comm and its buffers
-            out = comm.attention(q[b:e].contiguous(), ks[: e - b], vs[: e - b], mask, L, kernel=kernel)
+            out = comm.attention(q[b:e].contiguous(), ks[: e - b], vs[: e - b], mask, L, kernel=kernel,
+                                 exchange=exchange)
             torch.cuda.synchronize()
             if exact:
                 diff = (out.float() - full[b:e].float()).abs().amax(dim=(1, 2))
@@ -140,6 +157,15 @@ def _comm_case(rank, world, fam, kernel="auto"):
                 assert bad.numel() == 0, (fam, rank, bad.numel(), bad[:8].tolist(), diff.max().item())
             else:
                 assert (out.float() - full[b:e].float()).abs().max().item() < 2e-2, fam
+        # the oracle on rows around every shard boundary and a random sample
+        rng = np.random.default_rng(rank)
+        rows = set(int(x) for x in rng.integers(b, e, 64))
+        for x in (b, e):
+            rows |= set(range(max(b, x - reach - 256), min(e, x + reach + 256)))
+        rows = np.array(sorted(rows), dtype=np.int64)
+        want, _ = oracle.attention_seeded(17, "bf16", om, H, d, rows=rows)
+        got = out[torch.from_numpy(rows - b).cuda()].double().cpu().numpy()
+        assert np.abs(got - want).max() <= 2e-2, (fam, rank, np.abs(got - want).max())
         assert not comm.timed_out()
         comm.free(ks)
         comm.free(vs)
@@ -149,6 +175,12 @@ def _comm_case(rank, world, fam, kernel="auto"):
 
 @pytest.mark.parametrize("fam,kernel", [("window", "auto"), ("window", "edge"), ("window_unaligned", "auto"),
                                         ("longnet", "auto"), ("longnet", "tiled"), ("longnet", "edge"),
-                                        ("longnet_a3", "auto"), ("bigbird_csr", "auto")])
+                                        ("longnet_a3", "auto"), ("bigbird_csr", "auto"), ("bigbird_csr_ring", "auto"),
+                                        ("bigbird_implicit", "auto")])
 def test_comm_sharded_attention_two_ranks(fam, kernel):
     _spawn(functools.partial(_comm_case, fam=fam, kernel=kernel))
+
+
+@pytest.mark.parametrize("fam", ["window_unaligned", "bigbird_csr_ring", "longnet_a3"])
+def test_comm_sharded_attention_three_ranks(fam):
+    _spawn(functools.partial(_comm_case, fam=fam), world=3)

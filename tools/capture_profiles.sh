@@ -5,8 +5,8 @@
 set -u
 out=gpurun_out
 mkdir -p $out
-B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
-for c in ${CFGS:-cfg1 cfg2 cfg3 cfg4 cfg5}; do
+B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-per-config"
+for c in ${CFGS:-cfg1 cfg2 cfg3 cfg3i cfg4 cfg5}; do
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file $out/launches_$c.csv $B --config $c > $out/launches_$c.log 2>&1
 done

@@ -30,7 +30,7 @@ def launches(path):
 
 def ours(name):
     return any(s in name for s in ("ga::", "lnet", "band_kernel", "edge_kernel", "heavy_", "longnet", "scan_",
-                                   "window_tc", "csr_mma", "csr_tma", "full_rows", "full_merge", "coo_"))
+                                   "window_tc", "csr_mma", "csr_tma", "full_rows", "full_merge", "coo_", "bb::", "bwd::"))
 
 
 def main():
@@ -42,7 +42,7 @@ def main():
     summary = [f"{tag}: one bench.py step per config under `ncu --metrics gpu__time_duration.sum,"
                "dram__bytes_read.sum,dram__bytes_write.sum --clock-control none` (cold caches, serialised;",
                "shares, not absolute times, are comparable with the bench's CUDA-event timing)", ""]
-    for cfg in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"):
+    for cfg in ("cfg1", "cfg2", "cfg3", "cfg3i", "cfg4", "cfg5"):
         p = os.path.join(src, f"launches_{cfg}.csv")
         if not os.path.exists(p):
             continue
