@@ -83,8 +83,14 @@ typedef enum {
    window (the paper's "global minus local" kernel), the random columns.  They
    are disjoint and their union is the BigBird mask; Longformer = WINDOW + GLOBAL. */
 typedef enum { GA_BB_WINDOW = 1, GA_BB_GLOBAL = 2, GA_BB_RANDOM = 4 } ga_bigbird_part;
-/* LONGNET variant (ga_mask.parts): LongNet's multiset mixture (reading R11b). */
-enum { GA_LONGNET_MULTISET = 1 };
+/* LONGNET variants (ga_mask.parts bits):
+   GA_LONGNET_MULTISET     LongNet's multiset mixture (reading R11b);
+   GA_LONGNET_HEAD_OFFSETS per-head offsets (reading R11c, LongNet's s_j = j mod r): head h
+                           keeps, at level k, the positions whose in-segment offset is
+                           congruent to h modulo alpha^k (instead of 0), so each head has its
+                           own edge set.  Runs on the edge kernel (forward and backward);
+                           ga_mask_count / ga_mask_to_csr return GA_ERR_UNSUPPORTED. */
+enum { GA_LONGNET_MULTISET = 1, GA_LONGNET_HEAD_OFFSETS = 2 };
 
 /* Mask descriptor: the paper's "attention-specific parameters P_a" or explicit graph G
    (Algorithm 1 input).  Unused fields are ignored; zero-initialise. */

@@ -56,6 +56,7 @@ class _OrcMask(ctypes.Structure):
         ("seg", ctypes.c_int64),
         ("global_idx", ctypes.c_void_p), ("n_global", ctypes.c_int64),
         ("n_random", ctypes.c_int64), ("seed", ctypes.c_uint64), ("parts", ctypes.c_int64),
+        ("head", ctypes.c_int64),
     ]
 
 
@@ -115,7 +116,8 @@ class Mask:
     n_global: int = 0
     n_random: int = 0
     seed: int = 0
-    parts: int = 0                             # BigBird components (0 = all)
+    parts: int = 0                             # BigBird components (0 = all); LongNet variant bits
+    head: int = 0                              # LongNet per-head offsets: head of neighbors()
     row_ptr: Optional[np.ndarray] = None       # int64 [L+1]
     col_idx: Optional[np.ndarray] = None       # int32 [nnz]
     _keep: list = field(default_factory=list, repr=False)
@@ -126,6 +128,7 @@ class Mask:
         m.w0, m.alpha, m.seg = self.w0, self.alpha, self.seg
         m.n_global, m.n_random, m.seed = self.n_global, self.n_random, self.seed & (2**64 - 1)
         m.parts = self.parts
+        m.head = self.head
         self._keep = []
         if self.global_idx is not None:
             g = np.ascontiguousarray(self.global_idx, dtype=np.int64)
@@ -148,10 +151,12 @@ def block_dilated(L, seg, r=1):
     return Mask(BLOCK_DILATED, L, seg=seg, r=r)
 
 
-def longnet(L, w0, alpha=2, multiset=False):
+def longnet(L, w0, alpha=2, multiset=False, head_offsets=False, head=0):
     """LongNet (reading R11); multiset=True: LongNet's own mixture, the multiset union of the
-    levels' blocks (reading R11b)."""
-    return Mask(LONGNET, L, w0=w0, alpha=alpha, parts=1 if multiset else 0)
+    levels' blocks (reading R11b); head_offsets=True: head h keeps the
+    in-segment offsets congruent to h mod alpha^k at level k (reading R11c) — attention()
+    uses each head's own set, neighbors()/mask_to_csr() that of `head`."""
+    return Mask(LONGNET, L, w0=w0, alpha=alpha, parts=(1 if multiset else 0) | (2 if head_offsets else 0), head=head)
 
 
 BB_WINDOW, BB_GLOBAL, BB_RANDOM = 1, 2, 4  # BigBird components (disjoint; union = full mask)

@@ -29,13 +29,18 @@ def block_dilated_mask(L, seg, r=1):
     return (i // seg == j // seg) & ((i % seg) % r == 0) & ((j % seg) % r == 0)
 
 
-def longnet_mask(L, w0, alpha=2):
+def longnet_mask(L, w0, alpha=2, head=None):
+    """Union of BlockDilated(w0 alpha^k, alpha^k) levels; head given: LongNet's per-head
+    offsets (reading R11c), in-segment offsets congruent to head mod alpha^k."""
     K = 0
     while w0 * alpha ** (K + 1) <= L:
         K += 1
     m = np.zeros((L, L), dtype=bool)
+    i, j = _grid(L)
     for k in range(K + 1):
-        m |= block_dilated_mask(L, w0 * alpha ** k, alpha ** k)
+        seg, r = w0 * alpha ** k, alpha ** k
+        off = 0 if head is None else head % r
+        m |= (i // seg == j // seg) & ((i % seg) % r == off) & ((j % seg) % r == off)
     return m
 
 

@@ -67,7 +67,9 @@ typedef struct {
     int64_t n_global;
     int64_t n_random;
     uint64_t seed;
-    int64_t parts;          /* BigBird components (0 = all)                    */
+    int64_t parts;          /* BigBird components (0 = all); LongNet: bit 0 multiset,
+                               bit 1 per-head offsets (reading R11c)              */
+    int64_t head;           /* LongNet per-head offsets: the head whose set N(i) is enumerated */
 } orc_mask;
 
 enum { ORC_F32 = 0, ORC_BF16 = 1, ORC_F16 = 2, ORC_F64 = 3 };
@@ -257,18 +259,20 @@ int64_t orc_row_neighbors(const orc_mask *m, int64_t i, int64_t *out)
         return n;
     }
     case ORC_LONGNET: {
-        /* union over levels k of BlockDilated(seg_k = w0*alpha^k, r_k = alpha^k) */
+        /* union over levels k of BlockDilated(seg_k = w0*alpha^k, r_k = alpha^k); with per-head
+           offsets (parts bit 1, reading R11c: LongNet's s_j = j mod r) head h keeps the
+           in-segment offsets congruent to h mod r_k instead of 0 */
         int64_t K = orc_longnet_levels(m->w0, m->alpha, L);
         int64_t seg = m->w0, r = 1;
         for (int64_t k = 0; k <= K; ++k) {
-            int64_t b = i / seg;
-            if ((i % seg) % r == 0)
-                for (int64_t j = b * seg; j < (b + 1) * seg && j < L; j += r)
-                    if ((j % seg) % r == 0) out[n++] = j;
+            int64_t b = i / seg, off = (m->parts & 2) ? m->head % r : 0;
+            if ((i % seg) % r == off)
+                for (int64_t j = b * seg + off; j < (b + 1) * seg && j < L; j += r)
+                    if ((j % seg) % r == off) out[n++] = j;
             seg *= m->alpha;
             r *= m->alpha;
         }
-        if (m->parts == 1) { /* multiset union (LongNet's mixture, reading R11b): keep repeats */
+        if (m->parts & 1) { /* multiset union (LongNet's mixture, reading R11b): keep repeats */
             if (n > 1) qsort(out, (size_t)n, sizeof(int64_t), cmp_i64);
             return n;
         }
@@ -297,6 +301,17 @@ int64_t orc_row_neighbors(const orc_mask *m, int64_t i, int64_t *out)
     }
     }
     return 0;
+}
+
+/* Masks whose neighbour sets depend on the head (LongNet per-head offsets). */
+static int per_head(const orc_mask *m) { return m->kind == ORC_LONGNET && (m->parts & 2); }
+
+/* N(i) of head h. */
+int64_t orc_row_neighbors_head(const orc_mask *m, int64_t i, int64_t h, int64_t *out)
+{
+    orc_mask mh = *m;
+    mh.head = h;
+    return orc_row_neighbors(&mh, i, out);
 }
 
 /* Exact nnz and row_ptr (exclusive scan of degrees) / col_idx.  col_idx may be NULL. */
@@ -379,6 +394,7 @@ int64_t orc_attention(const orc_inputs *in, const orc_mask *m, int64_t H, int64_
             for (int64_t h = 0; h < H; ++h) {
                 double *o = out + ((size_t)t * (size_t)H + (size_t)h) * (size_t)d;
                 for (int64_t c = 0; c < d; ++c) o[c] = 0.0;
+                if (per_head(m)) n = orc_row_neighbors_head(m, i, h, nb);
                 if (n == 0) continue; /* empty row -> 0 (reading R6) */
                 load_row(in, 0, i, h, H, d, q);
                 double mx = -INFINITY;
@@ -428,6 +444,7 @@ int64_t orc_attention_alg1(const orc_inputs *in, const orc_mask *m, int64_t H, i
             for (int64_t h = 0; h < H; ++h) {
                 double *o = out + ((size_t)t * (size_t)H + (size_t)h) * (size_t)d;
                 for (int64_t c = 0; c < d; ++c) o[c] = 0.0;
+                if (per_head(m)) n = orc_row_neighbors_head(m, i, h, nb);
                 load_row(in, 0, i, h, H, d, q);
                 double mi = -INFINITY, li = 0.0;
                 for (int64_t e = 0; e < n; ++e) {
@@ -477,9 +494,10 @@ int64_t orc_attention_backward(const orc_inputs *in, const orc_mask *m, int64_t 
     memset(dk, 0, sizeof(double) * (size_t)(L * H * d));
     memset(dv, 0, sizeof(double) * (size_t)(L * H * d));
     for (int64_t i = 0; i < L; ++i) {
-        const int64_t n = orc_row_neighbors(m, i, nb);
-        if (n == 0) continue;
+        int64_t n = orc_row_neighbors(m, i, nb);
         for (int64_t h = 0; h < H; ++h) {
+            if (per_head(m)) n = orc_row_neighbors_head(m, i, h, nb);
+            if (n == 0) continue;
             const size_t ri = ((size_t)i * (size_t)H + (size_t)h) * (size_t)d;
             const double *g = dout + ri;
             load_row(in, 0, i, h, H, d, q);

@@ -18,7 +18,7 @@ GA_F32, GA_BF16, GA_F16 = 0, 1, 2
 GA_MASK_CSR, GA_MASK_WINDOW, GA_MASK_LONGNET, GA_MASK_BIGBIRD, GA_MASK_BLOCK_DILATED = 0, 1, 2, 3, 4
 GA_KERNEL_AUTO, GA_KERNEL_EDGE, GA_KERNEL_TILED, GA_KERNEL_TC = 0, 1, 2, 3
 GA_BB_WINDOW, GA_BB_GLOBAL, GA_BB_RANDOM = 1, 2, 4
-GA_LONGNET_MULTISET = 1
+GA_LONGNET_MULTISET, GA_LONGNET_HEAD_OFFSETS = 1, 2
 
 STATUS_NAMES = {0: "GA_OK", -1: "GA_ERR_INVALID_ARG", -2: "GA_ERR_UNSUPPORTED", -3: "GA_ERR_CUDA",
                 -4: "GA_ERR_COMM", -5: "GA_ERR_OOM", -6: "GA_ERR_MASK"}

@@ -75,8 +75,8 @@ static ga_status make_devmask(const ga_mask *m, int64_t L, DevMask &M)
         return GA_OK;
     case GA_MASK_LONGNET:
         if (m->w0 < 1 || m->alpha < 2) { set_error("LongNet needs w0 >= 1 and alpha >= 2"); return GA_ERR_INVALID_ARG; }
-        if (m->parts != 0 && m->parts != GA_LONGNET_MULTISET) {
-            set_error("LongNet parts must be 0 (set union) or GA_LONGNET_MULTISET");
+        if (m->parts < 0 || m->parts > (GA_LONGNET_MULTISET | GA_LONGNET_HEAD_OFFSETS)) {
+            set_error("LongNet parts: 0 (set union) or GA_LONGNET_MULTISET, optionally | GA_LONGNET_HEAD_OFFSETS");
             return GA_ERR_INVALID_ARG;
         }
         M.parts = m->parts;
@@ -785,6 +785,10 @@ ga_status ga_mask_count(const ga_mask *pattern, int64_t *nnz_out)
         return GA_OK;
     }
     case GA_MASK_LONGNET: {
+        if (M.parts & GA_LONGNET_HEAD_OFFSETS) {
+            set_error("LongNet with per-head offsets has one edge set per head: no single count");
+            return GA_ERR_UNSUPPORTED;
+        }
         // Per level t and level-t segment [s0,s1): rows with s = min(nu(i),K) == t contribute
         // all U multiples of alpha^t in the segment; rows with s > t contribute the U -
         // ceil(U/alpha) of them whose valuation is exactly t (masks.cuh decomposition).
@@ -837,6 +841,10 @@ ga_status ga_mask_to_csr(const ga_mask *pattern, int64_t *row_ptr, int32_t *col_
     if (st != GA_OK) return st;
     if (M.kind == GA_MASK_CSR) { set_error("mask is already CSR"); return GA_ERR_INVALID_ARG; }
     if (M.L > INT32_MAX) { set_error("CSR columns are int32: L must be < 2^31"); return GA_ERR_UNSUPPORTED; }
+    if (M.kind == GA_MASK_LONGNET && (M.parts & GA_LONGNET_HEAD_OFFSETS)) {
+        set_error("LongNet with per-head offsets has one edge set per head: no single CSR");
+        return GA_ERR_UNSUPPORTED;
+    }
     return maskgen_to_csr(M, row_ptr, col_idx, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -74,14 +74,14 @@ struct Nbrs {
     const int32_t *ci;
 };
 
-__device__ __forceinline__ int npieces(const DevMask &M, const Nbrs &nb, int64_t i)
+__device__ __forceinline__ int npieces(const DevMask &M, const Nbrs &nb, int64_t i, int h)
 {
-    return nb.rp ? 1 : num_pieces(M, i);
+    return nb.rp ? 1 : num_pieces_h(M, i, h);
 }
 
-__device__ __forceinline__ Piece piece(const DevMask &M, const Nbrs &nb, int64_t i, int pc)
+__device__ __forceinline__ Piece piece(const DevMask &M, const Nbrs &nb, int64_t i, int pc, int h)
 {
-    if (!nb.rp) return get_piece(M, i, pc);
+    if (!nb.rp) return get_piece_h(M, i, pc, h);
     Piece P;
     P.mode = P_CSR;
     P.cols = nb.ci;
@@ -117,14 +117,14 @@ __global__ void __launch_bounds__(256) row_kernel(const __grid_constant__ AttnPa
     load_slice<T, D>(a.dO, i, h, H, sub, dO);
     load_slice<T, D>(a.O, i, h, H, sub, x);
     const float Di = group_sum<Y::G>(dot<Y::PER>(dO, x));
-    const int np = npieces(p.mask, a.fwd, i);
+    const int np = npieces(p.mask, a.fwd, i, h);
     float lse;
     if (a.lse_in) {
         lse = a.lse_in[gw];
     } else { // log2-sum-exp2 of the row's scores: online (m, l) per lane group, then merged
         float m = -INFINITY, l = 0.f;
         for (int pc = 0; pc < np; ++pc) {
-            const Piece P = piece(p.mask, a.fwd, i, pc);
+            const Piece P = piece(p.mask, a.fwd, i, pc, h);
             for (int64_t k0 = 0; k0 < P.count; k0 += Y::E) {
                 const int64_t k = k0 + g;
                 const bool v = k < P.count;
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(256) row_kernel(const __grid_constant__ AttnPa
 #pragma unroll
     for (int e = 0; e < Y::PER; ++e) dq[e] = 0.f;
     for (int pc = 0; pc < np; ++pc) {
-        const Piece P = piece(p.mask, a.fwd, i, pc);
+        const Piece P = piece(p.mask, a.fwd, i, pc, h);
         for (int64_t k0 = 0; k0 < P.count; k0 += Y::E) {
             const int64_t k = k0 + g;
             const bool v = k < P.count;
@@ -204,9 +204,9 @@ __global__ void __launch_bounds__(256) col_kernel(const __grid_constant__ AttnPa
     load_slice<T, D>(p.V, j, h, H, sub, vj);
 #pragma unroll
     for (int e = 0; e < Y::PER; ++e) dk[e] = dv[e] = 0.f;
-    const int np = npieces(p.mask, a.tr, j);
+    const int np = npieces(p.mask, a.tr, j, h);
     for (int pc = 0; pc < np; ++pc) {
-        const Piece P = piece(p.mask, a.tr, j, pc);
+        const Piece P = piece(p.mask, a.tr, j, pc, h);
         for (int64_t k0 = 0; k0 < P.count; k0 += Y::E) {
             const int64_t k = k0 + g;
             const bool v = k < P.count;

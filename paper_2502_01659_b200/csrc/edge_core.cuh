@@ -299,9 +299,9 @@ __device__ __forceinline__ void edge_row(const AttnParams &p, int64_t t, int h, 
     EdgeAcc<T, D, false> acc;
     acc.init(p, t, h, lane);
     const int64_t i = p.q_begin + t;
-    const int np = num_pieces(p.mask, i);
+    const int np = num_pieces_h(p.mask, i, h);
     for (int pc = 0; pc < np; ++pc) {
-        const Piece P = get_piece(p.mask, i, pc);
+        const Piece P = get_piece_h(p.mask, i, pc, h);
         acc.run(P, 0, P.count);
     }
     acc.merge_groups();

@@ -34,9 +34,9 @@ __global__ void __launch_bounds__(256) edge_kernel(AttnParams p)
 
     EdgeAcc<T, D, PROBE> acc;
     acc.init(p, t, h, lane);
-    const int np = num_pieces(p.mask, i);
+    const int np = num_pieces_h(p.mask, i, h);
     for (int pc = 0; pc < np; ++pc) {
-        const Piece P = get_piece(p.mask, i, pc);
+        const Piece P = get_piece_h(p.mask, i, pc, h);
         if (P.mode == P_CSR) {
             int64_t kb = 0, ke = P.count;
             if (p.kv_clip) { // this key block's slice of the row's ascending columns

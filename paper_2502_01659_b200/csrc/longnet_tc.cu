@@ -363,7 +363,7 @@ template <typename T, int D> static ga_status launch_t(const LParams &lp, cudaSt
 bool longnet_tc_supported(const AttnParams &p, ga_dtype dt)
 {
     if (p.mask.kind != K_LONGNET || (dt != GA_BF16 && dt != GA_F16)) return false;
-    if (p.mask.parts == GA_LONGNET_MULTISET) return false; // overlapping pieces: edge kernel
+    if (p.mask.parts != 0) return false; // multiset (overlapping pieces) / per-head offsets: edge kernel
     return p.mask.K + 1 <= lnet::MAX_PIECES && p.mask.w0 >= 16;
 }
 

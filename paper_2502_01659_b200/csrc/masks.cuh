@@ -83,20 +83,36 @@ GA_HD int64_t ipow(int64_t a, int64_t e)
 
 GA_HD int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Number of pieces of row i.
-GA_HD int num_pieces(const DevMask &M, int64_t i)
+// LongNet variants (DevMask.parts bits): 1 = multiset mixture (reading R11b), 2 = per-head
+// offsets (reading R11c): head h keeps, at level t, the positions congruent
+// to h modulo alpha^t instead of 0 — LongNet's s_j = j mod r.  Since alpha^t divides the
+// level's segment length, that is (i - h) mod alpha^t == 0, so the disjoint decomposition of
+// the set union carries over with every valuation taken of (i - h): s = min(nu(|i - h|), K).
+enum { LN_MULTISET = 1, LN_HEAD_OFFSETS = 2 };
+
+// Number of pieces of row i (head h: only LongNet with per-head offsets depends on it).
+GA_HD int num_pieces_h(const DevMask &M, int64_t i, int h)
 {
     switch (M.kind) {
     case K_WINDOW:
     case K_CSR: return 1;
     case K_BLOCK_DILATED: return ((i % M.seg) % M.r == 0) ? 1 : 0;
-    case K_LONGNET: return (int)valuation(i, M.alpha, M.K) + 1;
+    case K_LONGNET: {
+        const int64_t x = (M.parts & LN_HEAD_OFFSETS) ? i - h : i;
+        return (int)valuation(x < 0 ? -x : x, M.alpha, M.K) + 1;
+    }
     default: return 0;
     }
 }
 
+GA_HD int num_pieces(const DevMask &M, int64_t i) { return num_pieces_h(M, i, 0); }
+
+GA_HD Piece get_piece_h(const DevMask &M, int64_t i, int pc, int h);
+
 // Piece pc of row i.  For LongNet pc = level t in [0, s].
-GA_HD Piece get_piece(const DevMask &M, int64_t i, int pc)
+GA_HD Piece get_piece(const DevMask &M, int64_t i, int pc) { return get_piece_h(M, i, pc, 0); }
+
+GA_HD Piece get_piece_h(const DevMask &M, int64_t i, int pc, int h)
 {
     Piece P;
     P.mode = P_AFFINE;
@@ -129,18 +145,21 @@ GA_HD Piece get_piece(const DevMask &M, int64_t i, int pc)
         return P;
     }
     case K_LONGNET: {
-        int64_t s = valuation(i, M.alpha, M.K);
+        const int64_t hoff = (M.parts & LN_HEAD_OFFSETS) ? h : 0;
+        const int64_t x = i - hoff;
+        int64_t s = valuation(x < 0 ? -x : x, M.alpha, M.K);
         int64_t stp = ipow(M.alpha, pc);
         int64_t segw = M.w0 * stp;
         int64_t s0 = (i / segw) * segw, s1 = imin(M.L, s0 + segw);
-        int64_t U = ceil_div(s1 - s0, stp); // multiples of alpha^t in the segment
-        P.base = s0;
+        const int64_t b = s0 + hoff % stp; // first position == h (mod a^t): a^t divides s0
+        int64_t U = b < s1 ? ceil_div(s1 - b, stp) : 0; // such positions in the segment
+        P.base = b;
         P.step = stp;
-        if (pc < s && M.parts != 1) { // parts 1 = GA_LONGNET_MULTISET: every level keeps all multiples
-            // keep j = s0 + a^t u with nu(j) == t exactly, i.e. (s0/a^t + u) mod a != 0:
-            // exclude the residue u == -(s0/a^t) (mod a)  (s0 is a multiple of a^t, and of
-            // a^(t+1) only when a | w0 * (segment index))
-            const int64_t c0 = (s0 / stp) % M.alpha;
+        if (pc < s && !(M.parts & LN_MULTISET)) { // multiset: every level keeps all of them
+            // keep j = b + a^t u with nu(j - h) == t exactly, i.e. ((b - h)/a^t + u) mod a != 0:
+            // exclude the residue u == -((b - h)/a^t) (mod a)  (b - h is a multiple of a^t)
+            const int64_t q0 = (b - hoff) / stp;
+            const int64_t c0 = ((q0 % M.alpha) + M.alpha) % M.alpha;
             const int64_t rx = (M.alpha - c0) % M.alpha;
             P.mode = P_SKIPMUL;
             P.alpha = (int32_t)M.alpha;

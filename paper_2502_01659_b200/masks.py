@@ -58,12 +58,14 @@ class LongNet(Mask):
     w0: int
     alpha: int = 2
     multiset: bool = False  # LongNet's mixture: a pair in n levels' blocks weighs n times (f4)
+    head_offsets: bool = False  # LongNet's per-head offsets s_h = h mod alpha^k (f4, reading R11c)
     kind = _abi.GA_MASK_LONGNET
 
     def to_c(self, L):
         m = self._base(L)
         m.w0, m.alpha = self.w0, self.alpha
-        m.parts = _abi.GA_LONGNET_MULTISET if self.multiset else 0
+        m.parts = (_abi.GA_LONGNET_MULTISET if self.multiset else 0) | (
+            _abi.GA_LONGNET_HEAD_OFFSETS if self.head_offsets else 0)
         return m
 
 

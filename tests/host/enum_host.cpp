@@ -15,7 +15,8 @@ int main(int argc, char **argv)
     M.kind = atoi(argv[1]);
     M.L = atoll(argv[2]);
     long long a = atoll(argv[3]), b = atoll(argv[4]);
-    M.parts = atoi(argv[5]); // LongNet: 1 = multiset mixture
+    M.parts = atoi(argv[5]); // LongNet: 1 = multiset mixture, 2 = per-head offsets
+    const int head = argc > 6 ? atoi(argv[6]) : 0;
     if (M.kind == ga::K_WINDOW) { M.w = a; M.r = b; M.m = (a - 1) / b; }
     if (M.kind == ga::K_BLOCK_DILATED) { M.seg = a; M.r = b; }
     if (M.kind == ga::K_LONGNET) {
@@ -24,16 +25,16 @@ int main(int argc, char **argv)
     }
     for (int64_t i = 0; i < M.L; ++i) {
         std::vector<int64_t> v;
-        int np = ga::num_pieces(M, i);
+        int np = ga::num_pieces_h(M, i, head);
         for (int pc = 0; pc < np; ++pc) {
-            ga::Piece P = ga::get_piece(M, i, pc);
+            ga::Piece P = ga::get_piece_h(M, i, pc, head);
             for (int64_t k = 0; k < P.count; ++k) v.push_back(ga::piece_at(P, k));
         }
         size_t n = v.size();
         std::sort(v.begin(), v.end());
         std::vector<int64_t> u = v;
         bool disjoint = std::unique(u.begin(), u.end()) == u.end();
-        if (ga::degree(M, i) != (int64_t)n) disjoint = false;
+        if (head == 0 && ga::degree(M, i) != (int64_t)n) disjoint = false;
         printf("%lld %d", (long long)i, disjoint ? 1 : 0);
         for (auto j : v) printf(" %lld", (long long)j);
         printf("\n");

@@ -20,8 +20,8 @@ def enum_bin(tmp_path_factory):
     return out
 
 
-def _run_enum(binary, kind, L, a, b, parts=0):
-    txt = subprocess.check_output([binary, str(kind), str(L), str(a), str(b), str(parts)], text=True)
+def _run_enum(binary, kind, L, a, b, parts=0, head=0):
+    txt = subprocess.check_output([binary, str(kind), str(L), str(a), str(b), str(parts), str(head)], text=True)
     rows = []
     for line in txt.splitlines():
         f = [int(x) for x in line.split()]
@@ -165,3 +165,20 @@ def test_bench_roofline_picks_binding_bound():
                                      edges // cfg["H"], [50.0])
         assert roof["bound"] == bound, (name, roof)
         assert 0 < roof["frac"] < 1
+
+
+@pytest.mark.parametrize("L,w0,alpha,parts", [(256, 16, 2, 2), (243, 9, 3, 2), (999, 7, 2, 2), (5000, 100, 3, 2),
+                                              (256, 16, 2, 3), (3000, 10, 4, 2)])
+@pytest.mark.parametrize("head", [0, 1, 2, 3, 5, 13])
+def test_enumerator_head_offsets_matches_oracle(orc, enum_bin, L, w0, alpha, parts, head):
+    """LongNet per-head offsets (f4, reading R11c): the product's shifted-valuation pieces list
+    exactly the oracle's per-head neighbour set (definition: offsets == h mod alpha^k), and
+    the set-union pieces are disjoint."""
+    om = orc.longnet(L, w0, alpha, multiset=bool(parts & 1), head_offsets=True, head=head)
+    rp, ci, nnz = orc.mask_to_csr(om)
+    rows = _run_enum(enum_bin, 2, L, w0, alpha, parts=parts, head=head)
+    assert len(rows) == L
+    for i, (disjoint, nb) in enumerate(rows):
+        if not parts & 1:
+            assert disjoint == 1, f"row {i}: pieces overlap"
+        assert np.array_equal(nb, ci[rp[i]:rp[i + 1]]), f"row {i} head {head}"

@@ -510,3 +510,25 @@ def test_backward_matches_torch_autograd_dense(orc, fam, L, args):
     assert edges == int(grid.sum()) * H
     for got, want in ((dq, tq.grad), (dk, tk.grad), (dv, tv.grad)):
         np.testing.assert_allclose(got, want.numpy(), rtol=1e-10, atol=1e-12)
+
+
+@pytest.mark.parametrize("L,w0,alpha", [(300, 8, 2), (250, 5, 3), (128, 16, 2)])
+def test_longnet_head_offsets_vs_dense(orc, L, w0, alpha):
+    """Per-head offsets (f4, reading R11c): the oracle's per-head attention equals the dense
+    brute force over each head's own predicate grid; head 0 equals plain LongNet."""
+    from oracle import dense
+
+    H, d = 6, 8
+    rng = np.random.default_rng(L)
+    q, k, v = (rng.random((L, H, d)) for _ in range(3))
+    got, edges = orc.attention(q, k, v, orc.longnet(L, w0, alpha, head_offsets=True))
+    total = 0
+    for h in range(H):
+        grid = dense.longnet_mask(L, w0, alpha, head=h)
+        total += int(grid.sum())
+        want = dense.masked_attention(q[:, h:h + 1], k[:, h:h + 1], v[:, h:h + 1], grid)
+        np.testing.assert_allclose(got[:, h:h + 1], want, rtol=0, atol=1e-12)
+    assert edges == total
+    plain, _ = orc.attention(q, k, v, orc.longnet(L, w0, alpha))
+    np.testing.assert_array_equal(got[:, 0], plain[:, 0])
+    assert np.array_equal(dense.longnet_mask(L, w0, alpha, head=0), dense.longnet_mask(L, w0, alpha))
