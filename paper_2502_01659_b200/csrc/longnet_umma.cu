@@ -368,7 +368,9 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
                     mma_ts(tmem + COL_O, tmem + COL_S + (c % NSB) * KC + kk * 8, sdesc_sw128(bv + kk * 16 * RB),
                            idO, (c > 0 || kk > 0));
                 mma_commit(mbO0 + 8 * (c & 1));
-                mma_commit(mbEmpty0 + 8 * (c % STAGES)); // S_c and P V_c have read the stage
+                // S_c and P V_c have read the stage — signalled only when the loader refills it
+                // (an arrive nobody waits for could land after the CTA exited; synccheck)
+                if (c + STAGES < nchunks) mma_commit(mbEmpty0 + 8 * (c % STAGES));
             }
             __syncwarp();
         };
@@ -393,7 +395,11 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
         static_assert(NSB == 3, "S_{c+2} reuses the buffer of P_{c-1}");
         for (int c = 0; c < nchunks; ++c) {
             issue_PV(c);
-            if (c >= 1 && c + 2 < nchunks) {
+            if (c >= 1 && c + 2 >= nchunks) {
+                // tail: no S left to issue, but every phase of the two-phase P V barrier is
+                // still observed before the barrier's next arrival (synccheck-clean)
+                mbar_wait(mbO0 + 8 * ((c - 1) & 1), ((c - 1) >> 1) & 1);
+            } else if (c >= 1) {
                 // S_{c+2} overwrites the TMEM columns P V_{c-1} read (P_{c-1}): wait for P V_{c-1}
                 // to complete first — issue order alone does not order an MMA's TMEM A-operand
                 // reads before a later MMA's accumulator writes (measured: sporadic corrupted
