@@ -47,3 +47,11 @@ w0 = [(t, e, c) for t, e, w, c in ev if w == 0 and e in (10, 12, 14)]
 wait = sum(per[(12, 0)][c] - per[(10, 0)][c] for c in per[(12, 0)] if c in per[(10, 0)])
 busy = sum(per[(14, 0)][c] - per[(12, 0)][c] for c in per[(14, 0)] if c in per[(12, 0)])
 print("softmax warp 0: waiting for S", wait, "cycles; working", busy, "cycles; chunks", len(per[(14, 0)]))
+print("per chunk: P arrive of softmax warps 0-3 and the MMA warp's P-arrived time")
+for c in range(0, 48):
+    xs = [per.get((14, w), {}).get(c, -1) for w in range(4)] + [per.get((3, 5), {}).get(c, -1)]
+    ss = [per.get((12, w), {}).get(c, -1) for w in range(4)]
+    if all(x < 0 for x in xs):
+        break
+    print(f"c={c:2d} S ready " + " ".join(f"{x:7d}" for x in ss) + " | P arrive " + " ".join(f"{x:7d}" for x in xs[:4]) +
+          f" | mma sees {xs[4]:7d} (+{xs[4] - max(xs[:4]):5d})")
