@@ -88,8 +88,16 @@ template <int D> __host__ __device__ constexpr uint32_t smem_bytes()
 // KC/2 columns of its S buffer), O at NSB KC: S0 S1 S2 | O = 256 columns at d = 64.  Three S
 // buffers let S_{c+3} be issued as soon as P V_c is (P_c read), so S_{c+1} is ready well
 // before the softmax of chunk c ends.
+#ifndef GA_LNET_SEPP
+#define GA_LNET_SEPP 1 // P in its own TMEM columns (S0 S1 | P0 P1 | O) instead of over its S buffer
+#endif
+#if GA_LNET_SEPP
+constexpr int NSB = 2, NPB = 2;
+constexpr uint32_t COL_S = 0, COL_P = NSB * KC, COL_O = COL_P + NPB * KC / 2;
+#else
 constexpr int NSB = 3;
 constexpr uint32_t COL_S = 0, COL_O = NSB * KC;
+#endif
 
 #ifdef GA_LNET_TRACE
 // debug timeline of one group-mode CTA (blockIdx.x == LNET_TRACE_CTA): per warp, lane 0
@@ -363,10 +371,14 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
             if (lane == 0) {
                 fence_after();
                 const uint32_t bv = sV0 + (c % STAGES) * KC * RB;
+#if GA_LNET_SEPP
+                const uint32_t tp = tmem + COL_P + (c % NPB) * (KC / 2);
+#else
+                const uint32_t tp = tmem + COL_S + (c % NSB) * KC;
+#endif
 #pragma unroll
                 for (int kk = 0; kk < KC / 16; ++kk) // 16 keys per MMA: 8 P columns, 16 V rows
-                    mma_ts(tmem + COL_O, tmem + COL_S + (c % NSB) * KC + kk * 8, sdesc_sw128(bv + kk * 16 * RB),
-                           idO, (c > 0 || kk > 0));
+                    mma_ts(tmem + COL_O, tp + kk * 8, sdesc_sw128(bv + kk * 16 * RB), idO, (c > 0 || kk > 0));
                 mma_commit(mbO0 + 8 * (c & 1));
                 // S_c and P V_c have read the stage — signalled only when the loader refills it
                 // (an arrive nobody waits for could land after the CTA exited; synccheck)
@@ -392,6 +404,14 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
         };
         if (nchunks > 0) mbar_wait(mbQ, 0);
         for (int c = 0; c < nchunks && c < NSB; ++c) issue_S(c);
+#if GA_LNET_SEPP
+        // S_{c+2} goes into S_c's buffer, free once the softmax has read it (P_c arrived: waited
+        // in issue_PV); P lives in its own columns, so no MMA completion gates the S issue
+        for (int c = 0; c < nchunks; ++c) {
+            issue_PV(c);
+            if (c + NSB < nchunks) issue_S(c + NSB);
+        }
+#else
         static_assert(NSB == 3, "S_{c+2} reuses the buffer of P_{c-1}");
         for (int c = 0; c < nchunks; ++c) {
             issue_PV(c);
@@ -412,6 +432,7 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
                 issue_S(c + 2);
             }
         }
+#endif
     }
 
     // =================== softmax warps: thread = row = TMEM lane ===================
@@ -504,7 +525,12 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
                 }
                 l_run += exps();
             }
+#if GA_LNET_SEPP
+            if (c >= NPB) wait_O(c - NPB); // P V_{c-2} has read P buffer c % 2
+            tmem_st32(tlane + COL_P + (c % NPB) * (KC / 2), pk);
+#else
             tmem_st32(tlane + COL_S + (c % NSB) * KC, pk);
+#endif
             tmem_wait_st();
             fence_before();
             mbar_arrive(mbP0 + 8 * (c % NSB));
@@ -515,6 +541,9 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
     const bool row_ok = warp < 4 && tid < nrows;
     float o[D];
     if (warp < 4 && nchunks > 0) {
+#if GA_LNET_SEPP
+        if (nchunks >= 2) wait_O(nchunks - 2); // every P V phase observed (synccheck-clean)
+#endif
         wait_O(nchunks - 1);
 #pragma unroll
         for (int q = 0; q < D / 32; ++q) tmem_ld32(tlane + COL_O + 32 * q, o + 32 * q);
