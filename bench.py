@@ -173,6 +173,49 @@ def oracle_rate(cfg_name, budget_s=15.0, max_rows=None):
     return e / t, oracle.num_threads(), sample, e, t
 
 
+def backward_line(ga, torch, dist, dev, flush, args):
+    """The backward pass (ga_attention_backward) on cfg2's workload: dQ, dK,
+    dV of out = attention(Q, K, V, Window(256, 2)) for a seeded dO, lse recomputed (the whole
+    backward: row pass lse + D + dQ, column pass dK + dV).  Roofline: CUDA-core kernels, so the
+    FP32 FMA pipe on the algorithmic flops (per head-edge 2d for s, 2d for dP, 2d for dQ in the
+    row pass plus 2d for the lse pass, and 2d s + 2d dP + 2d dK + 2d dV in the column pass =
+    16d) against the HBM bytes (Q, K, V, O, dO read once, dQ, dK, dV written once in fp32)."""
+    cfg = CONFIGS["cfg2"]
+    L, H, d = cfg["L"], cfg["H"], cfg["d"]
+    seed = SEEDS["cfg2"]
+    mask = ga.Window(*cfg["mask"][1:])
+    q, k, v = ga.qkv_device(seed, L, H, d, torch.bfloat16)
+    g = ga.qkv_device(seed + 7, L, H, d, torch.bfloat16, shift=-0.5)[0]
+    out = ga.attention(q, k, v, mask)
+
+    class W:  # the time_steps interface
+        pass
+    w = W()
+    w.ga = ga
+    w.step = lambda: ga.attention_backward(q, k, v, out, g, mask)
+    steps = max(3, min(args.steps, 10))
+    ms, ps, launches, _ = time_steps(torch, dist, 1, w, steps, 3, flush)
+    nnz = ga.mask_count(mask, L)
+    he = nnz * H
+    peaks, src = load_peaks()
+    s = statistics.median(ps) / 1e3
+    flops = 16 * d * he
+    fma = SMS * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6
+    byts = 5 * L * H * d * 2 + 3 * L * H * d * 4
+    t_f, t_m = flops / fma, byts / (peaks["hbm_gbs"] * 1e9)
+    roof = ({"bound": "alu", "achieved": round(flops / s / 1e12, 2), "peak": round(fma / 1e12, 1), "unit": "TFLOP/s",
+             "frac": round(t_f / s, 4), "peak_source": "FP32 FMA pipe (derived: 148 SMs x 128 FMA/clk x max clock)"}
+            if t_f >= t_m else
+            {"bound": "hbm", "achieved": round(byts / s / 1e9, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+             "frac": round(t_m / s, 4), "peak_source": f"hbm_gbs, {src} MEASURED_PEAKS.json"})
+    roof.update({"algorithmic": f"{byts} B and {flops} flop (16d x {he} head-edges) per backward",
+                 "lower_bound_us": {"fma": round(t_f * 1e6, 2), "hbm": round(t_m * 1e6, 2)},
+                 "kernel_ms_median": round(statistics.median(ps), 4)})
+    return {"workload": f"backward (dQ, dK, dV fp32) of cfg2: L={L}, {H} heads, d={d}, bf16, {mask_desc(cfg)}",
+            "value": he / (ms / 1e3), "unit": "edges/s", "ms_per_step": ms, "steps": steps, "warmup": 3, "nnz": nnz,
+            "gpu_launches": launches, "roofline": roof}
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -412,6 +455,8 @@ def main():
             w2.close()
             w2 = None
             torch.cuda.empty_cache()
+        per_config["cfg2_backward"] = backward_line(ga, torch, dist, dev, flush, args)
+        torch.cuda.empty_cache()
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None

@@ -60,10 +60,24 @@ constexpr int B_QFULL = 0, B_QEMPTY = 4, B_KVFULL = 8, B_KVEMPTY = 8 + NSLOT, B_
               B_PFULL = B_SFULL + 2 * NSB, B_OFULL = B_PFULL + 2 * NSB;
 constexpr int B_TMEM = B_OFULL + 4; // tcgen05.alloc writes the TMEM base here
 
+#ifndef GA_WTC_SEPP
+#define GA_WTC_SEPP 1
+#endif
+#if GA_WTC_SEPP
+// TMEM columns of warpgroup w: S[NSB] at 256w + 64 b, P[2] (chunk c's 16-bit pairs in P[c & 1],
+// 32 columns each), one O accumulator.  S_{c+NSB} reuses S_c's buffer as soon as the softmax
+// has read it (P_c arrived), with no wait for any MMA to complete; the softmax writes P_c only
+// after P V_{c-2} has read that P buffer.  One O suffices: a tile's epilogue reads O before the
+// same threads release P of the next tile's first chunk, so the next tile's first P V (which
+// overwrites O, accumulate = 0) is issued after those reads.
+constexpr uint32_t COL_S = 0, COL_P = NSB * KC, COL_O = COL_P + 2 * (KC / 2);
+static_assert(COL_O + D <= 256, "TMEM: 256 columns per warpgroup");
+#else
 // TMEM columns of warpgroup w: S[NSB] at 256w + 64 b (P of chunk c, 16-bit pairs, is written over
 // the first 32 columns of its S buffer), O[2] (tile k accumulates in O[k & 1]) after them
 constexpr uint32_t COL_S = 0, COL_O = NSB * KC;
 static_assert(NSB * KC + 2 * D <= 256, "TMEM: 256 columns per warpgroup");
+#endif
 
 struct TcParams {
     CUtensorMap tmQ, tmK, tmV, tmO; // one head, element stride r, 64-row boxes
@@ -391,7 +405,13 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 fence_after();
                 const int gi = (int)(g - P.lo), sl = (int)((uint32_t)g % NSLOT);
                 const uint32_t av = sbase + OFF_KV + (uint32_t)sl * 2 * CBYTES + CBYTES;
+#if GA_WTC_SEPP
+                const uint32_t tP = tmem + 256u * w + COL_P + (c & 1u) * (KC / 2);
+                const uint32_t tOacc = tmem + 256u * w + COL_O;
+#else
                 const uint32_t tP = tmem + 256u * w + COL_S + sb * KC;
+                const uint32_t tOacc = tmem + 256u * w + COL_O + (uint32_t)qb[w] * D;
+#endif
                 readers -= 1u << (4 * gi);
                 // the chunk's last reader: release its slot unless the next item keeps it
                 // (commit tracks every MMA this thread issued)
@@ -399,7 +419,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < KC / 16; ++kk) // 16 keys per MMA: 8 P columns, 16 V rows
-                        mma_ts(tmem + 256u * w + COL_O + (uint32_t)qb[w] * D, tP + kk * 8, dbase | ((av + kk * 16 * RB) >> 4), idO,
+                        mma_ts(tOacc, tP + kk * 8, dbase | ((av + kk * 16 * RB) >> 4), idO,
                                (j > 0 || kk > 0));
                     mma_commit(bar(bars, B_OFULL + 2 * w + (int)(c & 1)));
                     if (release) mma_commit(bar(bars, B_KVEMPTY + sl));
@@ -440,7 +460,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     if (j >= P.n[w]) continue;
                     issue_PV(w, j);
                     if (j + NSB < P.n[w]) {
-#ifndef GA_WTC_NO_WAR_WAIT
+#if !defined(GA_WTC_NO_WAR_WAIT) && !GA_WTC_SEPP
                         // S_w(j + NSB) overwrites the TMEM columns P V_w(j) reads (P over S): wait
                         // for P V_w(j) to complete — issue order alone did not keep the A-operand
                         // reads ahead of a later MMA's accumulator writes in the LongNet kernel
@@ -562,7 +582,11 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             if (cnt_prev >= 2) wait_O(cnt_prev - 2);
             wait_O(cnt_prev - 1);
             TRACE2(18 + w, 0);
+#if GA_WTC_SEPP
+            const uint32_t tO = tl + COL_O;
+#else
             const uint32_t tO = tl + COL_O + (tix_prev & 1) * D;
+#endif
             const float inv = l_prev > 0.f ? 1.f / l_prev : 0.f;
             const Tile Tq = tile_geo(tp, p_it, w);
             const int32_t p_c = Tq.c, p_h = Tq.h, p_a0 = Tq.a0, p_alo = Tq.a_lo, p_ahi = Tq.a_hi;
@@ -620,7 +644,11 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             const Tile Tt = tile_geo(tp, it, w);
             if (!Tt.valid) continue;
             const int32_t xr0 = Tt.a0 + 32 * q, x = xr0 + lane;
+#if GA_WTC_SEPP
+            const uint32_t tO = tl + COL_O; // this tile's O accumulator
+#else
             const uint32_t tO = tl + COL_O + (ntile & 1) * D; // this tile's O accumulator
+#endif
             // keys of this warp's rows: union [ulo, uhi], every row: [ilo, ihi]; this row: [klo, khi]
             const int32_t ulo = max(xr0 - mi, 0), uhi = min(xr0 + 31 + mi, Tt.Nc - 1);
             const int32_t ilo = max(xr0 + 31 - mi, 0), ihi = min(xr0 + mi, Tt.Nc - 1);
@@ -637,11 +665,19 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 mbar_wait(bar(bars, B_SFULL + NSB * w + (int)sb), sph);
                 fence_after();
                 TRACE(12 + w);
+#if GA_WTC_SEPP
+                const uint32_t tPw = tl + COL_P + (c & 1u) * (KC / 2); // P_c (written after P V_{c-2} read it)
+#else
+                const uint32_t tPw = tS;
+#endif
                 if (kmin > uhi || kmin + KC - 1 < ulo) { // no row of this warp reaches the chunk
                     uint32_t z[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) z[i] = 0u;
-                    tmem_st32(tS, z);
+#if GA_WTC_SEPP
+                    if (c >= 2) wait_O(c - 2);
+#endif
+                    tmem_st32(tPw, z);
                     tmem_wait_st();
                     if (pend_epi) epilogue(); // see below
                     fence_before();
@@ -723,7 +759,10 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                         }
                         l_run += exps();
                     }
-                    tmem_st32(tS, pk);
+#if GA_WTC_SEPP
+                    if (c >= 2) wait_O(c - 2);
+#endif
+                    tmem_st32(tPw, pk);
                     tmem_wait_st();
                     // the previous tile's epilogue with this tile's first chunk (its last P V has
                     // long completed), BEFORE P of this chunk is released: P V of this chunk could
