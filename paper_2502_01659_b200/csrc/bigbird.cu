@@ -24,7 +24,7 @@
 //
 // Every edge of the union is computed exactly once, except the window edges of the g global
 // rows (g * |W_i| products, computed by step 1 and superseded by step 3).
-#include "edge_core.cuh"
+#include "tc_common.cuh"
 
 namespace ga {
 namespace bb {
@@ -35,7 +35,10 @@ constexpr int CAP = 1024; // extra columns per row held in shared memory (n_glob
 struct Args {
     ga_state win;    // window-part state from step 1 ([q_rows, H] / [q_rows, H, d] fp32)
     int full_rows;   // global rows are handled by the full-row tiles (skip them here)
+    int globals_done; // the global columns were merged into `win` by globals_kernel
 };
+
+constexpr int GT_ROWS = 64, GT_THREADS = 128, GT_MAXG = 256; // globals kernel: row tile, threads, max |G|
 
 __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
@@ -82,10 +85,10 @@ struct View {
 
 // Extra columns of non-global row i — (G \ W_i) if parts has GA_BB_GLOBAL, R_i if it has
 // GA_BB_RANDOM — into buf (warp-collective; returns the warp-uniform count).
-__device__ int extras(const DevMask &M, const View &V, int parts, int32_t i, int32_t *buf, int lane)
+__device__ int extras(const DevMask &M, const View &V, int parts, int32_t i, int32_t *buf, int lane, bool skip_globals)
 {
     int n = 0;
-    if (parts & 2) {
+    if (parts & 2 && !skip_globals) {
         for (int32_t k0 = 0; k0 < V.ng; k0 += 32) {
             const int32_t k = k0 + lane;
             const int32_t gv = k < V.ng ? V.G[k] : 0;
@@ -177,7 +180,7 @@ __global__ void __launch_bounds__(WARPS * 32) extras_kernel(const __grid_constan
             with_window = false;
         } // else: window only (random columns are drawn for non-global rows, R10)
     } else {
-        const int n = extras(M, V, parts, i, cols[wib], lane);
+        const int n = extras(M, V, parts, i, cols[wib], lane, a.globals_done != 0);
         acc.template run_csr<csr_depth<T, D>()>(cols[wib], 0, n);
     }
     acc.merge_groups();
@@ -198,6 +201,167 @@ __global__ void __launch_bounds__(WARPS * 32) extras_kernel(const __grid_constan
     acc.store(p, t, h);
 }
 
+// Step 2a (bf16/fp16, |G| <= GT_MAXG): the global COLUMNS of every non-global row on the tensor
+// cores.  All rows share the same <= 256 global keys, so (row tile) x (global keys) is a dense
+// block, minus the globals inside a row's window (masked to weight 0: those edges belong to
+// the window part) and minus the global rows themselves (theirs run as full rows).  CTA = 4
+// warps x 16 rows on mma.sync with K_G, V_G staged once in shared memory; each row's partial
+// state is (+)-merged into the window state in place.  The extras kernel then gathers only the
+// random columns.
+template <typename T, int D>
+__device__ __forceinline__ void gblock(tc::MmaRows<T, D> &st, const uint32_t *kaddr, const uint32_t *vaddr,
+                                       uint32_t off, float sl2, const bool (*valid)[4])
+{
+    using G = tc::Geo<D>;
+    float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < G::KS; ++kk) {
+        uint32_t b0, b1, b2, b3;
+        tc::ldsm_x4(kaddr[kk] + off, b0, b1, b2, b3);
+        tc::mma16816<T>(sc[0], st.qa[kk], b0, b1);
+        tc::mma16816<T>(sc[1], st.qa[kk], b2, b3);
+    }
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sc[nb][e] = valid[nb][e] ? sc[nb][e] : -INFINITY;
+    constexpr float kTau = 8.f;
+    const float lm0 = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
+    const float lm1 = fmaxf(fmaxf(sc[0][2], sc[0][3]), fmaxf(sc[1][2], sc[1][3]));
+    const bool need = lm0 * sl2 > st.mr[0] + kTau || lm1 * sl2 > st.mr[1] + kTau;
+    if (__any_sync(0xffffffffu, need)) {
+        float bm0 = fmaxf(lm0, __shfl_xor_sync(0xffffffffu, lm0, 1));
+        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
+        float bm1 = fmaxf(lm1, __shfl_xor_sync(0xffffffffu, lm1, 1));
+        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
+        const float mn0 = fmaxf(st.mr[0], bm0 * sl2), mn1 = fmaxf(st.mr[1], bm1 * sl2);
+        st.scale_rows(ex2(st.mr[0] - mn0), ex2(st.mr[1] - mn1));
+        st.mr[0] = mn0;
+        st.mr[1] = mn1;
+    }
+    uint32_t pa[4];
+    st.softmax_pack(sc, sl2, pa); // masked: exp2(-inf) = 0 (the reference max is finite)
+#pragma unroll
+    for (int jj = 0; jj < G::NB8 / 2; ++jj) {
+        uint32_t b0, b1, b2, b3;
+        tc::ldsm_x4_t(vaddr[jj] + off, b0, b1, b2, b3);
+        tc::mma16816<T>(st.o[2 * jj], pa, b0, b1);
+        tc::mma16816<T>(st.o[2 * jj + 1], pa, b2, b3);
+    }
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(GT_THREADS) globals_kernel(const __grid_constant__ AttnParams p, const Args a)
+{
+    using G = tc::Geo<D>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ int32_t sG[GT_MAXG];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const DevMask &M = p.mask;
+    const int ng = (int)M.ng, nb16 = (ng + 15) / 16, h = (int)blockIdx.y;
+    const int H = p.H;
+    const uint32_t sQ = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t sK = sQ + GT_ROWS * G::RB, sV = sK + nb16 * 16 * G::RB;
+    const size_t row_bytes = (size_t)H * D * sizeof(T), hoff = (size_t)h * D * sizeof(T);
+    for (int k = tid; k < ng; k += GT_THREADS) sG[k] = (int32_t)bb_global_at(M, k);
+    // K_G, V_G once per CTA (keys past |G| zero)
+    for (int idx = tid; idx < nb16 * 16 * G::NC; idx += GT_THREADS) {
+        const int r = idx / G::NC, cc = idx % G::NC;
+        if (r < ng) {
+            const char *kr, *vr;
+            kv_row(p, (int64_t)bb_global_at(M, r), row_bytes, kr, vr);
+            tc::cp_async16(sK + tc::swz<D>(r, cc), kr + hoff + cc * 16);
+            tc::cp_async16(sV + tc::swz<D>(r, cc), vr + hoff + cc * 16);
+        } else {
+            tc::sts_zero16(sK + tc::swz<D>(r, cc));
+            tc::sts_zero16(sV + tc::swz<D>(r, cc));
+        }
+    }
+    tc::cp_async_commit();
+    const int32_t w = (int32_t)imin(M.w, M.L), r = (int32_t)imin(M.r, M.L);
+    const float sl2 = p.scale_log2;
+    const int g = lane >> 2, t4 = lane & 3;
+    uint32_t kaddr[G::KS], vaddr[G::NB8 / 2];
+    {
+        const int krow = (lane & 7) + (lane >> 4) * 8, vrow = (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+        for (int kk = 0; kk < G::KS; ++kk) kaddr[kk] = sK + tc::swz<D>(krow, 2 * kk + ((lane >> 3) & 1));
+#pragma unroll
+        for (int jj = 0; jj < G::NB8 / 2; ++jj) vaddr[jj] = sV + tc::swz<D>(vrow, 2 * jj + (lane >> 4));
+    }
+    const int64_t ntiles = (p.q_rows + GT_ROWS - 1) / GT_ROWS;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t t0 = tile * GT_ROWS;
+        const int nrows = (int)imin(GT_ROWS, p.q_rows - t0);
+        __syncthreads(); // the previous tile's Q reads are done
+        for (int idx = tid; idx < GT_ROWS * G::NC; idx += GT_THREADS) {
+            const int rr = idx / G::NC, cc = idx % G::NC;
+            if (rr < nrows)
+                tc::cp_async16(sQ + tc::swz<D>(rr, cc),
+                               reinterpret_cast<const char *>(p.Q) + (size_t)(t0 + rr) * row_bytes + hoff + cc * 16);
+            else
+                tc::sts_zero16(sQ + tc::swz<D>(rr, cc));
+        }
+        tc::cp_async_commit();
+        tc::cp_async_wait<0>();
+        __syncthreads();
+        tc::MmaRows<T, D> st;
+        st.init_empty();
+        st.mr[0] = st.mr[1] = -1e30f; // finite reference: a fully masked block leaves l = 0, no NaN
+        st.load_q(sQ, warp * 16, lane);
+        // this lane's rows (g, g + 8 of the warp's 16); global rows and pad rows see no key
+        int32_t ir[2];
+        bool live[2];
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) {
+            const int rr = warp * 16 + g + 8 * hr;
+            ir[hr] = (int32_t)(p.q_begin + t0 + rr);
+            bool isg = false;
+            for (int k = 0; k < ng && !isg; ++k) isg = sG[k] == ir[hr];
+            live[hr] = rr < nrows && !isg;
+        }
+        for (int b = 0; b < nb16; ++b) {
+            bool valid[2][4];
+#pragma unroll
+            for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int k = b * 16 + nb * 8 + 2 * t4 + (e & 1);
+                    const int hr = e >> 1;
+                    bool ok = live[hr] && k < ng;
+                    if (ok) {
+                        const int32_t dd = ir[hr] > sG[k] ? ir[hr] - sG[k] : sG[k] - ir[hr];
+                        ok = !(dd < w && (r == 1 || dd % r == 0)); // in the window: the window part's edge
+                    }
+                    valid[nb][e] = ok;
+                }
+            gblock<T, D>(st, kaddr, vaddr, (uint32_t)(b * 16 * G::RB), sl2, valid);
+        }
+        st.reduce_l();
+        // (+) into the window state of the row, in place
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) {
+            if (!live[hr] || !(st.lr[hr] > 0.f)) continue;
+            const size_t rh = (size_t)(t0 + warp * 16 + g + 8 * hr) * H + h;
+            const float l2 = a.win.l[rh], m2 = a.win.m[rh];
+            const float m1 = st.mr[hr], l1 = st.lr[hr];
+            const float mn = l2 > 0.f ? fmaxf(m1, m2) : m1;
+            const float x = ex2(m1 - mn), y = l2 > 0.f ? ex2(m2 - mn) : 0.f;
+            float *so = a.win.o + rh * D;
+#pragma unroll
+            for (int j = 0; j < G::NB8; ++j) {
+                float2 *pp = reinterpret_cast<float2 *>(so + 8 * j + 2 * t4);
+                const float2 u = *pp;
+                *pp = make_float2(st.o[j][2 * hr] * x + u.x * y, st.o[j][2 * hr + 1] * x + u.y * y);
+            }
+            if (t4 == 0) {
+                a.win.m[rh] = mn;
+                a.win.l[rh] = l1 * x + l2 * y;
+            }
+        }
+    }
+}
+
 // the global rows inside the query range, as local rows (G is sorted): full_row[] and the
 // packed count (bits 40-63) the full-row kernels read
 __global__ void full_prep_kernel(DevMask M, int64_t q_begin, int64_t q_rows, int64_t *full_row, int64_t *nfull)
@@ -213,6 +377,35 @@ __global__ void full_prep_kernel(DevMask M, int64_t q_begin, int64_t q_rows, int
         n += __popc(bal);
     }
     if (lane == 0) *nfull = n << 40;
+}
+
+template <typename T, int D> static ga_status launch_globals_t(const AttnParams &p, const Args &a, cudaStream_t s)
+{
+    using G = tc::Geo<D>;
+    const int nb16 = (int)((p.mask.ng + 15) / 16);
+    const uint32_t smem = GT_ROWS * G::RB + 2 * nb16 * 16 * G::RB;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(globals_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             GT_ROWS * G::RB + 2 * GT_MAXG * G::RB);
+        attr = true;
+    }
+    const int64_t ntiles = (p.q_rows + GT_ROWS - 1) / GT_ROWS;
+    const unsigned gx = (unsigned)imin(ntiles, 148 * 8);
+    globals_kernel<T, D><<<dim3(gx, (unsigned)p.H), GT_THREADS, smem, s>>>(p, a);
+    GA_CHECK_LAUNCH("bb::globals_kernel");
+    return GA_OK;
+}
+
+static ga_status launch_globals(const AttnParams &p, const Args &a, ga_dtype dt, cudaStream_t s)
+{
+    switch (p.d) {
+    case 32: return dt == GA_BF16 ? launch_globals_t<__nv_bfloat16, 32>(p, a, s) : launch_globals_t<__half, 32>(p, a, s);
+    case 64: return dt == GA_BF16 ? launch_globals_t<__nv_bfloat16, 64>(p, a, s) : launch_globals_t<__half, 64>(p, a, s);
+    case 128: return dt == GA_BF16 ? launch_globals_t<__nv_bfloat16, 128>(p, a, s) : launch_globals_t<__half, 128>(p, a, s);
+    }
+    set_error("d=%d unsupported", p.d);
+    return GA_ERR_UNSUPPORTED;
 }
 
 template <typename T> static ga_status launch_extras_d(const AttnParams &p, const Args &a, cudaStream_t s)
@@ -313,6 +506,12 @@ ga_status launch_bigbird(const AttnParams &p, ga_dtype dt, cudaStream_t s)
     pw.state = a.win;
     pw.state_mode = GA_STATE_WRITE;
     st = window_tc_supported(pw, dt) ? launch_window_tc(pw, dt, s) : launch_edge(pw, dt, s);
+    // 2a. global columns on the tensor cores (bf16/fp16, |G| <= GT_MAXG), merged into the state
+    const int parts = p.mask.parts ? p.mask.parts : 7;
+    if (st == GA_OK && (parts & 2) && p.mask.ng > 0 && p.mask.ng <= bb::GT_MAXG && dt != GA_F32) {
+        a.globals_done = 1;
+        st = bb::launch_globals(p, a, dt, s);
+    }
     // 2. extra columns of the non-global rows, merged with their window state
     if (st == GA_OK) {
         switch (dt) {
