@@ -268,6 +268,11 @@ static ga_status dispatch(AttnParams &p, ga_dtype dtype, const ga_opts *opts, in
             return GA_ERR_UNSUPPORTED;
         }
         if (kernel != GA_KERNEL_EDGE && !probe && window_tc_supported(p, dtype)) return launch_window_tc(p, dtype, s);
+        // explicit CSR on the mma.sync edge-block kernels (their epilogue merges the state);
+        // not with the heavy-row split (whose merge kernels write the output only)
+        if (kernel == GA_KERNEL_AUTO && !probe && p.mask.kind == GA_MASK_CSR && !p.kv_clip &&
+            csr_mma_supported(p, dtype) && !(opts && opts->workspace && opts->workspace_bytes > 0))
+            return launch_csr_mma(p, dtype, s);
         if (kernel == GA_KERNEL_TC) { set_error("tcgen05 path does not support this (mask, dtype, d) with a state"); return GA_ERR_UNSUPPORTED; }
         return launch_edge(p, dtype, s);
     }

@@ -29,6 +29,9 @@
 namespace ga {
 namespace bb {
 
+#ifndef GA_BB_DEPTH
+#define GA_BB_DEPTH 2
+#endif
 constexpr int WARPS = 8;
 constexpr int CAP = 1024; // extra columns per row held in shared memory (n_global + n_random)
 
@@ -181,7 +184,8 @@ __global__ void __launch_bounds__(WARPS * 32) extras_kernel(const __grid_constan
         } // else: window only (random columns are drawn for non-global rows, R10)
     } else {
         const int n = extras(M, V, parts, i, cols[wib], lane, a.globals_done != 0);
-        acc.template run_csr<csr_depth<T, D>()>(cols[wib], 0, n);
+        // edge steps in flight per warp: 2 measured best at cfg3i (4 / 8 cost occupancy)
+        acc.template run_csr<GA_BB_DEPTH>(cols[wib], 0, n);
     }
     acc.merge_groups();
     if (with_window && acc.g == 0) { // (+) the window part's state of this row

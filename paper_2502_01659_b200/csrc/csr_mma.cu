@@ -42,6 +42,41 @@ static bool getenv_flag(const char *name)
 constexpr int WARPS = 8;
 constexpr int THREADS = WARPS * 32;
 
+// Carried state (ga_opts.state) for one (row, head) at the end of a CSR row:
+// (m, l) of this call's edges (warp-uniform, log2 domain) and NV of this lane's unnormalised
+// o~ values at dims dim[k] (lanes may share dims: they hold equal values).  WRITE overwrites,
+// ACCUMULATE (+)-combines with the buffers; with p.out also the normalised row (bf16/fp16).
+// Returns the 1/l the caller's output uses.
+template <typename T, int NV>
+__device__ __forceinline__ float state_merge(const AttnParams &p, int64_t tq, int h, float m, float l, const int *dim,
+                                             float *val, bool writer)
+{
+    const size_t rh = (size_t)tq * p.H + h;
+    float *so = p.state.o + rh * p.d;
+    if (p.state_mode == GA_STATE_ACCUMULATE) {
+        const float l2 = p.state.l[rh];
+        if (l2 > 0.f) { // l == 0 marks an empty state (its m is ignored)
+            const float m2 = p.state.m[rh];
+            const float mn = l > 0.f ? fmaxf(m, m2) : m2;
+            const float a = l > 0.f ? ex2(m - mn) : 0.f, b = ex2(m2 - mn);
+#pragma unroll
+            for (int k = 0; k < NV; ++k) val[k] = val[k] * a + so[dim[k]] * b;
+            l = l * a + l2 * b;
+            m = mn;
+        }
+    }
+    __syncwarp(); // every lane has read the old state before any lane overwrites it
+    if (writer) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) so[dim[k]] = val[k];
+    }
+    if ((threadIdx.x & 31) == 0) {
+        p.state.m[rh] = m;
+        p.state.l[rh] = l;
+    }
+    return l > 0.f ? 1.f / l : 0.f;
+}
+
 template <typename T, int D>
 __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) csr_mma_kernel(const __grid_constant__ AttnParams p)
 {
@@ -63,8 +98,15 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) csr_mma_kernel(con
     acc.run(p, p.mask.col_idx + rb, cnt, h, lane);
     float r[2 * RowAcc<T, D>::KS];
     const float l = acc.finish(r);
+    float inv = l > 0.f ? 1.f / l : 0.f; // empty row -> 0 (reading R6)
+    if (p.state.m) { // lane (g, t = 0) holds dims g D/8 .. + D/8
+        int dims[2 * RowAcc<T, D>::KS];
+#pragma unroll
+        for (int k = 0; k < 2 * RowAcc<T, D>::KS; ++k) dims[k] = g * (D / 8) + k;
+        inv = state_merge<T, 2 * RowAcc<T, D>::KS>(p, tq, h, cnt > 0 ? acc.m : -INFINITY, l, dims, r, t == 0);
+        if (!p.out) return;
+    }
     if (t != 0) return;
-    const float inv = l > 0.f ? 1.f / l : 0.f; // empty row -> 0 (reading R6)
     uint32_t out[RowAcc<T, D>::KS];
 #pragma unroll
     for (int x = 0; x < RowAcc<T, D>::KS; ++x) out[x] = pack2<T>(r[2 * x] * inv, r[2 * x + 1] * inv);
@@ -347,15 +389,26 @@ __global__ void __launch_bounds__(TW * 32, 2) csr_tma_kernel(const __grid_consta
 
     float u[4], w[4];
     const float l = acc.finish(u, w);
-    const float inv = l > 0.f ? 1.f / l : 0.f; // empty row -> 0 (reading R6)
+    float inv = l > 0.f ? 1.f / l : 0.f; // empty row -> 0 (reading R6)
     // lane (g, t) stores dims 16t + g and 16t + g + 8 (all four t-lanes hold every column sum)
-    T *op = reinterpret_cast<T *>(p.out) + ((size_t)tq * H + h) * D;
     float uo = u[0], wo = w[0];
 #pragma unroll
     for (int x = 1; x < 4; ++x)
         if (t == x) { uo = u[x]; wo = w[x]; }
-    op[16 * t + g] = (T)(uo * inv);
-    op[16 * t + g + 8] = (T)(wo * inv);
+    bool store = true;
+    if (p.state.m) {
+        const int dims[2] = {16 * t + g, 16 * t + g + 8};
+        float vals[2] = {uo, wo};
+        inv = state_merge<T, 2>(p, tq, h, ncnt > 0 ? acc.m : -INFINITY, l, dims, vals, true);
+        uo = vals[0];
+        wo = vals[1];
+        store = p.out != nullptr;
+    }
+    if (store) {
+        T *op = reinterpret_cast<T *>(p.out) + ((size_t)tq * H + h) * D;
+        op[16 * t + g] = (T)(uo * inv);
+        op[16 * t + g + 8] = (T)(wo * inv);
+    }
     __syncwarp(); // the index ring and stages are reused by the next task
     }
 }

@@ -155,3 +155,33 @@ def test_window_tc_carried_state(ga, orc, with_out):
     got = ga.state_finalize(st, torch.bfloat16).double().cpu().numpy()
     want, _ = orc.attention(*f64, orc.bigbird(L, 128, 5, 16, seed))
     assert np.abs(got - want).max() <= 2e-2
+
+
+@pytest.mark.parametrize("d,variant", [(64, ""), (64, "GA_CSR_LDG"), (32, ""), (128, "")])
+def test_csr_tensor_core_carried_state(ga, orc, d, variant, monkeypatch):
+    """The explicit-CSR mma.sync kernels (csr_tma at d = 64, the LDG variant otherwise) write /
+    (+)-combine a carried state: BigBird = CSR(global | random) WRITE, then CSR(window)
+    ACCUMULATE with an output — equal to the oracle; the state's mass l 2^m matches the edge
+    kernel's."""
+    if variant:
+        monkeypatch.setenv(variant, "1")
+    L, H, seed = 3000, 2, 0xB16B12D
+    cpu = synth.qkv(13, L, H, d, "bf16", centred=True)
+    q, k, v = (x.cuda() for x in cpu)
+    rest = ga.mask_to_csr(ga.BigBird(64, 5, 16, seed=seed, parts=ga.BB_GLOBAL | ga.BB_RANDOM), L)
+    win = ga.mask_to_csr(ga.BigBird(64, 5, 16, seed=seed, parts=ga.BB_WINDOW), L)
+    st, st_e = ga.State.empty(L, H, d), ga.State.empty(L, H, d)
+    ga.attention(q, k, v, rest, state=st)
+    ga.attention(q, k, v, rest, state=st_e, kernel="edge")
+    torch.cuda.synchronize()
+    z = st.l.double() * torch.exp2(st.m.double())
+    ze = st_e.l.double() * torch.exp2(st_e.m.double())
+    ok = st_e.l > 0
+    assert torch.equal(st.l > 0, ok)
+    assert ((z - ze).abs()[ok] / ze[ok]).max().item() < 5e-3
+    out = torch.empty_like(q)
+    ga.attention(q, k, v, win, out, state=st, accumulate=True)
+    torch.cuda.synchronize()
+    want, _ = orc.attention(*(synth.as_f64(x) for x in cpu), orc.bigbird(L, 64, 5, 16, seed))
+    assert np.abs(out.double().cpu().numpy() - want).max() <= 2e-2
+    assert np.abs(ga.state_finalize(st, torch.bfloat16).double().cpu().numpy() - want).max() <= 2e-2
