@@ -704,8 +704,10 @@ def reference_arm(args, cfg, world, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: L={cfg['L']}, {cfg['H']} heads, d={cfg['d']}, {cfg['dtype']} inputs, "
-                               f"{mask_desc(cfg)}", "note": "fp64 CPU oracle (oracle/oracle.c), OpenMP over rows"},
+        # the same workload keys as the GPU arm's line (N = 1: the reference arm runs on rank 0 only)
+        "config": {"workload": f"{args.config}: L={cfg['L']} tokens, {cfg['H']} heads, d={cfg['d']}, {cfg['dtype']}, "
+                               f"{mask_desc(cfg)}", "L": cfg["L"], "heads": cfg["H"], "d": cfg["d"], "mask": mask_desc(cfg),
+                   "note": "fp64 CPU oracle (oracle/oracle.c), OpenMP over rows, on sampled query rows"},
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
