@@ -289,9 +289,14 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
                     const Piece &P = spiece[cur_t];
                     const int64_t j0 = piece_at(P, k0 - pstart[cur_t]);
                     const int lev = __ffsll((unsigned long long)P.step) - 1; // step = 2^lev
-                    if (lev < up.n_lat) {
-                        if (P.mode == P_SKIPMUL) { lt = 2 * lev; u0 = (j0 / P.step - 1) / 2; }
-                        else { lt = 2 * lev + 1; u0 = j0 / P.step; }
+                    // the lattice maps cover the local K/V rows [kv_begin, kv_begin + kv_rows)
+                    // (sharded runs: this rank's shard; a chunk reaching other ranks' rows
+                    // takes the cp.async path below)
+                    const int64_t jl = j0 - p.kv_begin;
+                    const int64_t jlast = jl + (int64_t)(KC - 1) * (P.mode == P_SKIPMUL ? 2 * P.step : P.step);
+                    if (lev < up.n_lat && jl >= 0 && jlast < p.kv_rows) {
+                        if (P.mode == P_SKIPMUL) { lt = 2 * lev; u0 = (jl / P.step - 1) / 2; }
+                        else { lt = 2 * lev + 1; u0 = jl / P.step; }
                     }
                 }
             }
@@ -786,18 +791,27 @@ static void set_lattice(UParams &up, const AttnParams &p)
 {
     up.n_lat = 0;
     const DevMask &M = p.mask;
-    if (M.alpha != 2 || p.k_peer != nullptr || p.kv_begin != 0 || p.d != 64 || getenv("GA_LNET_CPASYNC")) return;
+    if (M.alpha != 2 || p.d != 64 || getenv("GA_LNET_CPASYNC")) return;
+    // level t needs the local rows to start on the lattice: kv_begin a multiple of 2^(t+1)
+    // (0 on one GPU; a shard boundary of a sharded run)
+    int lat_max = MAX_LAT;
+    if (p.kv_begin != 0) {
+        lat_max = 0;
+        while (lat_max < MAX_LAT && p.kv_begin % ((int64_t)2 << lat_max) == 0) ++lat_max;
+    }
     struct Cache {
         const void *K, *V;
         int64_t rows;
-        int H, n;
+        int H, n, lmax;
         CUtensorMap k[2 * MAX_LAT], v[2 * MAX_LAT];
     };
     static Cache c{};
     static std::mutex mu;
     std::lock_guard<std::mutex> g(mu);
-    const int levels = (int)(M.K + 1 < MAX_LAT ? M.K + 1 : MAX_LAT);
-    if (!(c.K == p.K && c.V == p.V && c.rows == p.kv_rows && c.H == p.H && c.n == levels)) {
+    int levels = (int)(M.K + 1 < MAX_LAT ? M.K + 1 : MAX_LAT);
+    if (levels > lat_max) levels = lat_max;
+    if (levels <= 0) return;
+    if (!(c.K == p.K && c.V == p.V && c.rows == p.kv_rows && c.H == p.H && c.lmax == levels)) {
         c.n = 0;
         const size_t rb = (size_t)p.H * p.d * 2;
         for (int t = 0; t < levels; ++t) {
@@ -816,6 +830,7 @@ static void set_lattice(UParams &up, const AttnParams &p)
         c.V = p.V;
         c.rows = p.kv_rows;
         c.H = p.H;
+        c.lmax = levels;
         if (c.n != levels) c.n = 0; // all levels or none
     }
     up.n_lat = c.n;
