@@ -176,10 +176,9 @@ def oracle_rate(cfg_name, budget_s=15.0, max_rows=None):
 def backward_line(ga, torch, dist, dev, flush, args):
     """The backward pass (ga_attention_backward) on cfg2's workload: dQ, dK,
     dV of out = attention(Q, K, V, Window(256, 2)) for a seeded dO, lse recomputed (the whole
-    backward: row pass lse + D + dQ, column pass dK + dV).  Roofline: CUDA-core kernels, so the
-    FP32 FMA pipe on the algorithmic flops (per head-edge 2d for s, 2d for dP, 2d for dQ in the
-    row pass plus 2d for the lse pass, and 2d s + 2d dP + 2d dK + 2d dV in the column pass =
-    16d) against the HBM bytes (Q, K, V, O, dO read once, dQ, dK, dV written once in fp32)."""
+    backward: row pass lse + D + dQ, column pass dK + dV, on the tensor cores).  Algorithmic
+    flops per head-edge: 2d for s, 2d for dP, 2d for dQ in the row pass plus 2d for the lse
+    sweep, and 2d s + 2d dP + 2d dK + 2d dV in the column pass = 16d."""
     cfg = CONFIGS["cfg2"]
     L, H, d = cfg["L"], cfg["H"], cfg["d"]
     seed = SEEDS["cfg2"]
@@ -199,18 +198,28 @@ def backward_line(ga, torch, dist, dev, flush, args):
     he = nnz * H
     peaks, src = load_peaks()
     s = statistics.median(ps) / 1e3
+    # the band backward runs on the tensor cores (mma.sync, bf16 in, fp32 accumulate):
+    # flops against the measured dense bf16 peak; 3 exp2 per head-edge (lse sweep, row and
+    # column passes) on MUFU; Q, K, V, O, dO read and dQ, dK, dV (fp32) written once on HBM
     flops = 16 * d * he
-    fma = SMS * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6
+    t_f = flops / (peaks["bf16_tflops"] * 1e12)
+    t_m = (5 * L * H * d * 2 + 3 * L * H * d * 4) / (peaks["hbm_gbs"] * 1e9)
+    t_x = 3 * he / (MUFU_EX2_PER_CLK_SM * SMS * peaks.get("sm_max_mhz", 1965.0) * 1e6)
     byts = 5 * L * H * d * 2 + 3 * L * H * d * 4
-    t_f, t_m = flops / fma, byts / (peaks["hbm_gbs"] * 1e9)
-    roof = ({"bound": "alu", "achieved": round(flops / s / 1e12, 2), "peak": round(fma / 1e12, 1), "unit": "TFLOP/s",
-             "frac": round(t_f / s, 4), "peak_source": "FP32 FMA pipe (derived: 148 SMs x 128 FMA/clk x max clock)"}
-            if t_f >= t_m else
-            {"bound": "hbm", "achieved": round(byts / s / 1e9, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-             "frac": round(t_m / s, 4), "peak_source": f"hbm_gbs, {src} MEASURED_PEAKS.json"})
-    roof.update({"algorithmic": f"{byts} B and {flops} flop (16d x {he} head-edges) per backward",
-                 "lower_bound_us": {"fma": round(t_f * 1e6, 2), "hbm": round(t_m * 1e6, 2)},
-                 "kernel_ms_median": round(statistics.median(ps), 4)})
+    bound = max((t_m, "hbm"), (t_f, "tensor"), (t_x, "alu"))[1]
+    if bound == "hbm":
+        roof = {"bound": "hbm", "achieved": round(byts / s / 1e9, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(t_m / s, 4), "peak_source": f"hbm_gbs, {src} MEASURED_PEAKS.json"}
+    elif bound == "tensor":
+        roof = {"bound": "tensor", "achieved": round(flops / s / 1e12, 2), "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": round(t_f / s, 4), "peak_source": f"bf16 dense tensor ({src})"}
+    else:
+        roof = {"bound": "alu", "achieved": round(3 * he / s / 1e9, 1), "unit": "Gexp2/s", "frac": round(t_x / s, 4),
+                "peak_source": "MUFU.EX2 15.7/clk/SM measured x 148 SMs x max clock"}
+    roof.update({"algorithmic": f"{byts} B, {flops} flop (16d x {he} head-edges) and {3 * he} exp2 per backward",
+                 "lower_bound_us": {"tensor": round(t_f * 1e6, 2), "hbm": round(t_m * 1e6, 2), "mufu": round(t_x * 1e6, 2)},
+                 "kernel_ms_median": round(statistics.median(ps), 4),
+                 "kernels": "tensor-core band backward (backward_tc.cu): row pass (lse, D, dQ) + column pass (dK, dV)"})
     return {"workload": f"backward (dQ, dK, dV fp32) of cfg2: L={L}, {H} heads, d={d}, bf16, {mask_desc(cfg)}",
             "value": he / (ms / 1e3), "unit": "edges/s", "ms_per_step": ms, "steps": steps, "warmup": 3, "nnz": nnz,
             "gpu_launches": launches, "roofline": roof}

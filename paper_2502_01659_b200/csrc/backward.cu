@@ -22,6 +22,8 @@
 // formed, as in the forward).  Lane layout as in the forward edge kernel (edge_core.cuh): a
 // (row, head) vector is CH 16-byte chunks, a lane owns NC of them, G = CH / NC lanes per edge,
 // E = 32 / G edges in flight per warp.
+#include <cstdlib>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -297,6 +299,13 @@ template <typename T> static ga_status launch_d(const AttnParams &p, const Args 
 
 } // namespace bwd
 
+// GA_BWD_CUDACORE=1 forces the CUDA-core gather kernels (A/B against the tensor-core band path)
+static bool getenv_off(const char *name)
+{
+    const char *v = getenv(name);
+    return v != nullptr && v[0] != 0 && v[0] != '0';
+}
+
 ga_status attention_backward(const AttnParams &p, ga_dtype dt, const void *O, const void *dO, const float *lse_in,
                              float *dQ, float *dK, float *dV, cudaStream_t s)
 {
@@ -326,6 +335,11 @@ ga_status attention_backward(const AttnParams &p, ga_dtype dt, const void *O, co
     a.dK = dK;
     a.dV = dV;
     ga_status st = GA_OK;
+    if (backward_tc_supported(p, dt) && !getenv_off("GA_BWD_CUDACORE")) { // window bands on mma.sync
+        st = launch_backward_tc(p, dt, O, dO, lse_in, a.lse, a.Dv, dQ, dK, dV, s);
+        scratch_free(w, s);
+        return st;
+    }
     if (csr) {
         char *c = w + 2 * sLH;
         int32_t *rows = reinterpret_cast<int32_t *>(c), *rows_s = reinterpret_cast<int32_t *>(c + sE),

@@ -244,6 +244,9 @@ size_t bigbird_workspace(const AttnParams &p, ga_dtype dt);
 ga_status launch_bigbird(const AttnParams &p, ga_dtype dt, cudaStream_t s);
 ga_status attention_backward(const AttnParams &p, ga_dtype dt, const void *O, const void *dO, const float *lse_in,
                              float *dQ, float *dK, float *dV, cudaStream_t s);
+bool backward_tc_supported(const AttnParams &p, ga_dtype dt);
+ga_status launch_backward_tc(const AttnParams &p, ga_dtype dt, const void *O, const void *dO, const float *lse_in,
+                             float *lse, float *Dv, float *dQ, float *dK, float *dV, cudaStream_t s);
 
 ga_status maskgen_to_csr(const DevMask &M, int64_t *row_ptr, int32_t *col_idx, cudaStream_t s);
 ga_status mask_validate(const DevMask &M, cudaStream_t s, int *ok);

@@ -82,7 +82,9 @@ def test_backward_vs_oracle(ga, orc, fam, dt, d):
 
 
 def test_backward_lse_passthrough(ga):
-    """lse from a carried state (lse = m + log2 l) gives the gradients of the recomputing call."""
+    """lse from a carried state (lse = m + log2 l) gives the gradients of the recomputing call
+    (within the bf16 rounding of P and dS on the tensor-core band path: both are 2e-3-close to
+    the oracle, tests below)."""
     L, H, d = 3000, 2, 64
     q, k, v = ga.qkv_device(3, L, H, d, torch.bfloat16, shift=-0.5)
     g = ga.qkv_device(4, L, H, d, torch.bfloat16, shift=-0.5)[0]
@@ -94,7 +96,7 @@ def test_backward_lse_passthrough(ga):
     b = ga.attention_backward(q, k, v, out, g, m, lse=lse)
     torch.cuda.synchronize()
     for x, y in zip(a, b):
-        assert (x - y).abs().max().item() <= 1e-4 * x.abs().max().item()
+        assert (x - y).abs().max().item() <= 5e-3 * x.abs().max().item()
 
 
 def test_autograd_function_matches_torch_dense(ga):
@@ -124,3 +126,30 @@ def test_backward_rejects(ga):
     q, k, v = ga.qkv_device(1, L, 1, 64, torch.bfloat16)
     with pytest.raises(ga.GaError, match="UNSUPPORTED"):
         ga.attention_backward(q, k, v, q, q, ga.BigBird(8, 2, 2))
+
+
+@pytest.mark.parametrize("L,w,r,dt", [(3000, 256, 2, "bf16"), (2049, 128, 1, "f16"), (1500, 17, 1, "bf16"),
+                                      (4000, 400, 4, "bf16"), (700, 600, 1, "f16")])
+def test_backward_tensor_core_band_vs_oracle(ga, orc, L, w, r, dt):
+    """The tensor-core band backward (backward_tc.cu: Window masks, bf16/fp16, d = 64, m <=
+    255) against the fp64 oracle backward, ragged class lengths and sequences shorter than
+    the band included; and against the CUDA-core kernels (GA_BWD_CUDACORE=1)."""
+    import os
+
+    H, d = 2, 64
+    q, k, v = synth.qkv(600 + w, L, H, d, dt, centred=True)
+    g = synth.qkv(700 + w, L, H, d, dt, centred=True)[0]
+    m = ga.Window(w, r)
+    qd, kd, vd, gd = (x.cuda() for x in (q, k, v, g))
+    out = ga.attention(qd, kd, vd, m)
+    got = ga.attention_backward(qd, kd, vd, out, gd, m)
+    os.environ["GA_BWD_CUDACORE"] = "1"
+    try:
+        ref = ga.attention_backward(qd, kd, vd, out, gd, m)
+    finally:
+        del os.environ["GA_BWD_CUDACORE"]
+    torch.cuda.synchronize()
+    want = orc.attention_backward(*(synth.as_f64(x) for x in (q, k, v)), orc.window(L, w, r), synth.as_f64(g))
+    for name, a, b, c in zip(("dQ", "dK", "dV"), got, want[:3], ref):
+        _check(a.double().cpu().numpy(), b, TOL[dt], f"tc {name}")
+        _check(c.double().cpu().numpy(), b, TOL[dt], f"cuda-core {name}")
