@@ -217,6 +217,7 @@ template <typename T> __global__ void __launch_bounds__(THREADS) row_kernel(cons
     float dq[NB8][4];
 #pragma unroll
     for (int j = 0; j < NB8; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
+#pragma unroll 2
     for (int b = 0; b < nblk; ++b) {
         const int kb = 16 * warp + 16 * b;
         float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}}, dp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -286,6 +287,7 @@ template <typename T> __global__ void __launch_bounds__(THREADS) col_kernel(cons
     float dk[NB8][4], dv[NB8][4];
 #pragma unroll
     for (int j = 0; j < NB8; ++j) dk[j][0] = dk[j][1] = dk[j][2] = dk[j][3] = dv[j][0] = dv[j][1] = dv[j][2] = dv[j][3] = 0.f;
+#pragma unroll 2
     for (int b = 0; b < nblk; ++b) {
         const int qb = 16 * warp + 16 * b; // query band rows
         float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}}, dp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
