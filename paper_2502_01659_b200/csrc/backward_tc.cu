@@ -31,6 +31,10 @@ using tc::ldsm_x4_t;
 using tc::swz;
 constexpr int D = 64, RB = 2 * D, ROWS = 64, WARPS = 4, THREADS = 32 * WARPS, KS = D / 16, NB8 = D / 8;
 constexpr int64_t MAX_M = 255;
+#ifndef GA_BWD_UNROLL
+#define GA_BWD_UNROLL 2 // key / query blocks in flight per warp (1: 1.34 ms, 2: 1.16 ms at cfg2)
+#endif
+constexpr int UNROLL = GA_BWD_UNROLL;
 
 // the two 16-bit elements of a 32-bit word as floats
 template <typename T> __device__ __forceinline__ void unpack2(uint32_t w, float &lo, float &hi);
@@ -217,7 +221,7 @@ template <typename T> __global__ void __launch_bounds__(THREADS) row_kernel(cons
     float dq[NB8][4];
 #pragma unroll
     for (int j = 0; j < NB8; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
-#pragma unroll 2
+#pragma unroll UNROLL
     for (int b = 0; b < nblk; ++b) {
         const int kb = 16 * warp + 16 * b;
         float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}}, dp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -287,7 +291,7 @@ template <typename T> __global__ void __launch_bounds__(THREADS) col_kernel(cons
     float dk[NB8][4], dv[NB8][4];
 #pragma unroll
     for (int j = 0; j < NB8; ++j) dk[j][0] = dk[j][1] = dk[j][2] = dk[j][3] = dv[j][0] = dv[j][1] = dv[j][2] = dv[j][3] = 0.f;
-#pragma unroll 2
+#pragma unroll UNROLL
     for (int b = 0; b < nblk; ++b) {
         const int qb = 16 * warp + 16 * b; // query band rows
         float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}}, dp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
