@@ -14,5 +14,5 @@ e0.record()
 for _ in range(10): ga.attention_backward(q, k, v, o, g, m)
 e1.record(); torch.cuda.synchronize(); print(sys.argv[1], e0.elapsed_time(e1) / 10)
 PY
-for i in 1 2; do GA_LIB=$PWD/abtest/libga_bwd0.so python /tmp/bwd_t.py old; python /tmp/bwd_t.py new; done
+for i in 1 2; do python /tmp/bwd_t.py u2; GA_LIB=$PWD/abtest/libga_u3.so python /tmp/bwd_t.py u3; GA_LIB=$PWD/abtest/libga_u4.so python /tmp/bwd_t.py u4; done
 timeout 600 python -m pytest tests/test_gpu_backward.py -q -x -p no:cacheprovider -k "band or window or dilated" 2>&1 | tail -2

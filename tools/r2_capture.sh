@@ -21,5 +21,5 @@ o = ga.attention(q, k, v, m)
 for _ in range(2): ga.attention_backward(q, k, v, o, g, m)
 torch.cuda.synchronize()
 PY
-timeout 900 $full -k regex:bwd:: -s 2 -c 2 -o $out/full_cfg2_bwd python /tmp/bwd_once.py > /dev/null 2>&1
+timeout 900 $full -k "regex:row_kernel|col_kernel" -s 2 -c 2 -o $out/full_cfg2_bwd python /tmp/bwd_once.py > /dev/null 2>&1
 ls -la $out/*.ncu-rep $out/launches_*.csv
