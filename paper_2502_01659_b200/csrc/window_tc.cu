@@ -43,7 +43,16 @@ using namespace tc;
 using namespace umma;
 
 constexpr int ROWS = 128, KC = 64, NSLOT = 10, D = 64, RB = 2 * D;
-constexpr int THREADS = 320; // 8 softmax warps + loader + MMA
+#ifndef GA_WTC_DUAL
+#define GA_WTC_DUAL 0
+#endif
+// MMA issuer warps: one per softmax warpgroup (GA_WTC_DUAL = 1), or one for both.  Measured
+// (tools/r2_dual.sh, ms): cfg2 0.1256 / 0.1270 dual vs 0.1228 / 0.1219 single, cfg5 30.41 /
+// 30.44 vs 30.56 / 30.84 — within noise of each other: the cross-warpgroup head-of-line
+// blocking of one issuer is not what bounds the kernel.  Parity, synccheck and racecheck
+// pass for both.
+constexpr int NISSUE = GA_WTC_DUAL ? 2 : 1;
+constexpr int THREADS = 32 * (9 + NISSUE); // 8 softmax warps + loader + MMA issuer(s)
 constexpr uint32_t QBYTES = ROWS * RB;   // 16 KB
 constexpr uint32_t CBYTES = KC * RB;     // 8 KB: one K or V chunk
 constexpr uint32_t OFF_Q = 0;            // Q[wg][buf]: 4 x 16 KB
@@ -229,7 +238,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         }
         for (int s = 0; s < NSLOT; ++s) {
             mbar_init(bar(bars, B_KVFULL + s), 1);
-            mbar_init(bar(bars, B_KVEMPTY + s), 1);
+            mbar_init(bar(bars, B_KVEMPTY + s), NISSUE); // every issuer releases every fill
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -325,15 +334,23 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             prev_u = P.u;
             prev_hi = P.hi;
         }
-    } else if (warp == 9) {
-        // ============================ MMA issuer ============================
+    } else if (warp >= 9) {
+        // ============================ MMA issuer(s) ============================
         // Warp-uniform control flow (the whole warp runs the schedule and the blocking waits;
         // one elected lane issues), so descriptors and counters live in uniform registers.
         // Per warpgroup w the schedule keeps S one chunk ahead of the softmax:
         //     S_w(0), S_w(1); for j: [P_w(j)] P V_w(j), S_w(j+2)
-        // S_w(j+2) reuses S buffer j&1, which the softmax finished reading before P_w(j).  The
-        // two warpgroups interleave chunk by chunk; when one finishes its tile it starts the
-        // S MMAs of its next tile (chunks resident) while it runs its epilogue.
+        // S_w(j+2) reuses S buffer j&1, which the softmax finished reading before P_w(j).  When
+        // a warpgroup finishes its tile it starts the S MMAs of its next tile (chunks resident)
+        // while it runs its epilogue.  With GA_WTC_DUAL each warpgroup has its own issuer warp
+        // (warp 9 + w), so a warpgroup waiting for its softmax never holds up the other's MMAs
+        // (one issuer serving both interleaves them chunk by chunk and waits in order).  Both
+        // issuers walk the same items; every issuer arrives once on a slot's empty barrier per
+        // fill (count NISSUE): after its last P V reading the chunk, or — for a chunk its tile
+        // does not read — after it has observed the fill, so an arrival never lands in the
+        // previous fill's phase.
+        const bool mine0 = NISSUE == 1 || warp == 9, mine1 = NISSUE == 1 || warp == 10;
+        auto mine = [&](int w) { return w == 0 ? mine0 : mine1; };
         const uint32_t idS = idesc<T>(ROWS, KC, false), idO = idesc<T>(ROWS, D, true);
         // smem descriptors: constant high part | (address >> 4); the operand tiles stay below
         // 256 KB so the 14-bit start field never carries
@@ -343,7 +360,8 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         uint32_t cw[2] = {0, 0}; // running chunk counters per warpgroup (S/P/O buffer parity)
         int pre[2] = {0, 0};    // S MMAs of this item's tile already issued (end of the previous item)
         bool preq[2] = {false, false};
-        int32_t prev_stream = -1, prev_u = -1, prev_hi = -1;
+        int32_t prev_stream = -1, prev_u = -1, prev_lo = 0;
+        uint32_t waited = 0; // fills this issuer observed, bit g - lo of the previous item
         Pair N = pair_geo(tp, it_begin);
         for (int32_t it = it_begin; it < it_end; ++it) {
             const Pair P = N;
@@ -353,16 +371,17 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             const bool cont = P.stream == prev_stream && P.u == prev_u + 1;
             const bool next_cont = has_next && N.any && N.stream == P.stream && N.u == P.u + 1;
             const int32_t keep_from = next_cont ? N.lo : INT32_MAX;
-            uint32_t readers = 0, ready = 0; // 4 bits per chunk g - lo; 1 bit per chunk
+            uint32_t readers = 0; // 4 bits per chunk g - lo: this issuer's P V MMAs still to come
+            // chunks resident from the previous item whose fill this issuer already observed
+            uint32_t ready = cont ? waited >> (P.lo - prev_lo) : 0u;
 #pragma unroll
             for (int w = 0; w < 2; ++w)
-                for (int32_t j = 0; j < P.n[w]; ++j) readers += 1u << (4 * (P.F[w] + j - P.lo));
-            if (cont)
-                for (int32_t g = P.lo; g <= P.hi && g <= prev_hi; ++g) ready |= 1u << (g - P.lo);
+                if (mine(w))
+                    for (int32_t j = 0; j < P.n[w]; ++j) readers += 1u << (4 * (P.F[w] + j - P.lo));
             int qb[2] = {0, 0};
 #pragma unroll
             for (int w = 0; w < 2; ++w) {
-                if (!P.valid[w]) continue;
+                if (!mine(w) || !P.valid[w]) continue;
                 if (preq[w]) {
                     qb[w] = (nq[w] - 1) & 1;
                 } else {
@@ -382,6 +401,20 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 TRACE2(1, g);
                 fence_after();
             };
+            // release of a chunk released by this item that this issuer's tile does not read
+            auto release_unread = [&](int32_t g) {
+                chunk_ready(g);
+                if (elect_one()) mma_commit(bar(bars, B_KVEMPTY + (int)((uint32_t)g % NSLOT)));
+                __syncwarp();
+            };
+            // this issuer's chunk range [rf, re) (dual: its own tile's; single: the union)
+            int32_t rf = P.lo, re = P.hi + 1;
+            if (NISSUE == 2) {
+                const int32_t f = mine0 ? P.F[0] : P.F[1], n = mine0 ? P.n[0] : P.n[1]; // (static indices)
+                rf = n == 0 ? P.hi + 1 : f;
+                re = n == 0 ? P.hi + 1 : f + n;
+                for (int32_t g = P.lo; g < rf && g < keep_from; ++g) release_unread(g);
+            }
             auto issue_S = [&](int w, uint32_t c, int32_t g, int qbuf) {
                 const uint32_t aq = sbase + OFF_Q + (uint32_t)(2 * w + qbuf) * QBYTES;
                 const uint32_t ak = sbase + OFF_KV + ((uint32_t)g % NSLOT) * 2 * CBYTES;
@@ -413,8 +446,8 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 const uint32_t tOacc = tmem + 256u * w + COL_O + (uint32_t)qb[w] * D;
 #endif
                 readers -= 1u << (4 * gi);
-                // the chunk's last reader: release its slot unless the next item keeps it
-                // (commit tracks every MMA this thread issued)
+                // this issuer's last reader of the chunk: release its slot unless the next item
+                // keeps it (commit tracks every MMA this thread issued)
                 const bool release = ((readers >> (4 * gi)) & 15u) == 0 && g < keep_from;
                 if (elect_one()) {
 #pragma unroll
@@ -430,10 +463,11 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             // the buffer of chunk j, free once P V_w(j) has completed (waited below)
 #pragma unroll
             for (int w = 0; w < 2; ++w)
-                for (int32_t j = pre[w]; j < NSB && j < P.n[w]; ++j) {
-                    chunk_ready(P.F[w] + j);
-                    issue_S(w, cw[w] + j, P.F[w] + j, qb[w]);
-                }
+                if (mine(w))
+                    for (int32_t j = pre[w]; j < NSB && j < P.n[w]; ++j) {
+                        chunk_ready(P.F[w] + j);
+                        issue_S(w, cw[w] + j, P.F[w] + j, qb[w]);
+                    }
             int npre[2] = {0, 0};
             bool nqw[2] = {false, false};
             auto prefetch = [&](int w, bool block) { // next tile's first S MMAs (resident chunks)
@@ -453,11 +487,11 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     ++npre[w];
                 }
             };
-            const int32_t jmax = max(P.n[0], P.n[1]);
+            const int32_t jmax = max(mine0 ? P.n[0] : 0, mine1 ? P.n[1] : 0);
             for (int32_t j = 0; j < jmax; ++j) {
 #pragma unroll
                 for (int w = 0; w < 2; ++w) {
-                    if (j >= P.n[w]) continue;
+                    if (!mine(w) || j >= P.n[w]) continue;
                     issue_PV(w, j);
                     if (j + NSB < P.n[w]) {
 #if !defined(GA_WTC_NO_WAR_WAIT) && !GA_WTC_SEPP
@@ -474,9 +508,11 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     }
                 }
             }
+            if (NISSUE == 2)
+                for (int32_t g = max(re, P.lo); g <= P.hi && g < keep_from; ++g) release_unread(g);
 #pragma unroll
             for (int w = 0; w < 2; ++w)
-                if (next_cont && N.valid[w] && npre[w] == 0) prefetch(w, true);
+                if (mine(w) && next_cont && N.valid[w] && npre[w] == 0) prefetch(w, true);
             cw[0] += P.n[0];
             cw[1] += P.n[1];
             pre[0] = npre[0];
@@ -485,7 +521,8 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             preq[1] = nqw[1];
             prev_stream = P.stream;
             prev_u = P.u;
-            prev_hi = P.hi;
+            prev_lo = P.lo;
+            waited = ready;
         }
     } else {
         // ============================ softmax warpgroups ============================
