@@ -11,28 +11,36 @@
 //
 //   S  = Q K_g^T      tcgen05.mma.cta_group::1.kind::f16 M=128 N=64 (K=16 x 4), A (Q tile) and
 //                     B (K chunk) from 128B-swizzled shared memory, fp32 accumulator in TMEM
-//   softmax           each thread tcgen05.ld's its row of S; keys outside the row's band get
-//                     weight exactly 0; online softmax in the exp2 domain (lazy rescale, 2^8);
-//                     P (bf16/fp16 pairs) written back to TMEM with tcgen05.st.  A warp skips
-//                     chunks its 32 rows do not reach (P = 0 without reading S) and masks only
-//                     chunks its rows reach partially
+//   softmax           each thread tcgen05.ld's its row of S, 32 columns at a time; a 32-column
+//                     half no row of the warp reaches is neither loaded nor exponentiated
+//                     (P = 0), a half every row reaches fully is used as is, and only the
+//                     halves the band's edges cross are masked per element (keys outside the
+//                     row's band get weight exactly 0); chunk max first, online softmax in the
+//                     exp2 domain with lazy rescale (2^8); P (bf16/fp16 pairs) to TMEM
 //   O += P V_g        tcgen05.mma with A = P from TMEM, B = V_g (MN-major) from shared memory
 //
 // The tensor cores see whole 128 x 64 chunks (66% of the products valid at m = 127: 32,640
-// band edges of 49,152 per tile); exponentials, sums and weights are computed only for the
-// chunks a warp's rows reach, and a masked pair contributes exactly 0 — the result is the
-// Algorithm 1 result over the band's edges, computed in O(nnz d) work.
+// band edges of 49,152 per tile; reading R23); exponentials, sums and weights are computed
+// only for the 32-column halves a warp's rows reach, and a masked pair contributes exactly 0
+// — the result is the Algorithm 1 result over the band's edges.
 //
-// CTA organisation (persistent, one CTA per SM, 512 TMEM columns):
-//   warps 0-3  softmax warpgroup A: even tiles of a tile pair   (TMEM cols   0..255)
-//   warps 4-7  softmax warpgroup B: odd tiles                    (TMEM cols 256..511)
-//   warp 8     loader: TMA boxes of the Q tiles (2 x 64 class rows, element stride r) and the
-//              K/V chunks into an 8-slot ring (slot = g mod 8); peer rows (sharded runs) by
-//              cp.async from the owner's memory
-//   warp 9     MMA issuer (one elected lane)
-// A CTA walks a contiguous run of tile pairs of one (class, head) stream: consecutive pairs
-// share 4 of their 8 chunks, which stay resident (each K/V row is read from L2/HBM about once
-// per run), and the two warpgroups alternate on the tensor and MUFU pipes.
+// CTA organisation (persistent, one CTA per SM, 512 TMEM columns, 15 warps):
+//   warps 0-3   softmax warpgroup A: even tiles of a tile pair   (TMEM cols   0..255)
+//   warps 4-7   softmax warpgroup B: odd tiles                    (TMEM cols 256..511)
+//   warps 8-11  epilogue warpgroup: O of a finished tile from TMEM, normalised by the row sum
+//               the softmax left in shared memory, staged in the tile's Q buffer and stored by
+//               TMA (or the carried (m, l, o~) state) — off the softmax warps' critical path
+//   warp 12     loader: TMA boxes of the Q tiles (2 x 64 class rows, element stride r) and the
+//               K/V chunks into a 9-slot ring (slot = g mod 9); peer rows (sharded runs) by
+//               cp.async from the owner's memory
+//   warps 13-14 MMA issuers, one per softmax warpgroup (one elected lane issues)
+// TMEM of a warpgroup: S (64 columns) | P[2] (32 each) | O[2] (64 each).  S has ONE buffer: the
+// softmax releases it right after its tcgen05.ld (before any arithmetic), and the issuer then
+// writes S of the next chunk while the softmax works on this one.  P of chunk c goes to P[c & 1]
+// after P V_{c-2} read it; tile k accumulates in O[k & 1], so the epilogue of tile k overlaps
+// tile k + 1.  A CTA walks a contiguous run of tile pairs of one (class, head) stream:
+// consecutive pairs share 4 of their 8 chunks, which stay resident (each K/V row is read from
+// L2/HBM about once per run).
 #include "tc_common.cuh"
 #include "tma.cuh"
 #include "umma.cuh"
@@ -42,51 +50,41 @@ namespace wtc {
 using namespace tc;
 using namespace umma;
 
-constexpr int ROWS = 128, KC = 64, NSLOT = 10, D = 64, RB = 2 * D;
-#ifndef GA_WTC_DUAL
-#define GA_WTC_DUAL 0
+constexpr int ROWS = 128, KC = 64, NSLOT = 9, D = 64, RB = 2 * D;
+constexpr int W_EPI = 8, W_LOAD = 12, W_MMA = 13; // warp 15 only completes warpgroup 3
+constexpr int THREADS = 32 * 16;
+// registers per thread after setmaxnreg (per SM sub-partition: one warp of each warpgroup,
+// 2 x 168 + 104 + 72 = 512 = the 16K registers of the sub-partition / 32 lanes)
+#ifndef GA_WTC_REG_SMX
+#define GA_WTC_REG_SMX 168
 #endif
-// MMA issuer warps: one per softmax warpgroup (GA_WTC_DUAL = 1), or one for both.  Measured
-// (tools/r2_dual.sh, ms): cfg2 0.1256 / 0.1270 dual vs 0.1228 / 0.1219 single, cfg5 30.41 /
-// 30.44 vs 30.56 / 30.84 — within noise of each other: the cross-warpgroup head-of-line
-// blocking of one issuer is not what bounds the kernel.  Parity, synccheck and racecheck
-// pass for both.
-constexpr int NISSUE = GA_WTC_DUAL ? 2 : 1;
-constexpr int THREADS = 32 * (9 + NISSUE); // 8 softmax warps + loader + MMA issuer(s)
+constexpr int REG_SMX = GA_WTC_REG_SMX, REG_EPI = 104, REG_PROD = 512 - 2 * REG_SMX - REG_EPI;
 constexpr uint32_t QBYTES = ROWS * RB;   // 16 KB
 constexpr uint32_t CBYTES = KC * RB;     // 8 KB: one K or V chunk
-constexpr uint32_t OFF_Q = 0;            // Q[wg][buf]: 4 x 16 KB
+constexpr uint32_t OFF_Q = 0;            // Q[wg][buf]: 4 x 16 KB (a finished tile's O is staged in its Q buffer)
 constexpr uint32_t OFF_KV = 4 * QBYTES;  // slot s: K at OFF_KV + 2 s CBYTES, V right after
-constexpr uint32_t OFF_BAR = OFF_KV + NSLOT * 2 * CBYTES;
+constexpr uint32_t OFF_LM = OFF_KV + NSLOT * 2 * CBYTES; // float [wg][buf][l | m][128]
+constexpr uint32_t OFF_BAR = OFF_LM + 2 * 2 * 2 * ROWS * 4;
 constexpr uint32_t SMEM_BYTES = 1024 + OFF_BAR + 64 * 8;
+static_assert(SMEM_BYTES <= 232448, "shared memory");
 
-// mbarrier indices (8 bytes each from OFF_BAR)
-#ifndef GA_WTC_NSB
-#define GA_WTC_NSB 2
-#endif
-constexpr int NSB = GA_WTC_NSB; // S buffers per warpgroup (P is written over its S buffer)
-constexpr int B_QFULL = 0, B_QEMPTY = 4, B_KVFULL = 8, B_KVEMPTY = 8 + NSLOT, B_SFULL = 8 + 2 * NSLOT,
-              B_PFULL = B_SFULL + 2 * NSB, B_OFULL = B_PFULL + 2 * NSB;
-constexpr int B_TMEM = B_OFULL + 4; // tcgen05.alloc writes the TMEM base here
+// TMEM columns within a warpgroup's 256
+constexpr uint32_t COL_S = 0, COL_P = 64, COL_O = 128;
 
-#ifndef GA_WTC_SEPP
-#define GA_WTC_SEPP 1
-#endif
-#if GA_WTC_SEPP
-// TMEM columns of warpgroup w: S[NSB] at 256w + 64 b, P[2] (chunk c's 16-bit pairs in P[c & 1],
-// 32 columns each), one O accumulator.  S_{c+NSB} reuses S_c's buffer as soon as the softmax
-// has read it (P_c arrived), with no wait for any MMA to complete; the softmax writes P_c only
-// after P V_{c-2} has read that P buffer.  One O suffices: a tile's epilogue reads O before the
-// same threads release P of the next tile's first chunk, so the next tile's first P V (which
-// overwrites O, accumulate = 0) is issued after those reads.
-constexpr uint32_t COL_S = 0, COL_P = NSB * KC, COL_O = COL_P + 2 * (KC / 2);
-static_assert(COL_O + D <= 256, "TMEM: 256 columns per warpgroup");
-#else
-// TMEM columns of warpgroup w: S[NSB] at 256w + 64 b (P of chunk c, 16-bit pairs, is written over
-// the first 32 columns of its S buffer), O[2] (tile k accumulates in O[k & 1]) after them
-constexpr uint32_t COL_S = 0, COL_O = NSB * KC;
-static_assert(NSB * KC + 2 * D <= 256, "TMEM: 256 columns per warpgroup");
-#endif
+// mbarrier indices (8 bytes each from OFF_BAR); [w] = softmax warpgroup, [b] = buffer parity
+constexpr int B_QFULL = 0,             // [w][b] (loader TMA)
+    B_QEMPTY = 4,                      // [w][b] 4 epilogue warps: O store read the staging buffer
+    B_KVFULL = 8,                      // [slot]
+    B_KVEMPTY = B_KVFULL + NSLOT,      // [slot] 2 issuers
+    B_SFULL = B_KVEMPTY + NSLOT,       // [w] S MMA committed
+    B_SFREE = B_SFULL + 2,             // [w] 128 softmax threads read S
+    B_PFULL = B_SFREE + 2,             // [w][c & 1] 128 softmax threads wrote P
+    B_OFULL = B_PFULL + 4,             // [w][c & 1] P V MMA committed
+    B_OTILE = B_OFULL + 4,             // [w][k & 1] last P V of tile k committed
+    B_EPI = B_OTILE + 4,               // [w][k & 1] 128 softmax threads wrote (l, m) of tile k
+    B_OFREE = B_EPI + 4,               // [w][k & 1] 128 epilogue threads read O of tile k
+    B_TMEM = B_OFREE + 4;              // tcgen05.alloc writes the TMEM base here
+static_assert(B_TMEM < 64, "barrier area");
 
 struct TcParams {
     CUtensorMap tmQ, tmK, tmV, tmO; // one head, element stride r, 64-row boxes
@@ -187,10 +185,9 @@ __device__ __forceinline__ Tile tile_geo(const TcParams &tp, int32_t it, int w)
 __device__ __forceinline__ uint32_t bar(uint32_t base, int i) { return base + 8u * (uint32_t)i; }
 
 #ifdef GA_WTC_TRACE
-// debug timeline of CTA 0: (event << 48 | warp << 40 | (clock - t0)) per event
+// debug timeline of CTA 0: (value << 56 | event << 48 | warp << 40 | (clock - t0)) per event
 constexpr int TRACE_N = 16384;
 __device__ unsigned long long g_trace[TRACE_N];
-__device__ unsigned int g_trace_n;
 // per-warp private slots (no atomics: a trace point costs one store)
 #define TRACE2(ev, val) do { if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && t_cnt < TRACE_N / 16) { \
     g_trace[(threadIdx.x >> 5) * (TRACE_N / 16) + t_cnt++] = ((unsigned long long)((val) & 0xff) << 56) | \
@@ -202,14 +199,54 @@ __device__ unsigned int g_trace_n;
 #define TRACE2(ev, val)
 #endif
 
+// keys outside [il, ih] (row-relative column bounds within a 32-column half) -> -inf
+__device__ __forceinline__ void mask_half(float *s, int il, int ih, bool left, bool right)
+{
+    if (left) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[i] = i >= il ? s[i] : -INFINITY;
+    }
+    if (right) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[i] = i <= ih ? s[i] : -INFINITY;
+    }
+}
+
+__device__ __forceinline__ float max32(const float *s)
+{
+    float a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fmaxf(s[i], fmaxf(s[i + 8], s[i + 16]));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fmaxf(a[i], s[i + 24]);
+    return fmaxf(fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3])), fmaxf(fmaxf(a[4], a[5]), fmaxf(a[6], a[7])));
+}
+
+// P of one 32-column half: pk = pack(2^(s * sl2 - m)) (16 words), row-sum partials in acc
+template <typename T>
+__device__ __forceinline__ void exps_half(float *s, float sl2, float negm, uint32_t *pk, float2 *acc)
+{
+#pragma unroll
+    for (int i = 0; i < 16; ++i) ffma2_sm(s[2 * i], s[2 * i + 1], sl2, negm);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) s[i] = ex2(s[i]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        fadd2_acc(acc[i & 3], s[2 * i], s[2 * i + 1]);
+        pk[i] = pack2<T>(s[2 * i], s[2 * i + 1]);
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_constant__ TcParams tp)
 {
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;
+    unsigned char *const sgen = smem_raw + (sbase - raw); // generic pointer to sbase
     const uint32_t bars = sbase + OFF_BAR;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem_raw + (sbase - raw) + OFF_BAR + 8 * B_TMEM);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sgen + OFF_BAR + 8 * B_TMEM);
+    float *const lmbuf = reinterpret_cast<float *>(sgen + OFF_LM); // [w][b][l | m][128]
     const AttnParams &p = tp.p;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t m = tp.m, r = tp.r;
@@ -229,16 +266,20 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) {
             mbar_init(bar(bars, B_QFULL + i), 1);
-            mbar_init(bar(bars, B_QEMPTY + i), 4); // each warp's O store has read its rows
-            mbar_init(bar(bars, B_OFULL + i), 1);
-        }
-        for (int i = 0; i < 2 * NSB; ++i) {
-            mbar_init(bar(bars, B_SFULL + i), 1);
+            mbar_init(bar(bars, B_QEMPTY + i), 4);
             mbar_init(bar(bars, B_PFULL + i), 128);
+            mbar_init(bar(bars, B_OFULL + i), 1);
+            mbar_init(bar(bars, B_OTILE + i), 1);
+            mbar_init(bar(bars, B_EPI + i), 128);
+            mbar_init(bar(bars, B_OFREE + i), 128);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(bar(bars, B_SFULL + i), 1);
+            mbar_init(bar(bars, B_SFREE + i), 128);
         }
         for (int s = 0; s < NSLOT; ++s) {
             mbar_init(bar(bars, B_KVFULL + s), 1);
-            mbar_init(bar(bars, B_KVEMPTY + s), NISSUE); // every issuer releases every fill
+            mbar_init(bar(bars, B_KVEMPTY + s), 2); // both issuers release every fill
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -251,7 +292,9 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
     int t_cnt = 0;
 #endif
 
-    if (warp == 8) {
+    if (warp >= 12) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REG_PROD));
+    if (warp == W_LOAD) {
         // ============================ loader ============================
         // per slot: filled before (bit s of `used`), parity of the fill count (bit s of `par`);
         // bitmasks, not arrays (a dynamically indexed array would live in local memory)
@@ -276,13 +319,13 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     tma::load_3d(dst, &tp.tmQ, 0, P.h, tok, fb);
                     tma::load_3d(dst + QBYTES / 2, &tp.tmQ, 0, P.h, tok + 64 * (int)r, fb);
                 }
+                __syncwarp();
             }
             // K/V chunks not resident from the previous pair
             const bool cont = P.stream == prev_stream && P.u == prev_u + 1;
             for (int32_t g = P.lo; g <= P.hi; ++g) {
                 if (cont && g <= prev_hi) continue;
                 const int s = (int)((uint32_t)g % NSLOT);
-                TRACE2(21, g);
                 // fill n of slot s waits for release n - 1 (parity of n - 1 = complement of n's)
                 if ((used >> s) & 1u) mbar_wait(bar(bars, B_KVEMPTY + s), ((par >> s) & 1u) ^ 1u);
                 TRACE2(20, g);
@@ -334,32 +377,28 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             prev_u = P.u;
             prev_hi = P.hi;
         }
-    } else if (warp >= 9) {
-        // ============================ MMA issuer(s) ============================
-        // Warp-uniform control flow (the whole warp runs the schedule and the blocking waits;
-        // one elected lane issues), so descriptors and counters live in uniform registers.
-        // Per warpgroup w the schedule keeps S one chunk ahead of the softmax:
-        //     S_w(0), S_w(1); for j: [P_w(j)] P V_w(j), S_w(j+2)
-        // S_w(j+2) reuses S buffer j&1, which the softmax finished reading before P_w(j).  When
-        // a warpgroup finishes its tile it starts the S MMAs of its next tile (chunks resident)
-        // while it runs its epilogue.  With GA_WTC_DUAL each warpgroup has its own issuer warp
-        // (warp 9 + w), so a warpgroup waiting for its softmax never holds up the other's MMAs
-        // (one issuer serving both interleaves them chunk by chunk and waits in order).  Both
-        // issuers walk the same items; every issuer arrives once on a slot's empty barrier per
-        // fill (count NISSUE): after its last P V reading the chunk, or — for a chunk its tile
-        // does not read — after it has observed the fill, so an arrival never lands in the
-        // previous fill's phase.
-        const bool mine0 = NISSUE == 1 || warp == 9, mine1 = NISSUE == 1 || warp == 10;
-        auto mine = [&](int w) { return w == 0 ? mine0 : mine1; };
+    } else if (warp == W_MMA || warp == W_MMA + 1) {
+        // ============================ MMA issuers ============================
+        // Issuer w serves softmax warpgroup w (its tile of every item).  Warp-uniform control
+        // flow (the whole warp runs the schedule and the blocking waits; one elected lane
+        // issues).  Per chunk c of the warpgroup (running counter over its tiles):
+        //     S(c) once the softmax has read S(c-1) (single S buffer); then P V(c-1) once P(c-1)
+        //     arrived — so S(c) is computed while the softmax works on chunk c-1.
+        // The first S of the next tile is issued before the last P V of this one (when the next
+        // Q tile has landed).  Both issuers arrive once on a slot's empty barrier per fill: after
+        // their last P V reading the chunk, or — for a chunk their tile does not read — after
+        // observing the fill, so an arrival never lands in the previous fill's phase.
+        const int w = warp - W_MMA;
         const uint32_t idS = idesc<T>(ROWS, KC, false), idO = idesc<T>(ROWS, D, true);
         // smem descriptors: constant high part | (address >> 4); the operand tiles stay below
         // 256 KB so the 14-bit start field never carries
         const uint64_t dbase = sdesc_sw128(0);
+        const uint32_t tw = tmem + 256u * (uint32_t)w;
         uint32_t seen = 0;      // parity of the fills waited for, bit per slot
-        int nq[2] = {0, 0};     // Q tiles waited per warpgroup
-        uint32_t cw[2] = {0, 0}; // running chunk counters per warpgroup (S/P/O buffer parity)
-        int pre[2] = {0, 0};    // S MMAs of this item's tile already issued (end of the previous item)
-        bool preq[2] = {false, false};
+        int nq = 0;             // Q tiles waited
+        uint32_t cs = 0;        // S MMAs issued (chunk counter of the warpgroup)
+        uint32_t k = 0;         // tiles of the warpgroup (O buffer parity)
+        bool pre = false, preq = false; // S(0) of this item's tile already issued / its Q waited
         int32_t prev_stream = -1, prev_u = -1, prev_lo = 0;
         uint32_t waited = 0; // fills this issuer observed, bit g - lo of the previous item
         Pair N = pair_geo(tp, it_begin);
@@ -371,26 +410,10 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             const bool cont = P.stream == prev_stream && P.u == prev_u + 1;
             const bool next_cont = has_next && N.any && N.stream == P.stream && N.u == P.u + 1;
             const int32_t keep_from = next_cont ? N.lo : INT32_MAX;
-            uint32_t readers = 0; // 4 bits per chunk g - lo: this issuer's P V MMAs still to come
             // chunks resident from the previous item whose fill this issuer already observed
             uint32_t ready = cont ? waited >> (P.lo - prev_lo) : 0u;
-#pragma unroll
-            for (int w = 0; w < 2; ++w)
-                if (mine(w))
-                    for (int32_t j = 0; j < P.n[w]; ++j) readers += 1u << (4 * (P.F[w] + j - P.lo));
-            int qb[2] = {0, 0};
-#pragma unroll
-            for (int w = 0; w < 2; ++w) {
-                if (!mine(w) || !P.valid[w]) continue;
-                if (preq[w]) {
-                    qb[w] = (nq[w] - 1) & 1;
-                } else {
-                    qb[w] = nq[w] & 1;
-                    mbar_wait(bar(bars, B_QFULL + 2 * w + qb[w]), (nq[w] >> 1) & 1);
-                    ++nq[w];
-                }
-            }
-            fence_after();
+            const bool valid = w == 0 ? P.valid[0] : P.valid[1];
+            const int32_t f = w == 0 ? P.F[0] : P.F[1], n = valid ? (w == 0 ? P.n[0] : P.n[1]) : 0;
             auto chunk_ready = [&](int32_t g) {
                 const int gi = (int)(g - P.lo);
                 if ((ready >> gi) & 1u) return;
@@ -398,441 +421,344 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 mbar_wait(bar(bars, B_KVFULL + sl), (seen >> sl) & 1u);
                 seen ^= 1u << sl;
                 ready |= 1u << gi;
-                TRACE2(1, g);
                 fence_after();
             };
-            // release of a chunk released by this item that this issuer's tile does not read
             auto release_unread = [&](int32_t g) {
                 chunk_ready(g);
                 if (elect_one()) mma_commit(bar(bars, B_KVEMPTY + (int)((uint32_t)g % NSLOT)));
                 __syncwarp();
             };
-            // this issuer's chunk range [rf, re) (dual: its own tile's; single: the union)
-            int32_t rf = P.lo, re = P.hi + 1;
-            if (NISSUE == 2) {
-                const int32_t f = mine0 ? P.F[0] : P.F[1], n = mine0 ? P.n[0] : P.n[1]; // (static indices)
-                rf = n == 0 ? P.hi + 1 : f;
-                re = n == 0 ? P.hi + 1 : f + n;
-                for (int32_t g = P.lo; g < rf && g < keep_from; ++g) release_unread(g);
+            int qb = 0;
+            if (valid) {
+                if (preq) {
+                    qb = (nq - 1) & 1;
+                } else {
+                    qb = nq & 1;
+                    mbar_wait(bar(bars, B_QFULL + 2 * w + qb), (nq >> 1) & 1);
+                    ++nq;
+                    fence_after();
+                }
             }
-            auto issue_S = [&](int w, uint32_t c, int32_t g, int qbuf) {
+            // chunks of the item below this tile's range that the next item does not keep
+            for (int32_t g = P.lo; g < (n ? f : P.hi + 1) && g < keep_from; ++g) release_unread(g);
+            auto issue_S = [&](uint32_t c, int32_t g, int qbuf) {
+                if (c > 0) mbar_wait(bar(bars, B_SFREE + w), (c - 1) & 1u); // S(c-1) read
+                fence_after();
                 const uint32_t aq = sbase + OFF_Q + (uint32_t)(2 * w + qbuf) * QBYTES;
                 const uint32_t ak = sbase + OFF_KV + ((uint32_t)g % NSLOT) * 2 * CBYTES;
-                const uint32_t sb = (uint32_t)(c % NSB);
-                const uint32_t dS = tmem + 256u * w + COL_S + sb * KC;
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk)
-                        mma_ss(dS, dbase | ((aq + kk * 32) >> 4), dbase | ((ak + kk * 32) >> 4), idS, kk > 0);
-                    mma_commit(bar(bars, B_SFULL + NSB * w + (int)sb));
+                        mma_ss(tw + COL_S, dbase | ((aq + kk * 32) >> 4), dbase | ((ak + kk * 32) >> 4), idS, kk > 0);
+                    mma_commit(bar(bars, B_SFULL + w));
                 }
                 __syncwarp();
-                TRACE2(6 + w, g);
+                TRACE2(6, g);
             };
-            auto issue_PV = [&](int w, int32_t j) {
-                const uint32_t c = cw[w] + (uint32_t)j;
-                const int32_t g = P.F[w] + j;
-                const uint32_t sb = (uint32_t)(c % NSB);
-                mbar_wait(bar(bars, B_PFULL + NSB * w + (int)sb), (uint32_t)((c / NSB) & 1));
-                TRACE2(3 + w, g);
+            const uint32_t c0 = cs - (pre ? 1u : 0u); // chunk counter of this tile's chunk 0
+            auto issue_PV = [&](int32_t j) {
+                const uint32_t c = c0 + (uint32_t)j;
+                const int32_t g = f + j;
+                mbar_wait(bar(bars, B_PFULL + 2 * w + (int)(c & 1)), (c >> 1) & 1);
+                TRACE2(3, g);
+                if (j == 0 && k >= 2) mbar_wait(bar(bars, B_OFREE + 2 * w + (int)(k & 1)), ((k - 2) >> 1) & 1);
                 fence_after();
-                const int gi = (int)(g - P.lo), sl = (int)((uint32_t)g % NSLOT);
+                const int sl = (int)((uint32_t)g % NSLOT);
                 const uint32_t av = sbase + OFF_KV + (uint32_t)sl * 2 * CBYTES + CBYTES;
-#if GA_WTC_SEPP
-                const uint32_t tP = tmem + 256u * w + COL_P + (c & 1u) * (KC / 2);
-                const uint32_t tOacc = tmem + 256u * w + COL_O;
-#else
-                const uint32_t tP = tmem + 256u * w + COL_S + sb * KC;
-                const uint32_t tOacc = tmem + 256u * w + COL_O + (uint32_t)qb[w] * D;
-#endif
-                readers -= 1u << (4 * gi);
-                // this issuer's last reader of the chunk: release its slot unless the next item
-                // keeps it (commit tracks every MMA this thread issued)
-                const bool release = ((readers >> (4 * gi)) & 15u) == 0 && g < keep_from;
+                const uint32_t tP = tw + COL_P + (c & 1u) * (KC / 2);
+                const uint32_t tO = tw + COL_O + (k & 1u) * D;
+                const bool release = g < keep_from; // each chunk is read once per tile
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < KC / 16; ++kk) // 16 keys per MMA: 8 P columns, 16 V rows
-                        mma_ts(tOacc, tP + kk * 8, dbase | ((av + kk * 16 * RB) >> 4), idO,
-                               (j > 0 || kk > 0));
+                        mma_ts(tO, tP + kk * 8, dbase | ((av + kk * 16 * RB) >> 4), idO, (j > 0 || kk > 0));
                     mma_commit(bar(bars, B_OFULL + 2 * w + (int)(c & 1)));
+                    if (j == n - 1) mma_commit(bar(bars, B_OTILE + 2 * w + (int)(k & 1)));
                     if (release) mma_commit(bar(bars, B_KVEMPTY + sl));
                 }
                 __syncwarp();
             };
-            // S of the first NSB chunks of each tile (unless issued early); S_w(j + NSB) reuses
-            // the buffer of chunk j, free once P V_w(j) has completed (waited below)
-#pragma unroll
-            for (int w = 0; w < 2; ++w)
-                if (mine(w))
-                    for (int32_t j = pre[w]; j < NSB && j < P.n[w]; ++j) {
-                        chunk_ready(P.F[w] + j);
-                        issue_S(w, cw[w] + j, P.F[w] + j, qb[w]);
-                    }
-            int npre[2] = {0, 0};
-            bool nqw[2] = {false, false};
-            auto prefetch = [&](int w, bool block) { // next tile's first S MMAs (resident chunks)
-                for (int32_t jn = 0; jn < NSB && jn < N.n[w]; ++jn) {
-                    const int32_t g = N.F[w] + jn;
-                    if (g > P.hi || !((ready >> (int)(g - P.lo)) & 1u)) break;
-                    if (!nqw[w]) {
-                        const uint32_t qf = bar(bars, B_QFULL + 2 * w + (nq[w] & 1));
-                        const uint32_t ph = (nq[w] >> 1) & 1;
-                        if (block) mbar_wait(qf, ph);
-                        else if (!mbar_test(qf, ph)) return;
-                        ++nq[w];
-                        nqw[w] = true;
-                        fence_after();
-                    }
-                    issue_S(w, cw[w] + P.n[w] + jn, g, (nq[w] - 1) & 1);
-                    ++npre[w];
+            for (int32_t j = 0; j < n; ++j) {
+                if (j > 0 || !pre) {
+                    chunk_ready(f + j);
+                    issue_S(cs, f + j, qb);
+                    ++cs;
                 }
-            };
-            const int32_t jmax = max(mine0 ? P.n[0] : 0, mine1 ? P.n[1] : 0);
-            for (int32_t j = 0; j < jmax; ++j) {
-#pragma unroll
-                for (int w = 0; w < 2; ++w) {
-                    if (!mine(w) || j >= P.n[w]) continue;
-                    issue_PV(w, j);
-                    if (j + NSB < P.n[w]) {
-#if !defined(GA_WTC_NO_WAR_WAIT) && !GA_WTC_SEPP
-                        // S_w(j + NSB) overwrites the TMEM columns P V_w(j) reads (P over S): wait
-                        // for P V_w(j) to complete — issue order alone did not keep the A-operand
-                        // reads ahead of a later MMA's accumulator writes in the LongNet kernel
-                        // (tools/lnet_stress.py); costs ~1-2% here (tools/ab_war.sh)
-                        { const uint32_t cc = cw[w] + j; mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(cc & 1)), (uint32_t)((cc >> 1) & 1)); fence_after(); }
-#endif
-                        chunk_ready(P.F[w] + j + NSB);
-                        issue_S(w, cw[w] + j + NSB, P.F[w] + j + NSB, qb[w]);
-                    } else if (j == P.n[w] - 1 && next_cont && N.valid[w]) {
-                        prefetch(w, false); // only if the next Q tile already landed
+                if (j > 0) issue_PV(j - 1);
+            }
+            // next tile's first S before this tile's last P V (its chunk is resident)
+            bool npre = false, nqw = false;
+            if (n > 0 && next_cont && (w == 0 ? N.valid[0] : N.valid[1])) {
+                const int32_t g = w == 0 ? N.F[0] : N.F[1];
+                if (g <= P.hi && ((ready >> (int)(g - P.lo)) & 1u)) {
+                    const uint32_t qf = bar(bars, B_QFULL + 2 * w + (nq & 1));
+                    if (mbar_test(qf, (nq >> 1) & 1)) {
+                        ++nq;
+                        nqw = true;
+                        issue_S(cs, g, (nq - 1) & 1);
+                        ++cs;
+                        npre = true;
                     }
                 }
             }
-            if (NISSUE == 2)
-                for (int32_t g = max(re, P.lo); g <= P.hi && g < keep_from; ++g) release_unread(g);
-#pragma unroll
-            for (int w = 0; w < 2; ++w)
-                if (mine(w) && next_cont && N.valid[w] && npre[w] == 0) prefetch(w, true);
-            cw[0] += P.n[0];
-            cw[1] += P.n[1];
-            pre[0] = npre[0];
-            pre[1] = npre[1];
-            preq[0] = nqw[0];
-            preq[1] = nqw[1];
+            if (n > 0) {
+                issue_PV(n - 1);
+                ++k;
+            }
+            // chunks above this tile's range that the next item does not keep
+            for (int32_t g = (n ? f + n : P.hi + 1); g <= P.hi && g < keep_from; ++g) release_unread(g);
+            pre = npre;
+            preq = nqw;
             prev_stream = P.stream;
             prev_u = P.u;
             prev_lo = P.lo;
             waited = ready;
         }
-    } else {
-        // ============================ softmax warpgroups ============================
-        // A tile's epilogue (O from TMEM, normalise, store) is deferred to the first chunk of the
-        // warpgroup's next tile: O is double-buffered in TMEM (tile k accumulates in O[k & 1]), so
-        // the softmax never waits for the last P V of a tile.
-        const int w = warp >> 2, q = warp & 3;
-        const uint32_t tl = tmem + 256u * w + ((uint32_t)(q * 32) << 16); // this warp's TMEM lanes
-        const float sl2 = p.scale_log2;
-        constexpr float kTau = 8.f;
-        uint32_t cnt = 0; // running chunk counter (matches the MMA issuer's cw[w])
-        auto wait_O = [&](uint32_t c) {
-            mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(c & 1)), (c >> 1) & 1);
-            fence_after();
-        };
-        uint32_t ntile = 0; // tiles of this warpgroup (Q / O staging buffer and O buffer = index & 1)
-        // deferred epilogue of the previous tile
-        bool pend_epi = false, pend_rel = false;
-        int32_t p_it = 0; // previous tile's item (its geometry is recomputed: fewer live registers)
-        float l_prev = 0.f, m_prev = -INFINITY;
-        uint32_t cnt_prev = 0, tix_prev = 0;
-        auto release = [&]() { // the previous tile's O store has read its Q buffer: hand it back
+    }
+    } else if (warp >= W_EPI) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REG_EPI));
+        // ============================ epilogue warpgroup ============================
+        // Tiles in item order (A then B): wait for the tile's last P V and its row sums, read O
+        // (then hand the O buffer back to the issuer), normalise, store.  Warp q owns TMEM lanes
+        // 32q..32q+31 (rows 32q.. of both warpgroups' tiles).
+        const int q = warp - W_EPI;
+        uint32_t ke0 = 0, ke1 = 0; // tiles per warpgroup (scalars: no local memory)
+        bool pend_rel = false;
+        int pend_w = 0;
+        uint32_t pend_b = 0;
+        auto release = [&]() { // the previous O store has read its staging buffer
             if (lane == 0) {
                 tma::store_wait_read();
-                mbar_arrive(bar(bars, B_QEMPTY + 2 * w + (int)(tix_prev & 1)));
+                mbar_arrive(bar(bars, B_QEMPTY + 2 * pend_w + (int)pend_b));
             }
             __syncwarp();
             pend_rel = false;
         };
-        // carried-state epilogue (ga_opts.state): this row's (m, l, o~) in the
-        // log2 domain, written or (+)-combined into the caller's fp32 buffers (m is the row's
-        // softmax reference: its running max, or within 2^kTau of it after a lazy rescale —
-        // any reference combines exactly); with p.out also the normalised row
-        auto state_epilogue = [&](uint32_t tO, int32_t c, int32_t h, int32_t x, int32_t alo, int32_t ahi) {
-            const bool valid = x >= alo && x < ahi;
-            const int64_t t = (int64_t)c + (int64_t)x * r - p.q_begin; // local query row
-            const size_t rh = valid ? (size_t)t * H + h : 0;
-            float mm = m_prev, ll = l_prev, a = 1.f, b = 0.f;
-            bool mix = false;
-            if (valid && p.state_mode == GA_STATE_ACCUMULATE) {
-                const float l2 = p.state.l[rh];
-                if (l2 > 0.f) { // l == 0 marks an empty state (its m is ignored)
-                    const float m2 = p.state.m[rh];
-                    const float mn = ll > 0.f ? fmaxf(mm, m2) : m2;
-                    a = ll > 0.f ? ex2(mm - mn) : 0.f;
-                    b = ex2(m2 - mn);
-                    ll = ll * a + l2 * b;
-                    mm = mn;
-                    mix = true;
-                }
-            }
-            const float inv = ll > 0.f ? 1.f / ll : 0.f;
-            float4 *so = reinterpret_cast<float4 *>(p.state.o + rh * D);
-            char *orow = p.out ? reinterpret_cast<char *>(p.out) + (size_t)t * row_bytes + (size_t)h * D * sizeof(T)
-                               : nullptr;
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                float o[32];
-                tmem_ld32(tO + 32 * half, o); // warp-collective: every lane
+        for (int32_t it = it_begin; it < it_end; ++it) {
+#pragma unroll 1
+            for (int w = 0; w < 2; ++w) {
+                const Tile Tq = tile_geo(tp, it, w);
+                if (!Tq.valid) continue;
+                const uint32_t k = w == 0 ? ke0++ : ke1++, b = k & 1u;
+                mbar_wait(bar(bars, B_EPI + 2 * w + (int)b), (k >> 1) & 1);
+                mbar_wait(bar(bars, B_OTILE + 2 * w + (int)b), (k >> 1) & 1);
+                fence_after();
+                TRACE2(18 + w, 0);
+                const int row = 32 * q + lane;
+                const float l = lmbuf[((w * 2 + (int)b) * 2 + 0) * ROWS + row];
+                const float mrow = lmbuf[((w * 2 + (int)b) * 2 + 1) * ROWS + row];
+                const uint32_t tO = tmem + 256u * (uint32_t)w + ((uint32_t)(q * 32) << 16) + COL_O + b * D;
+                float o[64];
+                tmem_ld32(tO, o);
+                tmem_ld32(tO + 32, o + 32);
                 tmem_wait_ld();
-                if (!valid) continue;
+                fence_before();
+                mbar_arrive(bar(bars, B_OFREE + 2 * w + (int)b)); // O buffer and (l, m) read
+                if (pend_rel) release();
+                const int32_t x = Tq.a0 + row;
+                const bool cut = !(Tq.a0 >= Tq.a_lo && Tq.a0 + ROWS <= Tq.a_hi);
+                const bool xv = x >= Tq.a_lo && x < Tq.a_hi;
+                const int64_t t = (int64_t)Tq.c + (int64_t)x * r - p.q_begin; // local query row
+                if (p.state.m) {
+                    // carried state (ga_state): this row's (m, l, o~) in the log2
+                    // domain, written or (+)-combined into the caller's fp32 buffers (m is the
+                    // row's softmax reference: its running max, or within 2^8 of it after a lazy
+                    // rescale — any reference combines exactly); with p.out also the normalised row
+                    if (xv) {
+                        const size_t rh = (size_t)t * H + Tq.h;
+                        float mm = mrow, ll = l, a = 1.f, bb = 0.f;
+                        bool mix = false;
+                        if (p.state_mode == GA_STATE_ACCUMULATE) {
+                            const float l2 = p.state.l[rh];
+                            if (l2 > 0.f) { // l == 0 marks an empty state (its m is ignored)
+                                const float m2 = p.state.m[rh];
+                                const float mn = ll > 0.f ? fmaxf(mm, m2) : m2;
+                                a = ll > 0.f ? ex2(mm - mn) : 0.f;
+                                bb = ex2(m2 - mn);
+                                ll = ll * a + l2 * bb;
+                                mm = mn;
+                                mix = true;
+                            }
+                        }
+                        const float inv = ll > 0.f ? 1.f / ll : 0.f;
+                        float4 *so = reinterpret_cast<float4 *>(p.state.o + rh * D);
+#pragma unroll
+                        for (int qq = 0; qq < 16; ++qq) {
+                            float4 v = make_float4(o[4 * qq], o[4 * qq + 1], o[4 * qq + 2], o[4 * qq + 3]);
+                            if (mix) {
+                                const float4 uu = so[qq];
+                                v.x = v.x * a + uu.x * bb;
+                                v.y = v.y * a + uu.y * bb;
+                                v.z = v.z * a + uu.z * bb;
+                                v.w = v.w * a + uu.w * bb;
+                            }
+                            so[qq] = v;
+                            o[4 * qq] = v.x * inv;
+                            o[4 * qq + 1] = v.y * inv;
+                            o[4 * qq + 2] = v.z * inv;
+                            o[4 * qq + 3] = v.w * inv;
+                        }
+                        if (p.out) {
+                            char *orow = reinterpret_cast<char *>(p.out) + (size_t)t * row_bytes + (size_t)Tq.h * D * sizeof(T);
+#pragma unroll
+                            for (int qq = 0; qq < 8; ++qq) stg16(orow + qq * 16, pack<T>(o + 8 * qq));
+                        }
+                        p.state.m[rh] = mm;
+                        p.state.l[rh] = ll;
+                    }
+                    if (lane == 0) mbar_arrive(bar(bars, B_QEMPTY + 2 * w + (int)b));
+                    __syncwarp();
+                    continue;
+                }
+                const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+                for (int i = 0; i < 64; ++i) o[i] *= inv;
+                if (cut) {
+                    // tile cut by the query range / sequence end: plain stores of valid rows
+                    if (xv) {
+                        char *orow = reinterpret_cast<char *>(p.out) + (size_t)t * row_bytes + (size_t)Tq.h * D * sizeof(T);
+#pragma unroll
+                        for (int qq = 0; qq < 8; ++qq) stg16(orow + qq * 16, pack<T>(o + 8 * qq));
+                    }
+                    if (lane == 0) mbar_arrive(bar(bars, B_QEMPTY + 2 * w + (int)b));
+                    __syncwarp();
+                    continue;
+                }
+                // full tile: stage this warp's 32 rows in the tile's Q buffer (all the tile's S
+                // MMAs completed before the softmax finished) in the TMA layout and store them
+                // with one 32-row box; the buffer goes back to the loader after the store read it
+                const uint32_t sO = sbase + OFF_Q + (uint32_t)(2 * w + (int)b) * QBYTES;
 #pragma unroll
                 for (int qq = 0; qq < 8; ++qq) {
-                    float4 v = make_float4(o[4 * qq], o[4 * qq + 1], o[4 * qq + 2], o[4 * qq + 3]);
-                    if (mix) {
-                        const float4 u = so[8 * half + qq];
-                        v.x = v.x * a + u.x * b;
-                        v.y = v.y * a + u.y * b;
-                        v.z = v.z * a + u.z * b;
-                        v.w = v.w * a + u.w * b;
-                    }
-                    so[8 * half + qq] = v;
-                    o[4 * qq] = v.x * inv;
-                    o[4 * qq + 1] = v.y * inv;
-                    o[4 * qq + 2] = v.z * inv;
-                    o[4 * qq + 3] = v.w * inv;
+                    const uint4 v = pack<T>(o + 8 * qq);
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sO + swz<D>(row, qq)), "r"(v.x),
+                                 "r"(v.y), "r"(v.z), "r"(v.w)
+                                 : "memory");
                 }
-                if (orow) {
-#pragma unroll
-                    for (int qq = 0; qq < 4; ++qq) stg16(orow + (4 * half + qq) * 16, pack<T>(o + 8 * qq));
-                }
-            }
-            if (valid) {
-                p.state.m[rh] = mm;
-                p.state.l[rh] = ll;
-            }
-        };
-        auto epilogue = [&]() {
-            pend_epi = false;
-            // P V of the tile's last chunk completed.  The O barriers alternate per chunk and a
-            // parity wait is exact only if the barrier's previous phase completed: P V(e-2)'s
-            // predecessor P V(e-4) ran before S(e-1) (observed), and P V(e-2) completing implies
-            // P V(e-3), the predecessor of P V(e-1)
-            if (cnt_prev >= 2) wait_O(cnt_prev - 2);
-            wait_O(cnt_prev - 1);
-            TRACE2(18 + w, 0);
-#if GA_WTC_SEPP
-            const uint32_t tO = tl + COL_O;
-#else
-            const uint32_t tO = tl + COL_O + (tix_prev & 1) * D;
-#endif
-            const float inv = l_prev > 0.f ? 1.f / l_prev : 0.f;
-            const Tile Tq = tile_geo(tp, p_it, w);
-            const int32_t p_c = Tq.c, p_h = Tq.h, p_a0 = Tq.a0, p_alo = Tq.a_lo, p_ahi = Tq.a_hi;
-            const int32_t xr0 = p_a0 + 32 * q, x = xr0 + lane;
-            const bool cut = !(p_a0 >= p_alo && p_a0 + ROWS <= p_ahi);
-            // full tile: stage this warp's 32 rows in the tile's Q buffer (the tile's S MMAs
-            // completed) in the TMA layout and store them with one 32-row box, released to the
-            // loader later; tile cut by the query range / sequence end: plain stores of valid rows
-            if (p.state.m) { // carried state (ga_state): fp32 (m, l, o~) per row, plain stores
-                state_epilogue(tO, p_c, p_h, x, p_alo, p_ahi);
-                if (lane == 0) mbar_arrive(bar(bars, B_QEMPTY + 2 * w + (int)(tix_prev & 1)));
+                fence_proxy_async();
                 __syncwarp();
-                return;
-            }
-            const uint32_t sO = sbase + OFF_Q + (uint32_t)(2 * w + (tix_prev & 1)) * QBYTES;
-            char *orow = nullptr;
-            if (cut && x >= p_alo && x < p_ahi)
-                orow = reinterpret_cast<char *>(p.out) + (size_t)((int64_t)p_c + (int64_t)x * r - p.q_begin) * row_bytes +
-                       (size_t)p_h * D * sizeof(T);
-#pragma unroll
-            for (int half = 0; half < 2; ++half) { // 32 columns at a time (register pressure)
-                float o[32];
-                tmem_ld32(tO + 32 * half, o);
-                tmem_wait_ld();
-#pragma unroll
-                for (int qq = 0; qq < 4; ++qq) {
-                    float r8[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) r8[e] = o[8 * qq + e] * inv;
-                    const uint4 v = pack<T>(r8);
-                    if (!cut)
-                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sO + swz<D>(32 * q + lane, 4 * half + qq)),
-                                     "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                                     : "memory");
-                    else if (orow)
-                        stg16(orow + (4 * half + qq) * 16, v);
+                if (lane == 0) {
+                    const int tok = (int)((int64_t)Tq.c + (int64_t)(Tq.a0 + 32 * q) * r - p.q_begin);
+                    tma::store_3d(&tp.tmO, 0, Tq.h, tok, sO + (uint32_t)q * (32 * RB));
+                    tma::store_commit();
                 }
-            }
-            if (cut) {
-                if (lane == 0) mbar_arrive(bar(bars, B_QEMPTY + 2 * w + (int)(tix_prev & 1)));
                 __syncwarp();
-                return;
+                pend_rel = true;
+                pend_w = w;
+                pend_b = b;
             }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                const int tok = (int)((int64_t)p_c + (int64_t)xr0 * r - p.q_begin);
-                tma::store_3d(&tp.tmO, 0, p_h, tok, sO + (uint32_t)q * (32 * RB));
-                tma::store_commit();
-            }
-            pend_rel = true;
-        };
+        }
+        if (pend_rel) release();
+        if (lane == 0) tma::store_wait_all(); // bulk stores complete before the CTA exits
+        __syncwarp();
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REG_SMX));
+        // ============================ softmax warpgroups ============================
+        const int w = warp >> 2, q = warp & 3;
+        const uint32_t tl = tmem + 256u * w + ((uint32_t)(q * 32) << 16); // this warp's TMEM lanes
+        const float sl2 = p.scale_log2;
+        constexpr float kTau = 8.f;
         const int32_t mi = (int32_t)m;
+        uint32_t c = 0; // running chunk counter (matches the issuer's)
+        uint32_t k = 0; // tiles of this warpgroup
         for (int32_t it = it_begin; it < it_end; ++it) {
             const Tile Tt = tile_geo(tp, it, w);
             if (!Tt.valid) continue;
             const int32_t xr0 = Tt.a0 + 32 * q, x = xr0 + lane;
-#if GA_WTC_SEPP
-            const uint32_t tO = tl + COL_O; // this tile's O accumulator
-#else
-            const uint32_t tO = tl + COL_O + (ntile & 1) * D; // this tile's O accumulator
-#endif
+            const uint32_t tO = tl + COL_O + (k & 1u) * D; // this tile's O accumulator
             // keys of this warp's rows: union [ulo, uhi], every row: [ilo, ihi]; this row: [klo, khi]
             const int32_t ulo = max(xr0 - mi, 0), uhi = min(xr0 + 31 + mi, Tt.Nc - 1);
             const int32_t ilo = max(xr0 + 31 - mi, 0), ihi = min(xr0 + mi, Tt.Nc - 1);
             const int32_t klo = max(x - mi, 0), khi = min(x + mi, Tt.Nc - 1);
             float m_run = -INFINITY, l_run = 0.f;
             const int32_t n = Tt.n;
-            for (int32_t j = 0; j < n; ++j) {
-                const uint32_t c = cnt + (uint32_t)j, sb = c % NSB, sph = (c / NSB) & 1;
+            for (int32_t j = 0; j < n; ++j, ++c) {
                 const int32_t kmin = (Tt.F + j) * KC;
-                const uint32_t tS = tl + COL_S + sb * KC; // S of chunk c; P is written over it
-                // S_c is waited for even when skipped: every phase of the S barriers is then
-                // observed in order (a parity wait cannot tell phase k from phase k + 2)
+                // per 32-column half: skipped (no row of the warp reaches it), full (every row
+                // reaches all of it) or cut by the band's edges (warp-uniform)
+                const int32_t h0 = kmin, h1 = kmin + 32;
+                const bool ld0 = !(h0 > uhi || h0 + 31 < ulo), ld1 = !(h1 > uhi || h1 + 31 < ulo);
+                const bool full0 = h0 >= ilo && h0 + 31 <= ihi, full1 = h1 >= ilo && h1 + 31 <= ihi;
                 TRACE(10 + w);
-                mbar_wait(bar(bars, B_SFULL + NSB * w + (int)sb), sph);
+                mbar_wait(bar(bars, B_SFULL + w), c & 1u);
                 fence_after();
                 TRACE(12 + w);
-#if GA_WTC_SEPP
-                const uint32_t tPw = tl + COL_P + (c & 1u) * (KC / 2); // P_c (written after P V_{c-2} read it)
-#else
-                const uint32_t tPw = tS;
-#endif
-                if (kmin > uhi || kmin + KC - 1 < ulo) { // no row of this warp reaches the chunk
-                    uint32_t z[32];
+                float s[64];
+                if (ld0) tmem_ld32(tl + COL_S, s);
+                if (ld1) tmem_ld32(tl + COL_S + 32, s + 32);
+                tmem_wait_ld();
+                fence_before();
+                mbar_arrive(bar(bars, B_SFREE + w)); // the issuer may overwrite S now
+                // masks: left edge inside the half iff the last lane's klo is past its start
+                if (ld0 && !full0)
+                    mask_half(s, klo - h0, khi - h0, max(xr0 + 31 - mi, 0) > h0, min(xr0 + mi, Tt.Nc - 1) < h0 + 31);
+                if (ld1 && !full1)
+                    mask_half(s + 32, klo - h1, khi - h1, max(xr0 + 31 - mi, 0) > h1, min(xr0 + mi, Tt.Nc - 1) < h1 + 31);
+                // chunk max (log2 domain) and lazy rescale: a row moves its reference max only
+                // when the chunk's max exceeds it by more than kTau (weights stay <= 2^kTau); O
+                // needs rescaling only for rows that already hold weight
+                float lm = -INFINITY;
+                if (ld0) lm = max32(s);
+                if (ld1) lm = fmaxf(lm, max32(s + 32));
+                const float lm2 = lm * sl2;
+                const bool need = lm2 > m_run + kTau;
+                const float a = (need && m_run != -INFINITY) ? ex2(m_run - lm2) : 1.f;
+                if (__any_sync(0xffffffffu, a != 1.f) && j > 0) {
+                    // O stable: P V of the previous chunk completed
+                    mbar_wait(bar(bars, B_OFULL + 2 * w + (int)((c - 1) & 1)), ((c - 1) >> 1) & 1);
+                    fence_after();
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) z[i] = 0u;
-#if GA_WTC_SEPP
-                    if (c >= 2) wait_O(c - 2);
-#endif
-                    tmem_st32(tPw, z);
+                    for (int qq = 0; qq < D / 16; ++qq) { // 16 columns at a time (registers)
+                        uint32_t ov[16];
+                        tmem_ld16(tO + 16 * qq, ov);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * a);
+                        tmem_st16(tO + 16 * qq, ov);
+                    }
                     tmem_wait_st();
-                    if (pend_epi) epilogue(); // see below
-                    fence_before();
-                    mbar_arrive(bar(bars, B_PFULL + NSB * w + (int)sb));
-                } else {
-                    float sv[KC];
-                    tmem_ld32(tS, sv);
-                    tmem_ld32(tS + 32, sv + 32);
-                    tmem_wait_ld();
-                    if (!(kmin >= ilo && kmin + KC - 1 <= ihi)) { // partial: keep only this row's band
-                        const int il = max(klo - kmin, -1), ih = min(khi - kmin, KC);
-                        if (__any_sync(0xffffffffu, il > 0)) { // left edge of the band inside the chunk
-#pragma unroll
-                            for (int i = 0; i < KC; ++i) sv[i] = i >= il ? sv[i] : -INFINITY;
-                        }
-                        if (__any_sync(0xffffffffu, ih < KC - 1)) { // right edge
-#pragma unroll
-                            for (int i = 0; i < KC; ++i) sv[i] = i <= ih ? sv[i] : -INFINITY;
-                        }
-                    }
-                    uint32_t pk[KC / 2];
-                    auto exps = [&]() -> float { // pk = P (input type); returns the row's chunk sum
-                        const float m_use = m_run == -INFINITY ? 0.f : m_run;
-                        float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; // packed partial sums
-#pragma unroll
-                        for (int i = 0; i < KC / 2; ++i) {
-                            float x0 = sv[2 * i], x1 = sv[2 * i + 1];
-                            ffma2_sm(x0, x1, sl2, -m_use);
-                            x0 = ex2(x0);
-                            x1 = ex2(x1);
-                            fadd2_acc(ls[i & 1], x0, x1);
-                            pk[i] = pack2<T>(x0, x1);
-                        }
-                        return (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
-                    };
-                    // fast path once every row of the warp holds a reference max: weights against
-                    // it first; a rescale is needed iff some weight exceeds 2^kTau, which a chunk
-                    // sum <= 2^kTau rules out (then the chunk max is never computed); otherwise the
-                    // careful path repeats the chunk exactly as before (bit-identical results)
-                    bool fast = false;
-                    if (__all_sync(0xffffffffu, m_run != -INFINITY)) {
-                        const float lsum = exps();
-                        if (!__any_sync(0xffffffffu, !(lsum <= 256.f))) { // 2^kTau; NaN/inf -> careful
-                            l_run += lsum;
-                            fast = true;
-                        }
-                    }
-                    if (!fast) {
-                        float lmx[8];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) lmx[i] = sv[i];
-#pragma unroll
-                        for (int i = 8; i < KC; ++i) lmx[i & 7] = fmaxf(lmx[i & 7], sv[i]);
-                        const float lm = fmaxf(fmaxf(fmaxf(lmx[0], lmx[1]), fmaxf(lmx[2], lmx[3])),
-                                               fmaxf(fmaxf(lmx[4], lmx[5]), fmaxf(lmx[6], lmx[7])));
-                        // lazy rescale: a row moves its reference max only when the chunk's max exceeds
-                        // it by more than kTau (weights stay <= 2^kTau); O needs rescaling only for rows
-                        // that already hold weight (a row with m = -inf has O = 0 and l = 0)
-                        const float lm2 = lm * sl2;
-                        const bool need = lm2 > m_run + kTau;
-                        const float a = (need && m_run != -INFINITY) ? ex2(m_run - lm2) : 1.f;
-                        if (__any_sync(0xffffffffu, a != 1.f) && j > 0) {
-                            wait_O(c - 1); // O stable: P V of the previous chunk completed
-                            float ov[32];
-#pragma unroll
-                            for (int qq = 0; qq < D / 32; ++qq) {
-                                tmem_ld32(tO + 32 * qq, ov);
-                                tmem_wait_ld();
-                                uint32_t ob[32];
-#pragma unroll
-                                for (int i = 0; i < 32; ++i) ob[i] = __float_as_uint(ov[i] * a);
-                                tmem_st32(tO + 32 * qq, ob);
-                            }
-                            tmem_wait_st();
-                        }
-                        if (need) {
-                            l_run *= a;
-                            m_run = lm2;
-                        }
-                        l_run += exps();
-                    }
-#if GA_WTC_SEPP
-                    if (c >= 2) wait_O(c - 2);
-#endif
-                    tmem_st32(tPw, pk);
-                    tmem_wait_st();
-                    // the previous tile's epilogue with this tile's first chunk (its last P V has
-                    // long completed), BEFORE P of this chunk is released: P V of this chunk could
-                    // otherwise complete a second phase of the O barrier the epilogue waits on
-                    if (pend_epi) epilogue();
-                    fence_before();
-                    mbar_arrive(bar(bars, B_PFULL + NSB * w + (int)sb));
-                    TRACE(14 + w);
                 }
-                // the staging buffer goes back to the loader one chunk after the store
-                if (pend_rel && j > 0) release();
+                if (need) {
+                    l_run *= a;
+                    m_run = lm2;
+                }
+                const float negm = m_run == -INFINITY ? 0.f : -m_run;
+                // P buffer c & 1 is free once P V(c - 2) completed
+                if (c >= 2) mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(c & 1)), ((c - 2) >> 1) & 1);
+                fence_after();
+                const uint32_t tP = tl + COL_P + (c & 1u) * (KC / 2);
+                float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                 make_float2(0.f, 0.f)};
+                uint32_t pk[16];
+                if (ld0) {
+                    exps_half<T>(s, sl2, negm, pk, acc);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) pk[i] = 0u;
+                }
+                tmem_st16(tP, pk);
+                if (ld1) {
+                    exps_half<T>(s + 32, sl2, negm, pk, acc);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) pk[i] = 0u;
+                }
+                tmem_st16(tP + 16, pk);
+                l_run += (acc[0].x + acc[1].x) + (acc[2].x + acc[3].x) + ((acc[0].y + acc[1].y) + (acc[2].y + acc[3].y));
+                tmem_wait_st();
+                fence_before();
+                mbar_arrive(bar(bars, B_PFULL + 2 * w + (int)(c & 1)));
+                TRACE(14 + w);
             }
-            if (pend_epi) epilogue(); // (n >= 1: not reached)
-            if (pend_rel) release();  // one-chunk tile
-            cnt += (uint32_t)n;
-            pend_epi = true;
-            p_it = it;
-            l_prev = l_run;
-            m_prev = m_run;
-            cnt_prev = cnt;
-            tix_prev = ntile;
-            ++ntile;
-#ifndef GA_WTC_DEFER_EPILOGUE
-            // epilogue right away (measured faster than deferring it into the next tile, which
-            // needs more registers); O is still double-buffered, so the next tile's first P V
-            // never waits for these TMEM reads
-            epilogue();
-#endif
+            // row sum and reference max for the epilogue (its read of the previous use of
+            // this buffer, tile k - 2, completed before it released O[k & 1])
+            if (k >= 2) mbar_wait(bar(bars, B_OFREE + 2 * w + (int)(k & 1)), ((k - 2) >> 1) & 1);
+            const int row = 32 * q + lane;
+            lmbuf[((w * 2 + (int)(k & 1)) * 2 + 0) * ROWS + row] = l_run;
+            lmbuf[((w * 2 + (int)(k & 1)) * 2 + 1) * ROWS + row] = m_run;
+            mbar_arrive(bar(bars, B_EPI + 2 * w + (int)(k & 1)));
+            ++k;
         }
-        if (pend_epi) epilogue();
-        if (pend_rel) release();
-        if (lane == 0) tma::store_wait_all(); // bulk stores complete before the CTA exits
-        __syncwarp();
     }
     fence_before();
     __syncthreads();

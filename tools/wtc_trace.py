@@ -12,7 +12,7 @@ import torch  # noqa: E402
 
 import paper_2502_01659_b200 as ga  # noqa: E402
 
-L, H, w, r = 65536, 8, 256, 2
+L, H, w, r = (int(x) for x in os.environ.get("WTC_SHAPE", "65536,8,256,2").split(","))
 q, k, v = ga.qkv_device(1, L, H, 64, torch.bfloat16)
 m = ga.Window(w, r)
 lib = ga._abi.lib()
