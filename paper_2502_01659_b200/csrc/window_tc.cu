@@ -96,8 +96,52 @@ struct TcParams {
 
 __host__ __device__ inline int64_t floordiv(int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
-// Geometry of one work item (a pair of consecutive 128-row tiles of one stream); every role
-// derives it independently from the item index, so all agree without communication.
+// Position of a work item (a pair of consecutive 128-row tiles of one (class, head) stream).
+// A CTA walks a contiguous run of items, so every role keeps a cursor and advances it: the
+// divisions by runtime values (items per stream, heads, dilation) run once per stream, not per
+// tile — on sm_100 they use MUFU.RCP, which the softmax warps' exponentials keep busy.
+struct Cur {
+    int32_t st, u, c, h;    // stream = class * H + head, pair index in the stream
+    int32_t Nc, a_lo, a_hi; // class rows, query class rows [a_lo, a_hi)
+};
+
+__device__ __forceinline__ void cur_stream(const TcParams &tp, Cur &C)
+{
+    const AttnParams &p = tp.p;
+    const uint32_t r = (uint32_t)tp.r, L = (uint32_t)p.mask.L, c = (uint32_t)C.c;
+    const uint32_t Nc = c < L ? (L - c + r - 1) / r : 0;
+    const uint32_t qb = (uint32_t)p.q_begin, qe = (uint32_t)(p.q_begin + p.q_rows);
+    C.Nc = (int32_t)Nc;
+    C.a_lo = (int32_t)(qb > c ? (qb - c + r - 1) / r : 0);
+    C.a_hi = (int32_t)(qe > c ? min((qe - c + r - 1) / r, Nc) : 0);
+}
+
+__device__ __forceinline__ Cur cur_init(const TcParams &tp, int32_t it)
+{
+    // 32-bit arithmetic throughout: L < 2^31 (window_tc_supported)
+    const uint32_t H = (uint32_t)tp.p.H, pps = (uint32_t)tp.pps, iu = (uint32_t)it, st = iu / pps;
+    Cur C;
+    C.st = (int32_t)st;
+    C.u = (int32_t)(iu - st * pps);
+    C.c = (int32_t)(st / H);
+    C.h = (int32_t)(st - (uint32_t)C.c * H);
+    cur_stream(tp, C);
+    return C;
+}
+
+__device__ __forceinline__ void cur_next(const TcParams &tp, Cur &C)
+{
+    if (++C.u == (int32_t)tp.pps) {
+        C.u = 0;
+        ++C.st;
+        if (++C.h == tp.p.H) {
+            C.h = 0;
+            ++C.c;
+            cur_stream(tp, C);
+        }
+    }
+}
+
 struct Pair {
     int32_t stream, u, c, Nc, a_lo, a_hi;
     int h;
@@ -108,36 +152,26 @@ struct Pair {
     bool any;
 };
 
-__device__ __forceinline__ Pair pair_geo(const TcParams &tp, int32_t it)
+__device__ __forceinline__ Pair pair_at(const TcParams &tp, const Cur &C)
 {
-    // 32-bit arithmetic throughout: L < 2^31 (window_tc_supported), so class rows, tiles and
-    // item indices fit; 64-bit division would cost hundreds of instructions per item
-    const AttnParams &p = tp.p;
-    const uint32_t r = (uint32_t)tp.r, L = (uint32_t)p.mask.L, H = (uint32_t)p.H, pps = (uint32_t)tp.pps;
     const int32_t m = (int32_t)tp.m;
     Pair P;
-    const uint32_t iu = (uint32_t)it, st = iu / pps;
-    P.stream = st;
-    P.u = iu - st * pps;
-    const uint32_t c = st / H;
-    P.c = c;
-    P.h = (int)(st - c * H);
-    const uint32_t Nc = c < L ? (L - c + r - 1) / r : 0;
-    P.Nc = Nc;
-    const uint32_t qb = (uint32_t)p.q_begin, qe = (uint32_t)(p.q_begin + p.q_rows);
-    const uint32_t a_lo = qb > c ? (qb - c + r - 1) / r : 0;
-    const uint32_t a_hi = qe > c ? min((qe - c + r - 1) / r, Nc) : 0;
-    P.a_lo = a_lo;
-    P.a_hi = a_hi;
-    const int32_t t0 = (int32_t)(a_lo / ROWS + 2 * (uint32_t)P.u);
-    const int32_t lastc = ((int32_t)Nc - 1) >> 6; // KC = 64
+    P.stream = C.st;
+    P.u = C.u;
+    P.c = C.c;
+    P.h = C.h;
+    P.Nc = C.Nc;
+    P.a_lo = C.a_lo;
+    P.a_hi = C.a_hi;
+    const int32_t t0 = (C.a_lo >> 7) + 2 * C.u; // ROWS = 128
+    const int32_t lastc = (C.Nc - 1) >> 6;       // KC = 64
     P.lo = INT32_MAX;
     P.hi = -1;
 #pragma unroll
     for (int w = 0; w < 2; ++w) {
         const int32_t a0 = (t0 + w) * ROWS;
         P.a0[w] = a0;
-        P.valid[w] = a_lo < a_hi && (uint32_t)a0 < a_hi;
+        P.valid[w] = C.a_lo < C.a_hi && a0 < C.a_hi;
         // floor((a0 - m) / 64) by arithmetic shift (exact for negative values too)
         const int32_t f = max((a0 - m) >> 6, 0), e = min((a0 + ROWS - 1 + m) >> 6, lastc);
         P.F[w] = f;
@@ -158,27 +192,19 @@ struct Tile {
     bool valid;
 };
 
-__device__ __forceinline__ Tile tile_geo(const TcParams &tp, int32_t it, int w)
+__device__ __forceinline__ Tile tile_at(const TcParams &tp, const Cur &C, int w)
 {
-    const AttnParams &p = tp.p;
-    const uint32_t r = (uint32_t)tp.r, L = (uint32_t)p.mask.L, H = (uint32_t)p.H, pps = (uint32_t)tp.pps;
     const int32_t m = (int32_t)tp.m;
     Tile T;
-    const uint32_t iu = (uint32_t)it, st = iu / pps, u = iu - st * pps;
-    const uint32_t c = st / H;
-    T.c = (int32_t)c;
-    T.h = (int32_t)(st - c * H);
-    const uint32_t Nc = c < L ? (L - c + r - 1) / r : 0;
-    const uint32_t qb = (uint32_t)p.q_begin, qe = (uint32_t)(p.q_begin + p.q_rows);
-    const uint32_t a_lo = qb > c ? (qb - c + r - 1) / r : 0;
-    const uint32_t a_hi = qe > c ? min((qe - c + r - 1) / r, Nc) : 0;
-    T.Nc = (int32_t)Nc;
-    T.a_lo = (int32_t)a_lo;
-    T.a_hi = (int32_t)a_hi;
-    T.a0 = (int32_t)((a_lo / ROWS + 2 * u + (uint32_t)w) * ROWS);
-    T.valid = a_lo < a_hi && (uint32_t)T.a0 < a_hi;
+    T.c = C.c;
+    T.h = C.h;
+    T.Nc = C.Nc;
+    T.a_lo = C.a_lo;
+    T.a_hi = C.a_hi;
+    T.a0 = ((C.a_lo >> 7) + 2 * C.u + w) * ROWS;
+    T.valid = C.a_lo < C.a_hi && T.a0 < C.a_hi;
     T.F = max((T.a0 - m) >> 6, 0);
-    T.n = T.valid ? min((T.a0 + ROWS - 1 + m) >> 6, ((int32_t)Nc - 1) >> 6) - T.F + 1 : 0;
+    T.n = T.valid ? min((T.a0 + ROWS - 1 + m) >> 6, (C.Nc - 1) >> 6) - T.F + 1 : 0;
     return T;
 }
 
@@ -301,8 +327,9 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         uint32_t used = 0, par = 0;
         int nq[2] = {0, 0};
         int32_t prev_stream = -1, prev_u = -1, prev_hi = -1;
-        for (int32_t it = it_begin; it < it_end; ++it) {
-            const Pair P = pair_geo(tp, it);
+        Cur C = cur_init(tp, it_begin);
+        for (int32_t it = it_begin; it < it_end; ++it, cur_next(tp, C)) {
+            const Pair P = pair_at(tp, C);
             if (!P.any) continue;
             // Q tiles
 #pragma unroll
@@ -401,11 +428,13 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         bool pre = false, preq = false; // S(0) of this item's tile already issued / its Q waited
         int32_t prev_stream = -1, prev_u = -1, prev_lo = 0;
         uint32_t waited = 0; // fills this issuer observed, bit g - lo of the previous item
-        Pair N = pair_geo(tp, it_begin);
+        Cur C = cur_init(tp, it_begin);
+        Pair N = pair_at(tp, C);
         for (int32_t it = it_begin; it < it_end; ++it) {
             const Pair P = N;
             const bool has_next = it + 1 < it_end;
-            if (has_next) N = pair_geo(tp, it + 1);
+            cur_next(tp, C);
+            if (has_next) N = pair_at(tp, C);
             if (!P.any) continue;
             const bool cont = P.stream == prev_stream && P.u == prev_u + 1;
             const bool next_cont = has_next && N.any && N.stream == P.stream && N.u == P.u + 1;
@@ -534,10 +563,11 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             __syncwarp();
             pend_rel = false;
         };
-        for (int32_t it = it_begin; it < it_end; ++it) {
+        Cur C = cur_init(tp, it_begin);
+        for (int32_t it = it_begin; it < it_end; ++it, cur_next(tp, C)) {
 #pragma unroll 1
             for (int w = 0; w < 2; ++w) {
-                const Tile Tq = tile_geo(tp, it, w);
+                const Tile Tq = tile_at(tp, C, w);
                 if (!Tq.valid) continue;
                 const uint32_t k = w == 0 ? ke0++ : ke1++, b = k & 1u;
                 mbar_wait(bar(bars, B_EPI + 2 * w + (int)b), (k >> 1) & 1);
@@ -661,8 +691,9 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         const int32_t mi = (int32_t)m;
         uint32_t c = 0; // running chunk counter (matches the issuer's)
         uint32_t k = 0; // tiles of this warpgroup
-        for (int32_t it = it_begin; it < it_end; ++it) {
-            const Tile Tt = tile_geo(tp, it, w);
+        Cur C = cur_init(tp, it_begin);
+        for (int32_t it = it_begin; it < it_end; ++it, cur_next(tp, C)) {
+            const Tile Tt = tile_at(tp, C, w);
             if (!Tt.valid) continue;
             const int32_t xr0 = Tt.a0 + 32 * q, x = xr0 + lane;
             const uint32_t tO = tl + COL_O + (k & 1u) * D; // this tile's O accumulator
@@ -723,9 +754,8 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     m_run = lm2;
                 }
                 const float negm = m_run == -INFINITY ? 0.f : -m_run;
-                // P buffer c & 1 is free once P V(c - 2) completed
-                if (c >= 2) mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(c & 1)), ((c - 2) >> 1) & 1);
-                fence_after();
+                // P buffer c & 1 is free: P V(c - 2) completed, since the issuer committed S(c) (waited
+                // above) after issuing P V(c - 2), and a commit tracks every prior MMA of the thread
                 const uint32_t tP = tl + COL_P + (c & 1u) * (KC / 2);
                 float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                                  make_float2(0.f, 0.f)};
@@ -752,7 +782,9 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             }
             // row sum and reference max for the epilogue (its read of the previous use of
             // this buffer, tile k - 2, completed before it released O[k & 1])
+            TRACE(16 + w);
             if (k >= 2) mbar_wait(bar(bars, B_OFREE + 2 * w + (int)(k & 1)), ((k - 2) >> 1) & 1);
+            TRACE(22 + w);
             const int row = 32 * q + lane;
             lmbuf[((w * 2 + (int)(k & 1)) * 2 + 0) * ROWS + row] = l_run;
             lmbuf[((w * 2 + (int)(k & 1)) * 2 + 1) * ROWS + row] = m_run;

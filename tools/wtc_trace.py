@@ -26,9 +26,9 @@ ga.attention(q, k, v, m, kernel="tc")
 torch.cuda.synchronize()
 n = lib.ga_wtc_trace_read(buf, N)
 ev = sorted(((b & 0xffffffffff), (b >> 48) & 0xff, (b >> 40) & 0xff, b >> 56) for b in buf[:n] if b)
-names = {1: "mma: kv chunk landed", 3: "mma: P_A arrived", 4: "mma: P_B arrived", 6: "mma: S_A issued",
-         7: "mma: S_B issued", 10: "smx A: wait S start", 11: "smx B: wait S start", 12: "smx A: S ready",
-         13: "smx B: S ready", 14: "smx A: P arrive", 15: "smx B: P arrive", 16: "smx A: epilogue", 17: "smx B: epilogue", 18: "smx A: O ready", 19: "smx B: O ready", 30: "mma: item done (iterations)", 40: "mma: S issue begin", 42: "mma: P test (iter)", 21: "loader: wants slot", 20: "loader: slot free"}
+names = {3: "mma: P arrived", 6: "mma: S issued", 10: "smx A: wait S start", 11: "smx B: wait S start", 12: "smx A: S ready",
+         13: "smx B: S ready", 14: "smx A: P arrive", 15: "smx B: P arrive", 18: "epi: A tile ready", 19: "epi: B tile ready",
+         20: "loader: fill issued", 16: "smx A: tile end", 17: "smx B: tile end", 22: "smx A: OFREE ok", 23: "smx B: OFREE ok", 21: "loader: wants slot"}
 print(f"{n} events, span {ev[-1][0] - ev[0][0]} cycles")
 last = {}
 gaps = defaultdict(list)
