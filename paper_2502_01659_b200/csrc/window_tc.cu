@@ -68,17 +68,17 @@ constexpr uint32_t OFF_BAR = OFF_LM + 2 * 2 * 2 * ROWS * 4;
 constexpr uint32_t SMEM_BYTES = 1024 + OFF_BAR + 64 * 8;
 static_assert(SMEM_BYTES <= 232448, "shared memory");
 
-// TMEM columns within a warpgroup's 256
-constexpr uint32_t COL_S = 0, COL_P = 64, COL_O = 128;
+// TMEM columns within a warpgroup's 256: S[2] (P of chunk c is written over the first 32
+// columns of S[c & 1]), O[2]
+constexpr uint32_t COL_S = 0, COL_O = 128;
 
 // mbarrier indices (8 bytes each from OFF_BAR); [w] = softmax warpgroup, [b] = buffer parity
 constexpr int B_QFULL = 0,             // [w][b] (loader TMA)
     B_QEMPTY = 4,                      // [w][b] 4 epilogue warps: O store read the staging buffer
     B_KVFULL = 8,                      // [slot]
     B_KVEMPTY = B_KVFULL + NSLOT,      // [slot] 2 issuers
-    B_SFULL = B_KVEMPTY + NSLOT,       // [w] S MMA committed
-    B_SFREE = B_SFULL + 2,             // [w] 128 softmax threads read S
-    B_PFULL = B_SFREE + 2,             // [w][c & 1] 128 softmax threads wrote P
+    B_SFULL = B_KVEMPTY + NSLOT,       // [w][c & 1] S MMA committed
+    B_PFULL = B_SFULL + 4,             // [w][c & 1] 128 softmax threads read S and wrote P
     B_OFULL = B_PFULL + 4,             // [w][c & 1] P V MMA committed
     B_OTILE = B_OFULL + 4,             // [w][k & 1] last P V of tile k committed
     B_EPI = B_OTILE + 4,               // [w][k & 1] 128 softmax threads wrote (l, m) of tile k
@@ -299,10 +299,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             mbar_init(bar(bars, B_EPI + i), 128);
             mbar_init(bar(bars, B_OFREE + i), 128);
         }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(bar(bars, B_SFULL + i), 1);
-            mbar_init(bar(bars, B_SFREE + i), 128);
-        }
+        for (int i = 0; i < 4; ++i) mbar_init(bar(bars, B_SFULL + i), 1);
         for (int s = 0; s < NSLOT; ++s) {
             mbar_init(bar(bars, B_KVFULL + s), 1);
             mbar_init(bar(bars, B_KVEMPTY + s), 2); // both issuers release every fill
@@ -425,7 +422,8 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         int nq = 0;             // Q tiles waited
         uint32_t cs = 0;        // S MMAs issued (chunk counter of the warpgroup)
         uint32_t k = 0;         // tiles of the warpgroup (O buffer parity)
-        bool pre = false, preq = false; // S(0) of this item's tile already issued / its Q waited
+        int pre = 0;            // S MMAs of this item's tile already issued (end of the previous item)
+        bool preq = false;      // ... and its Q tile waited for
         int32_t prev_stream = -1, prev_u = -1, prev_lo = 0;
         uint32_t waited = 0; // fills this issuer observed, bit g - lo of the previous item
         Cur C = cur_init(tp, it_begin);
@@ -471,20 +469,23 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             // chunks of the item below this tile's range that the next item does not keep
             for (int32_t g = P.lo; g < (n ? f : P.hi + 1) && g < keep_from; ++g) release_unread(g);
             auto issue_S = [&](uint32_t c, int32_t g, int qbuf) {
-                if (c > 0) mbar_wait(bar(bars, B_SFREE + w), (c - 1) & 1u); // S(c-1) read
+                // S buffer c & 1 held S / P of chunk c - 2: free once P V(c - 2) completed
+                if (c >= 2) mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(c & 1)), ((c - 2) >> 1) & 1);
                 fence_after();
                 const uint32_t aq = sbase + OFF_Q + (uint32_t)(2 * w + qbuf) * QBYTES;
                 const uint32_t ak = sbase + OFF_KV + ((uint32_t)g % NSLOT) * 2 * CBYTES;
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk)
-                        mma_ss(tw + COL_S, dbase | ((aq + kk * 32) >> 4), dbase | ((ak + kk * 32) >> 4), idS, kk > 0);
-                    mma_commit(bar(bars, B_SFULL + w));
+                        mma_ss(tw + COL_S + (c & 1u) * KC, dbase | ((aq + kk * 32) >> 4), dbase | ((ak + kk * 32) >> 4),
+                               idS, kk > 0);
+                    mma_commit(bar(bars, B_SFULL + 2 * w + (int)(c & 1)));
                 }
                 __syncwarp();
                 TRACE2(6, g);
             };
-            const uint32_t c0 = cs - (pre ? 1u : 0u); // chunk counter of this tile's chunk 0
+            const uint32_t c0 = cs - (uint32_t)pre; // chunk counter of this tile's chunk 0
+            int32_t si = pre;                       // S MMAs of this tile issued
             auto issue_PV = [&](int32_t j) {
                 const uint32_t c = c0 + (uint32_t)j;
                 const int32_t g = f + j;
@@ -494,7 +495,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 fence_after();
                 const int sl = (int)((uint32_t)g % NSLOT);
                 const uint32_t av = sbase + OFF_KV + (uint32_t)sl * 2 * CBYTES + CBYTES;
-                const uint32_t tP = tw + COL_P + (c & 1u) * (KC / 2);
+                const uint32_t tP = tw + COL_S + (c & 1u) * KC;
                 const uint32_t tO = tw + COL_O + (k & 1u) * D;
                 const bool release = g < keep_from; // each chunk is read once per tile
                 if (elect_one()) {
@@ -507,33 +508,37 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 }
                 __syncwarp();
             };
+            // next tile's first S MMAs (chunks resident, Q landed): issued at the end of this tile
+            int npre = 0;
+            bool nqw = false;
+            const bool nvalid = n > 0 && next_cont && (w == 0 ? N.valid[0] : N.valid[1]);
+            const int32_t nf = w == 0 ? N.F[0] : N.F[1], nn = w == 0 ? N.n[0] : N.n[1];
+            auto prefetch = [&](int jn) {
+                if (!nvalid || jn >= nn || npre != jn) return;
+                const int32_t g = nf + jn;
+                if (g > P.hi || !((ready >> (int)(g - P.lo)) & 1u)) return;
+                if (!nqw) {
+                    const uint32_t qf = bar(bars, B_QFULL + 2 * w + (nq & 1));
+                    if (!mbar_test(qf, (nq >> 1) & 1)) return;
+                    ++nq;
+                    nqw = true;
+                }
+                issue_S(cs, g, (nq - 1) & 1);
+                ++cs;
+                ++npre;
+            };
             for (int32_t j = 0; j < n; ++j) {
-                if (j > 0 || !pre) {
-                    chunk_ready(f + j);
-                    issue_S(cs, f + j, qb);
+                // S two chunks ahead of the softmax (S[2] in TMEM)
+                for (; si <= min(j + 1, n - 1); ++si) {
+                    chunk_ready(f + si);
+                    issue_S(cs, f + si, qb);
                     ++cs;
                 }
-                if (j > 0) issue_PV(j - 1);
+                if (j == n - 1) prefetch(0);
+                issue_PV(j);
             }
-            // next tile's first S before this tile's last P V (its chunk is resident)
-            bool npre = false, nqw = false;
-            if (n > 0 && next_cont && (w == 0 ? N.valid[0] : N.valid[1])) {
-                const int32_t g = w == 0 ? N.F[0] : N.F[1];
-                if (g <= P.hi && ((ready >> (int)(g - P.lo)) & 1u)) {
-                    const uint32_t qf = bar(bars, B_QFULL + 2 * w + (nq & 1));
-                    if (mbar_test(qf, (nq >> 1) & 1)) {
-                        ++nq;
-                        nqw = true;
-                        issue_S(cs, g, (nq - 1) & 1);
-                        ++cs;
-                        npre = true;
-                    }
-                }
-            }
-            if (n > 0) {
-                issue_PV(n - 1);
-                ++k;
-            }
+            if (n > 0) ++k;
+            prefetch(1);
             // chunks above this tile's range that the next item does not keep
             for (int32_t g = (n ? f + n : P.hi + 1); g <= P.hi && g < keep_from; ++g) release_unread(g);
             pre = npre;
@@ -711,15 +716,14 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 const bool ld0 = !(h0 > uhi || h0 + 31 < ulo), ld1 = !(h1 > uhi || h1 + 31 < ulo);
                 const bool full0 = h0 >= ilo && h0 + 31 <= ihi, full1 = h1 >= ilo && h1 + 31 <= ihi;
                 TRACE(10 + w);
-                mbar_wait(bar(bars, B_SFULL + w), c & 1u);
+                mbar_wait(bar(bars, B_SFULL + 2 * w + (int)(c & 1)), (c >> 1) & 1);
                 fence_after();
                 TRACE(12 + w);
+                const uint32_t tS = tl + COL_S + (c & 1u) * KC; // S(c); P(c) is written over it
                 float s[64];
-                if (ld0) tmem_ld32(tl + COL_S, s);
-                if (ld1) tmem_ld32(tl + COL_S + 32, s + 32);
+                if (ld0) tmem_ld32(tS, s);
+                if (ld1) tmem_ld32(tS + 32, s + 32);
                 tmem_wait_ld();
-                fence_before();
-                mbar_arrive(bar(bars, B_SFREE + w)); // the issuer may overwrite S now
                 // masks: left edge inside the half iff the last lane's klo is past its start
                 if (ld0 && !full0)
                     mask_half(s, klo - h0, khi - h0, max(xr0 + 31 - mi, 0) > h0, min(xr0 + mi, Tt.Nc - 1) < h0 + 31);
@@ -754,9 +758,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     m_run = lm2;
                 }
                 const float negm = m_run == -INFINITY ? 0.f : -m_run;
-                // P buffer c & 1 is free: P V(c - 2) completed, since the issuer committed S(c) (waited
-                // above) after issuing P V(c - 2), and a commit tracks every prior MMA of the thread
-                const uint32_t tP = tl + COL_P + (c & 1u) * (KC / 2);
+                const uint32_t tP = tS;
                 float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                                  make_float2(0.f, 0.f)};
                 uint32_t pk[16];
