@@ -248,14 +248,28 @@ __device__ __forceinline__ float max32(const float *s)
     return fmaxf(fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3])), fmaxf(fmaxf(a[4], a[5]), fmaxf(a[6], a[7])));
 }
 
-// P of one 32-column half: pk = pack(2^(s * sl2 - m)) (16 words), row-sum partials in acc
-template <typename T>
+// P of one 32-column half: pk = pack(2^(s * sl2 - m)) (16 words), row-sum partials in acc.
+// With POLY > 0 the first POLY pairs take 2^x from a degree-3 polynomial on the FMA pipe
+// (ex2_poly2, relative error 7.6e-5, below the bf16/fp16 rounding of P) instead of MUFU, which
+// the two softmax warps of a sub-partition share; only for halves without masked keys
+// (ex2_poly2 maps -inf to 2^-126, not 0).
+#ifndef GA_WTC_POLY
+#define GA_WTC_POLY 0
+#endif
+template <typename T, int POLY>
 __device__ __forceinline__ void exps_half(float *s, float sl2, float negm, uint32_t *pk, float2 *acc)
 {
 #pragma unroll
     for (int i = 0; i < 16; ++i) ffma2_sm(s[2 * i], s[2 * i + 1], sl2, negm);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) s[i] = ex2(s[i]);
+    for (int i = 0; i < 16; ++i) {
+        if (i < POLY) {
+            ex2_poly2(s[2 * i], s[2 * i + 1]);
+        } else {
+            s[2 * i] = ex2(s[2 * i]);
+            s[2 * i + 1] = ex2(s[2 * i + 1]);
+        }
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         fadd2_acc(acc[i & 3], s[2 * i], s[2 * i + 1]);
@@ -763,14 +777,16 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                                  make_float2(0.f, 0.f)};
                 uint32_t pk[16];
                 if (ld0) {
-                    exps_half<T>(s, sl2, negm, pk, acc);
+                    if (full0) exps_half<T, GA_WTC_POLY>(s, sl2, negm, pk, acc);
+                    else exps_half<T, 0>(s, sl2, negm, pk, acc);
                 } else {
 #pragma unroll
                     for (int i = 0; i < 16; ++i) pk[i] = 0u;
                 }
                 tmem_st16(tP, pk);
                 if (ld1) {
-                    exps_half<T>(s + 32, sl2, negm, pk, acc);
+                    if (full1) exps_half<T, GA_WTC_POLY>(s + 32, sl2, negm, pk, acc);
+                    else exps_half<T, 0>(s + 32, sl2, negm, pk, acc);
                 } else {
 #pragma unroll
                     for (int i = 0; i < 16; ++i) pk[i] = 0u;
