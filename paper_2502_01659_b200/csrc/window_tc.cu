@@ -41,6 +41,8 @@
 // tile k + 1.  A CTA walks a contiguous run of tile pairs of one (class, head) stream:
 // consecutive pairs share 4 of their 8 chunks, which stay resident (each K/V row is read from
 // L2/HBM about once per run).
+#include <cstdlib>
+
 #include "tc_common.cuh"
 #include "tma.cuh"
 #include "umma.cuh"
@@ -901,7 +903,10 @@ ga_status launch_window_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s)
         set_error("tcgen05 window kernel: tensor-map encoding failed");
         return GA_ERR_UNSUPPORTED;
     }
-    const int64_t grid = imin(wtc::sm_count(), tp.items);
+    int64_t grid = imin(wtc::sm_count(), tp.items);
+    // debug: fewer CTAs, so each walks a long run of items (sanitizer coverage of the cursor,
+    // the ring reuse and the cross-item S prefetch at small shapes)
+    if (const char *e = getenv("GA_WTC_GRID")) grid = imax(1, imin(grid, (int64_t)atoi(e)));
     return dt == GA_BF16 ? wtc::launch_t<__nv_bfloat16>(tp, grid, s) : wtc::launch_t<__half>(tp, grid, s);
 }
 

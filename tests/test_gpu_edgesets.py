@@ -114,6 +114,28 @@ def test_window_tc_exact_edges(ga, orc, L, w, r, dt):
     run_counts(ga, orc, ga.Window(w, r), orc.window(L, w, r), L, 2, 64, dt, kernel="tc")
 
 
+@pytest.mark.parametrize("grid,L,w,r", [(1, 9001, 200, 2), (3, 20000, 128, 1), (7, 30001, 256, 2), (2, 12345, 400, 4)])
+def test_window_tc_long_runs_exact_edges(ga, orc, monkeypatch, grid, L, w, r):
+    """Few persistent CTAs (GA_WTC_GRID), so each walks a long run of work items across
+    stream (class, head) boundaries: the item cursor, the K/V ring reuse and the next tile's S
+    issued before the last P V all run many times; every row's edge multiset must stay exact.
+    (Stands in for the compute-sanitizer tier on this round's kernel: the pool's sanitizer is
+    closed.)"""
+    monkeypatch.setenv("GA_WTC_GRID", str(grid))
+    run_counts(ga, orc, ga.Window(w, r), orc.window(L, w, r), L, 2, 64, "bf16", kernel="tc")
+
+
+def test_window_tc_repeatable(ga):
+    """Ten runs of the cfg2 shape are bitwise identical (a race in the warp-specialised
+    pipeline — TMEM reuse, ring slots, staging buffers — shows up as run-to-run differences)."""
+    L, H, d = 65536, 8, 64
+    q, k, v = (x.cuda() for x in synth.qkv(11, L, H, d, "bf16", centred=True))
+    ref = ga.attention(q, k, v, ga.Window(256, 2), kernel="tc")
+    for _ in range(9):
+        out = ga.attention(q, k, v, ga.Window(256, 2), kernel="tc")
+        assert torch.equal(out, ref)
+
+
 def test_window_tc_is_auto(ga, orc):
     """The AUTO path for cfg2's shape is the tcgen05 kernel (same bits as kernel='tc')."""
     L, H, d = 4096, 2, 64

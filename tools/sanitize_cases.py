@@ -28,11 +28,27 @@ def run(name, mask, om, L, H, d, dt, **kw):
     assert err <= tol
 
 
+def run_env(env, *a, **kw):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        run(*a, **kw)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
 def main(cases):
     L = 2048
     bb = ga.mask_to_csr(ga.BigBird(64, 4, 16, seed=3), L)
     all_cases = {
         "window_tc": lambda: run("window_tc", ga.Window(256, 2), oracle.window(L, 256, 2), L, 2, 64, "bf16", kernel="tc"),
+        # many items per CTA (GA_WTC_GRID caps the persistent grid): cursor, ring reuse, S prefetch
+        "window_tc_run": lambda: run_env({"GA_WTC_GRID": "3"}, "window_tc_run", ga.Window(200, 2),
+                                         oracle.window(4 * L, 200, 2), 4 * L, 2, 64, "bf16", kernel="tc"),
         "band": lambda: run("band", ga.Window(64, 1), oracle.window(L, 64, 1), L, 2, 64, "bf16", kernel="tiled"),
         "edge": lambda: run("edge", ga.Window(40, 3), oracle.window(L, 40, 3), L, 2, 64, "f32", kernel="edge"),
         "longnet_umma": lambda: run("longnet_umma", ga.LongNet(512, 2), oracle.longnet(8192, 512, 2), 8192, 1, 64,
