@@ -12,6 +12,8 @@ import torch  # noqa: E402
 
 import paper_2502_01659_b200 as ga  # noqa: E402
 
+WL, WM = int(os.environ.get("LT_LOADER", "4")), int(os.environ.get("LT_MMA", "5"))  # loader / MMA warp
+
 L = 1 << 22
 q, k, v = ga.qkv_device(1, L, 1, 64, torch.bfloat16)
 m = ga.LongNet(2048, 2)
@@ -36,12 +38,12 @@ end = max(t for t, e, w, c in ev if e == 99)
 print("end of CTA at", end)
 for c in range(0, 48):
     row = []
-    for (e, w) in [(20, 4), (1, 5), (10, 0), (12, 0), (14, 0), (12, 3), (14, 3), (3, 5), (7, 5)]:
+    for (e, w) in [(20, WL), (1, WM), (10, 0), (12, 0), (14, 0), (12, 3), (14, 3), (3, WM), (7, WM)]:
         row.append(per.get((e, w), {}).get(c, -1))
     if all(x < 0 for x in row):
         break
     print(f"c={c:2d} " + " ".join(f"{names[e][:14]:>14s}={x:7d}" for (e, w), x in
-                               zip([(20, 4), (1, 5), (10, 0), (12, 0), (14, 0), (12, 3), (14, 3), (3, 5), (7, 5)], row)))
+                               zip([(20, WL), (1, WM), (10, 0), (12, 0), (14, 0), (12, 3), (14, 3), (3, WM), (7, WM)], row)))
 # softmax busy vs waiting
 w0 = [(t, e, c) for t, e, w, c in ev if w == 0 and e in (10, 12, 14)]
 wait = sum(per[(12, 0)][c] - per[(10, 0)][c] for c in per[(12, 0)] if c in per[(10, 0)])
