@@ -740,6 +740,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 if (ld0) tmem_ld32(tS, s);
                 if (ld1) tmem_ld32(tS + 32, s + 32);
                 tmem_wait_ld();
+                TRACE(24 + w);
                 // masks: left edge inside the half iff the last lane's klo is past its start
                 if (ld0 && !full0)
                     mask_half(s, klo - h0, khi - h0, max(xr0 + 31 - mi, 0) > h0, min(xr0 + mi, Tt.Nc - 1) < h0 + 31);
@@ -753,8 +754,13 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 if (ld1) lm = fmaxf(lm, max32(s + 32));
                 const float lm2 = lm * sl2;
                 const bool need = lm2 > m_run + kTau;
-                const float a = (need && m_run != -INFINITY) ? ex2(m_run - lm2) : 1.f;
-                if (__any_sync(0xffffffffu, a != 1.f) && j > 0) {
+                // rows whose O and l must be scaled by a = 2^(m_run - lm2) < 2^-kTau (never 1);
+                // the vote does not wait for an exponential (a MUFU op queued behind the other
+                // warpgroup's would delay it by up to one chunk of exponentials)
+                const bool resc = need && m_run != -INFINITY;
+                float a = 1.f;
+                if (__any_sync(0xffffffffu, resc)) { // (resc implies j > 0: m_run is -inf at a tile's start)
+                    a = resc ? ex2(m_run - lm2) : 1.f;
                     // O stable: P V of the previous chunk completed
                     mbar_wait(bar(bars, B_OFULL + 2 * w + (int)((c - 1) & 1)), ((c - 1) >> 1) & 1);
                     fence_after();
@@ -774,6 +780,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     m_run = lm2;
                 }
                 const float negm = m_run == -INFINITY ? 0.f : -m_run;
+                TRACE(26 + w);
                 const uint32_t tP = tS;
                 float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                                  make_float2(0.f, 0.f)};
@@ -795,7 +802,9 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 }
                 tmem_st16(tP + 16, pk);
                 l_run += (acc[0].x + acc[1].x) + (acc[2].x + acc[3].x) + ((acc[0].y + acc[1].y) + (acc[2].y + acc[3].y));
+                TRACE(28 + w);
                 tmem_wait_st();
+                TRACE(30 + w);
                 fence_before();
                 mbar_arrive(bar(bars, B_PFULL + 2 * w + (int)(c & 1)));
                 TRACE(14 + w);

@@ -1,0 +1,6 @@
+# A/B: in-tree lib vs abtest/libga_prev.so (built here from the previous commit)
+timeout 150 python tools/wtc_tiny.py 2048 1 || { echo "tiny case failed/hung"; exit 1; }
+timeout 300 python -m pytest tests/test_gpu_edgesets.py -q -x -p no:cacheprovider -k "window_tc" 2>&1 | tail -n 1
+for rep in 1 2 3; do for c in cfg5 cfg2; do for lib in abtest/libga_prev.so paper_2502_01659_b200/libga.so; do
+  GA_LIB=$PWD/$lib timeout 300 python bench.py --config $c --steps 10 --no-per-config --no-e2e --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c $lib', round(d['ms_per_step'],4))"
+done; done; done

@@ -28,7 +28,7 @@ n = lib.ga_wtc_trace_read(buf, N)
 ev = sorted(((b & 0xffffffffff), (b >> 48) & 0xff, (b >> 40) & 0xff, b >> 56) for b in buf[:n] if b)
 names = {3: "mma: P arrived", 6: "mma: S issued", 10: "smx A: wait S start", 11: "smx B: wait S start", 12: "smx A: S ready",
          13: "smx B: S ready", 14: "smx A: P arrive", 15: "smx B: P arrive", 18: "epi: A tile ready", 19: "epi: B tile ready",
-         20: "loader: fill issued", 16: "smx A: tile end", 17: "smx B: tile end", 22: "smx A: OFREE ok", 23: "smx B: OFREE ok", 21: "loader: wants slot"}
+         20: "loader: fill issued", 16: "smx A: tile end", 17: "smx B: tile end", 22: "smx A: OFREE ok", 23: "smx B: OFREE ok", 24: "smx A: S loaded", 25: "smx B: S loaded", 26: "smx A: max+vote done", 27: "smx B: max+vote done", 28: "smx A: exps+st issued", 29: "smx B: exps+st issued", 30: "smx A: st done", 31: "smx B: st done", 21: "loader: wants slot"}
 print(f"{n} events, span {ev[-1][0] - ev[0][0]} cycles")
 last = {}
 gaps = defaultdict(list)
