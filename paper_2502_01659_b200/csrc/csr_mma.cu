@@ -298,12 +298,23 @@ __global__ void __launch_bounds__(TW * 32, 2) csr_tma_kernel(const __grid_consta
     // PD + 2 pairs ahead, stored to the per-warp ring slot P % IR when pair P - PD retires,
     // and read from there by the issue of P's blocks (past the row's end: kv_begin -> row 0)
     const uint32_t sidx = sbase + TW * TS * STAGE + TW * TS * 8 + warp * IR * 128;
+    // Indices are stored relative to kv_begin, with one flag word per pair: bit k set iff block k
+    // of the pair is 16 consecutive columns (a window run: one 16-row TMA box) — every column
+    // checked, computed by the whole warp once per pair (a shuffle and a ballot) instead of by
+    // the issuing lane once per block.
+    const uint32_t sflag = sbase + TW * TS * STAGE + TW * TS * 8 + TW * IR * 128 + warp * IR * 4;
     auto ld_pair = [&](int P) -> int {
         const int e = P * 32 + lane;
-        return (P < npair && e < ncnt) ? cols[e] : kv0;
+        return (P < npair && e < ncnt) ? cols[e] - kv0 : 0;
     };
     auto st_pair = [&](int P, int v) {
+        const int nx = __shfl_down_sync(0xffffffffu, v, 1);
+        const unsigned bal = __ballot_sync(0xffffffffu, (lane & 15) == 15 || nx == v + 1);
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(sidx + (P % IR) * 128 + lane * 4), "r"(v) : "memory");
+        if (lane == 0) {
+            const uint32_t f = ((bal & 0xffffu) == 0xffffu ? 1u : 0u) | ((bal >> 16) == 0xffffu ? 2u : 0u);
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(sflag + (P % IR) * 4), "r"(f) : "memory");
+        }
     };
     int rA, rB;
     for (int P = 0; P < PD; ++P) st_pair(P, ld_pair(P));
@@ -313,8 +324,7 @@ __global__ void __launch_bounds__(TW * 32, 2) csr_tma_kernel(const __grid_consta
     const uint32_t row_bytes = (uint32_t)(H * D * sizeof(T));
     // lane (r8, c) copies 16-byte chunk c of the K and V rows of edges 4 r8 + q: its global
     // base folds in the head, the chunk and -kv_begin rows; its shared offsets are fixed
-    const char *kbase = reinterpret_cast<const char *>(p.K) + (size_t)h * D * sizeof(T) + (lane & 7) * 16 -
-                        (ptrdiff_t)kv0 * row_bytes;
+    const char *kbase = reinterpret_cast<const char *>(p.K) + (size_t)h * D * sizeof(T) + (lane & 7) * 16;
     const ptrdiff_t vdelta = reinterpret_cast<const char *>(p.V) - reinterpret_cast<const char *>(p.K);
     // block n -> stage s = n % TS (passed in by the caller's stage counter)
     auto issue = [&](int n, int s) {
@@ -337,25 +347,19 @@ __global__ void __launch_bounds__(TW * 32, 2) csr_tma_kernel(const __grid_consta
             // a block of 16 consecutive columns (e.g. the window run of a BigBird row) is one
             // 16-row box for K and one for V; otherwise 4 + 4 tile::gather4 loads.  Every
             // column is checked (duplicate columns of a multiset CSR can span 15 too).
-            uint4 jq[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) jq[q] = lds128(src + 16 * q);
-            const int jb = (int)jq[0].x;
-            bool run = true;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                run = run && (int)jq[q].x == jb + 4 * q && (int)jq[q].y == jb + 4 * q + 1 &&
-                      (int)jq[q].z == jb + 4 * q + 2 && (int)jq[q].w == jb + 4 * q + 3;
-            if (run) {
-                tma::load_3d(dst, &tp.tbK, 0, h, jb - kv0, bar);
-                tma::load_3d(dst + 2048, &tp.tbV, 0, h, jb - kv0, bar);
+            uint32_t f;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(f) : "r"(sflag + ((n >> 1) % IR) * 4));
+            if ((f >> (n & 1)) & 1u) {
+                int jb;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(jb) : "r"(src));
+                tma::load_3d(dst, &tp.tbK, 0, h, jb, bar);
+                tma::load_3d(dst + 2048, &tp.tbV, 0, h, jb, bar);
             } else {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const uint4 j = jq[q];
-                    const int j0 = (int)j.x - kv0, j1 = (int)j.y - kv0, j2 = (int)j.z - kv0, j3 = (int)j.w - kv0;
-                    tma::gather4(dst + q * 512, &tp.tmK, h * D, j0, j1, j2, j3, bar);
-                    tma::gather4(dst + 2048 + q * 512, &tp.tmV, h * D, j0, j1, j2, j3, bar);
+                    const uint4 j = lds128(src + 16 * q);
+                    tma::gather4(dst + q * 512, &tp.tmK, h * D, (int)j.x, (int)j.y, (int)j.z, (int)j.w, bar);
+                    tma::gather4(dst + 2048 + q * 512, &tp.tmV, h * D, (int)j.x, (int)j.y, (int)j.z, (int)j.w, bar);
                 }
             }
         }
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(TW * 32, 2) csr_tma_kernel(const __grid_consta
 
 template <typename T, bool CPA> static ga_status launch_tma_m(const TmaParams &tp, int64_t warps, cudaStream_t s)
 {
-    const int smem = TW * TS * STAGE + TW * TS * 8 + TW * IR * 128 + 1024;
+    const int smem = TW * TS * STAGE + TW * TS * 8 + TW * IR * 128 + TW * IR * 4 + 1024;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(csr_tma_kernel<T, CPA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
