@@ -531,7 +531,9 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
                 l_run += exps();
             }
 #if GA_LNET_SEPP
-            if (c >= NPB) wait_O(c - NPB); // P V_{c-2} has read P buffer c % 2
+            // P buffer c % 2 is free: P V_{c-2} completed, since the MMA warp committed S_c (waited
+            // above) after issuing P V_{c-2} and a commit tracks every prior MMA of the thread
+            // (the same argument keeps the parity waits on mbO below exact)
             tmem_st32(tlane + COL_P + (c % NPB) * (KC / 2), pk);
 #else
             tmem_st32(tlane + COL_S + (c % NSB) * KC, pk);
