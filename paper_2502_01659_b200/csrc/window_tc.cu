@@ -53,6 +53,9 @@ using namespace tc;
 using namespace umma;
 
 constexpr int ROWS = 128, KC = 64, NSLOT = 9, D = 64, RB = 2 * D;
+#ifndef GA_WTC_PRELOAD
+#define GA_WTC_PRELOAD 0 // 1: load S(c + 1) right after issuing the P(c) stores (measured slower: 25.5 vs 24.4 ms at cfg5)
+#endif
 constexpr int W_EPI = 8, W_LOAD = 12, W_MMA = 13; // warp 15 only completes warpgroup 3
 constexpr int THREADS = 32 * 16;
 // registers per thread after setmaxnreg (per SM sub-partition: one warp of each warpgroup,
@@ -724,21 +727,36 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             const int32_t klo = max(x - mi, 0), khi = min(x + mi, Tt.Nc - 1);
             float m_run = -INFINITY, l_run = 0.f;
             const int32_t n = Tt.n;
+            // the 32-column halves of chunk j this warp loads (no row of the warp reaches a
+            // skipped one) and those every row reaches fully (warp-uniform)
+            auto ldh = [&](int32_t j, int hh) { const int32_t b = (Tt.F + j) * KC + 32 * hh; return !(b > uhi || b + 31 < ulo); };
+            // S(c) is loaded at the end of the previous chunk of the tile (its TMEM load overlaps
+            // that chunk's P store, fence and arrival); the first chunk of a tile loads here
+            float s[64];
+#if GA_WTC_PRELOAD
+            auto load_S = [&](uint32_t cc, int32_t jj) {
+                mbar_wait(bar(bars, B_SFULL + 2 * w + (int)(cc & 1)), (cc >> 1) & 1);
+                fence_after();
+                const uint32_t tS = tl + COL_S + (cc & 1u) * KC;
+                if (ldh(jj, 0)) tmem_ld32(tS, s);
+                if (ldh(jj, 1)) tmem_ld32(tS + 32, s + 32);
+            };
+            load_S(c, 0);
+#endif
             for (int32_t j = 0; j < n; ++j, ++c) {
                 const int32_t kmin = (Tt.F + j) * KC;
-                // per 32-column half: skipped (no row of the warp reaches it), full (every row
-                // reaches all of it) or cut by the band's edges (warp-uniform)
                 const int32_t h0 = kmin, h1 = kmin + 32;
-                const bool ld0 = !(h0 > uhi || h0 + 31 < ulo), ld1 = !(h1 > uhi || h1 + 31 < ulo);
+                const bool ld0 = ldh(j, 0), ld1 = ldh(j, 1);
                 const bool full0 = h0 >= ilo && h0 + 31 <= ihi, full1 = h1 >= ilo && h1 + 31 <= ihi;
                 TRACE(10 + w);
+                const uint32_t tS = tl + COL_S + (c & 1u) * KC; // S(c); P(c) is written over it
+#if !GA_WTC_PRELOAD
                 mbar_wait(bar(bars, B_SFULL + 2 * w + (int)(c & 1)), (c >> 1) & 1);
                 fence_after();
                 TRACE(12 + w);
-                const uint32_t tS = tl + COL_S + (c & 1u) * KC; // S(c); P(c) is written over it
-                float s[64];
                 if (ld0) tmem_ld32(tS, s);
                 if (ld1) tmem_ld32(tS + 32, s + 32);
+#endif
                 tmem_wait_ld();
                 TRACE(24 + w);
                 // masks: left edge inside the half iff the last lane's klo is past its start
@@ -803,6 +821,9 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 tmem_st16(tP + 16, pk);
                 l_run += (acc[0].x + acc[1].x) + (acc[2].x + acc[3].x) + ((acc[0].y + acc[1].y) + (acc[2].y + acc[3].y));
                 TRACE(28 + w);
+#if GA_WTC_PRELOAD
+                if (j + 1 < n) load_S(c + 1, j + 1); // (S(c + 1) never waits for P(c))
+#endif
                 tmem_wait_st();
                 TRACE(30 + w);
                 fence_before();
