@@ -178,7 +178,15 @@ template <typename T> __global__ void __launch_bounds__(THREADS) row_kernel(cons
     const int64_t xg = x0 + 16 * warp + g, xg8 = xg + 8;
     const float Dg = sD[16 * warp + g], Dg8 = sD[16 * warp + g + 8];
     const int nblk = (16 + 2 * (int)m + 15) / 16; // key blocks of the warp: band rows 16w + 16b ..
-    auto valid = [&](int64_t x, int64_t y) { return x < Nc && y >= 0 && y < Nc && (x > y ? x - y : y - x) <= m; };
+    // keys of row x in band-row coordinates (y - y0, y0 = x0 - m): [max(0, x - m), min(Nc - 1,
+    // x + m)] - y0 = [max(m - x0, x - x0), min(Nc - 1 - y0, x - x0 + 2m)], empty for x >= Nc;
+    // 32-bit per-lane bounds instead of 64-bit tests per element
+    const int mi = (int)m, xl = 16 * warp + g;
+    const int blo = (int)imax(m - x0, 0);
+    const int bhi = (int)imin(Nc - 1 - y0, (int64_t)(16 * warp + 16 + 2 * mi + 16));
+    const int lo_g = max(blo, xl), hi_g = xg < Nc ? min(bhi, xl + 2 * mi) : -1;
+    const int lo_g8 = max(blo, xl + 8), hi_g8 = xg8 < Nc ? min(bhi, xl + 8 + 2 * mi) : -1;
+    auto valid = [&](int hr, int yb) { return hr ? (yb >= lo_g8 && yb <= hi_g8) : (yb >= lo_g && yb <= hi_g); };
     // lse of rows g, g + 8 (log2 domain)
     float lse_g, lse_g8;
     if (bp.lse_in) {
@@ -190,21 +198,26 @@ template <typename T> __global__ void __launch_bounds__(THREADS) row_kernel(cons
             const int kb = 16 * warp + 16 * b;
             float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
             mma_abt<T>(s, qa, sK, (uint32_t)kb * RB, lane);
+            // the block's valid scores: block max first, then one batch of exponentials
+            float v[2][4], bm[2] = {-INFINITY, -INFINITY};
 #pragma unroll
             for (int n = 0; n < 2; ++n)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int hr = e >> 1;
-                    const int64_t y = y0 + kb + n * 8 + 2 * t4 + (e & 1);
-                    if (!valid(hr ? xg8 : xg, y)) continue;
-                    const float v = s[n][e] * sl2;
-                    if (v > mx[hr]) {
-                        sm[hr] = sm[hr] * ex2(mx[hr] - v) + 1.f;
-                        mx[hr] = v;
-                    } else {
-                        sm[hr] += ex2(v - mx[hr]);
-                    }
+                    v[n][e] = valid(hr, kb + n * 8 + 2 * t4 + (e & 1)) ? s[n][e] * sl2 : -INFINITY;
+                    bm[hr] = fmaxf(bm[hr], v[n][e]);
                 }
+#pragma unroll
+            for (int hr = 0; hr < 2; ++hr) {
+                const float mn = fmaxf(mx[hr], bm[hr]);
+                if (mn == -INFINITY) continue; // nothing valid yet
+                float add = 0.f;
+#pragma unroll
+                for (int n = 0; n < 2; ++n) add += ex2(v[n][2 * hr] - mn) + ex2(v[n][2 * hr + 1] - mn);
+                sm[hr] = (mx[hr] == -INFINITY ? 0.f : sm[hr] * ex2(mx[hr] - mn)) + add;
+                mx[hr] = mn;
+            }
         }
 #pragma unroll
         for (int hr = 0; hr < 2; ++hr)
@@ -234,8 +247,7 @@ template <typename T> __global__ void __launch_bounds__(THREADS) row_kernel(cons
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int hr = e >> 1;
-                const int64_t y = y0 + kb + n * 8 + 2 * t4 + (e & 1);
-                const float pw = valid(hr ? xg8 : xg, y) ? ex2(s[n][e] * sl2 - (hr ? lse_g8 : lse_g)) : 0.f;
+                const float pw = valid(hr, kb + n * 8 + 2 * t4 + (e & 1)) ? ex2(s[n][e] * sl2 - (hr ? lse_g8 : lse_g)) : 0.f;
                 ds[e] = pw * (dp[n][e] - (hr ? Dg8 : Dg));
             }
             pa[2 * n] = pack2<T>(ds[0], ds[1]);
@@ -287,7 +299,14 @@ template <typename T> __global__ void __launch_bounds__(THREADS) col_kernel(cons
     load_a(sV, 16 * warp, lane, va);
     const int64_t yg = y0 + 16 * warp + g, yg8 = yg + 8;
     const int nblk = (16 + 2 * (int)m + 15) / 16;
-    auto valid = [&](int64_t y, int64_t x) { return y < Nc && x >= 0 && x < Nc && (x > y ? x - y : y - x) <= m; };
+    // queries of key y in query-band coordinates (x - x0, x0 = y0 - m): [max(0, y - m), min(Nc - 1,
+    // y + m)] - x0 (32-bit per-lane bounds, empty for y >= Nc)
+    const int mi = (int)m, yl = 16 * warp + g;
+    const int blo = (int)imax(m - y0, 0);
+    const int bhi = (int)imin(Nc - 1 - x0, (int64_t)(16 * warp + 16 + 2 * mi + 16));
+    const int lo_g = max(blo, yl), hi_g = yg < Nc ? min(bhi, yl + 2 * mi) : -1;
+    const int lo_g8 = max(blo, yl + 8), hi_g8 = yg8 < Nc ? min(bhi, yl + 8 + 2 * mi) : -1;
+    auto valid = [&](int hr, int xb) { return hr ? (xb >= lo_g8 && xb <= hi_g8) : (xb >= lo_g && xb <= hi_g); };
     float dk[NB8][4], dv[NB8][4];
 #pragma unroll
     for (int j = 0; j < NB8; ++j) dk[j][0] = dk[j][1] = dk[j][2] = dk[j][3] = dv[j][0] = dv[j][1] = dv[j][2] = dv[j][3] = 0.f;
@@ -304,8 +323,7 @@ template <typename T> __global__ void __launch_bounds__(THREADS) col_kernel(cons
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int hr = e >> 1, col = qb + n * 8 + 2 * t4 + (e & 1);
-                const int64_t x = x0 + col;
-                pw[e] = valid(hr ? yg8 : yg, x) ? ex2(s[n][e] * sl2 - sL[col]) : 0.f;
+                pw[e] = valid(hr, col) ? ex2(s[n][e] * sl2 - sL[col]) : 0.f;
                 ds[e] = pw[e] * (dp[n][e] - sD[col]);
             }
             pp[2 * n] = pack2<T>(pw[0], pw[1]);
