@@ -187,18 +187,46 @@ template <typename T> __global__ void __launch_bounds__(THREADS) row_kernel(cons
     const int lo_g = max(blo, xl), hi_g = xg < Nc ? min(bhi, xl + 2 * mi) : -1;
     const int lo_g8 = max(blo, xl + 8), hi_g8 = xg8 < Nc ? min(bhi, xl + 8 + 2 * mi) : -1;
     auto valid = [&](int hr, int yb) { return hr ? (yb >= lo_g8 && yb <= hi_g8) : (yb >= lo_g && yb <= hi_g); };
-    // lse of rows g, g + 8 (log2 domain)
-    float lse_g, lse_g8;
+    // lse of rows g, g + 8 (log2 domain): given (the forward's), or accumulated online in one
+    // sweep — dQ is then summed against the running reference max m (P' = 2^(s - m), lazy
+    // rescale with a 2^8 threshold like the forward) and divided by l at the end, so S is
+    // computed once instead of in a separate lse sweep
+    float lse_g = 0.f, lse_g8 = 0.f;
+    float dq[NB8][4];
+#pragma unroll
+    for (int j = 0; j < NB8; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
     if (bp.lse_in) {
         lse_g = xg < Nc ? bp.lse_in[(size_t)(c + xg * r) * H + h] : 0.f;
         lse_g8 = xg8 < Nc ? bp.lse_in[(size_t)(c + xg8 * r) * H + h] : 0.f;
-    } else {
-        float mx[2] = {-INFINITY, -INFINITY}, sm[2] = {0.f, 0.f};
+#pragma unroll UNROLL
         for (int b = 0; b < nblk; ++b) {
             const int kb = 16 * warp + 16 * b;
-            float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+            float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}}, dp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
             mma_abt<T>(s, qa, sK, (uint32_t)kb * RB, lane);
-            // the block's valid scores: block max first, then one batch of exponentials
+            mma_abt<T>(dp, da, sV, (uint32_t)kb * RB, lane);
+            uint32_t pa[4];
+#pragma unroll
+            for (int n = 0; n < 2; ++n) {
+                float ds[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int hr = e >> 1;
+                    const float pw = valid(hr, kb + n * 8 + 2 * t4 + (e & 1)) ? ex2(s[n][e] * sl2 - (hr ? lse_g8 : lse_g)) : 0.f;
+                    ds[e] = pw * (dp[n][e] - (hr ? Dg8 : Dg));
+                }
+                pa[2 * n] = pack2<T>(ds[0], ds[1]);
+                pa[2 * n + 1] = pack2<T>(ds[2], ds[3]);
+            }
+            mma_pb<T>(dq, pa, sK, (uint32_t)kb * RB, lane);
+        }
+    } else {
+        float mr[2] = {-INFINITY, -INFINITY}, lr[2] = {0.f, 0.f};
+#pragma unroll UNROLL
+        for (int b = 0; b < nblk; ++b) {
+            const int kb = 16 * warp + 16 * b;
+            float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}}, dp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+            mma_abt<T>(s, qa, sK, (uint32_t)kb * RB, lane);
+            mma_abt<T>(dp, da, sV, (uint32_t)kb * RB, lane);
             float v[2][4], bm[2] = {-INFINITY, -INFINITY};
 #pragma unroll
             for (int n = 0; n < 2; ++n)
@@ -209,51 +237,58 @@ template <typename T> __global__ void __launch_bounds__(THREADS) row_kernel(cons
                     bm[hr] = fmaxf(bm[hr], v[n][e]);
                 }
 #pragma unroll
-            for (int hr = 0; hr < 2; ++hr) {
-                const float mn = fmaxf(mx[hr], bm[hr]);
-                if (mn == -INFINITY) continue; // nothing valid yet
-                float add = 0.f;
-#pragma unroll
-                for (int n = 0; n < 2; ++n) add += ex2(v[n][2 * hr] - mn) + ex2(v[n][2 * hr + 1] - mn);
-                sm[hr] = (mx[hr] == -INFINITY ? 0.f : sm[hr] * ex2(mx[hr] - mn)) + add;
-                mx[hr] = mn;
+            for (int hr = 0; hr < 2; ++hr) { // the row's block max over its quad of lanes
+                bm[hr] = fmaxf(bm[hr], __shfl_xor_sync(0xffffffffu, bm[hr], 1));
+                bm[hr] = fmaxf(bm[hr], __shfl_xor_sync(0xffffffffu, bm[hr], 2));
             }
+            const bool n0 = bm[0] > mr[0] + 8.f, n1 = bm[1] > mr[1] + 8.f;
+            if (__any_sync(0xffffffffu, n0 || n1)) {
+                const float a0 = n0 ? (mr[0] == -INFINITY ? 0.f : ex2(mr[0] - bm[0])) : 1.f;
+                const float a1 = n1 ? (mr[1] == -INFINITY ? 0.f : ex2(mr[1] - bm[1])) : 1.f;
+                if (n0) mr[0] = bm[0];
+                if (n1) mr[1] = bm[1];
+                lr[0] *= a0;
+                lr[1] *= a1;
+#pragma unroll
+                for (int j = 0; j < NB8; ++j) {
+                    dq[j][0] *= a0;
+                    dq[j][1] *= a0;
+                    dq[j][2] *= a1;
+                    dq[j][3] *= a1;
+                }
+            }
+            const float mu0 = mr[0] == -INFINITY ? 0.f : mr[0], mu1 = mr[1] == -INFINITY ? 0.f : mr[1];
+            uint32_t pa[4];
+#pragma unroll
+            for (int n = 0; n < 2; ++n) {
+                float ds[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int hr = e >> 1;
+                    const float pw = ex2(v[n][e] - (hr ? mu1 : mu0)); // invalid: 2^-inf = 0
+                    lr[hr] += pw;
+                    ds[e] = pw * (dp[n][e] - (hr ? Dg8 : Dg));
+                }
+                pa[2 * n] = pack2<T>(ds[0], ds[1]);
+                pa[2 * n + 1] = pack2<T>(ds[2], ds[3]);
+            }
+            mma_pb<T>(dq, pa, sK, (uint32_t)kb * RB, lane);
         }
 #pragma unroll
-        for (int hr = 0; hr < 2; ++hr)
-#pragma unroll
-            for (int o = 1; o < 4; o <<= 1) {
-                const float m2 = __shfl_xor_sync(0xffffffffu, mx[hr], o), l2 = __shfl_xor_sync(0xffffffffu, sm[hr], o);
-                const float mn = fmaxf(mx[hr], m2);
-                sm[hr] = (mx[hr] == -INFINITY ? 0.f : sm[hr] * ex2(mx[hr] - mn)) + (m2 == -INFINITY ? 0.f : l2 * ex2(m2 - mn));
-                mx[hr] = mn;
-            }
-        lse_g = sm[0] > 0.f ? mx[0] + __log2f(sm[0]) : 0.f;
-        lse_g8 = sm[1] > 0.f ? mx[1] + __log2f(sm[1]) : 0.f;
-    }
-    float dq[NB8][4];
-#pragma unroll
-    for (int j = 0; j < NB8; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
-#pragma unroll UNROLL
-    for (int b = 0; b < nblk; ++b) {
-        const int kb = 16 * warp + 16 * b;
-        float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}}, dp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-        mma_abt<T>(s, qa, sK, (uint32_t)kb * RB, lane);
-        mma_abt<T>(dp, da, sV, (uint32_t)kb * RB, lane);
-        uint32_t pa[4];
-#pragma unroll
-        for (int n = 0; n < 2; ++n) {
-            float ds[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int hr = e >> 1;
-                const float pw = valid(hr, kb + n * 8 + 2 * t4 + (e & 1)) ? ex2(s[n][e] * sl2 - (hr ? lse_g8 : lse_g)) : 0.f;
-                ds[e] = pw * (dp[n][e] - (hr ? Dg8 : Dg));
-            }
-            pa[2 * n] = pack2<T>(ds[0], ds[1]);
-            pa[2 * n + 1] = pack2<T>(ds[2], ds[3]);
+        for (int hr = 0; hr < 2; ++hr) {
+            lr[hr] += __shfl_xor_sync(0xffffffffu, lr[hr], 1);
+            lr[hr] += __shfl_xor_sync(0xffffffffu, lr[hr], 2);
         }
-        mma_pb<T>(dq, pa, sK, (uint32_t)kb * RB, lane);
+        lse_g = lr[0] > 0.f ? mr[0] + __log2f(lr[0]) : 0.f;
+        lse_g8 = lr[1] > 0.f ? mr[1] + __log2f(lr[1]) : 0.f;
+        const float i0 = lr[0] > 0.f ? 1.f / lr[0] : 0.f, i1 = lr[1] > 0.f ? 1.f / lr[1] : 0.f;
+#pragma unroll
+        for (int j = 0; j < NB8; ++j) {
+            dq[j][0] *= i0;
+            dq[j][1] *= i0;
+            dq[j][2] *= i1;
+            dq[j][3] *= i1;
+        }
     }
     const float isd = sl2 * 0.69314718055994531f; // 1 / sqrt(d)
     const int64_t tg = c + xg * r, tg8 = c + xg8 * r;
