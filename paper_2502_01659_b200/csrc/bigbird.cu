@@ -34,6 +34,7 @@ namespace bb {
 #endif
 constexpr int WARPS = 8;
 constexpr int CAP = 1024; // extra columns per row held in shared memory (n_global + n_random)
+constexpr int BITS = 4096; // per-warp bitmap of the taken random columns (mod BITS)
 
 struct Args {
     ga_state win;    // window-part state from step 1 ([q_rows, H] / [q_rows, H, d] fp32)
@@ -88,7 +89,8 @@ struct View {
 
 // Extra columns of non-global row i — (G \ W_i) if parts has GA_BB_GLOBAL, R_i if it has
 // GA_BB_RANDOM — into buf (warp-collective; returns the warp-uniform count).
-__device__ int extras(const DevMask &M, const View &V, int parts, int32_t i, int32_t *buf, int lane, bool skip_globals)
+__device__ int extras(const DevMask &M, const View &V, int parts, int32_t i, int32_t *buf, int lane, bool skip_globals,
+                      uint32_t *bits)
 {
     int n = 0;
     if (parts & 2 && !skip_globals) {
@@ -122,11 +124,17 @@ __device__ int extras(const DevMask &M, const View &V, int parts, int32_t i, int
             const uint64_t base = splitmix64(M.seed);
             int32_t *R = buf + n;
             int got = 0;
+            // taken columns also set bit (c mod BITS) of a per-warp bitmap: a candidate whose bit
+            // is clear is certainly new (one shared load instead of a scan of the taken list;
+            // the scan runs only on a bit collision, ~got / BITS of the candidates)
+            for (int k = lane; k < BITS / 32; k += 32) bits[k] = 0u;
+            __syncwarp();
             for (uint64_t t0 = 0; got < target; t0 += 32) {
                 const int32_t c = (int32_t)bb_candidate(M, base, i, t0 + (uint64_t)lane);
                 bool valid = !V.in_window(i, c) && !V.is_global(c);
-                for (int q = 0; valid && q < got; ++q)
-                    if (R[q] == c) valid = false;
+                if (valid && ((bits[(c & (BITS - 1)) >> 5] >> (c & 31)) & 1u))
+                    for (int q = 0; valid && q < got; ++q)
+                        if (R[q] == c) valid = false;
                 const unsigned vm = __ballot_sync(0xffffffffu, valid);
                 bool first = false;
                 if (valid) {
@@ -135,7 +143,10 @@ __device__ int extras(const DevMask &M, const View &V, int parts, int32_t i, int
                 }
                 const unsigned fm = __ballot_sync(0xffffffffu, first);
                 const int rank = __popc(fm & lanemask_lt(lane));
-                if (first && got + rank < target) R[got + rank] = c;
+                if (first && got + rank < target) {
+                    R[got + rank] = c;
+                    atomicOr(&bits[(c & (BITS - 1)) >> 5], 1u << (c & 31));
+                }
                 __syncwarp();
                 got = min(target, got + __popc(fm));
             }
@@ -151,6 +162,7 @@ __global__ void __launch_bounds__(WARPS * 32) extras_kernel(const __grid_constan
 {
     __shared__ int32_t cols[WARPS][CAP];
     __shared__ int32_t sG[CAP];
+    __shared__ uint32_t sbits[WARPS][BITS / 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const DevMask &M = p.mask;
     for (int k = threadIdx.x; k < M.ng; k += WARPS * 32) sG[k] = (int32_t)bb_global_at(M, k);
@@ -183,7 +195,7 @@ __global__ void __launch_bounds__(WARPS * 32) extras_kernel(const __grid_constan
             with_window = false;
         } // else: window only (random columns are drawn for non-global rows, R10)
     } else {
-        const int n = extras(M, V, parts, i, cols[wib], lane, a.globals_done != 0);
+        const int n = extras(M, V, parts, i, cols[wib], lane, a.globals_done != 0, sbits[wib]);
         // edge steps in flight per warp: 2 measured best at cfg3i (4 / 8 cost occupancy)
         acc.template run_csr<GA_BB_DEPTH>(cols[wib], 0, n);
     }
