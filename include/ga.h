@@ -165,7 +165,8 @@ typedef struct ga_opts {
     void *workspace;
     size_t workspace_bytes;
     /* Debug / work-optimality probes ("probe build").  When non-NULL a slower
-       instrumented kernel runs:
+       instrumented kernel runs (the edge kernel; for bf16/fp16 d = 64 windows with only
+       edge_counter set, the production tcgen05 window kernel — see tensor_counter):
          edge_counter      DEVICE u64, atomically += number of q.k dot products computed
          row_fingerprint   DEVICE u64 [q_rows*3]: per processed row (head 0): degree,
                            sum of j, sum of splitmix64(j), all mod 2^64. */
@@ -190,6 +191,13 @@ typedef struct ga_opts {
        its rows' edges into that shard's key range only and (+)-merging the carried state
        (memory ~6 L / world per rank).  Ignored elsewhere. */
     int32_t exchange;
+    /* Probe of the tcgen05 window kernel (with edge_counter and without row_fingerprint the
+       window kernel itself is probed instead of the instrumented edge kernel):
+         tensor_counter    DEVICE u64, += q.k products the tensor cores computed (whole
+                           128 x 64 MMA tiles, masked pairs included: reading R23)
+       edge_counter then counts the (row, key) pairs that received a softmax weight (the
+       band's edges: nnz x heads when the kernel is work-exact in its weights). */
+    unsigned long long *tensor_counter;
 } ga_opts;
 
 enum { GA_EXCHANGE_ALLGATHER = 0, GA_EXCHANGE_RING = 1 };

@@ -51,6 +51,7 @@ class GaOpts(ctypes.Structure):
         ("edge_counter", ctypes.c_void_p), ("row_fingerprint", ctypes.c_void_p),
         ("kernel", ctypes.c_int32), ("heavy_threshold", ctypes.c_int32),
         ("state", GaState), ("state_mode", ctypes.c_int32), ("exchange", ctypes.c_int32),
+        ("tensor_counter", ctypes.c_void_p),
     ]
 
 

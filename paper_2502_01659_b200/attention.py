@@ -48,7 +48,7 @@ class State:
 
 
 def _opts(q_begin, q_rows, kv_begin, kv_rows, workspace, edge_counter, row_fingerprint, kernel, heavy,
-          state: Optional[State] = None, accumulate: bool = False):
+          state: Optional[State] = None, accumulate: bool = False, tensor_counter=None):
     o = _abi.GaOpts()
     if state is not None:
         o.state = state.c()
@@ -61,6 +61,8 @@ def _opts(q_begin, q_rows, kv_begin, kv_rows, workspace, edge_counter, row_finge
         o.edge_counter = edge_counter.data_ptr()
     if row_fingerprint is not None:
         o.row_fingerprint = row_fingerprint.data_ptr()
+    if tensor_counter is not None:
+        o.tensor_counter = tensor_counter.data_ptr()
     o.kernel = _KERNELS[kernel]
     o.heavy_threshold = heavy
     return o
@@ -80,7 +82,8 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: Mask, out
               L: Optional[int] = None, q_begin: int = 0, kv_begin: int = 0, kernel: str = "auto",
               workspace: Optional[torch.Tensor] = None, edge_counter: Optional[torch.Tensor] = None,
               row_fingerprint: Optional[torch.Tensor] = None, heavy_threshold: int = 0,
-              state: Optional[State] = None, accumulate: bool = False) -> Optional[torch.Tensor]:
+              state: Optional[State] = None, accumulate: bool = False,
+              tensor_counter: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
     """Graph-view masked attention (Algorithm 1) via ga_attention_ex.
 
     q: [q_rows, H, d] rows q_begin.. of the global sequence; k, v: [kv_rows, H, d] rows
@@ -88,7 +91,10 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: Mask, out
     pass `workspace` (uint8 CUDA tensor of workspace_size(...) bytes) to use the split path.
     With `state` (a State of q's rows) the call also writes — or with accumulate=True
     (+)-combines into — the carried (m, l, o) of its edges; `out` is then only produced when
-    given (returns out, or None).
+    given (returns out, or None).  Probes (int64 CUDA tensors of one element, added to):
+    edge_counter — q.k products that received a weight (with row_fingerprint, or outside the
+    tcgen05 window kernel's range, on the instrumented edge kernel); tensor_counter — products
+    the tcgen05 window kernel's MMA tiles computed (masked pairs included, reading R23).
     """
     if not (q.is_cuda and k.is_cuda and v.is_cuda):
         raise ValueError("q, k, v must be CUDA tensors (no CPU path)")
@@ -105,7 +111,7 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: Mask, out
         out = torch.empty_like(q)
     cm = mask.to_c(L)
     o = _opts(q_begin, rows, kv_begin, k.shape[0], workspace, edge_counter, row_fingerprint, kernel, heavy_threshold,
-              state, accumulate)
+              state, accumulate, tensor_counter)
     _abi.check(_abi.lib().ga_attention_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), ctypes.byref(cm),
                                           out.data_ptr() if out is not None else None, L, d, H, dtype_code(q.dtype),
                                           ctypes.byref(o), _stream(q.device)))

@@ -238,6 +238,7 @@ static ga_status resolve(const void *Q, const void *K, const void *V, const ga_m
     p.nnz = M.kind == GA_MASK_CSR ? mask->nnz : 0;
     p.edge_counter = o.edge_counter;
     p.row_fingerprint = o.row_fingerprint;
+    p.tensor_counter = o.tensor_counter;
     if (with_state) {
         p.state = o.state;
         p.state_mode = o.state_mode;
@@ -290,7 +291,10 @@ static ga_status dispatch(AttnParams &p, ga_dtype dtype, const ga_opts *opts, in
         }
         return mma ? launch_csr_mma(p, dtype, s) : launch_edge(p, dtype, s);
     }
-    if (!probe && (kernel == GA_KERNEL_TC || kernel == GA_KERNEL_AUTO) && window_tc_supported(p, dtype))
+    // the tcgen05 window kernel probes itself for edge_counter (weighted pairs) and
+    // tensor_counter (MMA tile products); a row fingerprint needs the instrumented edge kernel
+    const bool wtc_probe = p.edge_counter && !p.row_fingerprint;
+    if ((!probe || wtc_probe) && (kernel == GA_KERNEL_TC || kernel == GA_KERNEL_AUTO) && window_tc_supported(p, dtype))
         return launch_window_tc(p, dtype, s);
     if (!probe && (kernel == GA_KERNEL_TC || kernel == GA_KERNEL_AUTO) && longnet_tc_supported(p, dtype))
         return launch_longnet_tc(p, dtype, s, /*use_umma=*/true); // tcgen05 groups + mma.sync rest

@@ -184,6 +184,7 @@ struct AttnParams {
     int64_t heavy_threshold; // CSR: rows above this are skipped by the light kernel (0 = none)
     unsigned long long *edge_counter;
     unsigned long long *row_fingerprint;
+    unsigned long long *tensor_counter; // tcgen05 window kernel probe: MMA tile products
     // Sharded runs over peer memory (ga_attention_sharded): rank q holds K/V token rows
     // [q*shard_rows, (q+1)*shard_rows) at k_peer[q] / v_peer[q] (CUDA IPC mappings; the
     // local rank's own entry is its K/V).  Rows outside [kv_begin, kv_begin + kv_rows) are

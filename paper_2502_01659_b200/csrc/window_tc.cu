@@ -282,7 +282,7 @@ __device__ __forceinline__ void exps_half(float *s, float sl2, float negm, uint3
     }
 }
 
-template <typename T>
+template <typename T, bool PROBE> // PROBE: count (edge_counter / tensor_counter), a separate instantiation
 __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_constant__ TcParams tp)
 {
     extern __shared__ unsigned char smem_raw[];
@@ -499,6 +499,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                         mma_ss(tw + COL_S + (c & 1u) * KC, dbase | ((aq + kk * 32) >> 4), dbase | ((ak + kk * 32) >> 4),
                                idS, kk > 0);
                     mma_commit(bar(bars, B_SFULL + 2 * w + (int)(c & 1)));
+                    if (PROBE && p.tensor_counter) atomicAdd(p.tensor_counter, (unsigned long long)(ROWS * KC)); // probe
                 }
                 __syncwarp();
                 TRACE2(6, g);
@@ -727,6 +728,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             const int32_t klo = max(x - mi, 0), khi = min(x + mi, Tt.Nc - 1);
             float m_run = -INFINITY, l_run = 0.f;
             const int32_t n = Tt.n;
+            uint32_t ecnt = 0; // probe (edge_counter): this row's weighted pairs
             // the 32-column halves of chunk j this warp loads (no row of the warp reaches a
             // skipped one) and those every row reaches fully (warp-uniform)
             auto ldh = [&](int32_t j, int hh) { const int32_t b = (Tt.F + j) * KC + 32 * hh; return !(b > uhi || b + 31 < ulo); };
@@ -764,6 +766,10 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                     mask_half(s, klo - h0, khi - h0, max(xr0 + 31 - mi, 0) > h0, min(xr0 + mi, Tt.Nc - 1) < h0 + 31);
                 if (ld1 && !full1)
                     mask_half(s + 32, klo - h1, khi - h1, max(xr0 + 31 - mi, 0) > h1, min(xr0 + mi, Tt.Nc - 1) < h1 + 31);
+                if (PROBE && p.edge_counter) { // probe: pairs left unmasked (they get a weight) of a query row
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) ecnt += (ld0 && s[i] != -INFINITY) + (ld1 && s[32 + i] != -INFINITY);
+                }
                 // chunk max (log2 domain) and lazy rescale: a row moves its reference max only
                 // when the chunk's max exceeds it by more than kTau (weights stay <= 2^kTau); O
                 // needs rescaling only for rows that already hold weight
@@ -830,6 +836,10 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 mbar_arrive(bar(bars, B_PFULL + 2 * w + (int)(c & 1)));
                 TRACE(14 + w);
             }
+            if (PROBE && p.edge_counter) { // probe: query rows of the range only (others are not stored)
+                const uint32_t wc = __reduce_add_sync(0xffffffffu, x >= Tt.a_lo && x < Tt.a_hi ? ecnt : 0u);
+                if (lane == 0 && wc) atomicAdd(p.edge_counter, (unsigned long long)wc);
+            }
             // row sum and reference max for the epilogue (its read of the previous use of
             // this buffer, tile k - 2, completed before it released O[k & 1])
             TRACE(16 + w);
@@ -864,15 +874,15 @@ static int sm_count()
 // chunks spanned by a pair of tiles (the ring holds NSLOT)
 static int64_t pair_span(int64_t m) { return floordiv(2 * ROWS - 1 + m, KC) - floordiv(-m, KC) + 1; }
 
-template <typename T> static ga_status launch_t(const TcParams &tp, int64_t grid, cudaStream_t s)
+template <typename T, bool PROBE> static ga_status launch_t(const TcParams &tp, int64_t grid, cudaStream_t s)
 {
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(window_tc_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaError_t e = cudaFuncSetAttribute(window_tc_kernel<T, PROBE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         if (e != cudaSuccess) return cuda_fail(e, "window_tc_kernel: set smem");
         configured = true;
     }
-    window_tc_kernel<T><<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(tp);
+    window_tc_kernel<T, PROBE><<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(tp);
     GA_CHECK_LAUNCH("window_tc_kernel");
     return GA_OK;
 }
@@ -937,7 +947,9 @@ ga_status launch_window_tc(const AttnParams &p, ga_dtype dt, cudaStream_t s)
     // debug: fewer CTAs, so each walks a long run of items (sanitizer coverage of the cursor,
     // the ring reuse and the cross-item S prefetch at small shapes)
     if (const char *e = getenv("GA_WTC_GRID")) grid = imax(1, imin(grid, (int64_t)atoi(e)));
-    return dt == GA_BF16 ? wtc::launch_t<__nv_bfloat16>(tp, grid, s) : wtc::launch_t<__half>(tp, grid, s);
+    if (p.edge_counter || p.tensor_counter)
+        return dt == GA_BF16 ? wtc::launch_t<__nv_bfloat16, true>(tp, grid, s) : wtc::launch_t<__half, true>(tp, grid, s);
+    return dt == GA_BF16 ? wtc::launch_t<__nv_bfloat16, false>(tp, grid, s) : wtc::launch_t<__half, false>(tp, grid, s);
 }
 
 } // namespace ga

@@ -136,6 +136,30 @@ def test_window_tc_repeatable(ga):
         assert torch.equal(out, ref)
 
 
+@pytest.mark.parametrize("L,w,r,H", [(3000, 128, 1, 2), (2999, 256, 2, 3), (5000, 512, 4, 1), (70001, 128, 1, 1),
+                                     (20000, 200, 2, 2)])
+def test_window_tc_probe_counts(ga, orc, L, w, r, H):
+    """The production tcgen05 window kernel probed in place (a probe used to
+    force the edge kernel): the (row, key) pairs it weights number nnz x heads exactly, and
+    its MMA tiles compute a whole number of 128 x 64 tiles, between nnz x heads and the
+    reading-R23 bound (every row-tile meets at most floor((127 + 2m) / 64) + 2 key chunks)."""
+    q, k, v = ga.qkv_device(4, L, H, 64, torch.bfloat16)
+    m = ga.Window(w, r)
+    nnz = orc.mask_to_csr(orc.window(L, w, r))[2]
+    ec = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out = ga.attention(q, k, v, m, edge_counter=ec, tensor_counter=tc)
+    ref = ga.attention(q, k, v, m, kernel="tc")
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref), "probing must not change the production kernel's result"
+    assert int(ec.item()) == nnz * H
+    mm = (w - 1) // r
+    tiles = sum(-(-((L - c + r - 1) // r) // 128) for c in range(min(r, L))) * H
+    products = int(tc.item())
+    assert products % (128 * 64) == 0
+    assert nnz * H <= products <= tiles * ((127 + 2 * mm) // 64 + 2) * 128 * 64
+
+
 def test_window_tc_is_auto(ga, orc):
     """The AUTO path for cfg2's shape is the tcgen05 kernel (same bits as kernel='tc')."""
     L, H, d = 4096, 2, 64
