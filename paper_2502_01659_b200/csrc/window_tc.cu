@@ -24,7 +24,7 @@
 // only for the 32-column halves a warp's rows reach, and a masked pair contributes exactly 0
 // — the result is the Algorithm 1 result over the band's edges.
 //
-// CTA organisation (persistent, one CTA per SM, 512 TMEM columns, 15 warps):
+// CTA organisation (persistent, one CTA per SM, 512 TMEM columns, 16 warps = 4 warpgroups):
 //   warps 0-3   softmax warpgroup A: even tiles of a tile pair   (TMEM cols   0..255)
 //   warps 4-7   softmax warpgroup B: odd tiles                    (TMEM cols 256..511)
 //   warps 8-11  epilogue warpgroup: O of a finished tile from TMEM, normalised by the row sum
@@ -33,14 +33,16 @@
 //   warp 12     loader: TMA boxes of the Q tiles (2 x 64 class rows, element stride r) and the
 //               K/V chunks into a 9-slot ring (slot = g mod 9); peer rows (sharded runs) by
 //               cp.async from the owner's memory
-//   warps 13-14 MMA issuers, one per softmax warpgroup (one elected lane issues)
-// TMEM of a warpgroup: S (64 columns) | P[2] (32 each) | O[2] (64 each).  S has ONE buffer: the
-// softmax releases it right after its tcgen05.ld (before any arithmetic), and the issuer then
-// writes S of the next chunk while the softmax works on this one.  P of chunk c goes to P[c & 1]
-// after P V_{c-2} read it; tile k accumulates in O[k & 1], so the epilogue of tile k overlaps
-// tile k + 1.  A CTA walks a contiguous run of tile pairs of one (class, head) stream:
-// consecutive pairs share 4 of their 8 chunks, which stay resident (each K/V row is read from
-// L2/HBM about once per run).
+//   warps 13-14 MMA issuers, one per softmax warpgroup (one elected lane issues); warp 15 idle
+//               (it completes warpgroup 3 for setmaxnreg: softmax 168 registers, epilogue 104,
+//               loader / issuers 72)
+// TMEM of a warpgroup: S[2] (64 columns each; P of chunk c, 16-bit pairs, is written over the
+// first 32 columns of S[c & 1]) | O[2] (64 each).  S(c + 2) is issued into S(c)'s buffer once
+// P V(c) completed, so S is computed two chunks ahead of the softmax; tile k accumulates in
+// O[k & 1], so the epilogue of tile k overlaps tile k + 1.  A CTA walks a contiguous run of
+// tile pairs of one (class, head) stream (an item cursor, no per-tile divisions): consecutive
+// pairs share 4 of their 8 chunks, which stay resident (each K/V row is read from L2/HBM about
+// once per run).
 #include <cstdlib>
 
 #include "tc_common.cuh"
