@@ -316,10 +316,16 @@ __global__ void __launch_bounds__(TW * 32, 2) csr_tma_kernel(const __grid_consta
             asm volatile("st.shared.u32 [%0], %1;" ::"r"(sflag + (P % IR) * 4), "r"(f) : "memory");
         }
     };
-    int rA, rB;
+    // pairs PD .. PD + RQ - 1 in flight in registers (global loads of the column indices)
+#ifndef GA_CSR_RQ
+#define GA_CSR_RQ 4 // measured cfg3: 2 -> 8.86, 3 -> 8.83, 4 -> 8.78 ms
+#endif
+    constexpr int RQ = GA_CSR_RQ;
+    static_assert(RQ >= 2 && RQ <= 4, "index register queue");
+    int rq[4];
     for (int P = 0; P < PD; ++P) st_pair(P, ld_pair(P));
-    rA = ld_pair(PD);
-    rB = ld_pair(PD + 1);
+#pragma unroll
+    for (int u = 0; u < RQ; ++u) rq[u] = ld_pair(PD + u);
     __syncwarp();
     const uint32_t row_bytes = (uint32_t)(H * D * sizeof(T));
     // lane (r8, c) copies 16-byte chunk c of the K and V rows of edges 4 r8 + q: its global
@@ -365,9 +371,10 @@ __global__ void __launch_bounds__(TW * 32, 2) csr_tma_kernel(const __grid_consta
         }
         if (n & 1) { // pair n/2 retires: every lane's reads of its slot are done before the refill
             __syncwarp();
-            st_pair((n >> 1) + PD, rA);
-            rA = rB;
-            rB = ld_pair((n >> 1) + PD + 2);
+            st_pair((n >> 1) + PD, rq[0]);
+#pragma unroll
+            for (int u = 0; u + 1 < RQ; ++u) rq[u] = rq[u + 1];
+            rq[RQ - 1] = ld_pair((n >> 1) + PD + RQ);
             __syncwarp();
         }
     };
