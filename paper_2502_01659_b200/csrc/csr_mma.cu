@@ -127,8 +127,14 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) csr_mma_kernel(con
 // data costs no registers, so each warp keeps TS blocks (12 KB) in flight — what the random
 // columns of a CSR need to cover DRAM latency — and the per-edge address arithmetic of the
 // LDG variant disappears (TMA takes token coordinates).
-constexpr int TW = 8;       // warps per CTA
-constexpr int TS = 3;       // stages per warp
+#ifndef GA_CSR_TW
+#define GA_CSR_TW 8
+#endif
+#ifndef GA_CSR_TS
+#define GA_CSR_TS 3 // measured cfg3: TS 2 -> 8.77, 3 -> 8.79 ms; TS 4 with 6 warps -> 10.5 ms
+#endif
+constexpr int TW = GA_CSR_TW; // warps per CTA
+constexpr int TS = GA_CSR_TS; // stages per warp
 constexpr int STAGE = 4096; // bytes per stage
 constexpr int IR = 8;       // column-index ring slots per warp (32 edges each)
 constexpr int PD = 5;       // index pairs staged ahead
