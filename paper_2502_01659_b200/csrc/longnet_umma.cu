@@ -642,7 +642,10 @@ __global__ void __launch_bounds__(256) longnet_merge_kernel(const UParams up, in
     const int h = (int)(gw - r * H);
     const int64_t i = (first + r) * step_h0;
     int s = 0; // min(nu(i), K), nu(0) = K
+    const bool pow2 = (M.alpha & (M.alpha - 1)) == 0; // alpha = 2^la: valuations and slots by shifts
+    const int la = pow2 ? __ffsll((unsigned long long)M.alpha) - 1 : 0;
     if (i == 0) s = (int)M.K;
+    else if (pow2) s = (int)imin((int64_t)((__ffsll((unsigned long long)i) - 1) / la), M.K);
     else for (int64_t x = i; s < (int)M.K && x % M.alpha == 0; x /= M.alpha) ++s;
     constexpr int PER = D / 32;
     // lane t < s+1 fetches level t's (m, l) and its partial's address; one warp max and one
@@ -651,9 +654,16 @@ __global__ void __launch_bounds__(256) longnet_merge_kernel(const UParams up, in
     const float *src = nullptr;
     float mt = -INFINITY, lt = 0.f;
     if (lane <= s) {
-        int64_t stp = 1;
-        for (int u = 0; u < (lane > up.h0 ? lane : up.h0); ++u) stp *= M.alpha; // alpha^max(t, h0)
-        src = up.partials + ((size_t)(up.slot_off[lane] + i / stp - up.slot_first[lane]) * H + h) * (D + 4);
+        const int ex = lane > up.h0 ? lane : up.h0; // alpha^max(t, h0)
+        int64_t q;
+        if (pow2) {
+            q = i >> (ex * la);
+        } else {
+            int64_t stp = 1;
+            for (int u = 0; u < ex; ++u) stp *= M.alpha;
+            q = i / stp;
+        }
+        src = up.partials + ((size_t)(up.slot_off[lane] + q - up.slot_first[lane]) * H + h) * (D + 4);
         mt = src[0];
         lt = src[1];
     }
