@@ -193,18 +193,24 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
     // skip_res drops q with residue rx mod alpha (those have a higher valuation)
     const int64_t step = row_step;
     const int64_t lo = imax(S0, p.q_begin), hi = imin(S1, q_end);
-    const int64_t f0 = (lo + step - 1) / step;
-    const int64_t nq = lo < hi && f0 * step < hi ? (hi - 1) / step - f0 + 1 : 0;
-    const int64_t rx = (M.alpha - f0 % M.alpha) % M.alpha;
-    const int64_t count = !skip_res ? nq : nq - (nq > rx ? (nq - 1 - rx) / M.alpha + 1 : 0);
+    const bool a2 = M.alpha == 2; // the common alpha: step = 2^ls, divisions by shifts
+    const int ls = a2 ? __ffsll((unsigned long long)step) - 1 : 0;
+    const int64_t f0 = a2 ? (lo + step - 1) >> ls : (lo + step - 1) / step;
+    const int64_t nq = lo < hi && f0 * step < hi ? (a2 ? (hi - 1) >> ls : (hi - 1) / step) - f0 + 1 : 0;
+    const int64_t rx = a2 ? (2 - (f0 & 1)) & 1 : (M.alpha - f0 % M.alpha) % M.alpha;
+    const int64_t count = !skip_res ? nq : nq - (nq > rx ? (a2 ? (nq - 1 - rx) >> 1 : (nq - 1 - rx) / M.alpha) + 1 : 0);
     const int nrows = (int)imin(ROWS, count - (int64_t)tile * ROWS);
     if (nrows <= 0) return;
     if (tid < nrows) {
         const int64_t r = (int64_t)tile * ROWS + tid;
         int64_t q = r;
         if (skip_res) {
-            const int64_t a1 = M.alpha - 1, idx = r % a1;
-            q = (r / a1) * M.alpha + (idx < rx ? idx : idx + 1);
+            if (a2) { // a1 = 1: idx = 0
+                q = r * 2 + (0 < rx ? 0 : 1);
+            } else {
+                const int64_t a1 = M.alpha - 1, idx = r % a1;
+                q = (r / a1) * M.alpha + (idx < rx ? idx : idx + 1);
+            }
         }
         rows[tid] = (f0 + q) * step;
     }
@@ -295,8 +301,9 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
                     const int64_t jl = j0 - p.kv_begin;
                     const int64_t jlast = jl + (int64_t)(KC - 1) * (P.mode == P_SKIPMUL ? 2 * P.step : P.step);
                     if (lev < up.n_lat && jl >= 0 && jlast < p.kv_rows) {
-                        if (P.mode == P_SKIPMUL) { lt = 2 * lev; u0 = (jl / P.step - 1) / 2; }
-                        else { lt = 2 * lev + 1; u0 = jl / P.step; }
+                        // (step = 2^lev: shifts, not 64-bit divisions, on the loader's path)
+                        if (P.mode == P_SKIPMUL) { lt = 2 * lev; u0 = ((jl >> lev) - 1) >> 1; }
+                        else { lt = 2 * lev + 1; u0 = jl >> lev; }
                     }
                 }
             }
