@@ -66,9 +66,20 @@ GA_HD int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
 GA_HD int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
 
 // alpha-adic valuation capped at K; nu(0) = K.
+// trailing zero bits of x != 0 (the 2-adic valuation)
+GA_HD int ctz64(int64_t x)
+{
+#if defined(__CUDA_ARCH__)
+    return __ffsll((long long)x) - 1;
+#else
+    return __builtin_ctzll((unsigned long long)x);
+#endif
+}
+
 GA_HD int64_t valuation(int64_t x, int64_t alpha, int64_t K)
 {
     if (x == 0) return K;
+    if (alpha == 2) return imin((int64_t)ctz64(x), K); // the common alpha: no 64-bit divisions
     int64_t v = 0;
     while (v < K && x % alpha == 0) { x /= alpha; ++v; }
     return v;
@@ -148,6 +159,26 @@ GA_HD Piece get_piece_h(const DevMask &M, int64_t i, int pc, int h)
         const int64_t hoff = (M.parts & LN_HEAD_OFFSETS) ? h : 0;
         const int64_t x = i - hoff;
         int64_t s = valuation(x < 0 ? -x : x, M.alpha, M.K);
+        if (M.alpha == 2 && M.w0 > 0 && (M.w0 & (M.w0 - 1)) == 0) {
+            // alpha = 2 and w0 = 2^lw: the same quantities by shifts and masks (exact)
+            const int t = pc, lseg = ctz64(M.w0) + pc;
+            const int64_t stp = (int64_t)1 << t;
+            const int64_t s0 = (i >> lseg) << lseg, s1 = imin(M.L, s0 + ((int64_t)1 << lseg));
+            const int64_t b = s0 + (hoff & (stp - 1));
+            const int64_t U = b < s1 ? (s1 - b + stp - 1) >> t : 0;
+            P.base = b;
+            P.step = stp;
+            if (pc < s && !(M.parts & LN_MULTISET)) {
+                const int64_t rx = ((b - hoff) >> t) & 1; // (a^t divides b - hoff)
+                P.mode = P_SKIPMUL;
+                P.alpha = 2;
+                P.rexcl = (int32_t)rx;
+                P.count = U - (U > rx ? ((U - 1 - rx) >> 1) + 1 : 0);
+            } else {
+                P.count = U;
+            }
+            return P;
+        }
         int64_t stp = ipow(M.alpha, pc);
         int64_t segw = M.w0 * stp;
         int64_t s0 = (i / segw) * segw, s1 = imin(M.L, s0 + segw);
