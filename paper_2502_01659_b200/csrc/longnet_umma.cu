@@ -152,11 +152,12 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
     int s, tile, h, np, t_first;      // pieces t_first .. t_first + np - 1 of the rows
     bool skip_res;                    // drop the candidates whose q has residue rx mod alpha
     if (!up.blocked) {
-        const int64_t IH = (int64_t)up.n_items * H;
-        const int64_t segl = (int64_t)blockIdx.x / IH;
-        const int64_t rem = (int64_t)blockIdx.x - segl * IH;
-        const int64_t item = rem / H;
-        h = (int)(rem - item * H);
+        // 32-bit divisions (blockIdx.x < 2^31): a 64-bit one costs ~100 instructions per thread
+        const uint32_t IH = (uint32_t)up.n_items * (uint32_t)H, bx = blockIdx.x;
+        const uint32_t segl = bx / IH;
+        const uint32_t rem = bx - segl * IH;
+        const uint32_t item = rem / (uint32_t)H;
+        h = (int)(rem - item * (uint32_t)H);
         s = up.item_s[item];
         tile = up.item_tile[item];
         seg_len = M.w0;
@@ -169,11 +170,11 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
     } else {
         int e = 0;
         while (e + 1 < up.n_blk && up.blk_start[e + 1] <= (int64_t)blockIdx.x) ++e;
-        const int64_t rel = (int64_t)blockIdx.x - up.blk_start[e];
-        const int64_t TH = (int64_t)up.blk_tiles[e] * H;
-        const int64_t segl = rel / TH, rem = rel - segl * TH;
-        tile = (int)(rem / H);
-        h = (int)(rem - (int64_t)tile * H);
+        const uint32_t rel = (uint32_t)((int64_t)blockIdx.x - up.blk_start[e]);
+        const uint32_t TH = (uint32_t)up.blk_tiles[e] * (uint32_t)H;
+        const uint32_t segl = rel / TH, rem = rel - segl * TH;
+        tile = (int)(rem / (uint32_t)H);
+        h = (int)(rem - (uint32_t)tile * (uint32_t)H);
         const int t = up.blk_t[e];
         seg_len = M.w0;
         for (int u = 0; u < t; ++u) seg_len *= M.alpha;
