@@ -606,9 +606,16 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
         }
     }
     if (row_ok && up.blocked) { // partial state of (row, level s) for the merge kernel
-        int64_t stp = 1;
-        for (int u = 0; u < (s > up.h0 ? s : up.h0); ++u) stp *= M.alpha;
-        const int64_t slot = up.slot_off[s] + rows[tid] / stp - up.slot_first[s];
+        const int ex = s > up.h0 ? s : up.h0; // row / alpha^max(s, h0)
+        int64_t q;
+        if (M.alpha == 2) {
+            q = rows[tid] >> ex;
+        } else {
+            int64_t stp = 1;
+            for (int u = 0; u < ex; ++u) stp *= M.alpha;
+            q = rows[tid] / stp;
+        }
+        const int64_t slot = up.slot_off[s] + q - up.slot_first[s];
         float *dst = up.partials + ((size_t)slot * H + h) * (D + 4);
         *reinterpret_cast<float4 *>(dst) = make_float4(m_run, l_run, 0.f, 0.f);
 #pragma unroll
@@ -646,7 +653,7 @@ __global__ void __launch_bounds__(256) longnet_merge_kernel(const UParams up, in
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int H = p.H;
     if (gw >= n_high * H) return;
-    const int64_t r = gw / H;
+    const int64_t r = H == 1 ? gw : gw / H;
     const int h = (int)(gw - r * H);
     const int64_t i = (first + r) * step_h0;
     int s = 0; // min(nu(i), K), nu(0) = K
