@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(WARPS * 32) extras_kernel(const __grid_constan
     const int64_t gw = (int64_t)blockIdx.x * WARPS + wib;
     const int H = p.H;
     if (gw >= p.q_rows * H) return;
-    const int64_t t = gw / H;
+    const int64_t t = div_heads(gw, H);
     const int h = (int)(gw - t * H);
     const int32_t i = (int32_t)(p.q_begin + t);
     const int parts = M.parts ? M.parts : 7;

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(THREADS, (D <= 64 ? 2 : 1)) csr_mma_kernel(con
     const int64_t gw = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
     const int H = p.H;
     if (gw >= p.q_rows * H) return;
-    const int64_t tq = gw / H;
+    const int64_t tq = div_heads(gw, H);
     const int h = (int)(gw - tq * H);
     const int64_t i = p.q_begin + tq;
     const int64_t rb = p.mask.row_ptr[i], cnt = p.mask.row_ptr[i + 1] - rb;
@@ -280,12 +280,12 @@ __global__ void __launch_bounds__(TW * 32, 2) csr_tma_kernel(const __grid_consta
     // indices are prefetched into L2 while this one runs (its first index loads would
     // otherwise wait on DRAM once per row)
     for (int64_t gw = (int64_t)blockIdx.x * TW + warp; gw < ntask; gw += nwarps) {
-    const int64_t tq = gw / H;
+    const int64_t tq = div_heads(gw, H);
     const int h = (int)(gw - tq * H);
     const int64_t i = p.q_begin + tq;
     const int64_t rb = p.mask.row_ptr[i], cnt = p.mask.row_ptr[i + 1] - rb;
     if (gw + nwarps < ntask) {
-        const int64_t i2 = p.q_begin + (gw + nwarps) / H;
+        const int64_t i2 = p.q_begin + div_heads(gw + nwarps, H);
         const int64_t r2 = p.mask.row_ptr[i2], n2 = p.mask.row_ptr[i2 + 1] - r2;
         const char *c2 = reinterpret_cast<const char *>(p.mask.col_idx + r2);
         if (n2 <= p.heavy_threshold || p.heavy_threshold <= 0)
