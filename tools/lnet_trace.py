@@ -36,6 +36,9 @@ for t, e, w, c in ev:
     per[(e, w)].setdefault(c, t)
 end = max(t for t, e, w, c in ev if e == 99)
 print("end of CTA at", end)
+for e, nm in ((30, "TMEM + barriers ready"), (31, "pieces ready"), (32, "Q loads issued (loader)")):
+    ts = sorted(t for t, ev, w, c in ev_all if ev == e) if False else sorted(t for t, ev, w, c in ev if ev == e)
+    if ts: print(f"{nm}: first {ts[0]} last {ts[-1]}")
 for c in range(0, 48):
     row = []
     for (e, w) in [(20, WL), (1, WM), (10, 0), (12, 0), (14, 0), (12, 3), (14, 3), (3, WM), (7, WM)]:
