@@ -36,10 +36,11 @@
 //   warps 13-14 MMA issuers, one per softmax warpgroup (one elected lane issues); warp 15 idle
 //               (it completes warpgroup 3 for setmaxnreg: softmax 168 registers, epilogue 104,
 //               loader / issuers 72)
-// TMEM of a warpgroup: S[2] (64 columns each; P of chunk c, 16-bit pairs, is written over the
-// first 32 columns of S[c & 1]) | O[2] (64 each).  S(c + 2) is issued into S(c)'s buffer once
-// P V(c) completed, so S is computed two chunks ahead of the softmax; tile k accumulates in
-// O[k & 1], so the epilogue of tile k overlaps tile k + 1.  A CTA walks a contiguous run of
+// TMEM of a warpgroup: S[2] (64 columns each) | P[2] (32 each: 16-bit pairs) | O (64).  S(c + 2)
+// is issued into S(c)'s buffer as soon as P(c) arrived (the softmax has read S(c)), so S is
+// computed two chunks ahead of the softmax; the epilogue reads a finished tile's O while the
+// softmax works on the next tile's first chunk, before that chunk's P V may overwrite it
+// (GA_WTC_PSEP=0: P over S, S(c + 2) after P V(c) completed, O[k & 1]).  A CTA walks a contiguous run of
 // tile pairs of one (class, head) stream (an item cursor, no per-tile divisions): consecutive
 // pairs share 4 of their 8 chunks, which stay resident (each K/V row is read from L2/HBM about
 // once per run).
@@ -75,9 +76,19 @@ constexpr uint32_t OFF_BAR = OFF_LM + 2 * 2 * 2 * ROWS * 4;
 constexpr uint32_t SMEM_BYTES = 1024 + OFF_BAR + 64 * 8;
 static_assert(SMEM_BYTES <= 232448, "shared memory");
 
-// TMEM columns within a warpgroup's 256: S[2] (P of chunk c is written over the first 32
-// columns of S[c & 1]), O[2]
+// TMEM columns within a warpgroup's 256: S[2] | P[2] | O — P in columns of its own, so S(c + 2)
+// is issued as soon as P(c) arrived (no wait for P V(c)); one O accumulator: a tile's first
+// P V waits for the epilogue to have read the previous tile's O, which it does while the
+// softmax works on the tile's first chunk (cfg5 25.03 -> 24.81 ms, cfg2 109 -> 108 us, same
+// box).  GA_WTC_PSEP=0: P over the first 32 columns of S[c & 1], O[2].
+#ifndef GA_WTC_PSEP
+#define GA_WTC_PSEP 1
+#endif
+#if GA_WTC_PSEP
+constexpr uint32_t COL_S = 0, COL_P = 128, COL_O = 192;
+#else
 constexpr uint32_t COL_S = 0, COL_O = 128;
+#endif
 
 // mbarrier indices (8 bytes each from OFF_BAR); [w] = softmax warpgroup, [b] = buffer parity
 constexpr int B_QFULL = 0,             // [w][b] (loader TMA)
@@ -491,7 +502,8 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             for (int32_t g = P.lo; g < (n ? f : P.hi + 1) && g < keep_from; ++g) release_unread(g);
             auto issue_S = [&](uint32_t c, int32_t g, int qbuf) {
                 // S buffer c & 1 held S / P of chunk c - 2: free once P V(c - 2) completed
-                if (c >= 2) mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(c & 1)), ((c - 2) >> 1) & 1);
+                // (P in its own columns: once the softmax read S(c - 2), i.e. P(c - 2) arrived)
+                if (!GA_WTC_PSEP && c >= 2) mbar_wait(bar(bars, B_OFULL + 2 * w + (int)(c & 1)), ((c - 2) >> 1) & 1);
                 fence_after();
                 const uint32_t aq = sbase + OFF_Q + (uint32_t)(2 * w + qbuf) * QBYTES;
                 const uint32_t ak = sbase + OFF_KV + ((uint32_t)g % NSLOT) * 2 * CBYTES;
@@ -513,12 +525,21 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 const int32_t g = f + j;
                 mbar_wait(bar(bars, B_PFULL + 2 * w + (int)(c & 1)), (c >> 1) & 1);
                 TRACE2(3, g);
+#if GA_WTC_PSEP
+                if (j == 0 && k >= 1) mbar_wait(bar(bars, B_OFREE + 2 * w + (int)((k - 1) & 1)), ((k - 1) >> 1) & 1);
+#else
                 if (j == 0 && k >= 2) mbar_wait(bar(bars, B_OFREE + 2 * w + (int)(k & 1)), ((k - 2) >> 1) & 1);
+#endif
                 fence_after();
                 const int sl = (int)((uint32_t)g % NSLOT);
                 const uint32_t av = sbase + OFF_KV + (uint32_t)sl * 2 * CBYTES + CBYTES;
+#if GA_WTC_PSEP
+                const uint32_t tP = tw + COL_P + (c & 1u) * (KC / 2);
+                const uint32_t tO = tw + COL_O;
+#else
                 const uint32_t tP = tw + COL_S + (c & 1u) * KC;
                 const uint32_t tO = tw + COL_O + (k & 1u) * D;
+#endif
                 const bool release = g < keep_from; // each chunk is read once per tile
                 if (elect_one()) {
 #pragma unroll
@@ -604,7 +625,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 const int row = 32 * q + lane;
                 const float l = lmbuf[((w * 2 + (int)b) * 2 + 0) * ROWS + row];
                 const float mrow = lmbuf[((w * 2 + (int)b) * 2 + 1) * ROWS + row];
-                const uint32_t tO = tmem + 256u * (uint32_t)w + ((uint32_t)(q * 32) << 16) + COL_O + b * D;
+                const uint32_t tO = tmem + 256u * (uint32_t)w + ((uint32_t)(q * 32) << 16) + COL_O + (GA_WTC_PSEP ? 0u : b * D);
                 float o[64];
                 tmem_ld32(tO, o);
                 tmem_ld32(tO + 32, o + 32);
@@ -723,7 +744,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
             const Tile Tt = tile_at(tp, C, w);
             if (!Tt.valid) continue;
             const int32_t xr0 = Tt.a0 + 32 * q, x = xr0 + lane;
-            const uint32_t tO = tl + COL_O + (k & 1u) * D; // this tile's O accumulator
+            const uint32_t tO = tl + COL_O + (GA_WTC_PSEP ? 0u : (k & 1u) * D); // this tile's O accumulator
             // keys of this warp's rows: union [ulo, uhi], every row: [ilo, ihi]; this row: [klo, khi]
             const int32_t ulo = max(xr0 - mi, 0), uhi = min(xr0 + 31 + mi, Tt.Nc - 1);
             const int32_t ilo = max(xr0 + 31 - mi, 0), ihi = min(xr0 + mi, Tt.Nc - 1);
@@ -807,7 +828,13 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 }
                 const float negm = m_run == -INFINITY ? 0.f : -m_run;
                 TRACE(26 + w);
+#if GA_WTC_PSEP
+                // P(c) into P buffer c & 1: P V(c - 2) read it and completed, since the commit of
+                // S(c) (waited above) follows P V(c - 2) in the issuer's order
+                const uint32_t tP = tl + COL_P + (c & 1u) * (KC / 2);
+#else
                 const uint32_t tP = tS;
+#endif
                 float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                                  make_float2(0.f, 0.f)};
                 uint32_t pk[16];
@@ -843,7 +870,7 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
                 if (lane == 0 && wc) atomicAdd(p.edge_counter, (unsigned long long)wc);
             }
             // row sum and reference max for the epilogue (its read of the previous use of
-            // this buffer, tile k - 2, completed before it released O[k & 1])
+            // this buffer, tile k - 2, completed before it released that tile's O)
             TRACE(16 + w);
             if (k >= 2) mbar_wait(bar(bars, B_OFREE + 2 * w + (int)(k & 1)), ((k - 2) >> 1) & 1);
             TRACE(22 + w);
