@@ -49,9 +49,15 @@ constexpr int ROWS = 128, SM_THREADS = 128, THREADS = SM_THREADS + 64, KC = 64, 
 constexpr int MAX_ITEMS = 64, MAX_PIECES = 64;
 
 constexpr int MAX_BLK = 128; // block-mode work entries (level, kind)
+// of every GA_LNET_POLY_DEN exp2 pairs, GA_LNET_POLY run as a degree-3 polynomial on the FMA
+// pipe (ex2_poly2, relative error ~1e-4, below P's bf16 rounding).  Round 1 (issue-bound
+// softmax): 1/4 -> 27.15 ms vs 26.07.  Now MUFU is ~68% busy in the group kernel: 1/16 ->
+// 18.71-18.82 ms vs 18.88-18.90 (same box), 1/8 equal, 1/4 19.6.
+#ifndef GA_LNET_POLY_DEN
+#define GA_LNET_POLY_DEN 16
+#endif
 #ifndef GA_LNET_POLY
-#define GA_LNET_POLY 0 // of every 4 exp2 pairs, this many run as a polynomial on the FMA pipe (measured
-                       // cfg4: 0 -> 26.07 ms, 1 -> 27.15, 2 -> 28.74: the softmax warps are issue-bound)
+#define GA_LNET_POLY 1
 #endif
 constexpr int MAX_LAT = 24;  // TMA lattice levels (alpha = 2): 2^23 row pitch
 
@@ -485,7 +491,7 @@ __global__ void __launch_bounds__(THREADS, 2) longnet_umma_kernel(const __grid_c
                 for (int i = 0; i < KC / 2; ++i) {
                     float x0 = sv[2 * i], x1 = sv[2 * i + 1];
                     ffma2_sm(x0, x1, sl2, -m_run);
-                    if ((i & 3) < GA_LNET_POLY) { // part of the exponentials on the FMA pipe
+                    if ((i % GA_LNET_POLY_DEN) < GA_LNET_POLY) { // part of the exponentials on the FMA pipe
                         ex2_poly2(x0, x1);
                     } else {
                         x0 = ex2(x0);
