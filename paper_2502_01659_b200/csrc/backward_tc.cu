@@ -55,7 +55,7 @@ struct Params {
     int64_t m, r, tiles;
 };
 
-__host__ __device__ inline int64_t band_rows(int64_t m) { return ROWS + (2 * m + 15) / 16 * 16 + 16; }
+__host__ __device__ constexpr int64_t band_rows(int64_t m) { return ROWS + (2 * m + 15) / 16 * 16 + 16; }
 __host__ __device__ inline uint32_t smem_bytes(int64_t m) { return (uint32_t)(2 * ROWS * RB + 2 * band_rows(m) * RB + 2 * band_rows(m) * 4); }
 
 // A fragments (16 rows x 64) of a swizzled [rows][RB] tile, rows row0..row0+15
@@ -154,17 +154,26 @@ template <typename T> __global__ void __launch_bounds__(THREADS) row_kernel(cons
     stage<T>(sV, p.V, y0, nb, Nc, c, r, H, h);
     tc::cp_async_commit();
     // D = rowsum(dO o O) of the tile's rows (warp w: rows 16w..16w+15)
+    // all 32 loads of the warp's 16 rows issued before the first use (one memory round trip;
+    // a load-reduce loop per row waited ~16 of them, ~30% of the backward's stall samples)
     const size_t row_bytes = (size_t)H * D * sizeof(T);
+    uint32_t wdo[16], wo[16];
+#pragma unroll
     for (int rr = 0; rr < 16; ++rr) {
         const int64_t x = x0 + 16 * warp + rr;
-        float v = 0.f;
+        wdo[rr] = wo[rr] = 0u; // (0 unpacks to +0 in bf16 and fp16)
         if (x < Nc) {
             const size_t off = (size_t)(c + x * r) * row_bytes + (size_t)h * D * sizeof(T) + lane * 4;
-            float a0, a1, b0, b1;
-            unpack2<T>(*reinterpret_cast<const uint32_t *>(reinterpret_cast<const char *>(bp.dO) + off), a0, a1);
-            unpack2<T>(*reinterpret_cast<const uint32_t *>(reinterpret_cast<const char *>(bp.O) + off), b0, b1);
-            v = a0 * b0 + a1 * b1;
+            wdo[rr] = __ldg(reinterpret_cast<const unsigned int *>(reinterpret_cast<const char *>(bp.dO) + off));
+            wo[rr] = __ldg(reinterpret_cast<const unsigned int *>(reinterpret_cast<const char *>(bp.O) + off));
         }
+    }
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr) {
+        float a0, a1, b0, b1;
+        unpack2<T>(wdo[rr], a0, a1);
+        unpack2<T>(wo[rr], b0, b1);
+        float v = a0 * b0 + a1 * b1;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) sD[16 * warp + rr] = v;
@@ -320,11 +329,25 @@ template <typename T> __global__ void __launch_bounds__(THREADS) col_kernel(cons
     stage<T>(sQ, p.Q, x0, nb, Nc, c, r, H, h);
     stage<T>(sdO, bp.dO, x0, nb, Nc, c, r, H, h);
     tc::cp_async_commit();
-    for (int b = threadIdx.x; b < nb; b += THREADS) {
-        const int64_t x = x0 + b;
-        const bool in = x >= 0 && x < Nc;
-        sL[b] = in ? bp.lse[(size_t)(c + x * r) * H + h] : 0.f;
-        sD[b] = in ? bp.Dv[(size_t)(c + x * r) * H + h] : 0.f;
+    { // every load issued before the first store (one round trip)
+        constexpr int NL = (int)((band_rows(MAX_M) + THREADS - 1) / THREADS);
+        float lv[NL], dv[NL];
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+            const int b = threadIdx.x + k * THREADS;
+            const int64_t x = x0 + b;
+            const bool in = b < nb && x >= 0 && x < Nc;
+            lv[k] = in ? __ldg(bp.lse + (size_t)(c + x * r) * H + h) : 0.f;
+            dv[k] = in ? __ldg(bp.Dv + (size_t)(c + x * r) * H + h) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+            const int b = threadIdx.x + k * THREADS;
+            if (b < nb) {
+                sL[b] = lv[k];
+                sD[b] = dv[k];
+            }
+        }
     }
     tc::cp_async_wait<0>();
     __syncthreads();
