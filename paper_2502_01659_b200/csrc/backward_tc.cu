@@ -151,14 +151,9 @@ template <typename T> __global__ void __launch_bounds__(THREADS) row_kernel(cons
                    sV = sK + nb * RB;
     float *sD = reinterpret_cast<float *>(smem + 2 * ROWS * RB + 2 * nb * RB);
     const int64_t y0 = x0 - m; // band row 0
-    stage<T>(sQ, p.Q, x0, ROWS, Nc, c, r, H, h);
-    stage<T>(sdO, bp.dO, x0, ROWS, Nc, c, r, H, h);
-    stage<T>(sK, p.K, y0, nb, Nc, c, r, H, h);
-    stage<T>(sV, p.V, y0, nb, Nc, c, r, H, h);
-    tc::cp_async_commit();
-    // D = rowsum(dO o O) of the tile's rows (warp w: rows 16w..16w+15)
-    // all 32 loads of the warp's 16 rows issued before the first use (one memory round trip;
-    // a load-reduce loop per row waited ~16 of them, ~30% of the backward's stall samples)
+    // D = rowsum(dO o O) of the tile's rows (warp w: rows 16w..16w+15): the warp's 32 loads are
+    // issued first and used after the staging copies are issued (one memory round trip under
+    // the staging; a load-reduce loop per row waited ~16 of them, ~30% of the stall samples)
     const size_t row_bytes = (size_t)H * D * sizeof(T);
     uint32_t wdo[16], wo[16];
 #pragma unroll
@@ -171,6 +166,11 @@ template <typename T> __global__ void __launch_bounds__(THREADS) row_kernel(cons
             wo[rr] = __ldg(reinterpret_cast<const unsigned int *>(reinterpret_cast<const char *>(bp.O) + off));
         }
     }
+    stage<T>(sQ, p.Q, x0, ROWS, Nc, c, r, H, h);
+    stage<T>(sdO, bp.dO, x0, ROWS, Nc, c, r, H, h);
+    stage<T>(sK, p.K, y0, nb, Nc, c, r, H, h);
+    stage<T>(sV, p.V, y0, nb, Nc, c, r, H, h);
+    tc::cp_async_commit();
 #pragma unroll
     for (int rr = 0; rr < 16; ++rr) {
         float a0, a1, b0, b1;
@@ -327,29 +327,28 @@ template <typename T> __global__ void __launch_bounds__(THREADS) col_kernel(cons
                    sdO = sQ + nb * RB;
     float *sL = reinterpret_cast<float *>(smem + 2 * ROWS * RB + 2 * nb * RB), *sD = sL + nb;
     const int64_t x0 = y0 - m; // query band row 0
+    // lse and D of the query band: loads issued before the staging copies, stored after them
+    constexpr int NL = (int)((band_rows(MAX_M) + THREADS - 1) / THREADS);
+    float lsev[NL], dval[NL];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+        const int b = threadIdx.x + k * THREADS;
+        const int64_t x = x0 + b;
+        const bool in = b < nb && x >= 0 && x < Nc;
+        lsev[k] = in ? __ldg(bp.lse + (size_t)(c + x * r) * H + h) : 0.f;
+        dval[k] = in ? __ldg(bp.Dv + (size_t)(c + x * r) * H + h) : 0.f;
+    }
     stage<T>(sK, p.K, y0, ROWS, Nc, c, r, H, h);
     stage<T>(sV, p.V, y0, ROWS, Nc, c, r, H, h);
     stage<T>(sQ, p.Q, x0, nb, Nc, c, r, H, h);
     stage<T>(sdO, bp.dO, x0, nb, Nc, c, r, H, h);
     tc::cp_async_commit();
-    { // every load issued before the first store (one round trip)
-        constexpr int NL = (int)((band_rows(MAX_M) + THREADS - 1) / THREADS);
-        float lv[NL], dv[NL];
 #pragma unroll
-        for (int k = 0; k < NL; ++k) {
-            const int b = threadIdx.x + k * THREADS;
-            const int64_t x = x0 + b;
-            const bool in = b < nb && x >= 0 && x < Nc;
-            lv[k] = in ? __ldg(bp.lse + (size_t)(c + x * r) * H + h) : 0.f;
-            dv[k] = in ? __ldg(bp.Dv + (size_t)(c + x * r) * H + h) : 0.f;
-        }
-#pragma unroll
-        for (int k = 0; k < NL; ++k) {
-            const int b = threadIdx.x + k * THREADS;
-            if (b < nb) {
-                sL[b] = lv[k];
-                sD[b] = dv[k];
-            }
+    for (int k = 0; k < NL; ++k) {
+        const int b = threadIdx.x + k * THREADS;
+        if (b < nb) {
+            sL[b] = lsev[k];
+            sD[b] = dval[k];
         }
     }
     tc::cp_async_wait<0>();
