@@ -129,7 +129,8 @@ def test_backward_rejects(ga):
 
 
 @pytest.mark.parametrize("L,w,r,dt", [(3000, 256, 2, "bf16"), (2049, 128, 1, "f16"), (1500, 17, 1, "bf16"),
-                                      (4000, 400, 4, "bf16"), (700, 600, 1, "f16")])
+                                      (4000, 400, 4, "bf16"), (700, 600, 1, "f16"),
+                                      (2500, 256, 1, "bf16")])  # m = 255: the widest band (592 staged rows)
 def test_backward_tensor_core_band_vs_oracle(ga, orc, L, w, r, dt):
     """The tensor-core band backward (backward_tc.cu: Window masks, bf16/fp16, d = 64, m <=
     255) against the fp64 oracle backward, ragged class lengths and sequences shorter than
