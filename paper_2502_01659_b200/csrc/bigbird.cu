@@ -157,8 +157,13 @@ __device__ int extras(const DevMask &M, const View &V, int parts, int32_t i, int
     return n;
 }
 
+#ifndef GA_BB_MINB
+#define GA_BB_MINB 4 // CTAs per SM the register allocation targets: 4 -> 64 registers (36 B of spills
+                      // in cold paths) 4.44 ms at cfg3i; 3 -> 76, spill-free, 5.32; 5 -> 48, 4.50-4.60;
+                      // 6 -> 40, 6.5 (the gathers want warps in flight more than registers)
+#endif
 template <typename T, int D>
-__global__ void __launch_bounds__(WARPS * 32) extras_kernel(const __grid_constant__ AttnParams p, const Args a)
+__global__ void __launch_bounds__(WARPS * 32, GA_BB_MINB) extras_kernel(const __grid_constant__ AttnParams p, const Args a)
 {
     __shared__ int32_t cols[WARPS][CAP];
     __shared__ int32_t sG[CAP];
