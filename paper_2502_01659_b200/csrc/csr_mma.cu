@@ -324,11 +324,11 @@ __global__ void __launch_bounds__(TW * 32, 2) csr_tma_kernel(const __grid_consta
     };
     // pairs PD .. PD + RQ - 1 in flight in registers (global loads of the column indices)
 #ifndef GA_CSR_RQ
-#define GA_CSR_RQ 4 // measured cfg3: 2 -> 8.86, 3 -> 8.83, 4 -> 8.78 ms
+#define GA_CSR_RQ 6 // measured cfg3: 2 -> 8.86, 3 -> 8.83, 4 -> 8.78 ms; later, same box: 4 -> 8.727, 6 -> 8.709, 8 -> 8.832
 #endif
     constexpr int RQ = GA_CSR_RQ;
-    static_assert(RQ >= 2 && RQ <= 4, "index register queue");
-    int rq[4];
+    static_assert(RQ >= 2 && RQ <= 8, "index register queue");
+    int rq[RQ];
     for (int P = 0; P < PD; ++P) st_pair(P, ld_pair(P));
 #pragma unroll
     for (int u = 0; u < RQ; ++u) rq[u] = ld_pair(PD + u);
