@@ -137,7 +137,10 @@ constexpr int TW = GA_CSR_TW; // warps per CTA
 constexpr int TS = GA_CSR_TS; // stages per warp
 constexpr int STAGE = 4096; // bytes per stage
 constexpr int IR = 8;       // column-index ring slots per warp (32 edges each)
-constexpr int PD = 5;       // index pairs staged ahead
+#ifndef GA_CSR_PD
+#define GA_CSR_PD 7 // cfg3, same box: 3 -> 8.777, 5 -> 8.708, 7 -> 8.686 ms (7 = IR - 1, the most the ring allows)
+#endif
+constexpr int PD = GA_CSR_PD; // index pairs staged ahead
 static_assert(PD < IR, "a slot is refilled only after its pair was issued");
 
 struct TmaParams {
