@@ -69,6 +69,8 @@ constexpr int THREADS = 32 * 16;
 #define GA_WTC_REG_SMX 160
 #endif
 constexpr int REG_SMX = GA_WTC_REG_SMX, REG_EPI = 104, REG_PROD = 512 - 2 * REG_SMX - REG_EPI;
+static_assert(REG_SMX % 8 == 0 && REG_EPI % 8 == 0 && REG_PROD % 8 == 0 && REG_PROD >= 24 && REG_SMX <= 256,
+              "setmaxnreg takes multiples of 8 in [24, 256]");
 constexpr uint32_t QBYTES = ROWS * RB;   // 16 KB
 constexpr uint32_t CBYTES = KC * RB;     // 8 KB: one K or V chunk
 constexpr uint32_t OFF_Q = 0;            // Q[wg][buf]: 4 x 16 KB (a finished tile's O is staged in its Q buffer)
