@@ -64,11 +64,15 @@ constexpr int THREADS = 32 * 16;
 // registers per thread after setmaxnreg (per SM sub-partition: one warp of each warpgroup,
 // 2 x 160 + 104 + 88 = 512 = the 16K registers of the sub-partition / 32 lanes).  168 for the
 // softmax left the loader / issuers 72 and they spilled (20 B); 160 / 88 is spill-free and
-// measured 0.4-1.1% faster at cfg5 (same box); 176 spills 144 B.
+// measured 0.4-1.1% faster at cfg5 (same box); 176 spills 144 B, and the epilogue spills below
+// 104 (96: 24 B, 88 with the softmax at 168: 32 B).
 #ifndef GA_WTC_REG_SMX
 #define GA_WTC_REG_SMX 160
 #endif
-constexpr int REG_SMX = GA_WTC_REG_SMX, REG_EPI = 104, REG_PROD = 512 - 2 * REG_SMX - REG_EPI;
+#ifndef GA_WTC_REG_EPI
+#define GA_WTC_REG_EPI 104
+#endif
+constexpr int REG_SMX = GA_WTC_REG_SMX, REG_EPI = GA_WTC_REG_EPI, REG_PROD = 512 - 2 * REG_SMX - REG_EPI;
 static_assert(REG_SMX % 8 == 0 && REG_EPI % 8 == 0 && REG_PROD % 8 == 0 && REG_PROD >= 24 && REG_SMX <= 256,
               "setmaxnreg takes multiples of 8 in [24, 256]");
 constexpr uint32_t QBYTES = ROWS * RB;   // 16 KB
