@@ -446,8 +446,9 @@ __global__ void __launch_bounds__(THREADS, 1) window_tc_kernel(const __grid_cons
         // Issuer w serves softmax warpgroup w (its tile of every item).  Warp-uniform control
         // flow (the whole warp runs the schedule and the blocking waits; one elected lane
         // issues).  Per chunk j of a tile (c: running counter over the warpgroup's tiles):
-        //     S(c + 1) into S buffer (c + 1) & 1 once P V(c - 1) completed (P(c - 1) lives in that
-        //     buffer); then P V(c) once P(c) arrived — so S runs two chunks ahead of the softmax.
+        //     S(c + 1) into S buffer (c + 1) & 1, whose S(c - 1) the softmax has read (P(c - 1)
+        //     arrived; with GA_WTC_PSEP=0, P(c - 1) lives there and P V(c - 1) must complete
+        //     first); then P V(c) once P(c) arrived — so S runs two chunks ahead of the softmax.
         // The first two S of the next tile are issued around this tile's last P V (when the next
         // Q tile has landed).  Both issuers arrive once on a slot's empty barrier per fill: after
         // their last P V reading the chunk, or — for a chunk their tile does not read — after
